@@ -1,0 +1,626 @@
+// phmm_engine.cu — host engine + C-ABI of libphmm.so (see include/phmm.h).
+//
+// Host side (C++): validation, config binding (partition.py:20-37), pair enumeration
+// (model.py:123-136), haplotype pairing + length binning + LPT ordering of work units,
+// H2D upload, kernel launches on one stream, D2H and finishing (wavefront.py:428-434:
+// flag acc<=0/non-finite, log10(acc) - s*log10 2 with glibc log10 like CPython math.log10).
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "../../include/phmm.h"
+#include "phmm_kernels.cuh"
+
+using namespace phmm;
+
+namespace {
+
+constexpr double kLog10_2 = 0.30102999566398120;   // np.log10(2.0), prob.py:41
+
+template <class T>
+struct DBuf {
+  T* p = nullptr;
+  size_t cap = 0;
+  cudaError_t ensure(size_t n) {
+    if (n <= cap && p) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr; cap = 0;
+    size_t want = std::max<size_t>(n, 1);
+    cudaError_t e = cudaMalloc(&p, want * sizeof(T));
+    if (e == cudaSuccess) cap = want;
+    return e;
+  }
+  void release() { if (p) cudaFree(p); p = nullptr; cap = 0; }
+};
+
+struct FastGeom { int P, K; };
+// single-stripe widths W = P*K: 16 32 48 64 96 128 192 256 384 512
+const FastGeom kFastGeoms[] = {{4, 4}, {4, 8}, {4, 12}, {4, 16}, {8, 12},
+                               {8, 16}, {16, 12}, {16, 16}, {32, 12}, {32, 16}};
+constexpr int kNumFastGeoms = sizeof(kFastGeoms) / sizeof(kFastGeoms[0]);
+constexpr int kExactP[kNumExactP] = {4, 8, 16, 32};
+constexpr int kThreads = 128;
+
+struct Bin {
+  int geom, Q;
+  std::vector<FastUnit> units;
+  int64_t dev_off = 0;     // offset into the device unit array
+};
+
+// fast-kernel launcher table
+typedef void (*FastFn)(const EngineDev, const FastUnit*, int, int, int*, float2*, int);
+template <int P, int K>
+void launch_fast(dim3 g, size_t smem, cudaStream_t s, const EngineDev& E, const FastUnit* u, int nu,
+                 int Q, int* ctr, float2* col, int rows) {
+  k_fast<P, K><<<g, kThreads, smem, s>>>(E, u, nu, Q, ctr, col, rows);
+}
+typedef void (*FastLaunch)(dim3, size_t, cudaStream_t, const EngineDev&, const FastUnit*, int, int,
+                           int*, float2*, int);
+const FastLaunch kFastLaunch[kNumFastGeoms] = {
+    launch_fast<4, 4>,   launch_fast<4, 8>,   launch_fast<4, 12>,  launch_fast<4, 16>,
+    launch_fast<8, 12>,  launch_fast<8, 16>,  launch_fast<16, 12>, launch_fast<16, 16>,
+    launch_fast<32, 12>, launch_fast<32, 16>};
+const void* kFastFn[kNumFastGeoms] = {
+    (const void*)k_fast<4, 4>,   (const void*)k_fast<4, 8>,   (const void*)k_fast<4, 12>,
+    (const void*)k_fast<4, 16>,  (const void*)k_fast<8, 12>,  (const void*)k_fast<8, 16>,
+    (const void*)k_fast<16, 12>, (const void*)k_fast<16, 16>, (const void*)k_fast<32, 12>,
+    (const void*)k_fast<32, 16>};
+
+template <typename T, int P>
+void launch_exact(dim3 g, size_t smem, cudaStream_t s, const EngineDev& E, int slot, int* ctr, void* col,
+                  int rows) {
+  k_exact<T, P, kExactK><<<g, kThreads, smem, s>>>(E, slot, ctr, (T*)col, rows);
+}
+typedef void (*ExactLaunch)(dim3, size_t, cudaStream_t, const EngineDev&, int, int*, void*, int);
+const ExactLaunch kExact32[kNumExactP] = {launch_exact<float, 4>, launch_exact<float, 8>,
+                                          launch_exact<float, 16>, launch_exact<float, 32>};
+const ExactLaunch kExact64[kNumExactP] = {launch_exact<double, 4>, launch_exact<double, 8>,
+                                          launch_exact<double, 16>, launch_exact<double, 32>};
+const void* kExact32Fn[kNumExactP] = {(const void*)k_exact<float, 4, kExactK>, (const void*)k_exact<float, 8, kExactK>,
+                                      (const void*)k_exact<float, 16, kExactK>, (const void*)k_exact<float, 32, kExactK>};
+const void* kExact64Fn[kNumExactP] = {(const void*)k_exact<double, 4, kExactK>, (const void*)k_exact<double, 8, kExactK>,
+                                      (const void*)k_exact<double, 16, kExactK>, (const void*)k_exact<double, 32, kExactK>};
+
+int exact_slot_host(int m) { return (m + 1 <= 32) ? 0 : (m + 1 <= 64) ? 1 : (m + 1 <= 128) ? 2 : 3; }
+
+size_t fast_smem(int geom) {
+  const FastGeom g = kFastGeoms[geom];
+  return 96 * sizeof(double) + (size_t)(kThreads / 32) * (32 / g.P) * 5 * g.K * g.P * sizeof(float);
+}
+size_t exact_smem(int slot, size_t tsize) {
+  const int P = kExactP[slot];
+  return 96 * sizeof(double) + (size_t)(kThreads / 32) * (32 / P) * 5 * kExactK * P * tsize;
+}
+
+// Cost model for choosing a fast geometry: padded cells x (rows + fill/drain), plus a
+// per-step overhead worth ~2.5 cells per thread.
+// Single-stripe tilings (W >= m + 1) are preferred; reads longer than the widest tile
+// (m >= 512) stripe over P = 32 tiles.
+int choose_geom(int m, int nmax, int* Qout) {
+  double best = 1e300;
+  int bi = 0, bq = 1;
+  const bool stripe = m + 1 > kFastGeoms[kNumFastGeoms - 1].P * kFastGeoms[kNumFastGeoms - 1].K;
+  for (int g = 0; g < kNumFastGeoms; ++g) {
+    const int P = kFastGeoms[g].P, K = kFastGeoms[g].K, W = P * K;
+    const int Q = (m + 1 + W - 1) / W;
+    if (stripe ? P != 32 : Q != 1) continue;
+    const double cost = (double)Q * P * (K + 2.5) * (double)(nmax + P - 1);
+    if (cost < best - 1e-9) { best = cost; bi = g; bq = Q; }
+  }
+  *Qout = bq;
+  return bi;
+}
+
+}  // namespace
+
+struct phmm_ctx {
+  int device = 0;
+  int num_sms = 148;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev_start = nullptr, ev_fast0 = nullptr, ev_fast1 = nullptr, ev_end = nullptr;
+  std::string err;
+  std::vector<double> lut;
+
+  // device buffers
+  DBuf<int8_t> d_rbases, d_hbases;
+  DBuf<uint8_t> d_bq, d_iq, d_dq, d_gq, d_status, d_rflags;
+  DBuf<int64_t> d_roff, d_hoff;
+  DBuf<int> d_read_m, d_read_scale, d_read_ncap, d_counters;
+  DBuf<float> d_gsum;
+  DBuf<double> d_lut, d_acc;
+  DBuf<FastUnit> d_units;
+  DBuf<ExactItem> d_ex32[kNumExactP], d_ex64[kNumExactP];
+  DBuf<float2> d_colf;
+  DBuf<double> d_cold;
+  int* h_counts = nullptr;   // pinned: initial list counts (8) + zeros for work counters
+
+  // plan (host)
+  bool prepared = false, executed = false;
+  int64_t num_pairs = 0;
+  int64_t num_reads = 0, num_haps = 0, num_batches = 0;
+  std::vector<int64_t> batch_read_off, batch_hap_off, hap_len;
+  std::vector<int> read_m, read_scale, read_cfg;   // read_cfg -1 = too small
+  std::vector<Bin> bins;
+  int host_ex32[kNumExactP] = {0, 0, 0, 0}, host_ex64[kNumExactP] = {0, 0, 0, 0};
+  int max_n = 1;
+  int flags = 0;
+  int list_cap = 0;
+  int64_t h2d_bytes = 0;
+  double plan_ms = 0.0, h2d_ms = 0.0;
+  int last_launches = 0;
+  float last_dev_ms = 0.f, last_fast_ms = 0.f;
+  EngineDev dev{};
+
+  int fail(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    err = buf;
+    return code;
+  }
+  int cuda_fail(cudaError_t e, const char* what) {
+    return fail(PHMM_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+  }
+};
+
+#define CK(call)                                                        \
+  do {                                                                  \
+    cudaError_t _e = (call);                                            \
+    if (_e != cudaSuccess) return ctx->cuda_fail(_e, #call);            \
+  } while (0)
+
+extern "C" {
+
+int phmm_abi_version(void) { return PHMM_ABI_VERSION; }
+
+int phmm_create(phmm_ctx** out, int device, const double* phred_lut) {
+  if (!out || !phred_lut) return PHMM_ERR_INVALID;
+  *out = nullptr;
+  phmm_ctx* ctx = new (std::nothrow) phmm_ctx();
+  if (!ctx) return PHMM_ERR_NOMEM;
+  ctx->device = device;
+  ctx->lut.assign(phred_lut, phred_lut + 94);
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || device < 0 || device >= ndev) {
+    *out = ctx;
+    ctx->fail(PHMM_ERR_CUDA, "no CUDA device %d (%s)", device,
+              e != cudaSuccess ? cudaGetErrorString(e) : "out of range");
+    return PHMM_ERR_CUDA;
+  }
+  *out = ctx;
+  CK(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  CK(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10) return ctx->fail(PHMM_ERR_CUDA, "device %s is sm_%d%d; libphmm is built for sm_100a",
+                                         prop.name, prop.major, prop.minor);
+  ctx->num_sms = prop.multiProcessorCount;
+  CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+  CK(cudaEventCreate(&ctx->ev_start));
+  CK(cudaEventCreate(&ctx->ev_fast0));
+  CK(cudaEventCreate(&ctx->ev_fast1));
+  CK(cudaEventCreate(&ctx->ev_end));
+  CK(cudaMallocHost(&ctx->h_counts, 64 * sizeof(int)));
+  CK(ctx->d_lut.ensure(94));
+  CK(cudaMemcpy(ctx->d_lut.p, ctx->lut.data(), 94 * sizeof(double), cudaMemcpyHostToDevice));
+  for (int g = 0; g < kNumFastGeoms; ++g)
+    CK(cudaFuncSetAttribute(kFastFn[g], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fast_smem(g)));
+  for (int s = 0; s < kNumExactP; ++s) {
+    CK(cudaFuncSetAttribute(kExact32Fn[s], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)exact_smem(s, 4)));
+    CK(cudaFuncSetAttribute(kExact64Fn[s], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)exact_smem(s, 8)));
+  }
+  return PHMM_SUCCESS;
+}
+
+int phmm_destroy(phmm_ctx* ctx) {
+  if (!ctx) return PHMM_SUCCESS;
+  cudaSetDevice(ctx->device);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  ctx->d_rbases.release(); ctx->d_hbases.release(); ctx->d_bq.release(); ctx->d_iq.release();
+  ctx->d_dq.release(); ctx->d_gq.release(); ctx->d_status.release(); ctx->d_rflags.release();
+  ctx->d_roff.release(); ctx->d_hoff.release(); ctx->d_read_m.release(); ctx->d_read_scale.release();
+  ctx->d_read_ncap.release(); ctx->d_counters.release(); ctx->d_gsum.release(); ctx->d_lut.release();
+  ctx->d_acc.release(); ctx->d_units.release(); ctx->d_colf.release(); ctx->d_cold.release();
+  for (int s = 0; s < kNumExactP; ++s) { ctx->d_ex32[s].release(); ctx->d_ex64[s].release(); }
+  if (ctx->h_counts) cudaFreeHost(ctx->h_counts);
+  if (ctx->ev_start) cudaEventDestroy(ctx->ev_start);
+  if (ctx->ev_fast0) cudaEventDestroy(ctx->ev_fast0);
+  if (ctx->ev_fast1) cudaEventDestroy(ctx->ev_fast1);
+  if (ctx->ev_end) cudaEventDestroy(ctx->ev_end);
+  if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+  return PHMM_SUCCESS;
+}
+
+const char* phmm_last_error(const phmm_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+int phmm_prepare(phmm_ctx* ctx, const phmm_input* in, const phmm_options* opt, int64_t* num_pairs_out) {
+  if (!ctx) return PHMM_ERR_INVALID;
+  if (!in || !opt) return ctx->fail(PHMM_ERR_INVALID, "null input/options");
+  auto t0 = std::chrono::steady_clock::now();
+  CK(cudaSetDevice(ctx->device));
+  ctx->prepared = false;
+  ctx->executed = false;
+  const int64_t R = in->num_reads, H = in->num_haps, B = in->num_batches;
+  if (R < 0 || H < 0 || B < 0) return ctx->fail(PHMM_ERR_INVALID, "negative counts");
+  if (opt->num_configs < 0 || (opt->num_configs > 0 && (!opt->p || !opt->k || !opt->precision || !opt->scale_log2)))
+    return ctx->fail(PHMM_ERR_INVALID, "bad config table");
+  // ---- structure validation
+  if (B > 0 && (!in->batch_read_off || !in->batch_hap_off)) return ctx->fail(PHMM_ERR_INVALID, "null batch offsets");
+  if (B > 0) {
+    if (in->batch_read_off[0] != 0 || in->batch_hap_off[0] != 0 || in->batch_read_off[B] != R ||
+        in->batch_hap_off[B] != H)
+      return ctx->fail(PHMM_ERR_INVALID, "batch offsets do not cover the read/hap arrays");
+    for (int64_t b = 0; b < B; ++b)
+      if (in->batch_read_off[b + 1] <= in->batch_read_off[b] || in->batch_hap_off[b + 1] <= in->batch_hap_off[b])
+        return ctx->fail(PHMM_ERR_INVALID, "batch %lld must contain at least one read and one haplotype",
+                         (long long)b);
+  } else if (R != 0 || H != 0) {
+    return ctx->fail(PHMM_ERR_INVALID, "reads/haps given without batches");
+  }
+  const int64_t* roff = in->read_off;
+  const int64_t* hoff = in->hap_off;
+  if (R > 0 && (!roff || roff[0] != 0)) return ctx->fail(PHMM_ERR_INVALID, "read offsets must start at 0");
+  if (H > 0 && (!hoff || hoff[0] != 0)) return ctx->fail(PHMM_ERR_INVALID, "hap offsets must start at 0");
+  for (int64_t r = 0; r < R; ++r)
+    if (roff[r + 1] <= roff[r]) return ctx->fail(PHMM_ERR_INVALID, "read %lld must contain at least one base", (long long)r);
+  for (int64_t h = 0; h < H; ++h)
+    if (hoff[h + 1] <= hoff[h]) return ctx->fail(PHMM_ERR_INVALID, "haplotype %lld must contain at least one base", (long long)h);
+  const int64_t RL = R ? roff[R] : 0, HL = H ? hoff[H] : 0;
+  {
+    uint8_t bad = 0;
+    for (int64_t i = 0; i < RL; ++i) bad |= (uint8_t)((uint8_t)in->read_bases[i] > 4);
+    for (int64_t i = 0; i < HL; ++i) bad |= (uint8_t)((uint8_t)in->hap_bases[i] > 4);
+    if (bad) return ctx->fail(PHMM_ERR_INVALID, "base code outside A,C,G,T,N (0..4)");
+    uint8_t mx = 0;
+    for (int64_t i = 0; i < RL; ++i)
+      mx |= (uint8_t)((in->base_qual[i] > 93) | (in->ins_qual[i] > 93) | (in->del_qual[i] > 93) | (in->gcp_qual[i] > 93));
+    if (mx) return ctx->fail(PHMM_ERR_INVALID, "quality values must be in [0, 93]");
+  }
+  for (int c = 0; c < opt->num_configs; ++c) {
+    if (opt->p[c] < 1 || opt->k[c] < 1 || (opt->precision[c] != 0 && opt->precision[c] != 1) || opt->scale_log2[c] < 0)
+      return ctx->fail(PHMM_ERR_INVALID, "invalid config %d", c);
+  }
+  ctx->flags = opt->flags;
+  ctx->num_reads = R; ctx->num_haps = H; ctx->num_batches = B;
+  ctx->batch_read_off.assign(in->batch_read_off, in->batch_read_off + (B ? B + 1 : 0));
+  ctx->batch_hap_off.assign(in->batch_hap_off, in->batch_hap_off + (B ? B + 1 : 0));
+  ctx->hap_len.resize(H);
+  for (int64_t h = 0; h < H; ++h) ctx->hap_len[h] = hoff[h + 1] - hoff[h];
+
+  // ---- config binding: smallest p*k >= m, ties to fewer lanes (partition.py:20-37)
+  std::vector<int> order(opt->num_configs);
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
+    const int64_t ma = (int64_t)opt->p[a] * opt->k[a], mb = (int64_t)opt->p[b] * opt->k[b];
+    return ma != mb ? ma < mb : opt->p[a] < opt->p[b];
+  });
+  ctx->read_m.resize(R); ctx->read_scale.resize(R); ctx->read_cfg.resize(R);
+  std::vector<int> read_ncap(R, 1);
+  for (int64_t r = 0; r < R; ++r) {
+    const int64_t m = roff[r + 1] - roff[r];
+    if (m > (int64_t)1 << 30) return ctx->fail(PHMM_ERR_INVALID, "read too long");
+    ctx->read_m[r] = (int)m;
+    int cfg = -1;
+    for (int c : order)
+      if ((int64_t)opt->p[c] * opt->k[c] >= m) { cfg = c; break; }
+    ctx->read_cfg[r] = cfg;
+    ctx->read_scale[r] = cfg >= 0 ? opt->scale_log2[cfg] : 0;
+  }
+  // ---- pairs, hap pairing, units
+  int64_t N = 0;
+  for (int64_t b = 0; b < B; ++b)
+    N += (ctx->batch_read_off[b + 1] - ctx->batch_read_off[b]) * (ctx->batch_hap_off[b + 1] - ctx->batch_hap_off[b]);
+  if (N > INT32_MAX - 1) return ctx->fail(PHMM_ERR_INVALID, "too many pairs in one call (%lld)", (long long)N);
+  ctx->num_pairs = N;
+  const bool exact_mode = (opt->flags & PHMM_FLAG_EXACT) != 0;
+  ctx->bins.clear();
+  std::vector<int> bin_index(kNumFastGeoms * 64, -1);
+  std::vector<ExactItem> host32[kNumExactP], host64[kNumExactP];
+  int max_n = 1;
+  int64_t gid = 0;
+  std::vector<int> hidx;
+  for (int64_t b = 0; b < B; ++b) {
+    const int64_t r0 = ctx->batch_read_off[b], r1 = ctx->batch_read_off[b + 1];
+    const int64_t h0 = ctx->batch_hap_off[b], h1 = ctx->batch_hap_off[b + 1];
+    const int64_t nh = h1 - h0;
+    int ncap = 1;
+    for (int64_t h = h0; h < h1; ++h) ncap = (int)std::max<int64_t>(ncap, ctx->hap_len[h]);
+    max_n = std::max(max_n, ncap);
+    hidx.resize(nh);
+    std::iota(hidx.begin(), hidx.end(), (int)h0);
+    std::stable_sort(hidx.begin(), hidx.end(), [&](int a, int c) { return ctx->hap_len[a] > ctx->hap_len[c]; });
+    for (int64_t r = r0; r < r1; ++r, gid += nh) {
+      read_ncap[r] = ncap;
+      const int cfg = ctx->read_cfg[r];
+      if (cfg < 0) continue;                         // config-too-small: host-side status
+      const int m = ctx->read_m[r];
+      const int scale = opt->scale_log2[cfg];
+      const bool f64 = opt->precision[cfg] == 1;
+      if (f64 || exact_mode || scale > 126) {
+        for (int64_t h = h0; h < h1; ++h) {
+          ExactItem it{(int)(gid + (h - h0)), (int)r, (int)h, scale};
+          (f64 ? host64 : host32)[exact_slot_host(m)].push_back(it);
+        }
+        continue;
+      }
+      for (int64_t x = 0; x < nh; x += 2) {
+        const int ha = hidx[x], hb = (x + 1 < nh) ? hidx[x + 1] : hidx[x];
+        FastUnit u;
+        u.read = (int)r; u.hapA = ha; u.hapB = hb;
+        u.pairA = (int)(gid + (ha - h0));
+        u.pairB = (x + 1 < nh) ? (int)(gid + (hb - h0)) : -1;
+        u.nA = (int)ctx->hap_len[ha]; u.nB = (int)ctx->hap_len[hb];
+        u.pad = 0;
+        int Q;
+        const int g = choose_geom(m, std::max(u.nA, u.nB), &Q);
+        const int key = g * 64 + std::min(Q, 63);
+        if (bin_index[key] < 0) {
+          bin_index[key] = (int)ctx->bins.size();
+          ctx->bins.push_back(Bin{g, Q, {}, 0});
+        }
+        ctx->bins[bin_index[key]].units.push_back(u);
+      }
+    }
+  }
+  ctx->max_n = max_n;
+  // LPT: costliest units first inside every bin; stable for determinism
+  int64_t nunits = 0;
+  for (auto& bn : ctx->bins) {
+    std::stable_sort(bn.units.begin(), bn.units.end(), [](const FastUnit& a, const FastUnit& c) {
+      return std::max(a.nA, a.nB) > std::max(c.nA, c.nB);
+    });
+    bn.dev_off = nunits;
+    nunits += (int64_t)bn.units.size();
+  }
+  auto t1 = std::chrono::steady_clock::now();
+  ctx->plan_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
+
+  // ---- upload
+  int64_t bytes = 0;
+  auto up = [&](auto& buf, const auto* src, size_t n) -> cudaError_t {
+    cudaError_t e = buf.ensure(n);
+    if (e != cudaSuccess || n == 0) return e;
+    bytes += (int64_t)(n * sizeof(*src));
+    return cudaMemcpyAsync(buf.p, src, n * sizeof(*src), cudaMemcpyHostToDevice, ctx->stream);
+  };
+  CK(cudaEventRecord(ctx->ev_start, ctx->stream));
+  CK(up(ctx->d_rbases, in->read_bases, RL));
+  CK(up(ctx->d_bq, in->base_qual, RL));
+  CK(up(ctx->d_iq, in->ins_qual, RL));
+  CK(up(ctx->d_dq, in->del_qual, RL));
+  CK(up(ctx->d_gq, in->gcp_qual, RL));
+  CK(up(ctx->d_roff, roff, R ? R + 1 : 0));
+  CK(up(ctx->d_hbases, in->hap_bases, HL));
+  CK(up(ctx->d_hoff, hoff, H ? H + 1 : 0));
+  CK(up(ctx->d_read_m, ctx->read_m.data(), R));
+  CK(up(ctx->d_read_scale, ctx->read_scale.data(), R));
+  CK(up(ctx->d_read_ncap, read_ncap.data(), R));
+  std::vector<FastUnit> allu;
+  allu.reserve(nunits);
+  for (auto& bn : ctx->bins) allu.insert(allu.end(), bn.units.begin(), bn.units.end());
+  CK(up(ctx->d_units, allu.data(), allu.size()));
+  CK(ctx->d_gsum.ensure(R));
+  CK(ctx->d_rflags.ensure(R));
+  CK(ctx->d_acc.ensure(N));
+  CK(ctx->d_status.ensure(N));
+  CK(ctx->d_counters.ensure(64));
+  ctx->list_cap = (int)std::max<int64_t>(N, 1);
+  for (int s = 0; s < kNumExactP; ++s) {
+    ctx->host_ex32[s] = (int)host32[s].size();
+    ctx->host_ex64[s] = (int)host64[s].size();
+    CK(ctx->d_ex32[s].ensure(ctx->list_cap));
+    CK(ctx->d_ex64[s].ensure(ctx->list_cap));
+    if (!host32[s].empty()) CK(up(ctx->d_ex32[s], host32[s].data(), host32[s].size()));
+    if (!host64[s].empty()) CK(up(ctx->d_ex64[s], host64[s].data(), host64[s].size()));
+  }
+  // boundary-column scratch: 2 buffers x 3 values x (max_n + 1) rows per sub-warp slot
+  const int slots_per_sm = 2 * (kThreads / 32) * 8;   // <= 2 CTAs/SM x 4 warps x 8 sub-warps
+  const size_t col_elems = (size_t)ctx->num_sms * slots_per_sm * 2 * 3 * (size_t)(max_n + 1);
+  bool need_col = false, need_cold = false;
+  for (auto& bn : ctx->bins) need_col |= bn.Q > 1;
+  for (int s = 0; s < kNumExactP; ++s) need_cold |= true;
+  if (need_col) CK(ctx->d_colf.ensure(col_elems));
+  CK(ctx->d_cold.ensure(col_elems));   // exact kernels (f32 view uses half of it)
+  (void)need_cold;
+  CK(cudaEventRecord(ctx->ev_end, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  float h2d = 0.f;
+  cudaEventElapsedTime(&h2d, ctx->ev_start, ctx->ev_end);
+  ctx->h2d_ms = h2d;
+  ctx->h2d_bytes = bytes;
+
+  EngineDev& E = ctx->dev;
+  E.rbases = ctx->d_rbases.p; E.bq = ctx->d_bq.p; E.iq = ctx->d_iq.p; E.dq = ctx->d_dq.p; E.gq = ctx->d_gq.p;
+  E.roff = ctx->d_roff.p; E.hbases = ctx->d_hbases.p; E.hoff = ctx->d_hoff.p;
+  E.read_m = ctx->d_read_m.p; E.read_scale = ctx->d_read_scale.p; E.read_ncap = ctx->d_read_ncap.p;
+  E.read_gsum = ctx->d_gsum.p; E.read_flags = ctx->d_rflags.p; E.lut = ctx->d_lut.p;
+  E.acc = ctx->d_acc.p; E.status = ctx->d_status.p;
+  for (int s = 0; s < kNumExactP; ++s) { E.ex32[s] = ctx->d_ex32[s].p; E.ex64[s] = ctx->d_ex64[s].p; }
+  E.ex32_count = ctx->d_counters.p + 0;
+  E.ex64_count = ctx->d_counters.p + kNumExactP;
+  E.list_cap = ctx->list_cap;
+  E.retry_f64 = (opt->flags & PHMM_FLAG_RETRY_F64) ? 1 : 0;
+  ctx->prepared = true;
+  if (num_pairs_out) *num_pairs_out = N;
+  return PHMM_SUCCESS;
+}
+
+int phmm_execute(phmm_ctx* ctx) {
+  if (!ctx) return PHMM_ERR_INVALID;
+  if (!ctx->prepared) return ctx->fail(PHMM_ERR_STATE, "phmm_execute before phmm_prepare");
+  CK(cudaSetDevice(ctx->device));
+  cudaStream_t st = ctx->stream;
+  const EngineDev& E = ctx->dev;
+  const int64_t N = ctx->num_pairs;
+  int launches = 0;
+  // counters: [0,4) ex32 counts, [4,8) ex64 counts, [8,12) ex32 work, [12,16) ex64 work, [16..) fast bins
+  int* hc = ctx->h_counts;
+  memset(hc, 0, 64 * sizeof(int));
+  for (int s = 0; s < kNumExactP; ++s) { hc[s] = ctx->host_ex32[s]; hc[kNumExactP + s] = ctx->host_ex64[s]; }
+  const int nb = (int)ctx->bins.size();
+  if (16 + nb > 64 && ctx->d_counters.cap < (size_t)(16 + nb)) CK(ctx->d_counters.ensure(16 + nb));
+  CK(cudaEventRecord(ctx->ev_start, st));
+  CK(cudaMemcpyAsync(ctx->d_counters.p, hc, 16 * sizeof(int), cudaMemcpyHostToDevice, st));
+  CK(cudaMemsetAsync(ctx->d_counters.p + 16, 0, std::max(nb, 1) * sizeof(int), st));
+  if (N > 0) CK(cudaMemsetAsync(ctx->d_status.p, 0, N, st));
+  if (ctx->num_reads > 0) {
+    const int threads = 256;
+    const int64_t blocks = (ctx->num_reads * 32 + threads - 1) / threads;
+    k_precompute<<<(unsigned)blocks, threads, 0, st>>>(E, (int)ctx->num_reads);
+    ++launches;
+  }
+  CK(cudaEventRecord(ctx->ev_fast0, st));
+  for (int bi = 0; bi < nb; ++bi) {
+    const Bin& bn = ctx->bins[bi];
+    const int nu = (int)bn.units.size();
+    if (nu == 0) continue;
+    const int G = 32 / kFastGeoms[bn.geom].P;
+    const int groups = (nu + G - 1) / G;
+    const int max_blocks = ctx->num_sms * 2;
+    const int blocks = std::max(1, std::min(max_blocks, (groups + 3) / 4));
+    kFastLaunch[bn.geom](dim3(blocks), fast_smem(bn.geom), st, E, ctx->d_units.p + bn.dev_off, nu, bn.Q,
+                         ctx->d_counters.p + 16 + bi, ctx->d_colf.p, ctx->max_n + 1);
+    ++launches;
+  }
+  CK(cudaGetLastError());
+  CK(cudaEventRecord(ctx->ev_fast1, st));
+  for (int s = 0; s < kNumExactP; ++s) {
+    kExact32[s](dim3(ctx->num_sms * 2), exact_smem(s, 4), st, E, s, ctx->d_counters.p + 8 + s,
+                ctx->d_cold.p, ctx->max_n + 1);
+    ++launches;
+  }
+  for (int s = 0; s < kNumExactP; ++s) {
+    kExact64[s](dim3(ctx->num_sms * 2), exact_smem(s, 8), st, E, s, ctx->d_counters.p + 12 + s,
+                ctx->d_cold.p, ctx->max_n + 1);
+    ++launches;
+  }
+  CK(cudaGetLastError());
+  CK(cudaEventRecord(ctx->ev_end, st));
+  CK(cudaEventSynchronize(ctx->ev_end));
+  float dev = 0.f, fast = 0.f;
+  CK(cudaEventElapsedTime(&dev, ctx->ev_start, ctx->ev_end));
+  CK(cudaEventElapsedTime(&fast, ctx->ev_fast0, ctx->ev_fast1));
+  ctx->last_dev_ms = dev;
+  ctx->last_fast_ms = fast;
+  ctx->last_launches = launches;
+  ctx->executed = true;
+  return PHMM_SUCCESS;
+}
+
+int phmm_fetch(phmm_ctx* ctx, double* out_log10, uint8_t* out_status, phmm_stats* stats) {
+  if (!ctx) return PHMM_ERR_INVALID;
+  if (!ctx->executed) return ctx->fail(PHMM_ERR_STATE, "phmm_fetch before phmm_execute");
+  CK(cudaSetDevice(ctx->device));
+  const int64_t N = ctx->num_pairs;
+  std::vector<double> acc(N);
+  std::vector<uint8_t> st(N);
+  CK(cudaEventRecord(ctx->ev_start, ctx->stream));
+  if (N > 0) {
+    CK(cudaMemcpyAsync(acc.data(), ctx->d_acc.p, N * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpyAsync(st.data(), ctx->d_status.p, N, cudaMemcpyDeviceToHost, ctx->stream));
+  }
+  CK(cudaEventRecord(ctx->ev_end, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  float d2h = 0.f;
+  cudaEventElapsedTime(&d2h, ctx->ev_start, ctx->ev_end);
+  int64_t total_cells = 0, fast = 0, exact = 0, f64 = 0, flagged = 0;
+  int64_t gid = 0;
+  for (int64_t b = 0; b < ctx->num_batches; ++b) {
+    const int64_t r0 = ctx->batch_read_off[b], r1 = ctx->batch_read_off[b + 1];
+    const int64_t h0 = ctx->batch_hap_off[b], h1 = ctx->batch_hap_off[b + 1];
+    for (int64_t r = r0; r < r1; ++r) {
+      const int m = ctx->read_m[r];
+      const int cfg = ctx->read_cfg[r];
+      for (int64_t h = h0; h < h1; ++h, ++gid) {
+        uint8_t s = st[gid];
+        double v = NAN;
+        if (cfg < 0) {
+          s = PHMM_ST_CONFIG_TOO_SMALL;
+        } else {
+          const int kind = s & PHMM_ST_KIND_MASK;
+          const bool retried = (s & PHMM_ST_RETRIED_F64) != 0;
+          if (kind == PHMM_ST_OK) {
+            const double a = acc[gid];
+            if (a <= 0.0 || !std::isfinite(a)) {
+              s = (uint8_t)((s & ~PHMM_ST_KIND_MASK) | PHMM_ST_NUMERIC_OVERFLOW);
+            } else {
+              const int scale = retried ? 0 : ctx->read_scale[r];
+              v = std::log10(a) - scale * kLog10_2;
+            }
+          }
+          const int k2 = s & PHMM_ST_KIND_MASK;
+          if (k2 == PHMM_ST_OK || k2 == PHMM_ST_NUMERIC_OVERFLOW) total_cells += (int64_t)m * ctx->hap_len[h];
+          if (k2 == PHMM_ST_OK) {
+            if (retried) ++f64;
+            else if (s & PHMM_ST_EXACT_F32) ++exact;
+            else ++fast;
+          }
+          if (retried || k2 == PHMM_ST_NUMERIC_OVERFLOW) ++flagged;
+        }
+        if (out_log10) out_log10[gid] = v;
+        if (out_status) out_status[gid] = s;
+      }
+    }
+  }
+  if (stats) {
+    memset(stats, 0, sizeof(*stats));
+    stats->num_pairs = N;
+    stats->total_cells = total_cells;
+    int64_t comp = 0;
+    for (auto& bn : ctx->bins) {
+      const FastGeom g = kFastGeoms[bn.geom];
+      for (auto& u : bn.units) comp += 2LL * bn.Q * g.P * g.K * (std::max(u.nA, u.nB) + g.P - 1);
+    }
+    stats->computed_cells = comp;
+    stats->fast_pairs = fast;
+    stats->exact_pairs = exact;
+    stats->f64_pairs = f64;
+    stats->flagged_pairs = flagged;
+    stats->h2d_bytes = ctx->h2d_bytes;
+    stats->d2h_bytes = N * (int64_t)(sizeof(double) + 1);
+    stats->kernel_launches = ctx->last_launches;
+    stats->device_ms = ctx->last_dev_ms;
+    stats->fast_ms = ctx->last_fast_ms;
+    stats->h2d_ms = ctx->h2d_ms;
+    stats->d2h_ms = d2h;
+    stats->plan_ms = ctx->plan_ms;
+  }
+  return PHMM_SUCCESS;
+}
+
+int phmm_last_timing(const phmm_ctx* ctx, double* device_ms, double* fast_ms, int* launches) {
+  if (!ctx) return PHMM_ERR_INVALID;
+  if (device_ms) *device_ms = ctx->last_dev_ms;
+  if (fast_ms) *fast_ms = ctx->last_fast_ms;
+  if (launches) *launches = ctx->last_launches;
+  return PHMM_SUCCESS;
+}
+
+int phmm_fast_geometry(int m, int n, int* P, int* K, int* Q) {
+  if (m < 1 || n < 1 || !P || !K || !Q) return PHMM_ERR_INVALID;
+  int q = 1;
+  const int g = choose_geom(m, n, &q);
+  *P = kFastGeoms[g].P; *K = kFastGeoms[g].K; *Q = q;
+  return PHMM_SUCCESS;
+}
+
+int phmm_score(phmm_ctx* ctx, const phmm_input* in, const phmm_options* opt, double* out_log10,
+               uint8_t* out_status, phmm_stats* stats) {
+  int64_t n = 0;
+  int rc = phmm_prepare(ctx, in, opt, &n);
+  if (rc != PHMM_SUCCESS) return rc;
+  rc = phmm_execute(ctx);
+  if (rc != PHMM_SUCCESS) return rc;
+  return phmm_fetch(ctx, out_log10, out_status, stats);
+}
+
+}  // extern "C"

@@ -1,0 +1,512 @@
+// phmm_kernels.cuh — sm_100a kernels of the B200 Pair-HMM forward engine.
+//
+// Kernel family:
+//   k_precompute      per read: degenerate-transition flag (prob.py:71-75) and the
+//                     guard-band sensitivity sum Gsum used to decide when the fast
+//                     FP32 result provably equals the reference's flushed FP32 result.
+//   k_fast<P,K>       FP32 fast wavefront: one sub-warp of P threads scores ONE read
+//                     against TWO haplotypes packed in float2 lanes (FFMA2/FMUL2 with a
+//                     scalar-broadcast transition operand); each thread owns K read
+//                     positions; neighbour M/I/D cross threads by __shfl_up_sync
+//                     (PAPER.md:186-218); emissions come from a per-read shared-memory
+//                     table E[c][i].  Reads longer than P*K-1 are
+//                     processed in stripes with a boundary column in global memory.
+//   k_exact<T,P,K>    bit-exact restatement of the reference recursion (no FMA, per-store
+//                     flush, j-ordered accumulation) in T = float (guard band, exact
+//                     mode) or T = double (f64 configs, FP32-underflow retries).
+//
+// Read layout inside a kernel: Q stripes of W = P*K padded positions;
+//   [L left-padding positions][m real read positions][1 accumulator position],
+//   L = Q*W - m - 1.  Left padding carries the row-0 boundary D(0,j) = S/n down to the
+//   first real position; the accumulator position turns the D recurrence into the
+//   running sum  sum_j (M(m,j) + I(m,j))  (wavefront.py:156-160) so the result always
+//   sits in fixed registers of the last thread.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace phmm {
+
+constexpr int kStatusOk = 0, kStatusOverflow = 1, kStatusTooSmall = 2, kStatusDegenerate = 3;
+constexpr int kStatusExactF32 = 0x20, kStatusRetriedF64 = 0x40;
+constexpr int kNumExactP = 4;            // exact kernels for P in {4, 8, 16, 32}
+constexpr int kExactK = 8;
+
+struct FastUnit {                         // one read x two haplotypes (hapB may repeat hapA)
+  int read, hapA, hapB, pairA, pairB, nA, nB, pad;
+};
+struct ExactItem {                        // one read x one haplotype
+  int pair, read, hap, scale;
+};
+
+struct EngineDev {
+  const int8_t* rbases;
+  const uint8_t *bq, *iq, *dq, *gq;
+  const int64_t* roff;
+  const int8_t* hbases;
+  const int64_t* hoff;
+  const int* read_m;
+  const int* read_scale;
+  const int* read_ncap;
+  float* read_gsum;
+  uint8_t* read_flags;                    // bit0: degenerate
+  const double* lut;                      // PHRED_TO_PROB[94]
+  double* acc;                            // per pair raw accumulator (scaled)
+  uint8_t* status;                        // per pair status
+  ExactItem* ex32[kNumExactP];            // exact-f32 work lists (host + device appended)
+  int* ex32_count;                        // [kNumExactP]
+  ExactItem* ex64[kNumExactP];            // f64 work lists
+  int* ex64_count;                        // [kNumExactP]
+  int list_cap;
+  int retry_f64;
+};
+
+__device__ __forceinline__ int exact_slot_for(int m) {
+  // smallest W = P*8 >= m + 1 among P in {4,8,16,32}; longer reads stripe at P = 32
+  return (m + 1 <= 32) ? 0 : (m + 1 <= 64) ? 1 : (m + 1 <= 128) ? 2 : 3;
+}
+
+__device__ __forceinline__ void append_item(ExactItem* const* lists, int* counts, int cap,
+                                            int slot, ExactItem it) {
+  int pos = atomicAdd(&counts[slot], 1);
+  if (pos < cap) lists[slot][pos] = it;
+}
+
+// ---------------------------------------------------------------------------------
+// k_precompute: one warp per read.
+// Gsum bounds sum over positions i of the backward sensitivities B_M(i)+B_I(i)+B_D(i)
+// of the final accumulator w.r.t. a cell value, with every emission replaced by 1.
+// Flushing a value v < 2^-90 changes the final accumulator by at most v*B, so
+//   0 <= unflushed - flushed <= 2^-90 * n * Gsum        (guard band)
+// ---------------------------------------------------------------------------------
+__global__ void k_precompute(EngineDev E, int num_reads) {
+  const int lane = threadIdx.x & 31;
+  const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (r >= num_reads) return;
+  const int m = E.read_m[r];
+  const int64_t o = E.roff[r];
+  bool degen = false;
+  for (int i = lane; i < m; i += 32) degen |= (E.lut[E.iq[o + i]] + E.lut[E.dq[o + i]] >= 1.0);
+  degen = __any_sync(0xffffffffu, degen);
+  if (lane != 0) return;
+  const double ncap = (double)E.read_ncap[r];
+  double bm = 1.0, bi = 1.0, gsum = 2.0;           // i = m: B_M = B_I = 1, B_D = 0
+  for (int i = m - 1; i >= 1; --i) {               // 1-based position i; arrays 0-based
+    const double d1 = E.lut[E.iq[o + i]], z1 = E.lut[E.dq[o + i]], e1 = E.lut[E.gq[o + i]];
+    const double a1 = (1.0 - d1) - z1, b1 = 1.0 - e1;
+    const double e0 = E.lut[E.gq[o + i - 1]], z0 = E.lut[E.dq[o + i - 1]];
+    const double geo = (e0 >= 1.0) ? ncap : fmin(ncap, 1.0 / (1.0 - e0));
+    const double bd = b1 * bm * geo;
+    const double nbm = a1 * bm + d1 * bi + z0 * bd;
+    const double nbi = b1 * bm + e1 * bi;
+    bm = nbm; bi = nbi;
+    gsum += bm + bi + bd;
+  }
+  E.read_gsum[r] = (float)gsum;
+  E.read_flags[r] = degen ? 1 : 0;
+}
+
+// packed helpers: scalar-broadcast operand -> FFMA2 R.F32 form
+__device__ __forceinline__ float2 fma2s(float s, float2 a, float2 b) {
+  return __ffma2_rn(make_float2(s, s), a, b);
+}
+__device__ __forceinline__ float2 mul2s(float s, float2 a) {
+  return __fmul2_rn(make_float2(s, s), a);
+}
+__device__ __forceinline__ float comp(const float4& v, int i) {
+  return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w;
+}
+
+// Fast-path classification of a finished FP32 accumulator:
+//   a < 2^-93                    -> every final-row term flushes in the reference: flagged
+//   a < 2^16 * 2^-90 * n * Gsum  -> guard band: rerun on the bit-exact kernel
+//   score > -1.5 (short pairs)   -> bit-exact kernel (relative tolerance near log10 = 0)
+//   otherwise                    -> accept
+__device__ __forceinline__ void fast_finish(const EngineDev& E, float a, int pair, int read, int hap,
+                                            int n, int m, int scale) {
+  const float bound = 0x1p-74f * (float)n * E.read_gsum[read];   // 2^16 * 2^-90
+  const float hi = ldexpf(0.031622776f, scale);                   // 10^-1.5 * 2^scale
+  if (!(a >= 0x1p-93f)) {
+    if (E.retry_f64) {
+      E.status[pair] = kStatusRetriedF64;
+      append_item(E.ex64, E.ex64_count, E.list_cap, exact_slot_for(m), ExactItem{pair, read, hap, 0});
+    } else {
+      E.acc[pair] = 0.0;
+      E.status[pair] = kStatusOverflow;
+    }
+  } else if (a < bound || a > hi) {
+    E.status[pair] = kStatusExactF32;
+    append_item(E.ex32, E.ex32_count, E.list_cap, exact_slot_for(m), ExactItem{pair, read, hap, scale});
+  } else {
+    E.acc[pair] = (double)a;
+    E.status[pair] = kStatusOk;
+  }
+}
+
+// ---------------------------------------------------------------------------------
+// k_fast<P, K>: persistent; each warp takes G = 32/P units per atomic grab.
+// ---------------------------------------------------------------------------------
+template <int P, int K>
+__global__ void __launch_bounds__(128, 2)
+k_fast(const EngineDev E, const FastUnit* __restrict__ units, int num_units, int Q,
+       int* __restrict__ counter, float2* __restrict__ colbuf, int col_rows) {
+  constexpr int W = P * K, G = 32 / P, K4 = K / 4;
+  static_assert(K % 4 == 0 && K >= 4, "K multiple of 4");
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* s_lut = reinterpret_cast<double*>(smem_raw);
+  float4* s_E = reinterpret_cast<float4*>(smem_raw + 96 * sizeof(double));
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int sw = lane / P, t = lane % P;
+  for (int i = threadIdx.x; i < 94; i += blockDim.x) s_lut[i] = E.lut[i];
+  __syncthreads();
+  float4* Et = s_E + (size_t)((wib * G + sw) * 5 * K4) * P;
+  const int gwarp = blockIdx.x * (blockDim.x >> 5) + wib;
+  float2* colX = colbuf + (size_t)(gwarp * G + sw) * 2 * 3 * col_rows;
+  float2* colY = colX + 3 * col_rows;
+
+  for (;;) {
+    int g = 0;
+    if (lane == 0) g = atomicAdd(counter, 1);
+    g = __shfl_sync(0xffffffffu, g, 0);
+    if (g * G >= num_units) break;
+    const int u = g * G + sw;
+    const bool has = u < num_units;
+    const FastUnit U = units[has ? u : g * G];
+    const int r = U.read, m = E.read_m[r];
+    const int64_t ro = E.roff[r];
+    const bool degen = (E.read_flags[r] & 1) != 0;
+    const bool live = has && !degen;
+    const int nA = U.nA, nB = U.nB, nmax = max(nA, nB);
+    int steps = live ? nmax + P - 1 : 0;
+    steps = __reduce_max_sync(0xffffffffu, steps);
+    if (has && degen && t == 0) {
+      E.acc[U.pairA] = 0.0; E.status[U.pairA] = kStatusDegenerate;
+      if (U.pairB >= 0) { E.acc[U.pairB] = 0.0; E.status[U.pairB] = kStatusDegenerate; }
+    }
+    const int scale = E.read_scale[r];
+    const int Lp = Q * W - m - 1;
+    const double Sd = ldexp(1.0, scale);
+    const double bfirst = 1.0 - s_lut[E.gq[ro]];
+    const float2 bS = make_float2((float)(bfirst * Sd / nA), (float)(bfirst * Sd / nB));
+    const int8_t* hA = E.hbases + E.hoff[U.hapA];
+    const int8_t* hB = E.hbases + E.hoff[U.hapB];
+    float resA = 0.f, resB = 0.f;
+    float2* colPrev = colX;
+    float2* colNext = colY;
+
+    for (int q = 0; q < Q; ++q) {
+      // ---- per-stripe coefficients + emission table (each thread: its K positions)
+      float al[K], be[K], dl[K], ep[K], zp[K];
+      float2 M[K], I[K], D[K];
+#pragma unroll
+      for (int k4 = 0; k4 < K4; ++k4) {
+        float lam[5][4];
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+          const int k = k4 * 4 + kk;
+          const int p = q * W + t * K + k;
+          M[k] = make_float2(0.f, 0.f);
+          I[k] = make_float2(0.f, 0.f);
+          if (p < Lp) {                                   // left padding
+            al[k] = 0.f; be[k] = 0.f; dl[k] = 0.f; ep[k] = 1.f; zp[k] = 0.f;
+            D[k] = bS;
+#pragma unroll
+            for (int c = 0; c < 5; ++c) lam[c][kk] = 0.f;
+          } else if (p < Lp + m) {                        // real read position
+            const int i0 = p - Lp;
+            const double d = s_lut[E.iq[ro + i0]], z = s_lut[E.dq[ro + i0]];
+            const double e = s_lut[E.gq[ro + i0]], qe = s_lut[E.bq[ro + i0]];
+            const double bnext = (i0 + 1 < m) ? 1.0 - s_lut[E.gq[ro + i0 + 1]] : 0.0;
+            al[k] = (float)((1.0 - d) - z);
+            be[k] = (float)(1.0 - e);
+            dl[k] = (float)d;
+            ep[k] = (float)e;
+            zp[k] = (float)(bnext * z);                   // D' = beta_{i+1} * D
+            D[k] = make_float2(0.f, 0.f);
+            const int rc = E.rbases[ro + i0];
+            const float lm = (float)(1.0 - qe), lx = (float)(qe / 3.0);
+#pragma unroll
+            for (int c = 0; c < 5; ++c) lam[c][kk] = (rc == c || rc == 4 || c == 4) ? lm : lx;
+          } else {                                        // accumulator position
+            al[k] = 1.f; be[k] = 1.f; dl[k] = 0.f; ep[k] = 1.f; zp[k] = 1.f;
+            D[k] = make_float2(0.f, 0.f);
+#pragma unroll
+            for (int c = 0; c < 5; ++c) lam[c][kk] = 1.f;
+          }
+        }
+#pragma unroll
+        for (int c = 0; c < 5; ++c)
+          Et[(c * K4 + k4) * P + t] = make_float4(lam[c][0], lam[c][1], lam[c][2], lam[c][3]);
+      }
+      if (t == P - 1 && q < Q - 1) {
+        colNext[0] = M[K - 1]; colNext[col_rows] = I[K - 1]; colNext[2 * col_rows] = D[K - 1];
+      }
+      float2 nbM, nbI, nbD;
+      if (q == 0) {
+        nbM = make_float2(0.f, 0.f); nbI = nbM; nbD = bS;
+      } else {
+        nbM = colPrev[0]; nbI = colPrev[col_rows]; nbD = colPrev[2 * col_rows];
+      }
+      if (t != 0) { nbM = make_float2(0.f, 0.f); nbI = nbM; nbD = nbM; }
+      __syncwarp();
+
+      int cnA = 4, cnB = 4;                               // prefetched chars for row j
+      {
+        const int j = 1 - t;
+        if (live && j >= 1 && j <= nmax) {
+          cnA = (j <= nA) ? hA[j - 1] : 4;
+          cnB = (j <= nB) ? hB[j - 1] : 4;
+        }
+      }
+      for (int s = 1; s <= steps; ++s) {
+        const int j = s - t;
+        const float2 dgM = nbM, dgI = nbI, dgD = nbD;
+        {
+          const float2 lm = M[K - 1], li = I[K - 1], ld = D[K - 1];
+          nbM.x = __shfl_up_sync(0xffffffffu, lm.x, 1, P);
+          nbM.y = __shfl_up_sync(0xffffffffu, lm.y, 1, P);
+          nbI.x = __shfl_up_sync(0xffffffffu, li.x, 1, P);
+          nbI.y = __shfl_up_sync(0xffffffffu, li.y, 1, P);
+          nbD.x = __shfl_up_sync(0xffffffffu, ld.x, 1, P);
+          nbD.y = __shfl_up_sync(0xffffffffu, ld.y, 1, P);
+        }
+        if (t == 0) {
+          if (q == 0) {
+            nbM = make_float2(0.f, 0.f); nbI = nbM; nbD = bS;
+          } else {
+            const int jj = min(max(j, 0), nmax);
+            nbM = colPrev[jj]; nbI = colPrev[col_rows + jj]; nbD = colPrev[2 * col_rows + jj];
+          }
+        }
+        if (live && j >= 1 && j <= nmax) {
+          const int cA = cnA, cB = cnB;
+          // prefetch next row's characters
+          if (j + 1 <= nmax) {
+            cnA = (j + 1 <= nA) ? hA[j] : 4;
+            cnB = (j + 1 <= nB) ? hB[j] : 4;
+          }
+          const float4* EA = Et + (cA * K4) * P + t;
+          const float4* EB = Et + (cB * K4) * P + t;
+          // pass 1 (descending): D from the previous row, M from the previous-row diagonal
+#pragma unroll
+          for (int k4 = K4 - 1; k4 >= 0; --k4) {
+            const float4 la = EA[k4 * P];
+            const float4 lb = EB[k4 * P];
+#pragma unroll
+            for (int kk = 3; kk >= 0; --kk) {
+              const int k = k4 * 4 + kk;
+              D[k] = fma2s(ep[k], D[k], mul2s(zp[k], M[k]));
+              const float2 pm = (k > 0) ? M[k - 1] : dgM;
+              const float2 pi = (k > 0) ? I[k - 1] : dgI;
+              const float2 pd = (k > 0) ? D[k - 1] : dgD;
+              float2 x = fma2s(be[k], pi, pd);
+              x = fma2s(al[k], pm, x);
+              M[k].x = comp(la, kk) * x.x;
+              M[k].y = comp(lb, kk) * x.y;
+            }
+          }
+          // pass 2 (ascending): I chain along the read within the current row
+          float2 lM = nbM, lI = nbI;
+#pragma unroll
+          for (int k = 0; k < K; ++k) {
+            I[k] = fma2s(ep[k], lI, mul2s(dl[k], lM));
+            lM = M[k];
+            lI = I[k];
+          }
+          if (t == P - 1) {
+            if (q == Q - 1) {
+              if (j == nA) resA = (D[K - 1].x + M[K - 1].x) + (M[K - 2].x + I[K - 2].x);
+              if (j == nB) resB = (D[K - 1].y + M[K - 1].y) + (M[K - 2].y + I[K - 2].y);
+            } else {
+              colNext[j] = M[K - 1]; colNext[col_rows + j] = I[K - 1]; colNext[2 * col_rows + j] = D[K - 1];
+            }
+          }
+        }
+      }
+      __syncwarp();
+      float2* tmp = colPrev; colPrev = colNext; colNext = tmp;
+    }
+    if (live && t == P - 1) {
+      fast_finish(E, resA, U.pairA, r, U.hapA, nA, m, scale);
+      if (U.pairB >= 0) fast_finish(E, resB, U.pairB, r, U.hapB, nB, m, scale);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------
+// k_exact<T, P, K>: bit-exact reference recursion (reference.py:106-122,
+// wavefront.py:130-160) — no FMA, per-store flush, j-ordered accumulation.
+// ---------------------------------------------------------------------------------
+template <typename T> struct ExactTraits;
+template <> struct ExactTraits<float> {
+  static __device__ __forceinline__ float mul(float a, float b) { return __fmul_rn(a, b); }
+  static __device__ __forceinline__ float add(float a, float b) { return __fadd_rn(a, b); }
+  static __device__ __forceinline__ float flush_thr() { return 0x1p-90f; }
+};
+template <> struct ExactTraits<double> {
+  static __device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
+  static __device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
+  static __device__ __forceinline__ double flush_thr() { return 0x1p-970; }
+};
+
+template <typename T, int P, int K>
+__global__ void __launch_bounds__(128)
+k_exact(const EngineDev E, int slot, int* __restrict__ counter, T* __restrict__ colbuf, int col_rows) {
+  using X = ExactTraits<T>;
+  constexpr int W = P * K, G = 32 / P;
+  constexpr bool kIsF32 = sizeof(T) == 4;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* s_lut = reinterpret_cast<double*>(smem_raw);
+  T* s_E = reinterpret_cast<T*>(smem_raw + 96 * sizeof(double));
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int sw = lane / P, t = lane % P;
+  for (int i = threadIdx.x; i < 94; i += blockDim.x) s_lut[i] = E.lut[i];
+  __syncthreads();
+  T* Et = s_E + (size_t)((wib * G + sw) * 5 * K) * P;   // Et[(c*K + k)*P + t]
+  const int gwarp = blockIdx.x * (blockDim.x >> 5) + wib;
+  T* colX = colbuf + (size_t)(gwarp * G + sw) * 2 * 3 * col_rows;
+  T* colY = colX + 3 * col_rows;
+  const ExactItem* items = kIsF32 ? E.ex32[slot] : E.ex64[slot];
+  const int count = min(kIsF32 ? E.ex32_count[slot] : E.ex64_count[slot], E.list_cap);
+  const T thr = X::flush_thr();
+  const T zero = (T)0;
+
+  for (;;) {
+    int g = 0;
+    if (lane == 0) g = atomicAdd(counter, 1);
+    g = __shfl_sync(0xffffffffu, g, 0);
+    if (g * G >= count) break;
+    const int u = g * G + sw;
+    const bool has = u < count;
+    const ExactItem it = items[has ? u : g * G];
+    const int r = it.read, m = E.read_m[r];
+    const int64_t ro = E.roff[r];
+    const int n = (int)(E.hoff[it.hap + 1] - E.hoff[it.hap]);
+    const bool degen = (E.read_flags[r] & 1) != 0;
+    const bool live = has && !degen;
+    int steps = live ? n + P - 1 : 0;
+    steps = __reduce_max_sync(0xffffffffu, steps);
+    if (has && degen && t == 0) { E.acc[it.pair] = 0.0; E.status[it.pair] = kStatusDegenerate; }
+    const int Q = (m + 1 + W - 1) / W;
+    const int Lp = Q * W - m - 1;
+    const T bnd = (T)(ldexp(1.0, it.scale) / (double)n);     // wavefront.py:405-406
+    const int8_t* h = E.hbases + E.hoff[it.hap];
+    T res = zero;
+    T* colPrev = colX;
+    T* colNext = colY;
+
+    // Q is per item here; the warp iterates to the max over its sub-warps
+    const int Qw = __reduce_max_sync(0xffffffffu, live ? Q : 0);
+    for (int q = 0; q < Qw; ++q) {
+      const bool sact = live && q < Q;
+      T al[K], be[K], dl[K], ep[K], zt[K], M[K], I[K], D[K];
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const int p = q * W + t * K + k;
+        T lam[5];
+        M[k] = zero; I[k] = zero;
+        if (p < Lp) {
+          al[k] = zero; be[k] = zero; dl[k] = zero; ep[k] = (T)1; zt[k] = zero; D[k] = bnd;
+#pragma unroll
+          for (int c = 0; c < 5; ++c) lam[c] = zero;
+        } else if (p < Lp + m) {
+          const int i0 = p - Lp;
+          const double d = s_lut[E.iq[ro + i0]], z = s_lut[E.dq[ro + i0]];
+          const double e = s_lut[E.gq[ro + i0]], qe = s_lut[E.bq[ro + i0]];
+          al[k] = (T)((1.0 - d) - z);
+          be[k] = (T)(1.0 - e);
+          dl[k] = (T)d;
+          ep[k] = (T)e;
+          zt[k] = (i0 + 1 < m) ? (T)z : zero;        // D(m, .) never reaches the score
+          D[k] = zero;
+          const int rc = E.rbases[ro + i0];
+          const T lm = (T)(1.0 - qe), lx = (T)(qe / 3.0);
+#pragma unroll
+          for (int c = 0; c < 5; ++c) lam[c] = (rc == c || rc == 4 || c == 4) ? lm : lx;
+        } else {
+          al[k] = (T)1; be[k] = (T)1; dl[k] = zero; ep[k] = (T)1; zt[k] = (T)1; D[k] = zero;
+#pragma unroll
+          for (int c = 0; c < 5; ++c) lam[c] = (T)1;
+        }
+#pragma unroll
+        for (int c = 0; c < 5; ++c) Et[(c * K + k) * P + t] = lam[c];
+      }
+      if (sact && t == P - 1 && q < Q - 1) {
+        colNext[0] = M[K - 1]; colNext[col_rows] = I[K - 1]; colNext[2 * col_rows] = D[K - 1];
+      }
+      T nbM = zero, nbI = zero, nbD = zero;
+      if (t == 0) {
+        if (q == 0) { nbD = bnd; }
+        else if (sact) { nbM = colPrev[0]; nbI = colPrev[col_rows]; nbD = colPrev[2 * col_rows]; }
+      }
+      __syncwarp();
+      for (int s = 1; s <= steps; ++s) {
+        const int j = s - t;
+        const T dgM = nbM, dgI = nbI, dgD = nbD;
+        nbM = __shfl_up_sync(0xffffffffu, M[K - 1], 1, P);
+        nbI = __shfl_up_sync(0xffffffffu, I[K - 1], 1, P);
+        nbD = __shfl_up_sync(0xffffffffu, D[K - 1], 1, P);
+        if (t == 0) {
+          if (q == 0) { nbM = zero; nbI = zero; nbD = bnd; }
+          else if (sact) {
+            const int jj = min(max(j, 0), n);
+            nbM = colPrev[jj]; nbI = colPrev[col_rows + jj]; nbD = colPrev[2 * col_rows + jj];
+          }
+        }
+        if (sact && j >= 1 && j <= n) {
+          const int c = h[j - 1];
+          const T* Ec = Et + (c * K) * P + t;
+#pragma unroll
+          for (int k = K - 1; k >= 0; --k) {
+            // dv = zt*M(i,j-1) + ep*D(i,j-1)
+            const T dv = X::add(X::mul(zt[k], M[k]), X::mul(ep[k], D[k]));
+            D[k] = dv >= thr ? dv : zero;
+            const T pm = (k > 0) ? M[k - 1] : dgM;
+            const T pi = (k > 0) ? I[k - 1] : dgI;
+            const T pd = (k > 0) ? D[k - 1] : dgD;
+            // mv = lam*(al*M(i-1,j-1) + be*(I(i-1,j-1) + D(i-1,j-1)))
+            const T mv = X::mul(Ec[k * P], X::add(X::mul(al[k], pm), X::mul(be[k], X::add(pi, pd))));
+            M[k] = mv >= thr ? mv : zero;
+          }
+          T lM = nbM, lI = nbI;
+#pragma unroll
+          for (int k = 0; k < K; ++k) {
+            // iv = dl*M(i-1,j) + ep*I(i-1,j)
+            const T iv = X::add(X::mul(dl[k], lM), X::mul(ep[k], lI));
+            I[k] = iv >= thr ? iv : zero;
+            lM = M[k];
+            lI = I[k];
+          }
+          if (t == P - 1) {
+            if (q == Q - 1) {
+              if (j == n) res = X::add(X::add(D[K - 1], M[K - 1]), X::add(M[K - 2], I[K - 2]));
+            } else {
+              colNext[j] = M[K - 1]; colNext[col_rows + j] = I[K - 1]; colNext[2 * col_rows + j] = D[K - 1];
+            }
+          }
+        }
+      }
+      __syncwarp();
+      T* tmp = colPrev; colPrev = colNext; colNext = tmp;
+    }
+    if (live && t == P - 1) {
+      const bool bad = !(res > zero) || !isfinite((double)res);
+      if (kIsF32) {
+        if (bad && E.retry_f64) {
+          E.status[it.pair] = kStatusRetriedF64;
+          append_item(E.ex64, E.ex64_count, E.list_cap, exact_slot_for(m), ExactItem{it.pair, r, it.hap, 0});
+        } else {
+          E.acc[it.pair] = (double)res;
+          E.status[it.pair] = bad ? kStatusOverflow : kStatusExactF32;
+        }
+      } else {
+        E.acc[it.pair] = (double)res;
+        const uint8_t keep = E.status[it.pair] & kStatusRetriedF64;
+        E.status[it.pair] = (uint8_t)((bad ? kStatusOverflow : kStatusOk) | keep);
+      }
+    }
+  }
+}
+
+}  // namespace phmm

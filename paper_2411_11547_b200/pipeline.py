@@ -1,0 +1,120 @@
+"""run(): the drop-in batch-likelihood API (mirror of reference pipeline.py:77-142).
+
+    scores, report = run(batches, configs=None, budget_bytes=512 MiB, workers=1)
+
+Same inputs, outputs and error semantics as the reference: float64 log10 scores
+in global_id order (NaN where an item failed), a RunReport whose errors are
+(global_id, kind) pairs sorted by id, total_cells counting true m*n of every
+executed item (numeric-overflow items included; config-too-small /
+degenerate-transition / data excluded, pipeline.py:27,103-111), and GCUPS =
+total_cells / wall.  BudgetError (one item over the chunk budget) and
+ValueError (workers < 1) are raised like the reference.
+
+Underneath, the whole batch list is flattened once (FlatBatches) and scored by
+ONE call into libphmm.so on the GPU (GIL released).  ``workers`` is accepted
+for compatibility; GPU concurrency replaces the reference thread pool.
+Extra keyword-only options:
+  retry_f64  rerun FP32-underflowing pairs in FP64 (GATK behaviour); such items
+             get finite scores and are listed in report.retried instead of errors.
+  exact      run every FP32 pair on the bit-exact kernel (no fast path).
+  device     CUDA device ordinal.
+"""
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native
+from .errors import InvalidMeasurementError
+from .model import FlatBatches, default_configs
+from .partition import DEFAULT_BUDGET_BYTES, check_budget, config_index
+
+_NOT_EXECUTED = ("config-too-small", "degenerate-transition", "data")
+
+
+def throughput(total_cells: int, wall_seconds: float) -> float:
+    """Giga cell updates per second."""
+    if wall_seconds <= 0.0:
+        raise InvalidMeasurementError("non-positive runtime %r" % wall_seconds)
+    return total_cells / (wall_seconds * 1.0e9)
+
+
+@dataclass(frozen=True)
+class ConfigStats:
+    cells: int
+    seconds: float
+
+
+@dataclass(frozen=True)
+class RunReport:
+    total_cells: int
+    wall_seconds: float
+    gcups: float
+    per_config: dict = field(default_factory=dict)
+    errors: list = field(default_factory=list)
+    retried: list = field(default_factory=list)     # global ids rescued by the FP64 retry
+    engine: dict = field(default_factory=dict)      # libphmm phmm_stats of the call
+
+
+def config_tuples(configs):
+    return [(c.p, c.k, 0 if c.precision == "f32" else 1, c.scale_log2) for c in configs]
+
+
+def engine_flags(retry_f64: bool = False, exact: bool = False) -> int:
+    return (_native.FLAG_RETRY_F64 if retry_f64 else 0) | (_native.FLAG_EXACT if exact else 0)
+
+
+def score_flat(flat: FlatBatches, configs, retry_f64=False, exact=False, device=0):
+    """Engine call on flat arrays -> (scores, status, stats)."""
+    ctx = _native.context(device)
+    return ctx.score(flat, config_tuples(configs), engine_flags(retry_f64, exact))
+
+
+def errors_from_status(status: np.ndarray) -> list:
+    kinds = status & _native.ST_KIND_MASK
+    bad = np.flatnonzero(kinds != _native.ST_OK)
+    return [(int(g), _native.KIND_NAMES[int(kinds[g])]) for g in bad]
+
+
+def run(batches, configs=None, budget_bytes: int = DEFAULT_BUDGET_BYTES, workers: int = 1, *,
+        retry_f64: bool = False, exact: bool = False, device: int = 0):
+    """Score every work item of ``batches`` on the GPU; see the module docstring."""
+    if workers < 1:
+        raise ValueError("workers must be >= 1")
+    if configs is None:
+        configs = default_configs()
+    flat = batches if isinstance(batches, FlatBatches) else FlatBatches.from_batches(batches)
+    check_budget(flat, configs, budget_bytes)
+    n = flat.num_pairs
+    t0 = time.perf_counter()
+    if n:
+        scores, status, stats = score_flat(flat, configs, retry_f64, exact, device)
+        engine = stats.as_dict()
+    else:
+        scores, status, engine = np.zeros(0), np.zeros(0, np.uint8), {}
+    wall = time.perf_counter() - t0
+    errors = errors_from_status(status)
+    retried = np.flatnonzero((status & _native.ST_RETRIED_F64) != 0).tolist()
+
+    # per-config accounting keyed like the reference (geometry of the bound config)
+    per_config = {}
+    total_cells = 0
+    if n:
+        pr, ph = flat.pair_index()
+        kinds = status & _native.ST_KIND_MASK
+        executed = (kinds == _native.ST_OK) | (kinds == _native.ST_OVERFLOW)
+        cells = flat.read_len[pr] * flat.hap_len[ph]
+        cidx = config_index(flat.read_len, configs)[pr]
+        total_cells = int(cells[executed].sum())
+        dev_s = engine.get("device_ms", 0.0) * 1e-3
+        for i in np.unique(cidx[executed]).tolist():
+            c = int(cells[executed & (cidx == i)].sum())
+            geo = configs[i].geometry
+            prev = per_config.get(geo)
+            sec = dev_s * c / total_cells if total_cells else 0.0
+            per_config[geo] = ConfigStats(c + (prev.cells if prev else 0), sec + (prev.seconds if prev else 0.0))
+    report = RunReport(total_cells, wall, throughput(total_cells, wall), per_config, errors,
+                       retried, engine)
+    return scores, report
