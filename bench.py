@@ -187,79 +187,16 @@ def secondary(ctx, name, flags, steps=3):
     cfg = config_tuples(default_configs("f32"))
     ctx.prepare(flat, cfg, flags)
     ctx.execute()
-    ms = []
-    fast = []
+    ms, fast = [], []
     for _ in range(steps):
         ctx.execute()
-        _, status, st = ctx.fetch()
-        ms.append(st.device_ms)
-        fast.append(st.fast_ms)
+        d, f, _n = ctx.last_timing()
+        ms.append(d)
+        fast.append(f)
+    _, _, st = ctx.fetch()
     cells = st.total_cells
     return {"workload": WORKLOAD_TEXT.get(name, name), "gcups": cells / (np.mean(ms) * 1e-3) / 1e9,
-            "fast_kernel_gcups": None, "pairs": st.num_pairs, "fast_pairs": st.fast_pairs,
-            "exact_pairs": st.exact_pairs, "f64_retry_pairs": st.f64_pairs,
-            "device_ms": float(np.mean(ms)), "fast_ms": float(np.mean(fast)),
-            "flags": "retry_f64" if flags & 1 else "reference-f32"}
-
-
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="c2")
-    ap.add_argument("--cpu-seconds", type=float, default=10.0)
-    ap.add_argument("--no-secondary", action="store_true")
-    ap.add_argument("--no-cpu-baseline", action="store_true")
-    args = ap.parse_args()
-    ws, rank, local = dist_env()
-    if args.impl == "reference":
-        return run_reference(args, ws, rank)
-
-    import torch
-    import torch.distributed as dist
-    from paper_2411_11547_b200 import _native, datagen, default_configs
-    from paper_2411_11547_b200.build import build_native
-    from paper_2411_11547_b200.pipeline import config_tuples
-
-    build_native()
-    torch.cuda.set_device(local)
-    if ws > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-
-    flat = datagen.workload(args.workload, seed_offset=rank)
-    cfg = config_tuples(default_configs("f32"))
-    flags = 0                                        # reference f32 semantics (c2 has no underflow)
-    ctx = _native.Context(local)
-    n_pairs = ctx.prepare(flat, cfg, flags)
-    l2_flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
-
-    def barrier():
-        torch.cuda.synchronize()
-        if ws > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
-
-    for _ in range(args.warmup):
-        ctx.execute()
-    barrier()
-    dev_ms, fast_ms = [], []
-    launches = 0
-    with ClockSampler(local) as clocks:
-        for _ in range(args.steps):
-            l2_flush.zero_()                     # inputs < L2: flush between timed steps
-            torch.cuda.synchronize()
-            ctx.execute()                        # synchronous; CUDA events on the engine stream
-            d, f, n = ctx.last_timing()
-            dev_ms.append(d)
-            fast_ms.append(f)
-            launches += n
-        barrier()
-    scores, status, st = ctx.fetch()
-    cells = st.total_cells
-    return {"workload": WORKLOAD_TEXT.get(name, name), "gcups": cells / (np.mean(ms) * 1e-3) / 1e9,
-            "fast_kernel_gcups": None, "pairs": st.num_pairs, "fast_pairs": st.fast_pairs,
+            "pairs": st.num_pairs, "cells": cells, "fast_pairs": st.fast_pairs,
             "exact_pairs": st.exact_pairs, "f64_retry_pairs": st.f64_pairs,
             "device_ms": float(np.mean(ms)), "fast_ms": float(np.mean(fast)),
             "flags": "retry_f64" if flags & 1 else "reference-f32"}
@@ -314,13 +251,12 @@ def main():
             l2_flush.zero_()
             torch.cuda.synchronize()
             ctx.execute()
-            _, _, st = ctx.fetch() if _ == args.steps - 1 else (None, None, None)
-            launches_step = ctx_launches(ctx)
-            launches += launches_step
+            d, f, n = ctx.last_timing()          # CUDA events on the engine stream
+            dev_ms.append(d)
+            fast_ms.append(f)
+            launches += n
         barrier()
     scores, status, st = ctx.fetch()
-    # per-step device times were recorded by the engine each execute: rerun accounting
-    dev_ms, fast_ms = timed_executes(ctx, args.steps, l2_flush)
     cells = st.total_cells
     t_rank = float(np.sum(dev_ms)) * 1e-3
     t = torch.tensor([t_rank], dtype=torch.float64, device="cuda")

@@ -279,13 +279,12 @@ k_fast(const EngineDev E, const FastUnit* __restrict__ units, int num_units, int
             nbM = colPrev[jj]; nbI = colPrev[col_rows + jj]; nbD = colPrev[2 * col_rows + jj];
           }
         }
+        const int cA = cnA, cB = cnB;                     // characters of row j
+        if (live && j + 1 >= 1 && j + 1 <= nmax) {        // prefetch row j + 1
+          cnA = (j + 1 <= nA) ? hA[j] : 4;
+          cnB = (j + 1 <= nB) ? hB[j] : 4;
+        }
         if (live && j >= 1 && j <= nmax) {
-          const int cA = cnA, cB = cnB;
-          // prefetch next row's characters
-          if (j + 1 <= nmax) {
-            cnA = (j + 1 <= nA) ? hA[j] : 4;
-            cnB = (j + 1 <= nB) ? hB[j] : 4;
-          }
           const float4* EA = Et + (cA * K4) * P + t;
           const float4* EB = Et + (cB * K4) * P + t;
           // pass 1 (descending): D from the previous row, M from the previous-row diagonal
