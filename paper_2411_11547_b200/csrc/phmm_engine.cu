@@ -53,12 +53,14 @@ struct Bin {
   int64_t dev_off = 0;     // offset into the device unit array
 };
 
-// fast-kernel launcher table
-typedef void (*FastFn)(const EngineDev, const FastUnit*, int, int, int*, float2*, int);
+// fast-kernel launcher table: single-stripe and multi-stripe variant per geometry
 template <int P, int K>
 void launch_fast(dim3 g, size_t smem, cudaStream_t s, const EngineDev& E, const FastUnit* u, int nu,
                  int Q, int* ctr, float2* col, int rows) {
-  k_fast<P, K><<<g, kThreads, smem, s>>>(E, u, nu, Q, ctr, col, rows);
+  if (Q > 1)
+    k_fast<P, K, true><<<g, kThreads, smem, s>>>(E, u, nu, Q, ctr, col, rows);
+  else
+    k_fast<P, K, false><<<g, kThreads, smem, s>>>(E, u, nu, Q, ctr, col, rows);
 }
 typedef void (*FastLaunch)(dim3, size_t, cudaStream_t, const EngineDev&, const FastUnit*, int, int,
                            int*, float2*, int);
@@ -66,11 +68,11 @@ const FastLaunch kFastLaunch[kNumFastGeoms] = {
     launch_fast<4, 4>,   launch_fast<4, 8>,   launch_fast<4, 12>,  launch_fast<4, 16>,
     launch_fast<8, 12>,  launch_fast<8, 16>,  launch_fast<16, 12>, launch_fast<16, 16>,
     launch_fast<32, 12>, launch_fast<32, 16>};
-const void* kFastFn[kNumFastGeoms] = {
-    (const void*)k_fast<4, 4>,   (const void*)k_fast<4, 8>,   (const void*)k_fast<4, 12>,
-    (const void*)k_fast<4, 16>,  (const void*)k_fast<8, 12>,  (const void*)k_fast<8, 16>,
-    (const void*)k_fast<16, 12>, (const void*)k_fast<16, 16>, (const void*)k_fast<32, 12>,
-    (const void*)k_fast<32, 16>};
+#define FASTFN(P, K) (const void*)k_fast<P, K, false>, (const void*)k_fast<P, K, true>
+const void* kFastFn[2 * kNumFastGeoms] = {FASTFN(4, 4),   FASTFN(4, 8),   FASTFN(4, 12),  FASTFN(4, 16),
+                                          FASTFN(8, 12),  FASTFN(8, 16),  FASTFN(16, 12), FASTFN(16, 16),
+                                          FASTFN(32, 12), FASTFN(32, 16)};
+#undef FASTFN
 
 template <typename T, int P>
 void launch_exact(dim3 g, size_t smem, cudaStream_t s, const EngineDev& E, int slot, int* ctr, void* col,
@@ -211,8 +213,8 @@ int phmm_create(phmm_ctx** out, int device, const double* phred_lut) {
   CK(cudaMallocHost(&ctx->h_counts, 64 * sizeof(int)));
   CK(ctx->d_lut.ensure(94));
   CK(cudaMemcpy(ctx->d_lut.p, ctx->lut.data(), 94 * sizeof(double), cudaMemcpyHostToDevice));
-  for (int g = 0; g < kNumFastGeoms; ++g)
-    CK(cudaFuncSetAttribute(kFastFn[g], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fast_smem(g)));
+  for (int g = 0; g < 2 * kNumFastGeoms; ++g)
+    CK(cudaFuncSetAttribute(kFastFn[g], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fast_smem(g / 2)));
   for (int s = 0; s < kNumExactP; ++s) {
     CK(cudaFuncSetAttribute(kExact32Fn[s], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)exact_smem(s, 4)));
     CK(cudaFuncSetAttribute(kExact64Fn[s], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)exact_smem(s, 8)));
@@ -473,8 +475,8 @@ int phmm_execute(phmm_ctx* ctx) {
   CK(cudaMemsetAsync(ctx->d_counters.p + 16, 0, std::max(nb, 1) * sizeof(int), st));
   if (N > 0) CK(cudaMemsetAsync(ctx->d_status.p, 0, N, st));
   if (ctx->num_reads > 0) {
-    const int threads = 256;
-    const int64_t blocks = (ctx->num_reads * 32 + threads - 1) / threads;
+    const int threads = 128;
+    const int64_t blocks = (ctx->num_reads + threads - 1) / threads;
     k_precompute<<<(unsigned)blocks, threads, 0, st>>>(E, (int)ctx->num_reads);
     ++launches;
   }

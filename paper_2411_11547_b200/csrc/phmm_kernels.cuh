@@ -24,6 +24,7 @@
 #pragma once
 
 #include <cstdint>
+#include <type_traits>
 #include <cuda_runtime.h>
 
 namespace phmm {
@@ -81,27 +82,26 @@ __device__ __forceinline__ void append_item(ExactItem* const* lists, int* counts
 //   0 <= unflushed - flushed <= 2^-90 * n * Gsum        (guard band)
 // ---------------------------------------------------------------------------------
 __global__ void k_precompute(EngineDev E, int num_reads) {
-  const int lane = threadIdx.x & 31;
-  const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;     // one thread per read
   if (r >= num_reads) return;
   const int m = E.read_m[r];
   const int64_t o = E.roff[r];
-  bool degen = false;
-  for (int i = lane; i < m; i += 32) degen |= (E.lut[E.iq[o + i]] + E.lut[E.dq[o + i]] >= 1.0);
-  degen = __any_sync(0xffffffffu, degen);
-  if (lane != 0) return;
   const double ncap = (double)E.read_ncap[r];
-  double bm = 1.0, bi = 1.0, gsum = 2.0;           // i = m: B_M = B_I = 1, B_D = 0
-  for (int i = m - 1; i >= 1; --i) {               // 1-based position i; arrays 0-based
-    const double d1 = E.lut[E.iq[o + i]], z1 = E.lut[E.dq[o + i]], e1 = E.lut[E.gq[o + i]];
+  const double* lut = E.lut;
+  bool degen = lut[E.iq[o + m - 1]] + lut[E.dq[o + m - 1]] >= 1.0;
+  double bm = 1.0, bi = 1.0, gsum = 2.0;                  // i = m: B_M = B_I = 1, B_D = 0
+  double d1 = lut[E.iq[o + m - 1]], z1 = lut[E.dq[o + m - 1]], e1 = lut[E.gq[o + m - 1]];
+  for (int i = m - 1; i >= 1; --i) {                      // 1-based position i; arrays 0-based
     const double a1 = (1.0 - d1) - z1, b1 = 1.0 - e1;
-    const double e0 = E.lut[E.gq[o + i - 1]], z0 = E.lut[E.dq[o + i - 1]];
+    const double d0 = lut[E.iq[o + i - 1]], z0 = lut[E.dq[o + i - 1]], e0 = lut[E.gq[o + i - 1]];
+    degen |= (d0 + z0 >= 1.0);
     const double geo = (e0 >= 1.0) ? ncap : fmin(ncap, 1.0 / (1.0 - e0));
     const double bd = b1 * bm * geo;
     const double nbm = a1 * bm + d1 * bi + z0 * bd;
     const double nbi = b1 * bm + e1 * bi;
     bm = nbm; bi = nbi;
     gsum += bm + bi + bd;
+    d1 = d0; z1 = z0; e1 = e0;
   }
   E.read_gsum[r] = (float)gsum;
   E.read_flags[r] = degen ? 1 : 0;
@@ -145,14 +145,30 @@ __device__ __forceinline__ void fast_finish(const EngineDev& E, float a, int pai
 }
 
 // ---------------------------------------------------------------------------------
-// k_fast<P, K>: persistent; each warp takes G = 32/P units per atomic grab.
+// k_fast<P, K, MULTI>: persistent; each warp takes G = 32/P units per atomic grab.
+// MULTI = reads longer than one stripe (boundary column through global memory).
+//
+// Step loop (one haplotype row per step and thread; thread t is on row j = s - t):
+//   * neighbour exchange: __shfl_up_sync of the last position's M/I/D' (6 SHFL) and of
+//     the packed haplotype-character pair (1 SHFL); thread 0 takes the matrix boundary
+//     (or the previous stripe's column) instead and is the only thread loading
+//     haplotype characters, two rows ahead;
+//   * pass 1 (descending positions): D' from the previous row, M from the previous-row
+//     diagonal — in place, independent across positions;
+//   * pass 2 (ascending): the I chain along the read within the current row.
+// The steady phase (every thread of the warp on a valid row) runs without any
+// activity test; fill/drain steps and result capture use the checked variant.
 // ---------------------------------------------------------------------------------
-template <int P, int K>
-__global__ void __launch_bounds__(128, 2)
+#ifndef PHMM_FAST_MINB
+#define PHMM_FAST_MINB 2
+#endif
+template <int P, int K, bool MULTI>
+__global__ void __launch_bounds__(128, PHMM_FAST_MINB)
 k_fast(const EngineDev E, const FastUnit* __restrict__ units, int num_units, int Q,
        int* __restrict__ counter, float2* __restrict__ colbuf, int col_rows) {
   constexpr int W = P * K, G = 32 / P, K4 = K / 4;
   static_assert(K % 4 == 0 && K >= 4, "K multiple of 4");
+  constexpr unsigned FULL = 0xffffffffu;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double* s_lut = reinterpret_cast<double*>(smem_raw);
   float4* s_E = reinterpret_cast<float4*>(smem_raw + 96 * sizeof(double));
@@ -162,13 +178,14 @@ k_fast(const EngineDev E, const FastUnit* __restrict__ units, int num_units, int
   __syncthreads();
   float4* Et = s_E + (size_t)((wib * G + sw) * 5 * K4) * P;
   const int gwarp = blockIdx.x * (blockDim.x >> 5) + wib;
-  float2* colX = colbuf + (size_t)(gwarp * G + sw) * 2 * 3 * col_rows;
-  float2* colY = colX + 3 * col_rows;
+  float2* colX = MULTI ? colbuf + (size_t)(gwarp * G + sw) * 2 * 3 * col_rows : nullptr;
+  float2* colY = MULTI ? colX + 3 * col_rows : nullptr;
+  const float2 zero2 = make_float2(0.f, 0.f);
 
   for (;;) {
     int g = 0;
     if (lane == 0) g = atomicAdd(counter, 1);
-    g = __shfl_sync(0xffffffffu, g, 0);
+    g = __shfl_sync(FULL, g, 0);
     if (g * G >= num_units) break;
     const int u = g * G + sw;
     const bool has = u < num_units;
@@ -178,8 +195,8 @@ k_fast(const EngineDev E, const FastUnit* __restrict__ units, int num_units, int
     const bool degen = (E.read_flags[r] & 1) != 0;
     const bool live = has && !degen;
     const int nA = U.nA, nB = U.nB, nmax = max(nA, nB);
-    int steps = live ? nmax + P - 1 : 0;
-    steps = __reduce_max_sync(0xffffffffu, steps);
+    const int steps = __reduce_max_sync(FULL, live ? nmax + P - 1 : 0);
+    const int steady_end = min(steps, (int)__reduce_min_sync(FULL, live ? (unsigned)min(nA, nB) : 0x7fffffffu));
     if (has && degen && t == 0) {
       E.acc[U.pairA] = 0.0; E.status[U.pairA] = kStatusDegenerate;
       if (U.pairB >= 0) { E.acc[U.pairB] = 0.0; E.status[U.pairB] = kStatusDegenerate; }
@@ -195,9 +212,23 @@ k_fast(const EngineDev E, const FastUnit* __restrict__ units, int num_units, int
     float2* colPrev = colX;
     float2* colNext = colY;
 
+    // packed haplotype-character pair of one row (1-based); only thread 0 loads
+    auto load_code = [&](int row) -> unsigned {
+      unsigned a = 4u, b = 4u;
+      if (row >= 1 && row <= nA) a = (unsigned)(unsigned char)hA[row - 1];
+      if (row >= 1 && row <= nB) b = (unsigned)(unsigned char)hB[row - 1];
+      return a | (b << 8);
+    };
+
     for (int q = 0; q < Q; ++q) {
-      // ---- per-stripe coefficients + emission table (each thread: its K positions)
-      float al[K], be[K], dl[K], ep[K], zp[K];
+      // ---- per-stripe coefficients + emission table (each thread: its K positions).
+      // Folded state: Mt(i) = alpha_{i+1} M(i),  D'(i) = beta_{i+1} D(i):
+      //   Mt(i,j) = T_i(c_j) * (Mt(i-1,j-1) + beta_i I(i-1,j-1) + D'(i-1,j-1)),
+      //             T_i(c) = alpha_{i+1} * lambda_i(c)            (shared-memory table)
+      //   I(i,j)  = (delta_i / alpha_i) Mt(i-1,j) + eps_i I(i-1,j)
+      //   D'(i,j) = (beta_{i+1} zeta_i / alpha_{i+1}) Mt(i,j-1) + eps_i D'(i,j-1)
+      // 7 FP32 operations per cell, 4 coefficients per position.
+      float be[K], dl[K], ep[K], zp[K];
       float2 M[K], I[K], D[K];
 #pragma unroll
       for (int k4 = 0; k4 < K4; ++k4) {
@@ -206,10 +237,10 @@ k_fast(const EngineDev E, const FastUnit* __restrict__ units, int num_units, int
         for (int kk = 0; kk < 4; ++kk) {
           const int k = k4 * 4 + kk;
           const int p = q * W + t * K + k;
-          M[k] = make_float2(0.f, 0.f);
-          I[k] = make_float2(0.f, 0.f);
+          M[k] = zero2;
+          I[k] = zero2;
           if (p < Lp) {                                   // left padding
-            al[k] = 0.f; be[k] = 0.f; dl[k] = 0.f; ep[k] = 1.f; zp[k] = 0.f;
+            be[k] = 0.f; dl[k] = 0.f; ep[k] = 1.f; zp[k] = 0.f;
             D[k] = bS;
 #pragma unroll
             for (int c = 0; c < 5; ++c) lam[c][kk] = 0.f;
@@ -217,20 +248,25 @@ k_fast(const EngineDev E, const FastUnit* __restrict__ units, int num_units, int
             const int i0 = p - Lp;
             const double d = s_lut[E.iq[ro + i0]], z = s_lut[E.dq[ro + i0]];
             const double e = s_lut[E.gq[ro + i0]], qe = s_lut[E.bq[ro + i0]];
-            const double bnext = (i0 + 1 < m) ? 1.0 - s_lut[E.gq[ro + i0 + 1]] : 0.0;
-            al[k] = (float)((1.0 - d) - z);
+            const double a = (1.0 - d) - z;
+            double anext = 1.0, bnext = 0.0;
+            if (i0 + 1 < m) {
+              const double d1 = s_lut[E.iq[ro + i0 + 1]], z1 = s_lut[E.dq[ro + i0 + 1]];
+              anext = (1.0 - d1) - z1;
+              bnext = 1.0 - s_lut[E.gq[ro + i0 + 1]];
+            }
             be[k] = (float)(1.0 - e);
-            dl[k] = (float)d;
+            dl[k] = (float)(d / a);
             ep[k] = (float)e;
-            zp[k] = (float)(bnext * z);                   // D' = beta_{i+1} * D
-            D[k] = make_float2(0.f, 0.f);
+            zp[k] = (float)(bnext * z / anext);
+            D[k] = zero2;
             const int rc = E.rbases[ro + i0];
-            const float lm = (float)(1.0 - qe), lx = (float)(qe / 3.0);
+            const float lm = (float)(anext * (1.0 - qe)), lx = (float)(anext * (qe / 3.0));
 #pragma unroll
             for (int c = 0; c < 5; ++c) lam[c][kk] = (rc == c || rc == 4 || c == 4) ? lm : lx;
           } else {                                        // accumulator position
-            al[k] = 1.f; be[k] = 1.f; dl[k] = 0.f; ep[k] = 1.f; zp[k] = 1.f;
-            D[k] = make_float2(0.f, 0.f);
+            be[k] = 1.f; dl[k] = 0.f; ep[k] = 1.f; zp[k] = 1.f;
+            D[k] = zero2;
 #pragma unroll
             for (int c = 0; c < 5; ++c) lam[c][kk] = 1.f;
           }
@@ -239,55 +275,53 @@ k_fast(const EngineDev E, const FastUnit* __restrict__ units, int num_units, int
         for (int c = 0; c < 5; ++c)
           Et[(c * K4 + k4) * P + t] = make_float4(lam[c][0], lam[c][1], lam[c][2], lam[c][3]);
       }
-      if (t == P - 1 && q < Q - 1) {
+      const bool last_stripe = (q == Q - 1);
+      if (MULTI && t == P - 1 && !last_stripe) {
         colNext[0] = M[K - 1]; colNext[col_rows] = I[K - 1]; colNext[2 * col_rows] = D[K - 1];
       }
-      float2 nbM, nbI, nbD;
-      if (q == 0) {
-        nbM = make_float2(0.f, 0.f); nbI = nbM; nbD = bS;
-      } else {
-        nbM = colPrev[0]; nbI = colPrev[col_rows]; nbD = colPrev[2 * col_rows];
+      // thread-0 boundary source: stripe 0 -> matrix boundary, else previous column
+      float2 cbM = zero2, cbI = zero2, cbD = bS;          // boundary of row s (thread 0)
+      if (MULTI && q > 0 && t == 0) {
+        cbM = colPrev[0]; cbI = colPrev[col_rows]; cbD = colPrev[2 * col_rows];
       }
-      if (t != 0) { nbM = make_float2(0.f, 0.f); nbI = nbM; nbD = nbM; }
+      float2 nbM = (t == 0) ? cbM : zero2, nbI = (t == 0) ? cbI : zero2, nbD = (t == 0) ? cbD : zero2;
+      if (MULTI && q > 0 && t == 0) {                     // prefetch row 1
+        const int jj = min(1, nmax);
+        cbM = colPrev[jj]; cbI = colPrev[col_rows + jj]; cbD = colPrev[2 * col_rows + jj];
+      }
+      unsigned code = 0x0404u;
+      unsigned pf1 = load_code(t == 0 ? 1 : 0), pf2 = load_code(t == 0 ? 2 : 0);
       __syncwarp();
 
-      int cnA = 4, cnB = 4;                               // prefetched chars for row j
-      {
-        const int j = 1 - t;
-        if (live && j >= 1 && j <= nmax) {
-          cnA = (j <= nA) ? hA[j - 1] : 4;
-          cnB = (j <= nB) ? hB[j - 1] : 4;
-        }
-      }
-      for (int s = 1; s <= steps; ++s) {
+      auto step = [&](const int s, auto checked) {
+        constexpr bool CHECK = decltype(checked)::value;
         const int j = s - t;
         const float2 dgM = nbM, dgI = nbI, dgD = nbD;
         {
           const float2 lm = M[K - 1], li = I[K - 1], ld = D[K - 1];
-          nbM.x = __shfl_up_sync(0xffffffffu, lm.x, 1, P);
-          nbM.y = __shfl_up_sync(0xffffffffu, lm.y, 1, P);
-          nbI.x = __shfl_up_sync(0xffffffffu, li.x, 1, P);
-          nbI.y = __shfl_up_sync(0xffffffffu, li.y, 1, P);
-          nbD.x = __shfl_up_sync(0xffffffffu, ld.x, 1, P);
-          nbD.y = __shfl_up_sync(0xffffffffu, ld.y, 1, P);
+          nbM.x = __shfl_up_sync(FULL, lm.x, 1, P);
+          nbM.y = __shfl_up_sync(FULL, lm.y, 1, P);
+          nbI.x = __shfl_up_sync(FULL, li.x, 1, P);
+          nbI.y = __shfl_up_sync(FULL, li.y, 1, P);
+          nbD.x = __shfl_up_sync(FULL, ld.x, 1, P);
+          nbD.y = __shfl_up_sync(FULL, ld.y, 1, P);
+          const unsigned up = __shfl_up_sync(FULL, code, 1, P);
+          code = (t == 0) ? pf1 : up;
         }
         if (t == 0) {
-          if (q == 0) {
-            nbM = make_float2(0.f, 0.f); nbI = nbM; nbD = bS;
-          } else {
-            const int jj = min(max(j, 0), nmax);
-            nbM = colPrev[jj]; nbI = colPrev[col_rows + jj]; nbD = colPrev[2 * col_rows + jj];
-          }
+          nbM = cbM; nbI = cbI; nbD = cbD;
         }
-        const int cA = cnA, cB = cnB;                     // characters of row j
-        if (live && j + 1 >= 1 && j + 1 <= nmax) {        // prefetch row j + 1
-          cnA = (j + 1 <= nA) ? hA[j] : 4;
-          cnB = (j + 1 <= nB) ? hB[j] : 4;
+        pf1 = pf2;
+        pf2 = load_code(t == 0 ? s + 2 : 0);
+        if (MULTI && q > 0 && t == 0) {                   // next row's column entry
+          const int jj = min(s + 1, nmax);
+          cbM = colPrev[jj]; cbI = colPrev[col_rows + jj]; cbD = colPrev[2 * col_rows + jj];
         }
-        if (live && j >= 1 && j <= nmax) {
+        if (!CHECK || (live && j >= 1 && j <= nmax)) {
+          const int cA = code & 0xff, cB = (code >> 8) & 0xff;
           const float4* EA = Et + (cA * K4) * P + t;
           const float4* EB = Et + (cB * K4) * P + t;
-          // pass 1 (descending): D from the previous row, M from the previous-row diagonal
+          // pass 1 (descending): D' from the previous row, M from the previous-row diagonal
 #pragma unroll
           for (int k4 = K4 - 1; k4 >= 0; --k4) {
             const float4 la = EA[k4 * P];
@@ -300,7 +334,7 @@ k_fast(const EngineDev E, const FastUnit* __restrict__ units, int num_units, int
               const float2 pi = (k > 0) ? I[k - 1] : dgI;
               const float2 pd = (k > 0) ? D[k - 1] : dgD;
               float2 x = fma2s(be[k], pi, pd);
-              x = fma2s(al[k], pm, x);
+              x = __fadd2_rn(pm, x);
               M[k].x = comp(la, kk) * x.x;
               M[k].y = comp(lb, kk) * x.y;
             }
@@ -313,16 +347,21 @@ k_fast(const EngineDev E, const FastUnit* __restrict__ units, int num_units, int
             lM = M[k];
             lI = I[k];
           }
-          if (t == P - 1) {
-            if (q == Q - 1) {
-              if (j == nA) resA = (D[K - 1].x + M[K - 1].x) + (M[K - 2].x + I[K - 2].x);
-              if (j == nB) resB = (D[K - 1].y + M[K - 1].y) + (M[K - 2].y + I[K - 2].y);
-            } else {
-              colNext[j] = M[K - 1]; colNext[col_rows + j] = I[K - 1]; colNext[2 * col_rows + j] = D[K - 1];
-            }
+          if (MULTI && t == P - 1 && !last_stripe) {
+            colNext[j] = M[K - 1]; colNext[col_rows + j] = I[K - 1]; colNext[2 * col_rows + j] = D[K - 1];
+          }
+          if (CHECK && t == P - 1 && last_stripe) {
+            if (j == nA) resA = (D[K - 1].x + M[K - 1].x) + (M[K - 2].x + I[K - 2].x);
+            if (j == nB) resB = (D[K - 1].y + M[K - 1].y) + (M[K - 2].y + I[K - 2].y);
           }
         }
-      }
+      };
+
+      int s = 1;
+      const int fill_end = min(P - 1, steps);
+      for (; s <= fill_end; ++s) step(s, std::true_type{});
+      for (; s <= steady_end; ++s) step(s, std::false_type{});
+      for (; s <= steps; ++s) step(s, std::true_type{});
       __syncwarp();
       float2* tmp = colPrev; colPrev = colNext; colNext = tmp;
     }
@@ -360,6 +399,8 @@ k_exact(const EngineDev E, int slot, int* __restrict__ counter, T* __restrict__ 
   T* s_E = reinterpret_cast<T*>(smem_raw + 96 * sizeof(double));
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int sw = lane / P, t = lane % P;
+  const int count = min(kIsF32 ? E.ex32_count[slot] : E.ex64_count[slot], E.list_cap);
+  if (count == 0) return;
   for (int i = threadIdx.x; i < 94; i += blockDim.x) s_lut[i] = E.lut[i];
   __syncthreads();
   T* Et = s_E + (size_t)((wib * G + sw) * 5 * K) * P;   // Et[(c*K + k)*P + t]
@@ -367,7 +408,6 @@ k_exact(const EngineDev E, int slot, int* __restrict__ counter, T* __restrict__ 
   T* colX = colbuf + (size_t)(gwarp * G + sw) * 2 * 3 * col_rows;
   T* colY = colX + 3 * col_rows;
   const ExactItem* items = kIsF32 ? E.ex32[slot] : E.ex64[slot];
-  const int count = min(kIsF32 ? E.ex32_count[slot] : E.ex64_count[slot], E.list_cap);
   const T thr = X::flush_thr();
   const T zero = (T)0;
 
