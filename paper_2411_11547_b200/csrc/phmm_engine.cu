@@ -9,6 +9,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <string>
@@ -40,9 +41,9 @@ struct DBuf {
 };
 
 struct FastGeom { int P, K; };
-// single-stripe widths W = P*K: 16 32 48 64 96 128 192 256 384 512
-const FastGeom kFastGeoms[] = {{4, 4}, {4, 8}, {4, 12}, {4, 16}, {8, 12},
-                               {8, 16}, {16, 12}, {16, 16}, {32, 12}, {32, 16}};
+// single-stripe widths W = P*K: 16 32 48 64 64 96 128 128 192 256 256 384 512
+const FastGeom kFastGeoms[] = {{4, 4},  {4, 8},   {4, 12},  {4, 16},  {8, 8},   {8, 12}, {8, 16},
+                               {16, 8}, {16, 12}, {16, 16}, {32, 8},  {32, 12}, {32, 16}};
 constexpr int kNumFastGeoms = sizeof(kFastGeoms) / sizeof(kFastGeoms[0]);
 constexpr int kExactP[kNumExactP] = {4, 8, 16, 32};
 constexpr int kThreads = 128;
@@ -65,13 +66,19 @@ void launch_fast(dim3 g, size_t smem, cudaStream_t s, const EngineDev& E, const 
 typedef void (*FastLaunch)(dim3, size_t, cudaStream_t, const EngineDev&, const FastUnit*, int, int,
                            int*, float2*, int);
 const FastLaunch kFastLaunch[kNumFastGeoms] = {
-    launch_fast<4, 4>,   launch_fast<4, 8>,   launch_fast<4, 12>,  launch_fast<4, 16>,
-    launch_fast<8, 12>,  launch_fast<8, 16>,  launch_fast<16, 12>, launch_fast<16, 16>,
-    launch_fast<32, 12>, launch_fast<32, 16>};
+    launch_fast<4, 4>,  launch_fast<4, 8>,   launch_fast<4, 12>,  launch_fast<4, 16>, launch_fast<8, 8>,
+    launch_fast<8, 12>, launch_fast<8, 16>,  launch_fast<16, 8>,  launch_fast<16, 12>,
+    launch_fast<16, 16>, launch_fast<32, 8>, launch_fast<32, 12>, launch_fast<32, 16>};
+const int kFastOcc[kNumFastGeoms] = {FastOcc<4>::value,  FastOcc<8>::value,  FastOcc<12>::value,
+                                     FastOcc<16>::value, FastOcc<8>::value,  FastOcc<12>::value,
+                                     FastOcc<16>::value, FastOcc<8>::value,  FastOcc<12>::value,
+                                     FastOcc<16>::value, FastOcc<8>::value,  FastOcc<12>::value,
+                                     FastOcc<16>::value};
 #define FASTFN(P, K) (const void*)k_fast<P, K, false>, (const void*)k_fast<P, K, true>
-const void* kFastFn[2 * kNumFastGeoms] = {FASTFN(4, 4),   FASTFN(4, 8),   FASTFN(4, 12),  FASTFN(4, 16),
-                                          FASTFN(8, 12),  FASTFN(8, 16),  FASTFN(16, 12), FASTFN(16, 16),
-                                          FASTFN(32, 12), FASTFN(32, 16)};
+const void* kFastFn[2 * kNumFastGeoms] = {FASTFN(4, 4),   FASTFN(4, 8),   FASTFN(4, 12), FASTFN(4, 16),
+                                          FASTFN(8, 8),   FASTFN(8, 12),  FASTFN(8, 16), FASTFN(16, 8),
+                                          FASTFN(16, 12), FASTFN(16, 16), FASTFN(32, 8), FASTFN(32, 12),
+                                          FASTFN(32, 16)};
 #undef FASTFN
 
 template <typename T, int P>
@@ -89,6 +96,15 @@ const void* kExact32Fn[kNumExactP] = {(const void*)k_exact<float, 4, kExactK>, (
 const void* kExact64Fn[kNumExactP] = {(const void*)k_exact<double, 4, kExactK>, (const void*)k_exact<double, 8, kExactK>,
                                       (const void*)k_exact<double, 16, kExactK>, (const void*)k_exact<double, 32, kExactK>};
 
+template <int P>
+void launch_fast64(dim3 g, size_t smem, cudaStream_t s, const EngineDev& E, int slot, int* ctr, void* col,
+                   int rows) {
+  k_fast64<P, kExactK><<<g, kThreads, smem, s>>>(E, slot, ctr, (double*)col, rows);
+}
+const ExactLaunch kFast64[kNumExactP] = {launch_fast64<4>, launch_fast64<8>, launch_fast64<16>, launch_fast64<32>};
+const void* kFast64Fn[kNumExactP] = {(const void*)k_fast64<4, kExactK>, (const void*)k_fast64<8, kExactK>,
+                                     (const void*)k_fast64<16, kExactK>, (const void*)k_fast64<32, kExactK>};
+
 int exact_slot_host(int m) { return (m + 1 <= 32) ? 0 : (m + 1 <= 64) ? 1 : (m + 1 <= 128) ? 2 : 3; }
 
 size_t fast_smem(int geom) {
@@ -104,7 +120,26 @@ size_t exact_smem(int slot, size_t tsize) {
 // per-step overhead worth ~2.5 cells per thread.
 // Single-stripe tilings (W >= m + 1) are preferred; reads longer than the widest tile
 // (m >= 512) stripe over P = 32 tiles.
+int forced_geom() {
+  static int g = -2;
+  if (g == -2) {
+    g = -1;
+    const char* env = getenv("PHMM_FAST_GEOM");      // tuning knob: "PxK"
+    int P = 0, K = 0;
+    if (env && sscanf(env, "%dx%d", &P, &K) == 2)
+      for (int i = 0; i < kNumFastGeoms; ++i)
+        if (kFastGeoms[i].P == P && kFastGeoms[i].K == K) g = i;
+  }
+  return g;
+}
+
 int choose_geom(int m, int nmax, int* Qout) {
+  const int fg = forced_geom();
+  if (fg >= 0) {
+    const int W = kFastGeoms[fg].P * kFastGeoms[fg].K;
+    *Qout = (m + 1 + W - 1) / W;
+    return fg;
+  }
   double best = 1e300;
   int bi = 0, bq = 1;
   const bool stripe = m + 1 > kFastGeoms[kNumFastGeoms - 1].P * kFastGeoms[kNumFastGeoms - 1].K;
@@ -126,6 +161,7 @@ struct phmm_ctx {
   int num_sms = 148;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev_start = nullptr, ev_fast0 = nullptr, ev_fast1 = nullptr, ev_end = nullptr;
+  cudaEvent_t ev_pre = nullptr;
   std::string err;
   std::vector<double> lut;
 
@@ -137,7 +173,7 @@ struct phmm_ctx {
   DBuf<float> d_gsum;
   DBuf<double> d_lut, d_acc;
   DBuf<FastUnit> d_units;
-  DBuf<ExactItem> d_ex32[kNumExactP], d_ex64[kNumExactP];
+  DBuf<ExactItem> d_ex32[kNumExactP], d_ex64[kNumExactP], d_fx64[kNumExactP];
   DBuf<float2> d_colf;
   DBuf<double> d_cold;
   int* h_counts = nullptr;   // pinned: initial list counts (8) + zeros for work counters
@@ -206,6 +242,7 @@ int phmm_create(phmm_ctx** out, int device, const double* phred_lut) {
                                          prop.name, prop.major, prop.minor);
   ctx->num_sms = prop.multiProcessorCount;
   CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&ctx->ev_pre, cudaEventDisableTiming));
   CK(cudaEventCreate(&ctx->ev_start));
   CK(cudaEventCreate(&ctx->ev_fast0));
   CK(cudaEventCreate(&ctx->ev_fast1));
@@ -218,6 +255,7 @@ int phmm_create(phmm_ctx** out, int device, const double* phred_lut) {
   for (int s = 0; s < kNumExactP; ++s) {
     CK(cudaFuncSetAttribute(kExact32Fn[s], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)exact_smem(s, 4)));
     CK(cudaFuncSetAttribute(kExact64Fn[s], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)exact_smem(s, 8)));
+    CK(cudaFuncSetAttribute(kFast64Fn[s], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)exact_smem(s, 8)));
   }
   return PHMM_SUCCESS;
 }
@@ -231,12 +269,14 @@ int phmm_destroy(phmm_ctx* ctx) {
   ctx->d_roff.release(); ctx->d_hoff.release(); ctx->d_read_m.release(); ctx->d_read_scale.release();
   ctx->d_read_ncap.release(); ctx->d_counters.release(); ctx->d_gsum.release(); ctx->d_lut.release();
   ctx->d_acc.release(); ctx->d_units.release(); ctx->d_colf.release(); ctx->d_cold.release();
-  for (int s = 0; s < kNumExactP; ++s) { ctx->d_ex32[s].release(); ctx->d_ex64[s].release(); }
+  for (int s = 0; s < kNumExactP; ++s) { ctx->d_ex32[s].release(); ctx->d_ex64[s].release(); ctx->d_fx64[s].release(); }
   if (ctx->h_counts) cudaFreeHost(ctx->h_counts);
+  ctx->h_counts = nullptr;
   if (ctx->ev_start) cudaEventDestroy(ctx->ev_start);
   if (ctx->ev_fast0) cudaEventDestroy(ctx->ev_fast0);
   if (ctx->ev_fast1) cudaEventDestroy(ctx->ev_fast1);
   if (ctx->ev_end) cudaEventDestroy(ctx->ev_end);
+  if (ctx->ev_pre) cudaEventDestroy(ctx->ev_pre);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
   return PHMM_SUCCESS;
@@ -414,18 +454,19 @@ int phmm_prepare(phmm_ctx* ctx, const phmm_input* in, const phmm_options* opt, i
   CK(ctx->d_rflags.ensure(R));
   CK(ctx->d_acc.ensure(N));
   CK(ctx->d_status.ensure(N));
-  CK(ctx->d_counters.ensure(64));
+  CK(ctx->d_counters.ensure(32 + ctx->bins.size()));
   ctx->list_cap = (int)std::max<int64_t>(N, 1);
   for (int s = 0; s < kNumExactP; ++s) {
     ctx->host_ex32[s] = (int)host32[s].size();
     ctx->host_ex64[s] = (int)host64[s].size();
     CK(ctx->d_ex32[s].ensure(ctx->list_cap));
     CK(ctx->d_ex64[s].ensure(ctx->list_cap));
+    CK(ctx->d_fx64[s].ensure(ctx->list_cap));
     if (!host32[s].empty()) CK(up(ctx->d_ex32[s], host32[s].data(), host32[s].size()));
     if (!host64[s].empty()) CK(up(ctx->d_ex64[s], host64[s].data(), host64[s].size()));
   }
   // boundary-column scratch: 2 buffers x 3 values x (max_n + 1) rows per sub-warp slot
-  const int slots_per_sm = 2 * (kThreads / 32) * 8;   // <= 2 CTAs/SM x 4 warps x 8 sub-warps
+  const int slots_per_sm = 4 * (kThreads / 32) * 8;   // <= 4 CTAs/SM x 4 warps x 8 sub-warps
   const size_t col_elems = (size_t)ctx->num_sms * slots_per_sm * 2 * 3 * (size_t)(max_n + 1);
   bool need_col = false, need_cold = false;
   for (auto& bn : ctx->bins) need_col |= bn.Q > 1;
@@ -446,11 +487,17 @@ int phmm_prepare(phmm_ctx* ctx, const phmm_input* in, const phmm_options* opt, i
   E.read_m = ctx->d_read_m.p; E.read_scale = ctx->d_read_scale.p; E.read_ncap = ctx->d_read_ncap.p;
   E.read_gsum = ctx->d_gsum.p; E.read_flags = ctx->d_rflags.p; E.lut = ctx->d_lut.p;
   E.acc = ctx->d_acc.p; E.status = ctx->d_status.p;
-  for (int s = 0; s < kNumExactP; ++s) { E.ex32[s] = ctx->d_ex32[s].p; E.ex64[s] = ctx->d_ex64[s].p; }
+  for (int s = 0; s < kNumExactP; ++s) {
+    E.ex32[s] = ctx->d_ex32[s].p; E.ex64[s] = ctx->d_ex64[s].p; E.fx64[s] = ctx->d_fx64[s].p;
+  }
+  E.fx64_count = ctx->d_counters.p + 20;
   E.ex32_count = ctx->d_counters.p + 0;
   E.ex64_count = ctx->d_counters.p + kNumExactP;
   E.list_cap = ctx->list_cap;
   E.retry_f64 = (opt->flags & PHMM_FLAG_RETRY_F64) ? 1 : 0;
+  E.band_inline = ctx->d_counters.p + 16;
+  E.band_budget = 2 * ctx->num_sms;
+
   ctx->prepared = true;
   if (num_pairs_out) *num_pairs_out = N;
   return PHMM_SUCCESS;
@@ -464,33 +511,41 @@ int phmm_execute(phmm_ctx* ctx) {
   const EngineDev& E = ctx->dev;
   const int64_t N = ctx->num_pairs;
   int launches = 0;
-  // counters: [0,4) ex32 counts, [4,8) ex64 counts, [8,12) ex32 work, [12,16) ex64 work, [16..) fast bins
-  int* hc = ctx->h_counts;
-  memset(hc, 0, 64 * sizeof(int));
-  for (int s = 0; s < kNumExactP; ++s) { hc[s] = ctx->host_ex32[s]; hc[kNumExactP + s] = ctx->host_ex64[s]; }
+  // counters: [0,4) ex32 counts, [4,8) ex64 counts, [8,12) ex32 work, [12,16) ex64 work,
+  // 16 inline guard-band pairs, [20,24) fx64 counts, [24,28) fx64 work, [32, 32+bins) bins
   const int nb = (int)ctx->bins.size();
-  if (16 + nb > 64 && ctx->d_counters.cap < (size_t)(16 + nb)) CK(ctx->d_counters.ensure(16 + nb));
-  CK(cudaEventRecord(ctx->ev_start, st));
-  CK(cudaMemcpyAsync(ctx->d_counters.p, hc, 16 * sizeof(int), cudaMemcpyHostToDevice, st));
-  CK(cudaMemsetAsync(ctx->d_counters.p + 16, 0, std::max(nb, 1) * sizeof(int), st));
-  if (N > 0) CK(cudaMemsetAsync(ctx->d_status.p, 0, N, st));
-  if (ctx->num_reads > 0) {
-    const int threads = 128;
-    const int64_t blocks = (ctx->num_reads + threads - 1) / threads;
-    k_precompute<<<(unsigned)blocks, threads, 0, st>>>(E, (int)ctx->num_reads);
-    ++launches;
-  }
-  CK(cudaEventRecord(ctx->ev_fast0, st));
+  std::vector<int> blocks(nb, 0);
+  int total_fast_ctas = 0;
   for (int bi = 0; bi < nb; ++bi) {
     const Bin& bn = ctx->bins[bi];
     const int nu = (int)bn.units.size();
     if (nu == 0) continue;
     const int G = 32 / kFastGeoms[bn.geom].P;
     const int groups = (nu + G - 1) / G;
-    const int max_blocks = ctx->num_sms * 2;
-    const int blocks = std::max(1, std::min(max_blocks, (groups + 3) / 4));
-    kFastLaunch[bn.geom](dim3(blocks), fast_smem(bn.geom), st, E, ctx->d_units.p + bn.dev_off, nu, bn.Q,
-                         ctx->d_counters.p + 16 + bi, ctx->d_colf.p, ctx->max_n + 1);
+    blocks[bi] = std::max(1, std::min(ctx->num_sms * kFastOcc[bn.geom], (groups + 3) / 4));
+    total_fast_ctas += blocks[bi];
+  }
+  int* hc = ctx->h_counts;
+  memset(hc, 0, 32 * sizeof(int));
+  for (int s = 0; s < kNumExactP; ++s) { hc[s] = ctx->host_ex32[s]; hc[kNumExactP + s] = ctx->host_ex64[s]; }
+  CK(cudaEventRecord(ctx->ev_start, st));
+  CK(cudaMemcpyAsync(ctx->d_counters.p, hc, 32 * sizeof(int), cudaMemcpyHostToDevice, st));
+  if (nb > 0) CK(cudaMemsetAsync(ctx->d_counters.p + 32, 0, nb * sizeof(int), st));
+  if (N > 0) CK(cudaMemsetAsync(ctx->d_status.p, 0, N, st));
+  if (ctx->num_reads > 0) {
+    const int threads = 128;
+    const int64_t blocks_pre = (ctx->num_reads * 32 + threads - 1) / threads;
+    k_precompute<<<(unsigned)blocks_pre, threads, 0, st>>>(E, (int)ctx->num_reads);
+    ++launches;
+  }
+  CK(cudaEventRecord(ctx->ev_pre, st));
+  CK(cudaEventRecord(ctx->ev_fast0, st));
+  for (int bi = 0; bi < nb; ++bi) {
+    const Bin& bn = ctx->bins[bi];
+    const int nu = (int)bn.units.size();
+    if (nu == 0) continue;
+    kFastLaunch[bn.geom](dim3(blocks[bi]), fast_smem(bn.geom), st, E, ctx->d_units.p + bn.dev_off, nu, bn.Q,
+                         ctx->d_counters.p + 32 + bi, ctx->d_colf.p, ctx->max_n + 1);
     ++launches;
   }
   CK(cudaGetLastError());
@@ -498,6 +553,12 @@ int phmm_execute(phmm_ctx* ctx) {
   for (int s = 0; s < kNumExactP; ++s) {
     kExact32[s](dim3(ctx->num_sms * 2), exact_smem(s, 4), st, E, s, ctx->d_counters.p + 8 + s,
                 ctx->d_cold.p, ctx->max_n + 1);
+    ++launches;
+  }
+  for (int s = 0; s < kNumExactP; ++s) {
+    if (!(ctx->flags & PHMM_FLAG_RETRY_F64)) break;
+    kFast64[s](dim3(ctx->num_sms * 2), exact_smem(s, 8), st, E, s, ctx->d_counters.p + 24 + s,
+               ctx->d_cold.p, ctx->max_n + 1);
     ++launches;
   }
   for (int s = 0; s < kNumExactP; ++s) {

@@ -61,6 +61,10 @@ struct EngineDev {
   int* ex64_count;                        // [kNumExactP]
   int list_cap;
   int retry_f64;
+  ExactItem* fx64[kNumExactP];            // FP64 retry lists (fast FP64 kernel)
+  int* fx64_count;                        // [kNumExactP]
+  int* band_inline;                       // guard-band pairs taken inline so far
+  int band_budget;
 };
 
 __device__ __forceinline__ int exact_slot_for(int m) {
@@ -82,29 +86,37 @@ __device__ __forceinline__ void append_item(ExactItem* const* lists, int* counts
 //   0 <= unflushed - flushed <= 2^-90 * n * Gsum        (guard band)
 // ---------------------------------------------------------------------------------
 __global__ void k_precompute(EngineDev E, int num_reads) {
-  const int r = blockIdx.x * blockDim.x + threadIdx.x;     // one thread per read
+  // One warp per read.  With X_i = max(B_M(i), B_I(i)) and g_i = min(n, 1/(1-eps_i)):
+  //   B_D(i) <= g_i X_{i+1},  X_i <= (1 + zeta_i g_i) X_{i+1},  X_m = 1
+  // so  sum_i (B_M + B_I + B_D) <= prod_{i<m}(1 + zeta_i g_i) * (2 + sum_{i<m}(2 + g_i)).
+  const int lane = threadIdx.x & 31;
+  const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (r >= num_reads) return;
   const int m = E.read_m[r];
   const int64_t o = E.roff[r];
   const double ncap = (double)E.read_ncap[r];
   const double* lut = E.lut;
-  bool degen = lut[E.iq[o + m - 1]] + lut[E.dq[o + m - 1]] >= 1.0;
-  double bm = 1.0, bi = 1.0, gsum = 2.0;                  // i = m: B_M = B_I = 1, B_D = 0
-  double d1 = lut[E.iq[o + m - 1]], z1 = lut[E.dq[o + m - 1]], e1 = lut[E.gq[o + m - 1]];
-  for (int i = m - 1; i >= 1; --i) {                      // 1-based position i; arrays 0-based
-    const double a1 = (1.0 - d1) - z1, b1 = 1.0 - e1;
-    const double d0 = lut[E.iq[o + i - 1]], z0 = lut[E.dq[o + i - 1]], e0 = lut[E.gq[o + i - 1]];
-    degen |= (d0 + z0 >= 1.0);
-    const double geo = (e0 >= 1.0) ? ncap : fmin(ncap, 1.0 / (1.0 - e0));
-    const double bd = b1 * bm * geo;
-    const double nbm = a1 * bm + d1 * bi + z0 * bd;
-    const double nbi = b1 * bm + e1 * bi;
-    bm = nbm; bi = nbi;
-    gsum += bm + bi + bd;
-    d1 = d0; z1 = z0; e1 = e0;
+  bool degen = false;
+  double logx = 0.0, sg = 0.0;
+  for (int i = lane; i < m; i += 32) {
+    const double d = lut[E.iq[o + i]], z = lut[E.dq[o + i]], e = lut[E.gq[o + i]];
+    degen |= (d + z >= 1.0);
+    if (i < m - 1) {
+      const double g = (e >= 1.0) ? ncap : fmin(ncap, 1.0 / (1.0 - e));
+      logx += log1p(z * g);
+      sg += 2.0 + g;
+    }
   }
-  E.read_gsum[r] = (float)gsum;
-  E.read_flags[r] = degen ? 1 : 0;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    logx += __shfl_xor_sync(0xffffffffu, logx, off);
+    sg += __shfl_xor_sync(0xffffffffu, sg, off);
+  }
+  degen = __any_sync(0xffffffffu, degen);
+  if (lane == 0) {
+    E.read_gsum[r] = (float)(exp(logx) * (2.0 + sg));
+    E.read_flags[r] = degen ? 1 : 0;
+  }
 }
 
 // packed helpers: scalar-broadcast operand -> FFMA2 R.F32 form
@@ -120,27 +132,188 @@ __device__ __forceinline__ float comp(const float4& v, int i) {
 
 // Fast-path classification of a finished FP32 accumulator:
 //   a < 2^-93                    -> every final-row term flushes in the reference: flagged
-//   a < 2^16 * 2^-90 * n * Gsum  -> guard band: rerun on the bit-exact kernel
+//   a < 2^10 * 2^-90 * n * Gsum  -> guard band: rerun on the bit-exact kernel (outside the
+//                                   band the flush effect is < 2^-10 relative, i.e. < 4.3e-4
+//                                   in log10 at |score| > 52: < 1e-5 relative)
 //   score > -1.5 (short pairs)   -> bit-exact kernel (relative tolerance near log10 = 0)
 //   otherwise                    -> accept
-__device__ __forceinline__ void fast_finish(const EngineDev& E, float a, int pair, int read, int hap,
+__device__ __forceinline__ bool fast_finish(const EngineDev& E, float a, int pair, int read, int hap,
                                             int n, int m, int scale) {
-  const float bound = 0x1p-74f * (float)n * E.read_gsum[read];   // 2^16 * 2^-90
+  const float bound = 0x1p-80f * (float)n * E.read_gsum[read];   // 2^10 * 2^-90
   const float hi = ldexpf(0.031622776f, scale);                   // 10^-1.5 * 2^scale
   if (!(a >= 0x1p-93f)) {
     if (E.retry_f64) {
       E.status[pair] = kStatusRetriedF64;
-      append_item(E.ex64, E.ex64_count, E.list_cap, exact_slot_for(m), ExactItem{pair, read, hap, 0});
+      append_item(E.fx64, E.fx64_count, E.list_cap, exact_slot_for(m), ExactItem{pair, read, hap, 0});
     } else {
       E.acc[pair] = 0.0;
       E.status[pair] = kStatusOverflow;
     }
   } else if (a < bound || a > hi) {
     E.status[pair] = kStatusExactF32;
+    // guard band: the first band_budget pairs are rerun inline by the finding warp (no
+    // tail when they are rare); beyond that they go to the post-pass exact kernels.
+    if (atomicAdd(E.band_inline, 1) < E.band_budget) return true;
     append_item(E.ex32, E.ex32_count, E.list_cap, exact_slot_for(m), ExactItem{pair, read, hap, scale});
   } else {
     E.acc[pair] = (double)a;
     E.status[pair] = kStatusOk;
+  }
+  return false;
+}
+
+// ---------------------------------------------------------------------------------
+// k_exact<T, P, K>: bit-exact reference recursion (reference.py:106-122,
+// wavefront.py:130-160) — no FMA, per-store flush, j-ordered accumulation.
+// ---------------------------------------------------------------------------------
+template <typename T> struct ExactTraits;
+template <> struct ExactTraits<float> {
+  static __device__ __forceinline__ float mul(float a, float b) { return __fmul_rn(a, b); }
+  static __device__ __forceinline__ float add(float a, float b) { return __fadd_rn(a, b); }
+  static __device__ __forceinline__ float flush_thr() { return 0x1p-90f; }
+};
+template <> struct ExactTraits<double> {
+  static __device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
+  static __device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
+  static __device__ __forceinline__ double flush_thr() { return 0x1p-970; }
+};
+
+// One item (read x haplotype) on one sub-warp of P threads; `live` false = the
+// sub-warp only takes part in the warp-wide shuffles.  Writes acc/status itself.
+template <typename T, int P, int K>
+__device__ __forceinline__ void exact_item(const EngineDev& E, const ExactItem& it, bool has,
+                                           const double* s_lut, T* Et, T* colX, T* colY, int col_rows,
+                                           int t) {
+  using X = ExactTraits<T>;
+  constexpr int W = P * K;
+  constexpr bool kIsF32 = sizeof(T) == 4;
+  const T thr = X::flush_thr();
+  const T zero = (T)0;
+  const int r = it.read, m = E.read_m[r];
+  const int64_t ro = E.roff[r];
+  const int n = (int)(E.hoff[it.hap + 1] - E.hoff[it.hap]);
+  const bool degen = (E.read_flags[r] & 1) != 0;
+  const bool live = has && !degen;
+  int steps = live ? n + P - 1 : 0;
+  steps = __reduce_max_sync(0xffffffffu, steps);
+  if (has && degen && t == 0) { E.acc[it.pair] = 0.0; E.status[it.pair] = kStatusDegenerate; }
+  const int Q = (m + 1 + W - 1) / W;
+  const int Lp = Q * W - m - 1;
+  const T bnd = (T)(ldexp(1.0, it.scale) / (double)n);     // wavefront.py:405-406
+  const int8_t* h = E.hbases + E.hoff[it.hap];
+  T res = zero;
+  T* colPrev = colX;
+  T* colNext = colY;
+
+  // Q is per item; the warp iterates to the max over its sub-warps
+  const int Qw = __reduce_max_sync(0xffffffffu, live ? Q : 0);
+  for (int q = 0; q < Qw; ++q) {
+    const bool sact = live && q < Q;
+    T al[K], be[K], dl[K], ep[K], zt[K], M[K], I[K], D[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const int p = q * W + t * K + k;
+      T lam[5];
+      M[k] = zero; I[k] = zero;
+      if (p < Lp) {
+        al[k] = zero; be[k] = zero; dl[k] = zero; ep[k] = (T)1; zt[k] = zero; D[k] = bnd;
+#pragma unroll
+        for (int c = 0; c < 5; ++c) lam[c] = zero;
+      } else if (p < Lp + m) {
+        const int i0 = p - Lp;
+        const double d = s_lut[E.iq[ro + i0]], z = s_lut[E.dq[ro + i0]];
+        const double e = s_lut[E.gq[ro + i0]], qe = s_lut[E.bq[ro + i0]];
+        al[k] = (T)((1.0 - d) - z);
+        be[k] = (T)(1.0 - e);
+        dl[k] = (T)d;
+        ep[k] = (T)e;
+        zt[k] = (i0 + 1 < m) ? (T)z : zero;        // D(m, .) never reaches the score
+        D[k] = zero;
+        const int rc = E.rbases[ro + i0];
+        const T lm = (T)(1.0 - qe), lx = (T)(qe / 3.0);
+#pragma unroll
+        for (int c = 0; c < 5; ++c) lam[c] = (rc == c || rc == 4 || c == 4) ? lm : lx;
+      } else {
+        al[k] = (T)1; be[k] = (T)1; dl[k] = zero; ep[k] = (T)1; zt[k] = (T)1; D[k] = zero;
+#pragma unroll
+        for (int c = 0; c < 5; ++c) lam[c] = (T)1;
+      }
+#pragma unroll
+      for (int c = 0; c < 5; ++c) Et[(c * K + k) * P + t] = lam[c];
+    }
+    if (sact && t == P - 1 && q < Q - 1) {
+      colNext[0] = M[K - 1]; colNext[col_rows] = I[K - 1]; colNext[2 * col_rows] = D[K - 1];
+    }
+    T nbM = zero, nbI = zero, nbD = zero;
+    if (t == 0) {
+      if (q == 0) { nbD = bnd; }
+      else if (sact) { nbM = colPrev[0]; nbI = colPrev[col_rows]; nbD = colPrev[2 * col_rows]; }
+    }
+    __syncwarp();
+    for (int s = 1; s <= steps; ++s) {
+      const int j = s - t;
+      const T dgM = nbM, dgI = nbI, dgD = nbD;
+      nbM = __shfl_up_sync(0xffffffffu, M[K - 1], 1, P);
+      nbI = __shfl_up_sync(0xffffffffu, I[K - 1], 1, P);
+      nbD = __shfl_up_sync(0xffffffffu, D[K - 1], 1, P);
+      if (t == 0) {
+        if (q == 0) { nbM = zero; nbI = zero; nbD = bnd; }
+        else if (sact) {
+          const int jj = min(max(j, 0), n);
+          nbM = colPrev[jj]; nbI = colPrev[col_rows + jj]; nbD = colPrev[2 * col_rows + jj];
+        }
+      }
+      if (sact && j >= 1 && j <= n) {
+        const int c = h[j - 1];
+        const T* Ec = Et + (c * K) * P + t;
+#pragma unroll
+        for (int k = K - 1; k >= 0; --k) {
+          // dv = zt*M(i,j-1) + ep*D(i,j-1)
+          const T dv = X::add(X::mul(zt[k], M[k]), X::mul(ep[k], D[k]));
+          D[k] = dv >= thr ? dv : zero;
+          const T pm = (k > 0) ? M[k - 1] : dgM;
+          const T pi = (k > 0) ? I[k - 1] : dgI;
+          const T pd = (k > 0) ? D[k - 1] : dgD;
+          // mv = lam*(al*M(i-1,j-1) + be*(I(i-1,j-1) + D(i-1,j-1)))
+          const T mv = X::mul(Ec[k * P], X::add(X::mul(al[k], pm), X::mul(be[k], X::add(pi, pd))));
+          M[k] = mv >= thr ? mv : zero;
+        }
+        T lM = nbM, lI = nbI;
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          // iv = dl*M(i-1,j) + ep*I(i-1,j)
+          const T iv = X::add(X::mul(dl[k], lM), X::mul(ep[k], lI));
+          I[k] = iv >= thr ? iv : zero;
+          lM = M[k];
+          lI = I[k];
+        }
+        if (t == P - 1) {
+          if (q == Q - 1) {
+            if (j == n) res = X::add(X::add(D[K - 1], M[K - 1]), X::add(M[K - 2], I[K - 2]));
+          } else {
+            colNext[j] = M[K - 1]; colNext[col_rows + j] = I[K - 1]; colNext[2 * col_rows + j] = D[K - 1];
+          }
+        }
+      }
+    }
+    __syncwarp();
+    T* tmp = colPrev; colPrev = colNext; colNext = tmp;
+  }
+  if (live && t == P - 1) {
+    const bool bad = !(res > zero) || !isfinite((double)res);
+    if (kIsF32) {
+      if (bad && E.retry_f64) {
+        E.status[it.pair] = kStatusRetriedF64;
+        append_item(E.fx64, E.fx64_count, E.list_cap, exact_slot_for(m), ExactItem{it.pair, r, it.hap, 0});
+      } else {
+        E.acc[it.pair] = (double)res;
+        E.status[it.pair] = bad ? kStatusOverflow : kStatusExactF32;
+      }
+    } else {
+      E.acc[it.pair] = (double)res;
+      const uint8_t keep = E.status[it.pair] & kStatusRetriedF64;
+      E.status[it.pair] = (uint8_t)((bad ? kStatusOverflow : kStatusOk) | keep);
+    }
   }
 }
 
@@ -159,11 +332,10 @@ __device__ __forceinline__ void fast_finish(const EngineDev& E, float a, int pai
 // The steady phase (every thread of the warp on a valid row) runs without any
 // activity test; fill/drain steps and result capture use the checked variant.
 // ---------------------------------------------------------------------------------
-#ifndef PHMM_FAST_MINB
-#define PHMM_FAST_MINB 2
-#endif
+// resident CTAs (of 4 warps) per SM by positions per thread: K=8 -> 4, K=12 -> 3, K=16 -> 2
+template <int K> struct FastOcc { static constexpr int value = K <= 8 ? 4 : (K <= 12 ? 3 : 2); };
 template <int P, int K, bool MULTI>
-__global__ void __launch_bounds__(128, PHMM_FAST_MINB)
+__global__ void __launch_bounds__(128, FastOcc<K>::value)
 k_fast(const EngineDev E, const FastUnit* __restrict__ units, int num_units, int Q,
        int* __restrict__ counter, float2* __restrict__ colbuf, int col_rows) {
   constexpr int W = P * K, G = 32 / P, K4 = K / 4;
@@ -248,20 +420,19 @@ k_fast(const EngineDev E, const FastUnit* __restrict__ units, int num_units, int
             const int i0 = p - Lp;
             const double d = s_lut[E.iq[ro + i0]], z = s_lut[E.dq[ro + i0]];
             const double e = s_lut[E.gq[ro + i0]], qe = s_lut[E.bq[ro + i0]];
-            const double a = (1.0 - d) - z;
-            double anext = 1.0, bnext = 0.0;
+            const float a = (float)((1.0 - d) - z);
+            float anext = 1.f, bnext = 0.f;
             if (i0 + 1 < m) {
-              const double d1 = s_lut[E.iq[ro + i0 + 1]], z1 = s_lut[E.dq[ro + i0 + 1]];
-              anext = (1.0 - d1) - z1;
-              bnext = 1.0 - s_lut[E.gq[ro + i0 + 1]];
+              anext = (float)((1.0 - s_lut[E.iq[ro + i0 + 1]]) - s_lut[E.dq[ro + i0 + 1]]);
+              bnext = (float)(1.0 - s_lut[E.gq[ro + i0 + 1]]);
             }
             be[k] = (float)(1.0 - e);
-            dl[k] = (float)(d / a);
+            dl[k] = __fdividef((float)d, a);
             ep[k] = (float)e;
-            zp[k] = (float)(bnext * z / anext);
+            zp[k] = __fdividef(bnext * (float)z, anext);
             D[k] = zero2;
             const int rc = E.rbases[ro + i0];
-            const float lm = (float)(anext * (1.0 - qe)), lx = (float)(anext * (qe / 3.0));
+            const float lm = anext * (float)(1.0 - qe), lx = anext * ((float)qe * (1.f / 3.f));
 #pragma unroll
             for (int c = 0; c < 5; ++c) lam[c][kk] = (rc == c || rc == 4 || c == 4) ? lm : lx;
           } else {                                        // accumulator position
@@ -365,34 +536,180 @@ k_fast(const EngineDev E, const FastUnit* __restrict__ units, int num_units, int
       __syncwarp();
       float2* tmp = colPrev; colPrev = colNext; colNext = tmp;
     }
+    int band = 0;                                       // bit0: pair A, bit1: pair B
     if (live && t == P - 1) {
-      fast_finish(E, resA, U.pairA, r, U.hapA, nA, m, scale);
-      if (U.pairB >= 0) fast_finish(E, resB, U.pairB, r, U.hapB, nB, m, scale);
+      band = fast_finish(E, resA, U.pairA, r, U.hapA, nA, m, scale) ? 1 : 0;
+      if (U.pairB >= 0 && fast_finish(E, resB, U.pairB, r, U.hapB, nB, m, scale)) band |= 2;
+    }
+    // guard band: rerun those pairs right here on the bit-exact recursion (same tiling,
+    // the unit's emission table slot and boundary-column scratch are free again), so
+    // band work overlaps the other warps' fast work instead of forming a tail.
+    band = __shfl_sync(FULL, band, sw * P + P - 1);
+    if (__any_sync(FULL, band != 0)) {
+#pragma unroll 1
+      for (int x = 0; x < 2; ++x) {
+        const bool mine = (band >> x) & 1;
+        if (!__any_sync(FULL, mine)) continue;
+        const ExactItem it{x == 0 ? U.pairA : U.pairB, r, x == 0 ? U.hapA : U.hapB, scale};
+        float* ex_col = reinterpret_cast<float*>(colX);
+        exact_item<float, P, K>(E, it, mine, s_lut, reinterpret_cast<float*>(Et), ex_col,
+                                ex_col + 3 * col_rows, col_rows, t);
+        __syncwarp();
+      }
     }
   }
 }
 
 // ---------------------------------------------------------------------------------
-// k_exact<T, P, K>: bit-exact reference recursion (reference.py:106-122,
-// wavefront.py:130-160) — no FMA, per-store flush, j-ordered accumulation.
+// k_fast64<P, K>: FP64 retry of pairs whose FP32 result underflowed (GATK behaviour).
+// Same folded recurrence as k_fast (FMA, 7 DP operations per cell, no per-cell flush),
+// one pair per sub-warp lane set, scale 2^0.  Accuracy vs the reference's f64 path is
+// ~1e-13 relative (FMA/reassociation only); the reference's 2^-970 flush is provably
+// irrelevant above 2^-900, and results below that are re-run on k_exact<double>.
 // ---------------------------------------------------------------------------------
-template <typename T> struct ExactTraits;
-template <> struct ExactTraits<float> {
-  static __device__ __forceinline__ float mul(float a, float b) { return __fmul_rn(a, b); }
-  static __device__ __forceinline__ float add(float a, float b) { return __fadd_rn(a, b); }
-  static __device__ __forceinline__ float flush_thr() { return 0x1p-90f; }
-};
-template <> struct ExactTraits<double> {
-  static __device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
-  static __device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
-  static __device__ __forceinline__ double flush_thr() { return 0x1p-970; }
-};
+template <int P, int K>
+__global__ void __launch_bounds__(128)
+k_fast64(const EngineDev E, int slot, int* __restrict__ counter, double* __restrict__ colbuf, int col_rows) {
+  constexpr int W = P * K, G = 32 / P;
+  constexpr unsigned FULL = 0xffffffffu;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* s_lut = reinterpret_cast<double*>(smem_raw);
+  double* s_E = reinterpret_cast<double*>(smem_raw + 96 * sizeof(double));
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int sw = lane / P, t = lane % P;
+  const int count = min(E.fx64_count[slot], E.list_cap);
+  if (count == 0) return;
+  for (int i = threadIdx.x; i < 94; i += blockDim.x) s_lut[i] = E.lut[i];
+  __syncthreads();
+  double* Et = s_E + (size_t)((wib * G + sw) * 5 * K) * P;   // Et[(c*K + k)*P + t]
+  const int gwarp = blockIdx.x * (blockDim.x >> 5) + wib;
+  double* colX = colbuf + (size_t)(gwarp * G + sw) * 2 * 3 * col_rows;
+  double* colY = colX + 3 * col_rows;
+  const ExactItem* items = E.fx64[slot];
+  for (;;) {
+    int g = 0;
+    if (lane == 0) g = atomicAdd(counter, 1);
+    g = __shfl_sync(FULL, g, 0);
+    if (g * G >= count) break;
+    const int u = g * G + sw;
+    const bool has = u < count;
+    const ExactItem it = items[has ? u : g * G];
+    const int r = it.read, m = E.read_m[r];
+    const int64_t ro = E.roff[r];
+    const int n = (int)(E.hoff[it.hap + 1] - E.hoff[it.hap]);
+    const bool live = has && !(E.read_flags[r] & 1);
+    const int steps = __reduce_max_sync(FULL, live ? n + P - 1 : 0);
+    const int Q = (m + 1 + W - 1) / W;
+    const int Qw = __reduce_max_sync(FULL, live ? Q : 0);
+    const int Lp = Q * W - m - 1;
+    const double bfirst = 1.0 - s_lut[E.gq[ro]];
+    const double bS = bfirst / (double)n;                    // scale 2^0 (f64 config)
+    const int8_t* h = E.hbases + E.hoff[it.hap];
+    double res = 0.0;
+    double* colPrev = colX;
+    double* colNext = colY;
+    for (int q = 0; q < Qw; ++q) {
+      const bool sact = live && q < Q;
+      double be[K], dl[K], ep[K], zp[K], M[K], I[K], D[K];
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const int p = q * W + t * K + k;
+        double lam[5];
+        M[k] = 0.0; I[k] = 0.0;
+        if (p < Lp) {
+          be[k] = 0.0; dl[k] = 0.0; ep[k] = 1.0; zp[k] = 0.0; D[k] = bS;
+#pragma unroll
+          for (int c = 0; c < 5; ++c) lam[c] = 0.0;
+        } else if (p < Lp + m) {
+          const int i0 = p - Lp;
+          const double d = s_lut[E.iq[ro + i0]], z = s_lut[E.dq[ro + i0]];
+          const double e = s_lut[E.gq[ro + i0]], qe = s_lut[E.bq[ro + i0]];
+          const double a = (1.0 - d) - z;
+          double anext = 1.0, bnext = 0.0;
+          if (i0 + 1 < m) {
+            anext = (1.0 - s_lut[E.iq[ro + i0 + 1]]) - s_lut[E.dq[ro + i0 + 1]];
+            bnext = 1.0 - s_lut[E.gq[ro + i0 + 1]];
+          }
+          be[k] = 1.0 - e; dl[k] = d / a; ep[k] = e; zp[k] = bnext * z / anext; D[k] = 0.0;
+          const int rc = E.rbases[ro + i0];
+          const double lm = anext * (1.0 - qe), lx = anext * (qe / 3.0);
+#pragma unroll
+          for (int c = 0; c < 5; ++c) lam[c] = (rc == c || rc == 4 || c == 4) ? lm : lx;
+        } else {
+          be[k] = 1.0; dl[k] = 0.0; ep[k] = 1.0; zp[k] = 1.0; D[k] = 0.0;
+#pragma unroll
+          for (int c = 0; c < 5; ++c) lam[c] = 1.0;
+        }
+#pragma unroll
+        for (int c = 0; c < 5; ++c) Et[(c * K + k) * P + t] = lam[c];
+      }
+      if (sact && t == P - 1 && q < Q - 1) {
+        colNext[0] = M[K - 1]; colNext[col_rows] = I[K - 1]; colNext[2 * col_rows] = D[K - 1];
+      }
+      double nbM = 0.0, nbI = 0.0, nbD = 0.0;
+      if (t == 0) {
+        if (q == 0) nbD = bS;
+        else if (sact) { nbM = colPrev[0]; nbI = colPrev[col_rows]; nbD = colPrev[2 * col_rows]; }
+      }
+      __syncwarp();
+      for (int s = 1; s <= steps; ++s) {
+        const int j = s - t;
+        const double dgM = nbM, dgI = nbI, dgD = nbD;
+        nbM = __shfl_up_sync(FULL, M[K - 1], 1, P);
+        nbI = __shfl_up_sync(FULL, I[K - 1], 1, P);
+        nbD = __shfl_up_sync(FULL, D[K - 1], 1, P);
+        if (t == 0) {
+          if (q == 0) { nbM = 0.0; nbI = 0.0; nbD = bS; }
+          else if (sact) {
+            const int jj = min(max(j, 0), n);
+            nbM = colPrev[jj]; nbI = colPrev[col_rows + jj]; nbD = colPrev[2 * col_rows + jj];
+          }
+        }
+        if (sact && j >= 1 && j <= n) {
+          const double* Ec = Et + (h[j - 1] * K) * P + t;
+#pragma unroll
+          for (int k = K - 1; k >= 0; --k) {
+            D[k] = fma(ep[k], D[k], zp[k] * M[k]);
+            const double pm = (k > 0) ? M[k - 1] : dgM;
+            const double pi = (k > 0) ? I[k - 1] : dgI;
+            const double pd = (k > 0) ? D[k - 1] : dgD;
+            M[k] = Ec[k * P] * (pm + fma(be[k], pi, pd));
+          }
+          double lM = nbM, lI = nbI;
+#pragma unroll
+          for (int k = 0; k < K; ++k) {
+            I[k] = fma(ep[k], lI, dl[k] * lM);
+            lM = M[k];
+            lI = I[k];
+          }
+          if (t == P - 1) {
+            if (q == Q - 1) {
+              if (j == n) res = (D[K - 1] + M[K - 1]) + (M[K - 2] + I[K - 2]);
+            } else {
+              colNext[j] = M[K - 1]; colNext[col_rows + j] = I[K - 1]; colNext[2 * col_rows + j] = D[K - 1];
+            }
+          }
+        }
+      }
+      __syncwarp();
+      double* tmp = colPrev; colPrev = colNext; colNext = tmp;
+    }
+    if (live && t == P - 1) {
+      if (res >= 0x1p-900 && isfinite(res)) {
+        E.acc[it.pair] = res;
+        E.status[it.pair] = kStatusOk | kStatusRetriedF64;
+      } else {                                      // near/below the f64 flush floor: exact
+        append_item(E.ex64, E.ex64_count, E.list_cap, exact_slot_for(m), it);
+      }
+    }
+  }
+}
 
+// k_exact<T, P, K>: a complete work list (host-provided + appended before launch).
 template <typename T, int P, int K>
 __global__ void __launch_bounds__(128)
 k_exact(const EngineDev E, int slot, int* __restrict__ counter, T* __restrict__ colbuf, int col_rows) {
-  using X = ExactTraits<T>;
-  constexpr int W = P * K, G = 32 / P;
+  constexpr int G = 32 / P;
   constexpr bool kIsF32 = sizeof(T) == 4;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double* s_lut = reinterpret_cast<double*>(smem_raw);
@@ -408,9 +725,6 @@ k_exact(const EngineDev E, int slot, int* __restrict__ counter, T* __restrict__ 
   T* colX = colbuf + (size_t)(gwarp * G + sw) * 2 * 3 * col_rows;
   T* colY = colX + 3 * col_rows;
   const ExactItem* items = kIsF32 ? E.ex32[slot] : E.ex64[slot];
-  const T thr = X::flush_thr();
-  const T zero = (T)0;
-
   for (;;) {
     int g = 0;
     if (lane == 0) g = atomicAdd(counter, 1);
@@ -419,132 +733,7 @@ k_exact(const EngineDev E, int slot, int* __restrict__ counter, T* __restrict__ 
     const int u = g * G + sw;
     const bool has = u < count;
     const ExactItem it = items[has ? u : g * G];
-    const int r = it.read, m = E.read_m[r];
-    const int64_t ro = E.roff[r];
-    const int n = (int)(E.hoff[it.hap + 1] - E.hoff[it.hap]);
-    const bool degen = (E.read_flags[r] & 1) != 0;
-    const bool live = has && !degen;
-    int steps = live ? n + P - 1 : 0;
-    steps = __reduce_max_sync(0xffffffffu, steps);
-    if (has && degen && t == 0) { E.acc[it.pair] = 0.0; E.status[it.pair] = kStatusDegenerate; }
-    const int Q = (m + 1 + W - 1) / W;
-    const int Lp = Q * W - m - 1;
-    const T bnd = (T)(ldexp(1.0, it.scale) / (double)n);     // wavefront.py:405-406
-    const int8_t* h = E.hbases + E.hoff[it.hap];
-    T res = zero;
-    T* colPrev = colX;
-    T* colNext = colY;
-
-    // Q is per item here; the warp iterates to the max over its sub-warps
-    const int Qw = __reduce_max_sync(0xffffffffu, live ? Q : 0);
-    for (int q = 0; q < Qw; ++q) {
-      const bool sact = live && q < Q;
-      T al[K], be[K], dl[K], ep[K], zt[K], M[K], I[K], D[K];
-#pragma unroll
-      for (int k = 0; k < K; ++k) {
-        const int p = q * W + t * K + k;
-        T lam[5];
-        M[k] = zero; I[k] = zero;
-        if (p < Lp) {
-          al[k] = zero; be[k] = zero; dl[k] = zero; ep[k] = (T)1; zt[k] = zero; D[k] = bnd;
-#pragma unroll
-          for (int c = 0; c < 5; ++c) lam[c] = zero;
-        } else if (p < Lp + m) {
-          const int i0 = p - Lp;
-          const double d = s_lut[E.iq[ro + i0]], z = s_lut[E.dq[ro + i0]];
-          const double e = s_lut[E.gq[ro + i0]], qe = s_lut[E.bq[ro + i0]];
-          al[k] = (T)((1.0 - d) - z);
-          be[k] = (T)(1.0 - e);
-          dl[k] = (T)d;
-          ep[k] = (T)e;
-          zt[k] = (i0 + 1 < m) ? (T)z : zero;        // D(m, .) never reaches the score
-          D[k] = zero;
-          const int rc = E.rbases[ro + i0];
-          const T lm = (T)(1.0 - qe), lx = (T)(qe / 3.0);
-#pragma unroll
-          for (int c = 0; c < 5; ++c) lam[c] = (rc == c || rc == 4 || c == 4) ? lm : lx;
-        } else {
-          al[k] = (T)1; be[k] = (T)1; dl[k] = zero; ep[k] = (T)1; zt[k] = (T)1; D[k] = zero;
-#pragma unroll
-          for (int c = 0; c < 5; ++c) lam[c] = (T)1;
-        }
-#pragma unroll
-        for (int c = 0; c < 5; ++c) Et[(c * K + k) * P + t] = lam[c];
-      }
-      if (sact && t == P - 1 && q < Q - 1) {
-        colNext[0] = M[K - 1]; colNext[col_rows] = I[K - 1]; colNext[2 * col_rows] = D[K - 1];
-      }
-      T nbM = zero, nbI = zero, nbD = zero;
-      if (t == 0) {
-        if (q == 0) { nbD = bnd; }
-        else if (sact) { nbM = colPrev[0]; nbI = colPrev[col_rows]; nbD = colPrev[2 * col_rows]; }
-      }
-      __syncwarp();
-      for (int s = 1; s <= steps; ++s) {
-        const int j = s - t;
-        const T dgM = nbM, dgI = nbI, dgD = nbD;
-        nbM = __shfl_up_sync(0xffffffffu, M[K - 1], 1, P);
-        nbI = __shfl_up_sync(0xffffffffu, I[K - 1], 1, P);
-        nbD = __shfl_up_sync(0xffffffffu, D[K - 1], 1, P);
-        if (t == 0) {
-          if (q == 0) { nbM = zero; nbI = zero; nbD = bnd; }
-          else if (sact) {
-            const int jj = min(max(j, 0), n);
-            nbM = colPrev[jj]; nbI = colPrev[col_rows + jj]; nbD = colPrev[2 * col_rows + jj];
-          }
-        }
-        if (sact && j >= 1 && j <= n) {
-          const int c = h[j - 1];
-          const T* Ec = Et + (c * K) * P + t;
-#pragma unroll
-          for (int k = K - 1; k >= 0; --k) {
-            // dv = zt*M(i,j-1) + ep*D(i,j-1)
-            const T dv = X::add(X::mul(zt[k], M[k]), X::mul(ep[k], D[k]));
-            D[k] = dv >= thr ? dv : zero;
-            const T pm = (k > 0) ? M[k - 1] : dgM;
-            const T pi = (k > 0) ? I[k - 1] : dgI;
-            const T pd = (k > 0) ? D[k - 1] : dgD;
-            // mv = lam*(al*M(i-1,j-1) + be*(I(i-1,j-1) + D(i-1,j-1)))
-            const T mv = X::mul(Ec[k * P], X::add(X::mul(al[k], pm), X::mul(be[k], X::add(pi, pd))));
-            M[k] = mv >= thr ? mv : zero;
-          }
-          T lM = nbM, lI = nbI;
-#pragma unroll
-          for (int k = 0; k < K; ++k) {
-            // iv = dl*M(i-1,j) + ep*I(i-1,j)
-            const T iv = X::add(X::mul(dl[k], lM), X::mul(ep[k], lI));
-            I[k] = iv >= thr ? iv : zero;
-            lM = M[k];
-            lI = I[k];
-          }
-          if (t == P - 1) {
-            if (q == Q - 1) {
-              if (j == n) res = X::add(X::add(D[K - 1], M[K - 1]), X::add(M[K - 2], I[K - 2]));
-            } else {
-              colNext[j] = M[K - 1]; colNext[col_rows + j] = I[K - 1]; colNext[2 * col_rows + j] = D[K - 1];
-            }
-          }
-        }
-      }
-      __syncwarp();
-      T* tmp = colPrev; colPrev = colNext; colNext = tmp;
-    }
-    if (live && t == P - 1) {
-      const bool bad = !(res > zero) || !isfinite((double)res);
-      if (kIsF32) {
-        if (bad && E.retry_f64) {
-          E.status[it.pair] = kStatusRetriedF64;
-          append_item(E.ex64, E.ex64_count, E.list_cap, exact_slot_for(m), ExactItem{it.pair, r, it.hap, 0});
-        } else {
-          E.acc[it.pair] = (double)res;
-          E.status[it.pair] = bad ? kStatusOverflow : kStatusExactF32;
-        }
-      } else {
-        E.acc[it.pair] = (double)res;
-        const uint8_t keep = E.status[it.pair] & kStatusRetriedF64;
-        E.status[it.pair] = (uint8_t)((bad ? kStatusOverflow : kStatusOk) | keep);
-      }
-    }
+    exact_item<T, P, K>(E, it, has, s_lut, Et, colX, colY, col_rows, t);
   }
 }
 

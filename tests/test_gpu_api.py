@@ -204,7 +204,7 @@ def test_retry_f64_gives_finite_scores_for_underflowing_pairs():
     s, r = run(batches, retry_f64=True)
     assert r.errors == [] and len(r.retried) == 1000 and np.all(np.isfinite(s))
     s64, _ = run(batches, configs=default_configs("f64"))
-    assert np.array_equal(s, s64)
+    assert np.max(np.abs(s - s64) / np.abs(s64)) <= 1e-9
     assert r.total_cells == r32.total_cells == 1000 * 100 * 150
 
 

@@ -4,8 +4,8 @@ Bars (BASELINE.json north_star):
   * exact mode and f64 configs: bit-identical to the reference (same kernel arithmetic);
   * fast FP32 mode: identical numeric-overflow (retry) set, per-pair log10 within
     1e-4 relative (REL_TOL below);
-  * FP64 retry: retried pairs bit-identical to the reference's f64 scores (tolerance
-    1e-9 relative is the stated bar; the exact FP64 kernel meets it with 0 error).
+  * FP64 retry: retried pairs within 1e-9 relative of the reference's f64 scores (the
+    fast FP64 kernel, FMA + folded recurrence); f64 CONFIGS use the bit-exact FP64 kernel.
 Golden fixtures come from the reference itself (tests/golden/make_golden.py); the
 full-size configs are checked against the C oracle, which tests/test_oracle_golden.py
 pins bit-exactly to the reference.
@@ -78,7 +78,6 @@ def test_retry_f64_rescues_exactly_the_reference_flag_set(engine, name):
     assert np.array_equal(np.isfinite(got), fin)
     if fin.any():
         assert _rel(got[fin], want[fin]).max() <= RETRY_REL_TOL
-        assert np.array_equal(got[fin], want[fin])          # exact FP64 kernel: bit-identical
     rest = ~retried
     _check_fast(scores[rest], status[rest], z["ref_f32"][rest], z["ref_f32_kind"][rest], name)
 
@@ -102,7 +101,7 @@ def test_full_size_configs_against_oracle(engine, wl, batches):
         ref64 = oracle.finish(acc64, st64, 0)
         assert np.array_equal(status[idx] & KIND, st64)
         fin = st64 == 0
-        assert np.array_equal(scores[idx][fin], ref64[fin])
+        assert _rel(scores[idx][fin], ref64[fin]).max() <= RETRY_REL_TOL
     assert stats.total_cells == int((flat.read_len[flat.pair_index()[0]]
                                      * flat.hap_len[flat.pair_index()[1]]).sum())
 
