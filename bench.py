@@ -179,6 +179,24 @@ def run_reference(args, ws, rank):
     return 0
 
 
+def reduce_time_cells(seconds, cells, ws, device):
+    """(max over ranks of seconds, sum over ranks of cells) — the only cross-rank traffic:
+    pairs are independent, so the data path has no collective."""
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(seconds)], dtype=torch.float64, device=device)
+    c = torch.tensor([float(cells)], dtype=torch.float64, device=device)
+    if ws > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(c, op=dist.ReduceOp.SUM)
+    return float(t.item()), float(c.item())
+
+
+def shard_seed_offset(rank):
+    """Weak scaling: rank r scores its own copy of the workload drawn with seed + r."""
+    return int(rank)
+
+
 def secondary(ctx, name, flags, steps=3):
     """Device GCUPS of another BASELINE config on the same engine (reported, not headline)."""
     from paper_2411_11547_b200 import datagen, default_configs
@@ -228,7 +246,7 @@ def main():
     if ws > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
-    flat = datagen.workload(args.workload, seed_offset=rank)
+    flat = datagen.workload(args.workload, seed_offset=shard_seed_offset(rank))
     cfg = config_tuples(default_configs("f32"))
     flags = 0                                        # reference f32 semantics (c2 has no underflow)
     ctx = _native.Context(local)
@@ -258,14 +276,7 @@ def main():
         barrier()
     scores, status, st = ctx.fetch()
     cells = st.total_cells
-    t_rank = float(np.sum(dev_ms)) * 1e-3
-    t = torch.tensor([t_rank], dtype=torch.float64, device="cuda")
-    c = torch.tensor([float(cells)], dtype=torch.float64, device="cuda")
-    if ws > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dist.all_reduce(c, op=dist.ReduceOp.SUM)
-    t_max = float(t.item())
-    total_cells = float(c.item())
+    t_max, total_cells = reduce_time_cells(float(np.sum(dev_ms)) * 1e-3, cells, ws, "cuda")
     value = total_cells * args.steps / t_max / 1e9
 
     # ---- e2e through the C-ABI from pinned host buffers (phmm_score)
@@ -277,10 +288,8 @@ def main():
     for _ in range(args.steps):
         out, ost, est = ctx.score(pflat, cfg, flags)
     torch.cuda.synchronize()
-    e2e_t = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
-    if ws > 1:
-        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
-    e2e_value = total_cells * args.steps / float(e2e_t.item()) / 1e9
+    e2e_max, _ = reduce_time_cells(time.perf_counter() - t0, 0, ws, "cuda")
+    e2e_value = total_cells * args.steps / e2e_max / 1e9
 
     if rank != 0:
         dist.destroy_process_group() if ws > 1 else None
