@@ -81,6 +81,35 @@ const void* kFastFn[2 * kNumFastGeoms] = {FASTFN(4, 4),   FASTFN(4, 8),   FASTFN
                                           FASTFN(32, 16)};
 #undef FASTFN
 
+// streaming kernel (single-stripe reads): same geometry table as k_fast
+template <int P, int K>
+void launch_stream(dim3 g, size_t smem, cudaStream_t s, const EngineDev& E, const StreamUnit* u,
+                   const StreamHap* h, int nu, int* ctr) {
+  k_stream<P, K><<<g, kThreads, smem, s>>>(E, u, h, nu, ctr);
+}
+typedef void (*StreamLaunch)(dim3, size_t, cudaStream_t, const EngineDev&, const StreamUnit*, const StreamHap*,
+                             int, int*);
+const StreamLaunch kStreamLaunch[kNumFastGeoms] = {
+    launch_stream<4, 4>,   launch_stream<4, 8>,   launch_stream<4, 12>, launch_stream<4, 16>,
+    launch_stream<8, 8>,   launch_stream<8, 12>,  launch_stream<8, 16>, launch_stream<16, 8>,
+    launch_stream<16, 12>, launch_stream<16, 16>, launch_stream<32, 8>, launch_stream<32, 12>,
+    launch_stream<32, 16>};
+const void* kStreamFn[kNumFastGeoms] = {
+    (const void*)k_stream<4, 4>,   (const void*)k_stream<4, 8>,   (const void*)k_stream<4, 12>,
+    (const void*)k_stream<4, 16>,  (const void*)k_stream<8, 8>,   (const void*)k_stream<8, 12>,
+    (const void*)k_stream<8, 16>,  (const void*)k_stream<16, 8>,  (const void*)k_stream<16, 12>,
+    (const void*)k_stream<16, 16>, (const void*)k_stream<32, 8>,  (const void*)k_stream<32, 12>,
+    (const void*)k_stream<32, 16>};
+const int kStreamOcc[kNumFastGeoms] = {StreamOcc<4>::value,  StreamOcc<8>::value,  StreamOcc<12>::value,
+                                       StreamOcc<16>::value, StreamOcc<8>::value,  StreamOcc<12>::value,
+                                       StreamOcc<16>::value, StreamOcc<8>::value,  StreamOcc<12>::value,
+                                       StreamOcc<16>::value, StreamOcc<8>::value,  StreamOcc<12>::value,
+                                       StreamOcc<16>::value};
+int stream_cap(int P) {
+  return P == 4 ? StreamCap<4>::value : P == 8 ? StreamCap<8>::value : P == 16 ? StreamCap<16>::value
+                                                                             : StreamCap<32>::value;
+}
+
 template <typename T, int P>
 void launch_exact(dim3 g, size_t smem, cudaStream_t s, const EngineDev& E, int slot, int* ctr, void* col,
                   int rows) {
@@ -110,6 +139,9 @@ int exact_slot_host(int m) { return (m + 1 <= 32) ? 0 : (m + 1 <= 64) ? 1 : (m +
 size_t fast_smem(int geom) {
   const FastGeom g = kFastGeoms[geom];
   return 96 * sizeof(double) + (size_t)(kThreads / 32) * (32 / g.P) * 5 * g.K * g.P * sizeof(float);
+}
+size_t stream_smem(int geom) {
+  return fast_smem(geom) + kStreamCodeBytesPerCta;
 }
 size_t exact_smem(int slot, size_t tsize) {
   const int P = kExactP[slot];
@@ -154,6 +186,36 @@ int choose_geom(int m, int nmax, int* Qout) {
   return bi;
 }
 
+// Streaming tiling for a read of length m whose batch has haplotype lengths summing to
+// `total` (longest `nmax`): units of two lanes of ~total/2 rows, split when a lane would
+// exceed the geometry's row-code capacity.  -1: no single-stripe streaming geometry.
+int choose_stream_geom(int m, int64_t total, int nmax) {
+  const int fg = forced_geom();
+  double best = 1e300;
+  int bi = -1;
+  for (int g = 0; g < kNumFastGeoms; ++g) {
+    if (fg >= 0 && g != fg) continue;
+    const int P = kFastGeoms[g].P, K = kFastGeoms[g].K, W = P * K;
+    if (m + 1 > W) continue;
+    const int cap = stream_cap(P);
+    if (nmax > cap) continue;
+    const double units = std::ceil((double)total / (2.0 * cap));
+    const double rows = std::min<double>(cap, std::ceil((double)total / (2.0 * units)));
+    const double cost = units * P * (K + 2.5) * (rows + P - 1);
+    if (cost < best - 1e-9) { best = cost; bi = g; }
+  }
+  return bi;
+}
+
+bool streaming_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* env = getenv("PHMM_NO_STREAM");
+    v = (env && env[0] == '1') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 }  // namespace
 
 struct phmm_ctx {
@@ -162,6 +224,9 @@ struct phmm_ctx {
   cudaStream_t stream = nullptr;
   cudaEvent_t ev_start = nullptr, ev_fast0 = nullptr, ev_fast1 = nullptr, ev_end = nullptr;
   cudaEvent_t ev_pre = nullptr;
+  static constexpr int kAux = 4;              // side streams: fast-kernel bins run concurrently
+  cudaStream_t aux[kAux] = {};
+  cudaEvent_t ev_join[kAux] = {};
   std::string err;
   std::vector<double> lut;
 
@@ -173,6 +238,8 @@ struct phmm_ctx {
   DBuf<float> d_gsum;
   DBuf<double> d_lut, d_acc;
   DBuf<FastUnit> d_units;
+  DBuf<StreamUnit> d_sunits;
+  DBuf<StreamHap> d_shaps;
   DBuf<ExactItem> d_ex32[kNumExactP], d_ex64[kNumExactP], d_fx64[kNumExactP];
   DBuf<float2> d_colf;
   DBuf<double> d_cold;
@@ -185,6 +252,13 @@ struct phmm_ctx {
   std::vector<int64_t> batch_read_off, batch_hap_off, hap_len;
   std::vector<int> read_m, read_scale, read_cfg;   // read_cfg -1 = too small
   std::vector<Bin> bins;
+  struct SBin {
+    int geom;
+    std::vector<StreamUnit> units;
+    int64_t dev_off = 0;
+  };
+  std::vector<SBin> sbins;
+  std::vector<StreamHap> shaps;
   int host_ex32[kNumExactP] = {0, 0, 0, 0}, host_ex64[kNumExactP] = {0, 0, 0, 0};
   int max_n = 1;
   int flags = 0;
@@ -243,6 +317,10 @@ int phmm_create(phmm_ctx** out, int device, const double* phred_lut) {
   ctx->num_sms = prop.multiProcessorCount;
   CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
   CK(cudaEventCreateWithFlags(&ctx->ev_pre, cudaEventDisableTiming));
+  for (int a = 0; a < phmm_ctx::kAux; ++a) {
+    CK(cudaStreamCreateWithFlags(&ctx->aux[a], cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&ctx->ev_join[a], cudaEventDisableTiming));
+  }
   CK(cudaEventCreate(&ctx->ev_start));
   CK(cudaEventCreate(&ctx->ev_fast0));
   CK(cudaEventCreate(&ctx->ev_fast1));
@@ -252,6 +330,8 @@ int phmm_create(phmm_ctx** out, int device, const double* phred_lut) {
   CK(cudaMemcpy(ctx->d_lut.p, ctx->lut.data(), 94 * sizeof(double), cudaMemcpyHostToDevice));
   for (int g = 0; g < 2 * kNumFastGeoms; ++g)
     CK(cudaFuncSetAttribute(kFastFn[g], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fast_smem(g / 2)));
+  for (int g = 0; g < kNumFastGeoms; ++g)
+    CK(cudaFuncSetAttribute(kStreamFn[g], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)stream_smem(g)));
   for (int s = 0; s < kNumExactP; ++s) {
     CK(cudaFuncSetAttribute(kExact32Fn[s], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)exact_smem(s, 4)));
     CK(cudaFuncSetAttribute(kExact64Fn[s], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)exact_smem(s, 8)));
@@ -268,7 +348,7 @@ int phmm_destroy(phmm_ctx* ctx) {
   ctx->d_dq.release(); ctx->d_gq.release(); ctx->d_status.release(); ctx->d_rflags.release();
   ctx->d_roff.release(); ctx->d_hoff.release(); ctx->d_read_m.release(); ctx->d_read_scale.release();
   ctx->d_read_ncap.release(); ctx->d_counters.release(); ctx->d_gsum.release(); ctx->d_lut.release();
-  ctx->d_acc.release(); ctx->d_units.release(); ctx->d_colf.release(); ctx->d_cold.release();
+  ctx->d_acc.release(); ctx->d_units.release(); ctx->d_sunits.release(); ctx->d_shaps.release(); ctx->d_colf.release(); ctx->d_cold.release();
   for (int s = 0; s < kNumExactP; ++s) { ctx->d_ex32[s].release(); ctx->d_ex64[s].release(); ctx->d_fx64[s].release(); }
   if (ctx->h_counts) cudaFreeHost(ctx->h_counts);
   ctx->h_counts = nullptr;
@@ -277,6 +357,10 @@ int phmm_destroy(phmm_ctx* ctx) {
   if (ctx->ev_fast1) cudaEventDestroy(ctx->ev_fast1);
   if (ctx->ev_end) cudaEventDestroy(ctx->ev_end);
   if (ctx->ev_pre) cudaEventDestroy(ctx->ev_pre);
+  for (int a = 0; a < phmm_ctx::kAux; ++a) {
+    if (ctx->aux[a]) { cudaStreamSynchronize(ctx->aux[a]); cudaStreamDestroy(ctx->aux[a]); }
+    if (ctx->ev_join[a]) cudaEventDestroy(ctx->ev_join[a]);
+  }
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
   return PHMM_SUCCESS;
@@ -365,7 +449,11 @@ int phmm_prepare(phmm_ctx* ctx, const phmm_input* in, const phmm_options* opt, i
   ctx->num_pairs = N;
   const bool exact_mode = (opt->flags & PHMM_FLAG_EXACT) != 0;
   ctx->bins.clear();
+  ctx->sbins.clear();
+  ctx->shaps.clear();
+  const bool use_stream = streaming_enabled();
   std::vector<int> bin_index(kNumFastGeoms * 64, -1);
+  std::vector<int> sbin_index(kNumFastGeoms, -1);
   std::vector<ExactItem> host32[kNumExactP], host64[kNumExactP];
   int max_n = 1;
   int64_t gid = 0;
@@ -375,7 +463,11 @@ int phmm_prepare(phmm_ctx* ctx, const phmm_input* in, const phmm_options* opt, i
     const int64_t h0 = ctx->batch_hap_off[b], h1 = ctx->batch_hap_off[b + 1];
     const int64_t nh = h1 - h0;
     int ncap = 1;
-    for (int64_t h = h0; h < h1; ++h) ncap = (int)std::max<int64_t>(ncap, ctx->hap_len[h]);
+    int64_t batch_total = 0;
+    for (int64_t h = h0; h < h1; ++h) {
+      ncap = (int)std::max<int64_t>(ncap, ctx->hap_len[h]);
+      batch_total += ctx->hap_len[h];
+    }
     max_n = std::max(max_n, ncap);
     hidx.resize(nh);
     std::iota(hidx.begin(), hidx.end(), (int)h0);
@@ -393,6 +485,45 @@ int phmm_prepare(phmm_ctx* ctx, const phmm_input* in, const phmm_options* opt, i
           (f64 ? host64 : host32)[exact_slot_host(m)].push_back(it);
         }
         continue;
+      }
+      if (use_stream) {
+        const int sg = choose_stream_geom(m, batch_total, ncap);
+        if (sg >= 0) {
+          // greedy LPT over the length-sorted haplotypes: each to the lighter lane; a new
+          // unit when the lane would exceed the geometry's row capacity
+          const int cap = stream_cap(kFastGeoms[sg].P);
+          int key = sg;
+          if (sbin_index[key] < 0) {
+            sbin_index[key] = (int)ctx->sbins.size();
+            ctx->sbins.push_back(phmm_ctx::SBin{sg, {}, 0});
+          }
+          auto& sb = ctx->sbins[sbin_index[key]];
+          std::vector<int> lanes[2];
+          int rows[2] = {0, 0};
+          auto flush = [&]() {
+            if (lanes[0].empty() && lanes[1].empty()) return;
+            StreamUnit su;
+            su.read = (int)r;
+            su.list = (int)ctx->shaps.size();
+            su.cntA = (int)lanes[0].size(); su.cntB = (int)lanes[1].size();
+            su.rowsA = rows[0]; su.rowsB = rows[1];
+            su.pad0 = su.pad1 = 0;
+            for (int ln = 0; ln < 2; ++ln)
+              for (int h : lanes[ln]) ctx->shaps.push_back(StreamHap{h, (int)(gid + (h - h0))});
+            sb.units.push_back(su);
+            lanes[0].clear(); lanes[1].clear(); rows[0] = rows[1] = 0;
+          };
+          for (int64_t x = 0; x < nh; ++x) {
+            const int h = hidx[x];
+            const int n = (int)ctx->hap_len[h];
+            int ln = rows[0] <= rows[1] ? 0 : 1;
+            if (rows[ln] + n > cap || (int)lanes[ln].size() >= kStreamMaxLaneHaps) { flush(); ln = 0; }
+            lanes[ln].push_back(h);
+            rows[ln] += n;
+          }
+          flush();
+          continue;
+        }
       }
       for (int64_t x = 0; x < nh; x += 2) {
         const int ha = hidx[x], hb = (x + 1 < nh) ? hidx[x + 1] : hidx[x];
@@ -423,6 +554,14 @@ int phmm_prepare(phmm_ctx* ctx, const phmm_input* in, const phmm_options* opt, i
     bn.dev_off = nunits;
     nunits += (int64_t)bn.units.size();
   }
+  int64_t nsunits = 0;
+  for (auto& sb : ctx->sbins) {
+    std::stable_sort(sb.units.begin(), sb.units.end(), [](const StreamUnit& a, const StreamUnit& c) {
+      return std::max(a.rowsA, a.rowsB) > std::max(c.rowsA, c.rowsB);
+    });
+    sb.dev_off = nsunits;
+    nsunits += (int64_t)sb.units.size();
+  }
   auto t1 = std::chrono::steady_clock::now();
   ctx->plan_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
 
@@ -450,11 +589,16 @@ int phmm_prepare(phmm_ctx* ctx, const phmm_input* in, const phmm_options* opt, i
   allu.reserve(nunits);
   for (auto& bn : ctx->bins) allu.insert(allu.end(), bn.units.begin(), bn.units.end());
   CK(up(ctx->d_units, allu.data(), allu.size()));
+  std::vector<StreamUnit> alls;
+  alls.reserve(nsunits);
+  for (auto& sb : ctx->sbins) alls.insert(alls.end(), sb.units.begin(), sb.units.end());
+  CK(up(ctx->d_sunits, alls.data(), alls.size()));
+  CK(up(ctx->d_shaps, ctx->shaps.data(), ctx->shaps.size()));
   CK(ctx->d_gsum.ensure(R));
   CK(ctx->d_rflags.ensure(R));
   CK(ctx->d_acc.ensure(N));
   CK(ctx->d_status.ensure(N));
-  CK(ctx->d_counters.ensure(32 + ctx->bins.size()));
+  CK(ctx->d_counters.ensure(32 + ctx->bins.size() + ctx->sbins.size()));
   ctx->list_cap = (int)std::max<int64_t>(N, 1);
   for (int s = 0; s < kNumExactP; ++s) {
     ctx->host_ex32[s] = (int)host32[s].size();
@@ -530,7 +674,8 @@ int phmm_execute(phmm_ctx* ctx) {
   for (int s = 0; s < kNumExactP; ++s) { hc[s] = ctx->host_ex32[s]; hc[kNumExactP + s] = ctx->host_ex64[s]; }
   CK(cudaEventRecord(ctx->ev_start, st));
   CK(cudaMemcpyAsync(ctx->d_counters.p, hc, 32 * sizeof(int), cudaMemcpyHostToDevice, st));
-  if (nb > 0) CK(cudaMemsetAsync(ctx->d_counters.p + 32, 0, nb * sizeof(int), st));
+  const int nsb = (int)ctx->sbins.size();
+  if (nb + nsb > 0) CK(cudaMemsetAsync(ctx->d_counters.p + 32, 0, (nb + nsb) * sizeof(int), st));
   if (N > 0) CK(cudaMemsetAsync(ctx->d_status.p, 0, N, st));
   if (ctx->num_reads > 0) {
     const int threads = 128;
@@ -540,13 +685,40 @@ int phmm_execute(phmm_ctx* ctx) {
   }
   CK(cudaEventRecord(ctx->ev_pre, st));
   CK(cudaEventRecord(ctx->ev_fast0, st));
+  // Fast-kernel bins (one persistent launch per tiling) go round-robin onto side streams
+  // so a bin's tail (its last CTAs draining) overlaps the next bin's work.
+  int nlaunch = 0;
+  // legacy k_fast bins share the boundary-column scratch: they stay serialized on the last
+  // side stream; streaming bins rotate over the others
+  constexpr int kStreamAux = phmm_ctx::kAux - 1;
+  auto side = [&](int i) -> cudaStream_t { return ctx->aux[i % kStreamAux]; };
+  bool used[phmm_ctx::kAux] = {};
+  for (int a = 0; a < phmm_ctx::kAux; ++a) CK(cudaStreamWaitEvent(ctx->aux[a], ctx->ev_pre, 0));
+  for (int bi = 0; bi < nsb; ++bi) {
+    const auto& sb = ctx->sbins[bi];
+    const int nu = (int)sb.units.size();
+    if (nu == 0) continue;
+    const int G = 32 / kFastGeoms[sb.geom].P;
+    const int groups = (nu + G - 1) / G;
+    const int blk = std::max(1, std::min(ctx->num_sms * kStreamOcc[sb.geom], (groups + 3) / 4));
+    used[nlaunch % kStreamAux] = true;
+    kStreamLaunch[sb.geom](dim3(blk), stream_smem(sb.geom), side(nlaunch++), E, ctx->d_sunits.p + sb.dev_off,
+                           ctx->d_shaps.p, nu, ctx->d_counters.p + 32 + nb + bi);
+    ++launches;
+  }
   for (int bi = 0; bi < nb; ++bi) {
     const Bin& bn = ctx->bins[bi];
     const int nu = (int)bn.units.size();
     if (nu == 0) continue;
-    kFastLaunch[bn.geom](dim3(blocks[bi]), fast_smem(bn.geom), st, E, ctx->d_units.p + bn.dev_off, nu, bn.Q,
-                         ctx->d_counters.p + 32 + bi, ctx->d_colf.p, ctx->max_n + 1);
+    used[phmm_ctx::kAux - 1] = true;
+    kFastLaunch[bn.geom](dim3(blocks[bi]), fast_smem(bn.geom), ctx->aux[phmm_ctx::kAux - 1], E, ctx->d_units.p + bn.dev_off, nu,
+                         bn.Q, ctx->d_counters.p + 32 + bi, ctx->d_colf.p, ctx->max_n + 1);
     ++launches;
+  }
+  for (int a = 0; a < phmm_ctx::kAux; ++a) {
+    if (!used[a]) continue;
+    CK(cudaEventRecord(ctx->ev_join[a], ctx->aux[a]));
+    CK(cudaStreamWaitEvent(st, ctx->ev_join[a], 0));
   }
   CK(cudaGetLastError());
   CK(cudaEventRecord(ctx->ev_fast1, st));
@@ -642,6 +814,10 @@ int phmm_fetch(phmm_ctx* ctx, double* out_log10, uint8_t* out_status, phmm_stats
     for (auto& bn : ctx->bins) {
       const FastGeom g = kFastGeoms[bn.geom];
       for (auto& u : bn.units) comp += 2LL * bn.Q * g.P * g.K * (std::max(u.nA, u.nB) + g.P - 1);
+    }
+    for (auto& sb : ctx->sbins) {
+      const FastGeom g = kFastGeoms[sb.geom];
+      for (auto& u : sb.units) comp += 2LL * g.P * g.K * (std::max(u.rowsA, u.rowsB) + g.P - 1);
     }
     stats->computed_cells = comp;
     stats->fast_pairs = fast;

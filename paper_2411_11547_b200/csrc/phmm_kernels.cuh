@@ -137,9 +137,10 @@ __device__ __forceinline__ float comp(const float4& v, int i) {
 //                                   in log10 at |score| > 52: < 1e-5 relative)
 //   score > -1.5 (short pairs)   -> bit-exact kernel (relative tolerance near log10 = 0)
 //   otherwise                    -> accept
-__device__ __forceinline__ bool fast_finish(const EngineDev& E, float a, int pair, int read, int hap,
-                                            int n, int m, int scale) {
-  const float bound = 0x1p-80f * (float)n * E.read_gsum[read];   // 2^10 * 2^-90
+__device__ __forceinline__ bool fast_finish_g(const EngineDev& E, float a, int pair, int read, int hap,
+                                              int n, int m, int scale, float gsum, bool allow_inline = false,
+                                              bool band_to_caller = false) {
+  const float bound = 0x1p-80f * (float)n * gsum;                // 2^10 * 2^-90
   const float hi = ldexpf(0.031622776f, scale);                   // 10^-1.5 * 2^scale
   if (!(a >= 0x1p-93f)) {
     if (E.retry_f64) {
@@ -153,7 +154,8 @@ __device__ __forceinline__ bool fast_finish(const EngineDev& E, float a, int pai
     E.status[pair] = kStatusExactF32;
     // guard band: the first band_budget pairs are rerun inline by the finding warp (no
     // tail when they are rare); beyond that they go to the post-pass exact kernels.
-    if (atomicAdd(E.band_inline, 1) < E.band_budget) return true;
+    if (allow_inline && atomicAdd(E.band_inline, 1) < E.band_budget) return true;
+    if (band_to_caller) return true;
     append_item(E.ex32, E.ex32_count, E.list_cap, exact_slot_for(m), ExactItem{pair, read, hap, scale});
   } else {
     E.acc[pair] = (double)a;
@@ -166,6 +168,11 @@ __device__ __forceinline__ bool fast_finish(const EngineDev& E, float a, int pai
 // k_exact<T, P, K>: bit-exact reference recursion (reference.py:106-122,
 // wavefront.py:130-160) — no FMA, per-store flush, j-ordered accumulation.
 // ---------------------------------------------------------------------------------
+__device__ __forceinline__ bool fast_finish(const EngineDev& E, float a, int pair, int read, int hap,
+                                            int n, int m, int scale) {
+  return fast_finish_g(E, a, pair, read, hap, n, m, scale, E.read_gsum[read], true);
+}
+
 template <typename T> struct ExactTraits;
 template <> struct ExactTraits<float> {
   static __device__ __forceinline__ float mul(float a, float b) { return __fmul_rn(a, b); }
@@ -556,6 +563,345 @@ k_fast(const EngineDev E, const FastUnit* __restrict__ units, int num_units, int
                                 ex_col + 3 * col_rows, col_rows, t);
         __syncwarp();
       }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------
+// k_stream<P, K>: read-stationary haplotype streaming (single-stripe reads).
+//
+// A StreamUnit is one read and two LANES of haplotypes (float2 .x = lane A, .y = lane B);
+// each lane is the concatenation of several of the batch's haplotypes, scored one after
+// the other without leaving the wavefront: the read's coefficients and emission table
+// are set up once per unit, and the wavefront's fill/drain (P-1 steps) is paid once per
+// unit instead of once per pair.  Haplotype boundaries travel down the sub-warp with the
+// per-row code (the same shuffle that carries the haplotype characters):
+//   FIRST(lane): the thread's row is row 1 of a new haplotype: its lane state is reset to
+//                row 0 of that pair (M = I = 0, D' = S'/n in the left padding, else 0) and
+//                the diagonal input becomes the matrix boundary;
+//   LAST(lane):  the row is the pair's last: thread P-1 reads the accumulator position and
+//                classifies the result (fast_finish).
+// Rows outside a thread's stream (fill, drain, the shorter lane's tail) compute values
+// that are never read: every pair starts with a FIRST reset.
+// ---------------------------------------------------------------------------------
+struct StreamUnit {                       // 32 B
+  int read;
+  int list;                               // StreamHap entries: lane A [list, list+cntA),
+  int cntA, cntB;                         //                    lane B [list+cntA, +cntB)
+  int rowsA, rowsB;                       // sum of the lane's haplotype lengths
+  int pad0, pad1;
+};
+struct StreamHap { int hap, pair; };
+
+constexpr int kCodeFirst = 8, kCodeLast = 16;          // code byte: base | FIRST | LAST
+constexpr int kStreamCodeBytesPerCta = 32768;          // row-code staging, shared memory
+constexpr int kStreamMaxLaneHaps = 15;                 // haplotypes per lane of one unit
+constexpr int kStreamMaxWin = 2 * (kStreamMaxLaneHaps + 1);
+constexpr int kStreamBandCap = 8;                      // guard-band pairs rerun in-warp per unit
+template <int P> struct StreamCap {                    // max rows per lane of one unit
+  static constexpr int bytes = kStreamCodeBytesPerCta / (4 * (32 / P));
+  static constexpr int value = bytes / 2 - 2;
+};
+template <int K> struct StreamOcc { static constexpr int value = K <= 8 ? 4 : (K <= 12 ? 3 : 2); };
+
+template <int L> __device__ __forceinline__ float& lane_ref(float2& v) { return L == 0 ? v.x : v.y; }
+
+template <int P, int K>
+__global__ void __launch_bounds__(128, StreamOcc<K>::value)
+k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHap* __restrict__ shaps,
+         int num_units, int* __restrict__ counter) {
+  constexpr int W = P * K, G = 32 / P, K4 = K / 4;
+  constexpr int CB = StreamCap<P>::bytes;
+  static_assert(K % 4 == 0 && K >= 4, "K multiple of 4");
+  constexpr unsigned FULL = 0xffffffffu;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* s_lut = reinterpret_cast<double*>(smem_raw);
+  float4* s_E = reinterpret_cast<float4*>(smem_raw + 96 * sizeof(double));
+  unsigned char* s_code = smem_raw + 96 * sizeof(double) + (size_t)4 * G * 5 * K4 * P * sizeof(float4);
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int sw = lane / P, t = lane % P;
+  for (int i = threadIdx.x; i < 94; i += blockDim.x) s_lut[i] = E.lut[i];
+  __syncthreads();
+  float4* Et = s_E + (size_t)((wib * G + sw) * 5 * K4) * P;
+  unsigned char* cd = s_code + (size_t)(wib * G + sw) * CB;
+  const unsigned short* cd16 = reinterpret_cast<const unsigned short*>(cd);
+  const float2 zero2 = make_float2(0.f, 0.f);
+  __shared__ StreamUnit s_unit[4 * G];
+  __shared__ int s_hc[2 * 128];
+  __shared__ int s_win[4 * G * kStreamMaxWin];
+  __shared__ float s_bs[4 * G * 2 * kStreamMaxLaneHaps];
+  __shared__ int s_meta[4 * G * 4];
+  __shared__ ExactItem s_band[4 * G * kStreamBandCap];
+  __shared__ int s_nband[4 * G];
+  __shared__ int s_nwin[4 * G];
+
+  for (;;) {
+    int g = 0;
+    if (lane == 0) g = atomicAdd(counter, 1);
+    g = __shfl_sync(FULL, g, 0);
+    if (g * G >= num_units) break;
+    const int u = g * G + sw;
+    const bool has = u < num_units;
+    const StreamUnit U = units[has ? u : g * G];
+    const int r = U.read, m = E.read_m[r];
+    const int64_t ro = E.roff[r];
+    const bool degen = (E.read_flags[r] & 1) != 0;
+    const bool live = has && !degen;
+    const int rows = live ? max(U.rowsA, U.rowsB) : 0;
+    const int steps = __reduce_max_sync(FULL, rows) + P - 1;
+    if (has && degen) {
+      for (int e = t; e < U.cntA + U.cntB; e += P) {
+        const int pr = shaps[U.list + e].pair;
+        E.acc[pr] = 0.0; E.status[pr] = kStatusDegenerate;
+      }
+    }
+    const int Lp = W - m - 1;
+
+    // ---- coefficients + emission table (k_fast's folded recurrence)
+    float be[K], dl[K], ep[K], zp[K];
+    float2 M[K], I[K], D[K];
+#pragma unroll
+    for (int k4 = 0; k4 < K4; ++k4) {
+      float lam[5][4];
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        const int k = k4 * 4 + kk;
+        const int p = t * K + k;
+        M[k] = zero2; I[k] = zero2; D[k] = zero2;
+        if (p < Lp) {                                   // left padding
+          be[k] = 0.f; dl[k] = 0.f; ep[k] = 1.f; zp[k] = 0.f;
+#pragma unroll
+          for (int c = 0; c < 5; ++c) lam[c][kk] = 0.f;
+        } else if (p < Lp + m) {                        // real read position
+          const int i0 = p - Lp;
+          const double d = s_lut[E.iq[ro + i0]], z = s_lut[E.dq[ro + i0]];
+          const double e = s_lut[E.gq[ro + i0]], qe = s_lut[E.bq[ro + i0]];
+          const float a = (float)((1.0 - d) - z);
+          float anext = 1.f, bnext = 0.f;
+          if (i0 + 1 < m) {
+            anext = (float)((1.0 - s_lut[E.iq[ro + i0 + 1]]) - s_lut[E.dq[ro + i0 + 1]]);
+            bnext = (float)(1.0 - s_lut[E.gq[ro + i0 + 1]]);
+          }
+          be[k] = (float)(1.0 - e);
+          dl[k] = __fdividef((float)d, a);
+          ep[k] = (float)e;
+          zp[k] = __fdividef(bnext * (float)z, anext);
+          const int rc = E.rbases[ro + i0];
+          const float lm = anext * (float)(1.0 - qe), lx = anext * ((float)qe * (1.f / 3.f));
+#pragma unroll
+          for (int c = 0; c < 5; ++c) lam[c][kk] = (rc == c || rc == 4 || c == 4) ? lm : lx;
+        } else {                                        // accumulator position
+          be[k] = 1.f; dl[k] = 0.f; ep[k] = 1.f; zp[k] = 1.f;
+#pragma unroll
+          for (int c = 0; c < 5; ++c) lam[c][kk] = 1.f;
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < 5; ++c)
+        Et[(c * K4 + k4) * P + t] = make_float4(lam[c][0], lam[c][1], lam[c][2], lam[c][3]);
+    }
+
+    // ---- row codes of both lanes into shared memory (row 0 = idle code N|N), and the
+    // unit's window starts: every row where a haplotype begins in either lane, plus the
+    // row after each lane's end (its last LAST event).  Events (FIRST for thread t at
+    // step b + t, LAST for thread P-1 at step b + P - 2) fall in windows [b, b + P).
+    const int slot = wib * G + sw;
+    if (t == 0) reinterpret_cast<unsigned short*>(cd)[0] = 0x0404;
+    if (live) {
+#pragma unroll 1
+      for (int ln = 0; ln < 2; ++ln) {
+        const int cnt = ln ? U.cntB : U.cntA;
+        const int e0 = U.list + (ln ? U.cntA : 0);
+        int row = 1;
+#pragma unroll 1
+        for (int e = 0; e < cnt; ++e) {
+          const int h = shaps[e0 + e].hap;
+          const int64_t h0 = E.hoff[h];
+          const int n = (int)(E.hoff[h + 1] - h0);
+          const int8_t* src = E.hbases + h0;
+          for (int x = t; x < n; x += P)
+            cd[2 * (row + x) + ln] = (unsigned char)(src[x] | (x == 0 ? kCodeFirst : 0) | (x == n - 1 ? kCodeLast : 0));
+          row += n;
+        }
+        for (int x = row + t; x <= rows; x += P) cd[2 * x + ln] = 4;
+      }
+      if (t == 0) {                                   // merge the two lanes' window starts
+        int* wb = s_win + slot * kStreamMaxWin;
+        int ia = 0, ib = 0, ra = 1, rb = 1, nw = 0;
+        const int ca = U.cntA, cbn = U.cntB;
+        auto lenA = [&](int i) { const int h = shaps[U.list + i].hap; return (int)(E.hoff[h + 1] - E.hoff[h]); };
+        auto lenB = [&](int i) { const int h = shaps[U.list + ca + i].hap; return (int)(E.hoff[h + 1] - E.hoff[h]); };
+        // lane starts: rows 1, 1+n1, ..., and the end sentinel (sum + 1)
+        while (ia <= ca || ib <= cbn) {
+          const int va = ia <= ca ? ra : 0x7fffffff, vb = ib <= cbn ? rb : 0x7fffffff;
+          const int v = min(va, vb);
+          if (nw == 0 || wb[nw - 1] != v) wb[nw++] = v;
+          if (va == v) { if (ia < ca) ra += lenA(ia); ++ia; }
+          if (vb == v) { if (ib < cbn) rb += lenB(ib); ++ib; }
+        }
+        s_nwin[slot] = nw;
+      }
+    } else if (t == 0) {
+      s_nwin[slot] = 0;
+    }
+    if (t == 0) s_unit[slot] = U;
+    if (live) {                                        // per-pair boundary S'/n, read metadata
+      const double sdf = (1.0 - s_lut[E.gq[ro]]) * ldexp(1.0, E.read_scale[r]);
+      for (int e = t; e < U.cntA + U.cntB; e += P) {
+        const int h = shaps[U.list + e].hap;
+        s_bs[slot * 2 * kStreamMaxLaneHaps + e] = (float)(sdf / (double)(E.hoff[h + 1] - E.hoff[h]));
+      }
+      if (t == 0) {
+        s_meta[slot * 4 + 0] = Lp;
+        s_meta[slot * 4 + 1] = E.read_scale[r];
+        s_meta[slot * 4 + 2] = __float_as_int(E.read_gsum[r]);
+        s_meta[slot * 4 + 3] = m;
+      }
+    }
+    if (t == 0) s_nband[slot] = 0;
+    s_hc[2 * threadIdx.x] = -1;                         // current haplotype per lane
+    s_hc[2 * threadIdx.x + 1] = -1;
+    __syncwarp();
+
+    // ---- the stream
+    float2 cb = zero2;                                  // thread 0: boundary D of row s
+    float2 nbM = zero2, nbI = zero2, nbD = zero2;
+    unsigned code = 0x0404u;
+    auto ld_code = [&](int s) -> unsigned { return (t == 0 && s <= rows) ? (unsigned)cd16[s] : 0x0404u; };
+    unsigned pf1 = ld_code(1), pf2 = ld_code(2);
+
+    // FIRST(lane L): reset the lane to row 0 of its next haplotype.  Event paths run
+    // only inside windows and reload what they need instead of pinning registers.
+    auto first_event = [&](auto lconst, float2& dgM, float2& dgI, float2& dgD) {
+      constexpr int L = decltype(lconst)::value;
+      const int hc = ++s_hc[2 * threadIdx.x + L];
+      const int lp = s_meta[slot * 4 + 0];
+      const float b = s_bs[slot * 2 * kStreamMaxLaneHaps + (L == 0 ? 0 : s_unit[slot].cntA) + hc];
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        lane_ref<L>(M[k]) = 0.f;
+        lane_ref<L>(I[k]) = 0.f;
+        lane_ref<L>(D[k]) = (t * K + k < lp) ? b : 0.f;
+      }
+      lane_ref<L>(dgM) = 0.f;
+      lane_ref<L>(dgI) = 0.f;
+      lane_ref<L>(dgD) = (t == 0 || t * K - 1 < lp) ? b : 0.f;
+      if (t == 0) {
+        lane_ref<L>(cb) = b;
+        lane_ref<L>(nbM) = 0.f; lane_ref<L>(nbI) = 0.f; lane_ref<L>(nbD) = b;
+      }
+    };
+    // LAST(lane L), thread P-1: the accumulator position holds the pair's sum
+    auto last_event = [&](auto lconst) {
+      constexpr int L = decltype(lconst)::value;
+      const StreamUnit& SU = s_unit[slot];
+      const int hc = s_hc[2 * threadIdx.x + L];
+      const StreamHap sh = shaps[SU.list + (L == 0 ? 0 : SU.cntA) + hc];
+      const int n = (int)(E.hoff[sh.hap + 1] - E.hoff[sh.hap]);
+      const float res = (lane_ref<L>(D[K - 1]) + lane_ref<L>(M[K - 1])) +
+                        (lane_ref<L>(M[K - 2]) + lane_ref<L>(I[K - 2]));
+      const int sc = s_meta[slot * 4 + 1];
+      if (fast_finish_g(E, res, sh.pair, SU.read, sh.hap, n, s_meta[slot * 4 + 3], sc,
+                        __int_as_float(s_meta[slot * 4 + 2]), false, true)) {
+        // guard band: queue for the bit-exact rerun this warp does after the unit
+        const ExactItem it{sh.pair, SU.read, sh.hap, sc};
+        const int c = s_nband[slot];
+        if (c < kStreamBandCap && atomicAdd(E.band_inline, 1) < E.band_budget) {
+          s_band[slot * kStreamBandCap + c] = it;
+          s_nband[slot] = c + 1;
+        }
+        else append_item(E.ex32, E.ex32_count, E.list_cap, exact_slot_for(s_meta[slot * 4 + 3]), it);
+      }
+    };
+
+    auto step = [&](const int s, auto checked) {
+      constexpr bool CHECK = decltype(checked)::value;
+      float2 dgM = nbM, dgI = nbI, dgD = nbD;
+      {
+        const float2 lm = M[K - 1], li = I[K - 1], ld = D[K - 1];
+        nbM.x = __shfl_up_sync(FULL, lm.x, 1, P);
+        nbM.y = __shfl_up_sync(FULL, lm.y, 1, P);
+        nbI.x = __shfl_up_sync(FULL, li.x, 1, P);
+        nbI.y = __shfl_up_sync(FULL, li.y, 1, P);
+        nbD.x = __shfl_up_sync(FULL, ld.x, 1, P);
+        nbD.y = __shfl_up_sync(FULL, ld.y, 1, P);
+        const unsigned up = __shfl_up_sync(FULL, code, 1, P);
+        code = (t == 0) ? pf1 : up;
+      }
+      if (t == 0) { nbM = zero2; nbI = zero2; nbD = cb; }
+      pf1 = pf2;
+      pf2 = ld_code(s + 2);
+      if (CHECK && (code & ((kCodeFirst << 8) | kCodeFirst))) {
+        if (code & kCodeFirst) first_event(std::integral_constant<int, 0>{}, dgM, dgI, dgD);
+        if (code & (kCodeFirst << 8)) first_event(std::integral_constant<int, 1>{}, dgM, dgI, dgD);
+      }
+      const int cA = code & 7, cB = (code >> 8) & 7;
+      const float4* EA = Et + (cA * K4) * P + t;
+      const float4* EB = Et + (cB * K4) * P + t;
+      // pass 1 (descending): D' from the previous row, M from the previous-row diagonal
+#pragma unroll
+      for (int k4 = K4 - 1; k4 >= 0; --k4) {
+        const float4 la = EA[k4 * P];
+        const float4 lb = EB[k4 * P];
+#pragma unroll
+        for (int kk = 3; kk >= 0; --kk) {
+          const int k = k4 * 4 + kk;
+          D[k] = fma2s(ep[k], D[k], mul2s(zp[k], M[k]));
+          const float2 pm = (k > 0) ? M[k - 1] : dgM;
+          const float2 pi = (k > 0) ? I[k - 1] : dgI;
+          const float2 pd = (k > 0) ? D[k - 1] : dgD;
+          float2 x = fma2s(be[k], pi, pd);
+          x = __fadd2_rn(pm, x);
+          M[k].x = comp(la, kk) * x.x;
+          M[k].y = comp(lb, kk) * x.y;
+        }
+      }
+      // pass 2 (ascending): I chain along the read within the current row
+      {
+        float2 lM = nbM, lI = nbI;
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          I[k] = fma2s(ep[k], lI, mul2s(dl[k], lM));
+          lM = M[k];
+          lI = I[k];
+        }
+      }
+      if (CHECK && (code & ((kCodeLast << 8) | kCodeLast)) && t == P - 1) {
+        if (code & kCodeLast) last_event(std::integral_constant<int, 0>{});
+        if (code & (kCodeLast << 8)) last_event(std::integral_constant<int, 1>{});
+      }
+    };
+
+    // event-free stretches run the plain step; windows run the event-checking one
+    const int nwin = s_nwin[slot];
+    const int* wb = s_win + slot * kStreamMaxWin;
+    int wi = 0;
+    int s = 1;
+#pragma unroll 1
+    while (s <= steps) {
+      while (wi < nwin && wb[wi] + P <= s) ++wi;
+      const int e_sw = wi < nwin ? wb[wi] : 0x7fffffff;
+      const int e = max((int)__reduce_min_sync(FULL, (unsigned)e_sw), s);
+      const int fend = min(e, steps + 1);
+#pragma unroll 1
+      for (; s < fend; ++s) step(s, std::false_type{});
+      if (s > steps) break;
+      const int wend = min(e + P, steps + 1);
+#pragma unroll 1
+      for (; s < wend; ++s) step(s, std::true_type{});
+    }
+    __syncwarp();
+    // guard-band pairs found in this unit: bit-exact FP32 rerun by the same warp (same
+    // tiling; the emission-table slot is free again), overlapping other warps' work
+    const int nbd = s_nband[slot];
+    const int nbmax = __reduce_max_sync(FULL, (unsigned)nbd);
+#pragma unroll 1
+    for (int x = 0; x < nbmax; ++x) {
+      const bool mine = x < nbd;
+      const ExactItem it = mine ? s_band[slot * kStreamBandCap + x]
+                                : ExactItem{-1, U.read, shaps[U.list].hap, 0};
+      exact_item<float, P, K>(E, it, mine, s_lut, reinterpret_cast<float*>(Et), nullptr, nullptr, 0, t);
+      __syncwarp();
     }
   }
 }
