@@ -47,6 +47,7 @@ const FastGeom kFastGeoms[] = {{4, 4},  {4, 8},   {4, 12},  {4, 16},  {8, 8},   
 constexpr int kNumFastGeoms = sizeof(kFastGeoms) / sizeof(kFastGeoms[0]);
 constexpr int kExactP[kNumExactP] = {4, 8, 16, 32};
 constexpr int kThreads = 128;
+constexpr int kBinCounters = 64;          // fixed counter slots before the per-bin counters
 
 struct Bin {
   int geom, Q;
@@ -81,11 +82,12 @@ const void* kFastFn[2 * kNumFastGeoms] = {FASTFN(4, 4),   FASTFN(4, 8),   FASTFN
                                           FASTFN(32, 16)};
 #undef FASTFN
 
-// streaming kernel (single-stripe reads): same geometry table as k_fast
+// streaming kernel (single-stripe reads): FP32 over the k_fast geometry table, FP64 retry
+// over the r64 geometries (phmm_kernels.cuh: r64_geom_for)
 template <int P, int K>
 void launch_stream(dim3 g, size_t smem, cudaStream_t s, const EngineDev& E, const StreamUnit* u,
                    const StreamHap* h, int nu, int* ctr) {
-  k_stream<P, K><<<g, kThreads, smem, s>>>(E, u, h, nu, ctr);
+  k_stream<false, P, K><<<g, kThreads, smem, s>>>(E, u, h, nu, nullptr, ctr);
 }
 typedef void (*StreamLaunch)(dim3, size_t, cudaStream_t, const EngineDev&, const StreamUnit*, const StreamHap*,
                              int, int*);
@@ -95,16 +97,34 @@ const StreamLaunch kStreamLaunch[kNumFastGeoms] = {
     launch_stream<16, 12>, launch_stream<16, 16>, launch_stream<32, 8>, launch_stream<32, 12>,
     launch_stream<32, 16>};
 const void* kStreamFn[kNumFastGeoms] = {
-    (const void*)k_stream<4, 4>,   (const void*)k_stream<4, 8>,   (const void*)k_stream<4, 12>,
-    (const void*)k_stream<4, 16>,  (const void*)k_stream<8, 8>,   (const void*)k_stream<8, 12>,
-    (const void*)k_stream<8, 16>,  (const void*)k_stream<16, 8>,  (const void*)k_stream<16, 12>,
-    (const void*)k_stream<16, 16>, (const void*)k_stream<32, 8>,  (const void*)k_stream<32, 12>,
-    (const void*)k_stream<32, 16>};
+    (const void*)k_stream<false, 4, 4>,   (const void*)k_stream<false, 4, 8>,   (const void*)k_stream<false, 4, 12>,
+    (const void*)k_stream<false, 4, 16>,  (const void*)k_stream<false, 8, 8>,   (const void*)k_stream<false, 8, 12>,
+    (const void*)k_stream<false, 8, 16>,  (const void*)k_stream<false, 16, 8>,  (const void*)k_stream<false, 16, 12>,
+    (const void*)k_stream<false, 16, 16>, (const void*)k_stream<false, 32, 8>,  (const void*)k_stream<false, 32, 12>,
+    (const void*)k_stream<false, 32, 16>};
 const int kStreamOcc[kNumFastGeoms] = {StreamOcc<4>::value,  StreamOcc<8>::value,  StreamOcc<12>::value,
                                        StreamOcc<16>::value, StreamOcc<8>::value,  StreamOcc<12>::value,
                                        StreamOcc<16>::value, StreamOcc<8>::value,  StreamOcc<12>::value,
                                        StreamOcc<16>::value, StreamOcc<8>::value,  StreamOcc<12>::value,
                                        StreamOcc<16>::value};
+// FP64 retry stream geometries: W = 32, 64, 96, 128, 192, 256
+const FastGeom kR64Geoms[kNumR64Geoms] = {{8, 4}, {16, 4}, {16, 6}, {16, 8}, {32, 6}, {32, 8}};
+template <int P, int K>
+void launch_stream64(dim3 g, size_t smem, cudaStream_t s, const EngineDev& E, int geom, int* ctr) {
+  k_stream<true, P, K><<<g, kThreads, smem, s>>>(E, E.r64_units[geom], E.r64_haps, 0, E.r64_count + geom, ctr);
+}
+typedef void (*Stream64Launch)(dim3, size_t, cudaStream_t, const EngineDev&, int, int*);
+const Stream64Launch kStream64Launch[kNumR64Geoms] = {launch_stream64<8, 4>,  launch_stream64<16, 4>,
+                                                      launch_stream64<16, 6>, launch_stream64<16, 8>,
+                                                      launch_stream64<32, 6>, launch_stream64<32, 8>};
+const void* kStream64Fn[kNumR64Geoms] = {(const void*)k_stream<true, 8, 4>,  (const void*)k_stream<true, 16, 4>,
+                                         (const void*)k_stream<true, 16, 6>, (const void*)k_stream<true, 16, 8>,
+                                         (const void*)k_stream<true, 32, 6>, (const void*)k_stream<true, 32, 8>};
+int stream64_occ(int g) { return kR64Geoms[g].K <= 4 ? 3 : 2; }
+size_t stream64_smem(int g) {
+  const FastGeom G = kR64Geoms[g];
+  return 96 * sizeof(double) + (size_t)4 * (32 / G.P) * 5 * G.K * G.P * sizeof(double) + kStreamCodeBytesPerCta;
+}
 int stream_cap(int P) {
   return P == 4 ? StreamCap<4>::value : P == 8 ? StreamCap<8>::value : P == 16 ? StreamCap<16>::value
                                                                              : StreamCap<32>::value;
@@ -240,6 +260,8 @@ struct phmm_ctx {
   DBuf<FastUnit> d_units;
   DBuf<StreamUnit> d_sunits;
   DBuf<StreamHap> d_shaps;
+  DBuf<StreamUnit> d_r64u[kNumR64Geoms];
+  DBuf<StreamHap> d_r64h;
   DBuf<ExactItem> d_ex32[kNumExactP], d_ex64[kNumExactP], d_fx64[kNumExactP];
   DBuf<float2> d_colf;
   DBuf<double> d_cold;
@@ -247,6 +269,7 @@ struct phmm_ctx {
 
   // plan (host)
   bool prepared = false, executed = false;
+  bool r64_enabled = false;
   int64_t num_pairs = 0;
   int64_t num_reads = 0, num_haps = 0, num_batches = 0;
   std::vector<int64_t> batch_read_off, batch_hap_off, hap_len;
@@ -325,13 +348,15 @@ int phmm_create(phmm_ctx** out, int device, const double* phred_lut) {
   CK(cudaEventCreate(&ctx->ev_fast0));
   CK(cudaEventCreate(&ctx->ev_fast1));
   CK(cudaEventCreate(&ctx->ev_end));
-  CK(cudaMallocHost(&ctx->h_counts, 64 * sizeof(int)));
+  CK(cudaMallocHost(&ctx->h_counts, kBinCounters * sizeof(int)));
   CK(ctx->d_lut.ensure(94));
   CK(cudaMemcpy(ctx->d_lut.p, ctx->lut.data(), 94 * sizeof(double), cudaMemcpyHostToDevice));
   for (int g = 0; g < 2 * kNumFastGeoms; ++g)
     CK(cudaFuncSetAttribute(kFastFn[g], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fast_smem(g / 2)));
   for (int g = 0; g < kNumFastGeoms; ++g)
     CK(cudaFuncSetAttribute(kStreamFn[g], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)stream_smem(g)));
+  for (int g = 0; g < kNumR64Geoms; ++g)
+    CK(cudaFuncSetAttribute(kStream64Fn[g], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)stream64_smem(g)));
   for (int s = 0; s < kNumExactP; ++s) {
     CK(cudaFuncSetAttribute(kExact32Fn[s], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)exact_smem(s, 4)));
     CK(cudaFuncSetAttribute(kExact64Fn[s], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)exact_smem(s, 8)));
@@ -348,7 +373,9 @@ int phmm_destroy(phmm_ctx* ctx) {
   ctx->d_dq.release(); ctx->d_gq.release(); ctx->d_status.release(); ctx->d_rflags.release();
   ctx->d_roff.release(); ctx->d_hoff.release(); ctx->d_read_m.release(); ctx->d_read_scale.release();
   ctx->d_read_ncap.release(); ctx->d_counters.release(); ctx->d_gsum.release(); ctx->d_lut.release();
-  ctx->d_acc.release(); ctx->d_units.release(); ctx->d_sunits.release(); ctx->d_shaps.release(); ctx->d_colf.release(); ctx->d_cold.release();
+  ctx->d_acc.release(); ctx->d_units.release(); ctx->d_sunits.release(); ctx->d_shaps.release();
+  for (int g = 0; g < kNumR64Geoms; ++g) ctx->d_r64u[g].release();
+  ctx->d_r64h.release(); ctx->d_colf.release(); ctx->d_cold.release();
   for (int s = 0; s < kNumExactP; ++s) { ctx->d_ex32[s].release(); ctx->d_ex64[s].release(); ctx->d_fx64[s].release(); }
   if (ctx->h_counts) cudaFreeHost(ctx->h_counts);
   ctx->h_counts = nullptr;
@@ -598,7 +625,7 @@ int phmm_prepare(phmm_ctx* ctx, const phmm_input* in, const phmm_options* opt, i
   CK(ctx->d_rflags.ensure(R));
   CK(ctx->d_acc.ensure(N));
   CK(ctx->d_status.ensure(N));
-  CK(ctx->d_counters.ensure(32 + ctx->bins.size() + ctx->sbins.size()));
+  CK(ctx->d_counters.ensure(kBinCounters + ctx->bins.size() + ctx->sbins.size()));
   ctx->list_cap = (int)std::max<int64_t>(N, 1);
   for (int s = 0; s < kNumExactP; ++s) {
     ctx->host_ex32[s] = (int)host32[s].size();
@@ -625,6 +652,15 @@ int phmm_prepare(phmm_ctx* ctx, const phmm_input* in, const phmm_options* opt, i
   ctx->h2d_ms = h2d;
   ctx->h2d_bytes = bytes;
 
+  // FP64 stream-retry lists: sized for every streamed pair (worst case: all underflow)
+  int64_t streamed = 0;
+  for (auto& sb : ctx->sbins)
+    for (auto& su : sb.units) streamed += su.cntA + su.cntB;
+  const bool r64 = (opt->flags & PHMM_FLAG_RETRY_F64) && streamed > 0;
+  if (r64) {
+    for (int g = 0; g < kNumR64Geoms; ++g) CK(ctx->d_r64u[g].ensure(streamed));
+    CK(ctx->d_r64h.ensure(streamed));
+  }
   EngineDev& E = ctx->dev;
   E.rbases = ctx->d_rbases.p; E.bq = ctx->d_bq.p; E.iq = ctx->d_iq.p; E.dq = ctx->d_dq.p; E.gq = ctx->d_gq.p;
   E.roff = ctx->d_roff.p; E.hbases = ctx->d_hbases.p; E.hoff = ctx->d_hoff.p;
@@ -641,6 +677,13 @@ int phmm_prepare(phmm_ctx* ctx, const phmm_input* in, const phmm_options* opt, i
   E.retry_f64 = (opt->flags & PHMM_FLAG_RETRY_F64) ? 1 : 0;
   E.band_inline = ctx->d_counters.p + 16;
   E.band_budget = 2 * ctx->num_sms;
+  for (int g = 0; g < kNumR64Geoms; ++g) E.r64_units[g] = r64 ? ctx->d_r64u[g].p : nullptr;
+  E.r64_haps = r64 ? ctx->d_r64h.p : nullptr;
+  E.r64_count = ctx->d_counters.p + 32;
+  E.r64_hap_count = ctx->d_counters.p + 32 + kNumR64Geoms;
+  E.r64_unit_cap = r64 ? (int)streamed : 0;
+  E.r64_hap_cap = r64 ? (int)streamed : 0;
+  ctx->r64_enabled = r64;
 
   ctx->prepared = true;
   if (num_pairs_out) *num_pairs_out = N;
@@ -656,10 +699,11 @@ int phmm_execute(phmm_ctx* ctx) {
   const int64_t N = ctx->num_pairs;
   int launches = 0;
   // counters: [0,4) ex32 counts, [4,8) ex64 counts, [8,12) ex32 work, [12,16) ex64 work,
-  // 16 inline guard-band pairs, [20,24) fx64 counts, [24,28) fx64 work, [32, 32+bins) bins
+  // 16 inline guard-band pairs, [20,24) fx64 counts, [24,28) fx64 work, [32,38) FP64
+  // stream-retry unit counts, 38 their haplotype count, [40,46) their work counters,
+  // [kBinCounters, +bins) fast-kernel bins
   const int nb = (int)ctx->bins.size();
   std::vector<int> blocks(nb, 0);
-  int total_fast_ctas = 0;
   for (int bi = 0; bi < nb; ++bi) {
     const Bin& bn = ctx->bins[bi];
     const int nu = (int)bn.units.size();
@@ -667,15 +711,15 @@ int phmm_execute(phmm_ctx* ctx) {
     const int G = 32 / kFastGeoms[bn.geom].P;
     const int groups = (nu + G - 1) / G;
     blocks[bi] = std::max(1, std::min(ctx->num_sms * kFastOcc[bn.geom], (groups + 3) / 4));
-    total_fast_ctas += blocks[bi];
   }
   int* hc = ctx->h_counts;
-  memset(hc, 0, 32 * sizeof(int));
+  memset(hc, 0, kBinCounters * sizeof(int));
   for (int s = 0; s < kNumExactP; ++s) { hc[s] = ctx->host_ex32[s]; hc[kNumExactP + s] = ctx->host_ex64[s]; }
   CK(cudaEventRecord(ctx->ev_start, st));
-  CK(cudaMemcpyAsync(ctx->d_counters.p, hc, 32 * sizeof(int), cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(ctx->d_counters.p, hc, kBinCounters * sizeof(int), cudaMemcpyHostToDevice, st));
   const int nsb = (int)ctx->sbins.size();
-  if (nb + nsb > 0) CK(cudaMemsetAsync(ctx->d_counters.p + 32, 0, (nb + nsb) * sizeof(int), st));
+  int* bin_ctr = ctx->d_counters.p + kBinCounters;
+  if (nb + nsb > 0) CK(cudaMemsetAsync(bin_ctr, 0, (nb + nsb) * sizeof(int), st));
   if (N > 0) CK(cudaMemsetAsync(ctx->d_status.p, 0, N, st));
   if (ctx->num_reads > 0) {
     const int threads = 128;
@@ -686,14 +730,31 @@ int phmm_execute(phmm_ctx* ctx) {
   CK(cudaEventRecord(ctx->ev_pre, st));
   CK(cudaEventRecord(ctx->ev_fast0, st));
   // Fast-kernel bins (one persistent launch per tiling) go round-robin onto side streams
-  // so a bin's tail (its last CTAs draining) overlaps the next bin's work.
-  int nlaunch = 0;
-  // legacy k_fast bins share the boundary-column scratch: they stay serialized on the last
-  // side stream; streaming bins rotate over the others
+  // so a bin's tail (its last CTAs draining) overlaps the next bin's work.  Legacy k_fast
+  // bins share the boundary-column scratch: they stay serialized on the last side stream.
   constexpr int kStreamAux = phmm_ctx::kAux - 1;
+  int nlaunch = 0;
   auto side = [&](int i) -> cudaStream_t { return ctx->aux[i % kStreamAux]; };
   bool used[phmm_ctx::kAux] = {};
-  for (int a = 0; a < phmm_ctx::kAux; ++a) CK(cudaStreamWaitEvent(ctx->aux[a], ctx->ev_pre, 0));
+#define CKE(call) do { cudaError_t _e = (call); if (_e != cudaSuccess) return _e; } while (0)
+  auto fork = [&]() -> cudaError_t {
+    CKE(cudaEventRecord(ctx->ev_pre, st));
+    for (int a = 0; a < phmm_ctx::kAux; ++a) {
+      used[a] = false;
+      CKE(cudaStreamWaitEvent(ctx->aux[a], ctx->ev_pre, 0));
+    }
+    return cudaSuccess;
+  };
+  auto join = [&]() -> cudaError_t {
+    for (int a = 0; a < phmm_ctx::kAux; ++a) {
+      if (!used[a]) continue;
+      CKE(cudaEventRecord(ctx->ev_join[a], ctx->aux[a]));
+      CKE(cudaStreamWaitEvent(st, ctx->ev_join[a], 0));
+    }
+    return cudaSuccess;
+  };
+#undef CKE
+  CK(fork());
   for (int bi = 0; bi < nsb; ++bi) {
     const auto& sb = ctx->sbins[bi];
     const int nu = (int)sb.units.size();
@@ -703,7 +764,7 @@ int phmm_execute(phmm_ctx* ctx) {
     const int blk = std::max(1, std::min(ctx->num_sms * kStreamOcc[sb.geom], (groups + 3) / 4));
     used[nlaunch % kStreamAux] = true;
     kStreamLaunch[sb.geom](dim3(blk), stream_smem(sb.geom), side(nlaunch++), E, ctx->d_sunits.p + sb.dev_off,
-                           ctx->d_shaps.p, nu, ctx->d_counters.p + 32 + nb + bi);
+                           ctx->d_shaps.p, nu, bin_ctr + nb + bi);
     ++launches;
   }
   for (int bi = 0; bi < nb; ++bi) {
@@ -711,28 +772,40 @@ int phmm_execute(phmm_ctx* ctx) {
     const int nu = (int)bn.units.size();
     if (nu == 0) continue;
     used[phmm_ctx::kAux - 1] = true;
-    kFastLaunch[bn.geom](dim3(blocks[bi]), fast_smem(bn.geom), ctx->aux[phmm_ctx::kAux - 1], E, ctx->d_units.p + bn.dev_off, nu,
-                         bn.Q, ctx->d_counters.p + 32 + bi, ctx->d_colf.p, ctx->max_n + 1);
+    kFastLaunch[bn.geom](dim3(blocks[bi]), fast_smem(bn.geom), ctx->aux[phmm_ctx::kAux - 1], E,
+                         ctx->d_units.p + bn.dev_off, nu, bn.Q, bin_ctr + bi, ctx->d_colf.p, ctx->max_n + 1);
     ++launches;
   }
-  for (int a = 0; a < phmm_ctx::kAux; ++a) {
-    if (!used[a]) continue;
-    CK(cudaEventRecord(ctx->ev_join[a], ctx->aux[a]));
-    CK(cudaStreamWaitEvent(st, ctx->ev_join[a], 0));
-  }
+  CK(join());
   CK(cudaGetLastError());
   CK(cudaEventRecord(ctx->ev_fast1, st));
+  // Post-pass, two concurrent chains: (a) guard-band overflow on the bit-exact FP32
+  // kernels, then per-pair FP64 retries (legacy path, fed by (a) and by k_fast);
+  // (b) FP64 stream retries (FP64 pipe, overlaps (a) on the FP32 pipe).  Then the
+  // bit-exact FP64 kernels, fed by everything before.
+  CK(fork());
+  used[0] = true;
   for (int s = 0; s < kNumExactP; ++s) {
-    kExact32[s](dim3(ctx->num_sms * 2), exact_smem(s, 4), st, E, s, ctx->d_counters.p + 8 + s,
+    kExact32[s](dim3(ctx->num_sms * 2), exact_smem(s, 4), ctx->aux[0], E, s, ctx->d_counters.p + 8 + s,
                 ctx->d_cold.p, ctx->max_n + 1);
     ++launches;
   }
   for (int s = 0; s < kNumExactP; ++s) {
     if (!(ctx->flags & PHMM_FLAG_RETRY_F64)) break;
-    kFast64[s](dim3(ctx->num_sms * 2), exact_smem(s, 8), st, E, s, ctx->d_counters.p + 24 + s,
+    kFast64[s](dim3(ctx->num_sms * 2), exact_smem(s, 8), ctx->aux[0], E, s, ctx->d_counters.p + 24 + s,
                ctx->d_cold.p, ctx->max_n + 1);
     ++launches;
   }
+  if (ctx->r64_enabled) {
+    for (int g = kNumR64Geoms - 1; g >= 0; --g) {
+      const int a = 1 + (g % (phmm_ctx::kAux - 1));
+      used[a] = true;
+      kStream64Launch[g](dim3(ctx->num_sms * stream64_occ(g)), stream64_smem(g), ctx->aux[a], E, g,
+                         ctx->d_counters.p + 40 + g);
+      ++launches;
+    }
+  }
+  CK(join());
   for (int s = 0; s < kNumExactP; ++s) {
     kExact64[s](dim3(ctx->num_sms * 2), exact_smem(s, 8), st, E, s, ctx->d_counters.p + 12 + s,
                 ctx->d_cold.p, ctx->max_n + 1);

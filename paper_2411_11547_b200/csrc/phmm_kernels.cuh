@@ -41,6 +41,15 @@ struct ExactItem {                        // one read x one haplotype
   int pair, read, hap, scale;
 };
 
+struct StreamUnit {                       // 32 B
+  int read;
+  int list;                               // StreamHap entries: lane A [list, list+cntA),
+  int cntA, cntB;                         //                    lane B [list+cntA, +cntB)
+  int rowsA, rowsB;                       // sum of the lane's haplotype lengths
+  int pad0, pad1;
+};
+struct StreamHap { int hap, pair; };
+
 struct EngineDev {
   const int8_t* rbases;
   const uint8_t *bq, *iq, *dq, *gq;
@@ -65,6 +74,12 @@ struct EngineDev {
   int* fx64_count;                        // [kNumExactP]
   int* band_inline;                       // guard-band pairs taken inline so far
   int band_budget;
+  // FP64 stream retry units, appended by the FP32 stream kernel (one list per geometry)
+  StreamUnit* r64_units[6];
+  int* r64_count;                         // [6]
+  StreamHap* r64_haps;
+  int* r64_hap_count;
+  int r64_unit_cap, r64_hap_cap;
 };
 
 __device__ __forceinline__ int exact_slot_for(int m) {
@@ -584,14 +599,6 @@ k_fast(const EngineDev E, const FastUnit* __restrict__ units, int num_units, int
 // Rows outside a thread's stream (fill, drain, the shorter lane's tail) compute values
 // that are never read: every pair starts with a FIRST reset.
 // ---------------------------------------------------------------------------------
-struct StreamUnit {                       // 32 B
-  int read;
-  int list;                               // StreamHap entries: lane A [list, list+cntA),
-  int cntA, cntB;                         //                    lane B [list+cntA, +cntB)
-  int rowsA, rowsB;                       // sum of the lane's haplotype lengths
-  int pad0, pad1;
-};
-struct StreamHap { int hap, pair; };
 
 constexpr int kCodeFirst = 8, kCodeLast = 16;          // code byte: base | FIRST | LAST
 constexpr int kStreamCodeBytesPerCta = 32768;          // row-code staging, shared memory
@@ -604,36 +611,105 @@ template <int P> struct StreamCap {                    // max rows per lane of o
 };
 template <int K> struct StreamOcc { static constexpr int value = K <= 8 ? 4 : (K <= 12 ? 3 : 2); };
 
-template <int L> __device__ __forceinline__ float& lane_ref(float2& v) { return L == 0 ? v.x : v.y; }
+// FP64 retry geometries (P, K): W = 32, 64, 96, 128, 192, 256; longer reads use k_fast64
+constexpr int kNumR64Geoms = 6;
+__host__ __device__ __forceinline__ int r64_geom_for(int m) {
+  const int w = m + 1;
+  return w <= 32 ? 0 : w <= 64 ? 1 : w <= 96 ? 2 : w <= 128 ? 3 : w <= 192 ? 4 : w <= 256 ? 5 : -1;
+}
+__host__ __device__ __forceinline__ int r64_geom_P(int g) { return g == 0 ? 8 : (g <= 3 ? 16 : 32); }
+__host__ __device__ __forceinline__ int r64_cap(int g) {
+  const int P = r64_geom_P(g);
+  return kStreamCodeBytesPerCta / (4 * (32 / P)) / 2 - 2;
+}
 
-template <int P, int K>
-__global__ void __launch_bounds__(128, StreamOcc<K>::value)
+struct Dbl2 { double x, y; };
+
+// Two-lane value algebra of the streaming kernel: FP32 = packed float2 (FFMA2/FMUL2/FADD2
+// with a scalar-broadcast coefficient), FP64 = two independent DFMA chains.
+template <bool F64> struct Lanes;
+template <> struct Lanes<false> {
+  using S = float;
+  using V = float2;
+  using EV = float4;                      // emission chunk: 4 positions (LDS.128)
+  static constexpr int EW = 4;
+  static __device__ __forceinline__ V zero() { return make_float2(0.f, 0.f); }
+  static __device__ __forceinline__ V fma(S s, V a, V b) { return __ffma2_rn(make_float2(s, s), a, b); }
+  static __device__ __forceinline__ V mul(S s, V a) { return __fmul2_rn(make_float2(s, s), a); }
+  static __device__ __forceinline__ V add(V a, V b) { return __fadd2_rn(a, b); }
+  static __device__ __forceinline__ S comp(const EV& v, int i) {
+    return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w;
+  }
+  static __device__ __forceinline__ EV pack(const S* l) { return make_float4(l[0], l[1], l[2], l[3]); }
+};
+template <> struct Lanes<true> {
+  using S = double;
+  using V = Dbl2;
+  using EV = double2;                     // emission chunk: 2 positions (LDS.128)
+  static constexpr int EW = 2;
+  static __device__ __forceinline__ V zero() { return Dbl2{0.0, 0.0}; }
+  static __device__ __forceinline__ V fma(S s, V a, V b) { return Dbl2{::fma(s, a.x, b.x), ::fma(s, a.y, b.y)}; }
+  static __device__ __forceinline__ V mul(S s, V a) { return Dbl2{s * a.x, s * a.y}; }
+  static __device__ __forceinline__ V add(V a, V b) { return Dbl2{a.x + b.x, a.y + b.y}; }
+  static __device__ __forceinline__ S comp(const EV& v, int i) { return i == 0 ? v.x : v.y; }
+  static __device__ __forceinline__ EV pack(const S* l) { return make_double2(l[0], l[1]); }
+};
+template <int L, class V> __device__ __forceinline__ auto& lane_ref(V& v) { return L == 0 ? v.x : v.y; }
+
+// Classification of a finished FP32 stream accumulator; returns 0 = written, 1 = guard
+// band (caller queues the bit-exact rerun), 2 = FP32 underflow to retry in FP64 (caller).
+__device__ __forceinline__ int stream_finish32(const EngineDev& E, float a, int pair, int n, float gsum, int scale) {
+  const float bound = 0x1p-80f * (float)n * gsum;                // 2^10 * 2^-90
+  const float hi = ldexpf(0.031622776f, scale);                   // 10^-1.5 * 2^scale
+  if (!(a >= 0x1p-93f)) {
+    if (E.retry_f64) { E.status[pair] = kStatusRetriedF64; return 2; }
+    E.acc[pair] = 0.0;
+    E.status[pair] = kStatusOverflow;
+    return 0;
+  }
+  if (a < bound || a > hi) { E.status[pair] = kStatusExactF32; return 1; }
+  E.acc[pair] = (double)a;
+  E.status[pair] = kStatusOk;
+  return 0;
+}
+
+template <bool F64, int P, int K>
+__global__ void __launch_bounds__(128, F64 ? (K <= 4 ? 3 : 2) : StreamOcc<K>::value)
 k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHap* __restrict__ shaps,
-         int num_units, int* __restrict__ counter) {
-  constexpr int W = P * K, G = 32 / P, K4 = K / 4;
-  constexpr int CB = StreamCap<P>::bytes;
-  static_assert(K % 4 == 0 && K >= 4, "K multiple of 4");
+         int num_units_arg, const int* __restrict__ num_units_dev, int* __restrict__ counter) {
+  using A = Lanes<F64>;
+  using S = typename A::S;
+  using V = typename A::V;
+  using EV = typename A::EV;
+  constexpr int EW = A::EW;
+  constexpr int W = P * K, G = 32 / P, KE = K / EW;
+  constexpr int CB = kStreamCodeBytesPerCta / (4 * G);
+  static_assert(K % EW == 0 && K >= 4, "K multiple of the emission chunk");
   constexpr unsigned FULL = 0xffffffffu;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double* s_lut = reinterpret_cast<double*>(smem_raw);
-  float4* s_E = reinterpret_cast<float4*>(smem_raw + 96 * sizeof(double));
-  unsigned char* s_code = smem_raw + 96 * sizeof(double) + (size_t)4 * G * 5 * K4 * P * sizeof(float4);
+  EV* s_E = reinterpret_cast<EV*>(smem_raw + 96 * sizeof(double));
+  unsigned char* s_code = smem_raw + 96 * sizeof(double) + (size_t)4 * G * 5 * KE * P * sizeof(EV);
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int sw = lane / P, t = lane % P;
+  const int slot = wib * G + sw;
+  const int num_units = num_units_dev ? min(*num_units_dev, E.r64_unit_cap) : num_units_arg;
+  if (num_units == 0) return;
   for (int i = threadIdx.x; i < 94; i += blockDim.x) s_lut[i] = E.lut[i];
   __syncthreads();
-  float4* Et = s_E + (size_t)((wib * G + sw) * 5 * K4) * P;
-  unsigned char* cd = s_code + (size_t)(wib * G + sw) * CB;
+  EV* Et = s_E + (size_t)(slot * 5 * KE) * P;
+  unsigned char* cd = s_code + (size_t)slot * CB;
   const unsigned short* cd16 = reinterpret_cast<const unsigned short*>(cd);
-  const float2 zero2 = make_float2(0.f, 0.f);
+  const V zero2 = A::zero();
   __shared__ StreamUnit s_unit[4 * G];
   __shared__ int s_hc[2 * 128];
   __shared__ int s_win[4 * G * kStreamMaxWin];
-  __shared__ float s_bs[4 * G * 2 * kStreamMaxLaneHaps];
+  __shared__ S s_bs[4 * G * 2 * kStreamMaxLaneHaps];
   __shared__ int s_meta[4 * G * 4];
-  __shared__ ExactItem s_band[4 * G * kStreamBandCap];
+  __shared__ ExactItem s_band[F64 ? 1 : 4 * G * kStreamBandCap];
   __shared__ int s_nband[4 * G];
   __shared__ int s_nwin[4 * G];
+  __shared__ unsigned s_flag[4 * G * 2];          // FP32: per lane, entries that underflowed
 
   for (;;) {
     int g = 0;
@@ -657,55 +733,66 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
     }
     const int Lp = W - m - 1;
 
-    // ---- coefficients + emission table (k_fast's folded recurrence)
-    float be[K], dl[K], ep[K], zp[K];
-    float2 M[K], I[K], D[K];
+    // ---- coefficients + emission table, folded recurrence:
+    //   Mt(i) = alpha_{i+1} M(i), D'(i) = beta_{i+1} D(i); 7 operations per cell
+    S be[K], dl[K], ep[K], zp[K];
+    V M[K], I[K], D[K];
 #pragma unroll
-    for (int k4 = 0; k4 < K4; ++k4) {
-      float lam[5][4];
+    for (int ke = 0; ke < KE; ++ke) {
+      S lam[5][EW];
 #pragma unroll
-      for (int kk = 0; kk < 4; ++kk) {
-        const int k = k4 * 4 + kk;
+      for (int kk = 0; kk < EW; ++kk) {
+        const int k = ke * EW + kk;
         const int p = t * K + k;
         M[k] = zero2; I[k] = zero2; D[k] = zero2;
         if (p < Lp) {                                   // left padding
-          be[k] = 0.f; dl[k] = 0.f; ep[k] = 1.f; zp[k] = 0.f;
+          be[k] = 0; dl[k] = 0; ep[k] = 1; zp[k] = 0;
 #pragma unroll
-          for (int c = 0; c < 5; ++c) lam[c][kk] = 0.f;
+          for (int c = 0; c < 5; ++c) lam[c][kk] = 0;
         } else if (p < Lp + m) {                        // real read position
           const int i0 = p - Lp;
           const double d = s_lut[E.iq[ro + i0]], z = s_lut[E.dq[ro + i0]];
           const double e = s_lut[E.gq[ro + i0]], qe = s_lut[E.bq[ro + i0]];
-          const float a = (float)((1.0 - d) - z);
-          float anext = 1.f, bnext = 0.f;
-          if (i0 + 1 < m) {
-            anext = (float)((1.0 - s_lut[E.iq[ro + i0 + 1]]) - s_lut[E.dq[ro + i0 + 1]]);
-            bnext = (float)(1.0 - s_lut[E.gq[ro + i0 + 1]]);
-          }
-          be[k] = (float)(1.0 - e);
-          dl[k] = __fdividef((float)d, a);
-          ep[k] = (float)e;
-          zp[k] = __fdividef(bnext * (float)z, anext);
           const int rc = E.rbases[ro + i0];
-          const float lm = anext * (float)(1.0 - qe), lx = anext * ((float)qe * (1.f / 3.f));
+          S lm, lx;
+          if constexpr (F64) {                          // k_fast64's coefficients
+            const double a = (1.0 - d) - z;
+            double anext = 1.0, bnext = 0.0;
+            if (i0 + 1 < m) {
+              anext = (1.0 - s_lut[E.iq[ro + i0 + 1]]) - s_lut[E.dq[ro + i0 + 1]];
+              bnext = 1.0 - s_lut[E.gq[ro + i0 + 1]];
+            }
+            be[k] = 1.0 - e; dl[k] = d / a; ep[k] = e; zp[k] = bnext * z / anext;
+            lm = anext * (1.0 - qe); lx = anext * (qe / 3.0);
+          } else {                                      // k_fast's coefficients
+            const float a = (float)((1.0 - d) - z);
+            float anext = 1.f, bnext = 0.f;
+            if (i0 + 1 < m) {
+              anext = (float)((1.0 - s_lut[E.iq[ro + i0 + 1]]) - s_lut[E.dq[ro + i0 + 1]]);
+              bnext = (float)(1.0 - s_lut[E.gq[ro + i0 + 1]]);
+            }
+            be[k] = (float)(1.0 - e);
+            dl[k] = __fdividef((float)d, a);
+            ep[k] = (float)e;
+            zp[k] = __fdividef(bnext * (float)z, anext);
+            lm = anext * (float)(1.0 - qe); lx = anext * ((float)qe * (1.f / 3.f));
+          }
 #pragma unroll
           for (int c = 0; c < 5; ++c) lam[c][kk] = (rc == c || rc == 4 || c == 4) ? lm : lx;
         } else {                                        // accumulator position
-          be[k] = 1.f; dl[k] = 0.f; ep[k] = 1.f; zp[k] = 1.f;
+          be[k] = 1; dl[k] = 0; ep[k] = 1; zp[k] = 1;
 #pragma unroll
-          for (int c = 0; c < 5; ++c) lam[c][kk] = 1.f;
+          for (int c = 0; c < 5; ++c) lam[c][kk] = 1;
         }
       }
 #pragma unroll
-      for (int c = 0; c < 5; ++c)
-        Et[(c * K4 + k4) * P + t] = make_float4(lam[c][0], lam[c][1], lam[c][2], lam[c][3]);
+      for (int c = 0; c < 5; ++c) Et[(c * KE + ke) * P + t] = A::pack(lam[c]);
     }
 
     // ---- row codes of both lanes into shared memory (row 0 = idle code N|N), and the
     // unit's window starts: every row where a haplotype begins in either lane, plus the
-    // row after each lane's end (its last LAST event).  Events (FIRST for thread t at
-    // step b + t, LAST for thread P-1 at step b + P - 2) fall in windows [b, b + P).
-    const int slot = wib * G + sw;
+    // row after each lane's end.  Events (FIRST for thread t at step b + t, LAST for
+    // thread P-1 at step b + P - 2) fall in windows [b, b + P).
     if (t == 0) reinterpret_cast<unsigned short*>(cd)[0] = 0x0404;
     if (live) {
 #pragma unroll 1
@@ -731,7 +818,6 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
         const int ca = U.cntA, cbn = U.cntB;
         auto lenA = [&](int i) { const int h = shaps[U.list + i].hap; return (int)(E.hoff[h + 1] - E.hoff[h]); };
         auto lenB = [&](int i) { const int h = shaps[U.list + ca + i].hap; return (int)(E.hoff[h + 1] - E.hoff[h]); };
-        // lane starts: rows 1, 1+n1, ..., and the end sentinel (sum + 1)
         while (ia <= ca || ib <= cbn) {
           const int va = ia <= ca ? ra : 0x7fffffff, vb = ib <= cbn ? rb : 0x7fffffff;
           const int v = min(va, vb);
@@ -741,15 +827,11 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
         }
         s_nwin[slot] = nw;
       }
-    } else if (t == 0) {
-      s_nwin[slot] = 0;
-    }
-    if (t == 0) s_unit[slot] = U;
-    if (live) {                                        // per-pair boundary S'/n, read metadata
-      const double sdf = (1.0 - s_lut[E.gq[ro]]) * ldexp(1.0, E.read_scale[r]);
+      // per-pair boundary S'/n (FP32: scale 2^s; FP64 retry: 2^0) and read metadata
+      const double sdf = (1.0 - s_lut[E.gq[ro]]) * (F64 ? 1.0 : ldexp(1.0, E.read_scale[r]));
       for (int e = t; e < U.cntA + U.cntB; e += P) {
         const int h = shaps[U.list + e].hap;
-        s_bs[slot * 2 * kStreamMaxLaneHaps + e] = (float)(sdf / (double)(E.hoff[h + 1] - E.hoff[h]));
+        s_bs[slot * 2 * kStreamMaxLaneHaps + e] = (S)(sdf / (double)(E.hoff[h + 1] - E.hoff[h]));
       }
       if (t == 0) {
         s_meta[slot * 4 + 0] = Lp;
@@ -757,38 +839,45 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
         s_meta[slot * 4 + 2] = __float_as_int(E.read_gsum[r]);
         s_meta[slot * 4 + 3] = m;
       }
+    } else if (t == 0) {
+      s_nwin[slot] = 0;
     }
-    if (t == 0) s_nband[slot] = 0;
+    if (t == 0) {
+      s_unit[slot] = U;
+      s_nband[slot] = 0;
+      s_flag[2 * slot] = 0u;
+      s_flag[2 * slot + 1] = 0u;
+    }
     s_hc[2 * threadIdx.x] = -1;                         // current haplotype per lane
     s_hc[2 * threadIdx.x + 1] = -1;
     __syncwarp();
 
     // ---- the stream
-    float2 cb = zero2;                                  // thread 0: boundary D of row s
-    float2 nbM = zero2, nbI = zero2, nbD = zero2;
+    V cb = zero2;                                       // thread 0: boundary D of row s
+    V nbM = zero2, nbI = zero2, nbD = zero2;
     unsigned code = 0x0404u;
     auto ld_code = [&](int s) -> unsigned { return (t == 0 && s <= rows) ? (unsigned)cd16[s] : 0x0404u; };
     unsigned pf1 = ld_code(1), pf2 = ld_code(2);
 
-    // FIRST(lane L): reset the lane to row 0 of its next haplotype.  Event paths run
-    // only inside windows and reload what they need instead of pinning registers.
-    auto first_event = [&](auto lconst, float2& dgM, float2& dgI, float2& dgD) {
+    // FIRST(lane L): reset the lane to row 0 of its next haplotype (event paths only run
+    // inside windows and read their inputs from shared memory)
+    auto first_event = [&](auto lconst, V& dgM, V& dgI, V& dgD) {
       constexpr int L = decltype(lconst)::value;
       const int hc = ++s_hc[2 * threadIdx.x + L];
       const int lp = s_meta[slot * 4 + 0];
-      const float b = s_bs[slot * 2 * kStreamMaxLaneHaps + (L == 0 ? 0 : s_unit[slot].cntA) + hc];
+      const S b = s_bs[slot * 2 * kStreamMaxLaneHaps + (L == 0 ? 0 : s_unit[slot].cntA) + hc];
 #pragma unroll
       for (int k = 0; k < K; ++k) {
-        lane_ref<L>(M[k]) = 0.f;
-        lane_ref<L>(I[k]) = 0.f;
-        lane_ref<L>(D[k]) = (t * K + k < lp) ? b : 0.f;
+        lane_ref<L>(M[k]) = 0;
+        lane_ref<L>(I[k]) = 0;
+        lane_ref<L>(D[k]) = (t * K + k < lp) ? b : (S)0;
       }
-      lane_ref<L>(dgM) = 0.f;
-      lane_ref<L>(dgI) = 0.f;
-      lane_ref<L>(dgD) = (t == 0 || t * K - 1 < lp) ? b : 0.f;
+      lane_ref<L>(dgM) = 0;
+      lane_ref<L>(dgI) = 0;
+      lane_ref<L>(dgD) = (t == 0 || t * K - 1 < lp) ? b : (S)0;
       if (t == 0) {
         lane_ref<L>(cb) = b;
-        lane_ref<L>(nbM) = 0.f; lane_ref<L>(nbI) = 0.f; lane_ref<L>(nbD) = b;
+        lane_ref<L>(nbM) = 0; lane_ref<L>(nbI) = 0; lane_ref<L>(nbD) = b;
       }
     };
     // LAST(lane L), thread P-1: the accumulator position holds the pair's sum
@@ -797,28 +886,44 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
       const StreamUnit& SU = s_unit[slot];
       const int hc = s_hc[2 * threadIdx.x + L];
       const StreamHap sh = shaps[SU.list + (L == 0 ? 0 : SU.cntA) + hc];
-      const int n = (int)(E.hoff[sh.hap + 1] - E.hoff[sh.hap]);
-      const float res = (lane_ref<L>(D[K - 1]) + lane_ref<L>(M[K - 1])) +
-                        (lane_ref<L>(M[K - 2]) + lane_ref<L>(I[K - 2]));
-      const int sc = s_meta[slot * 4 + 1];
-      if (fast_finish_g(E, res, sh.pair, SU.read, sh.hap, n, s_meta[slot * 4 + 3], sc,
-                        __int_as_float(s_meta[slot * 4 + 2]), false, true)) {
-        // guard band: queue for the bit-exact rerun this warp does after the unit
-        const ExactItem it{sh.pair, SU.read, sh.hap, sc};
-        const int c = s_nband[slot];
-        if (c < kStreamBandCap && atomicAdd(E.band_inline, 1) < E.band_budget) {
-          s_band[slot * kStreamBandCap + c] = it;
-          s_nband[slot] = c + 1;
+      const S res = (lane_ref<L>(D[K - 1]) + lane_ref<L>(M[K - 1])) +
+                    (lane_ref<L>(M[K - 2]) + lane_ref<L>(I[K - 2]));
+      if constexpr (F64) {
+        // FP64 retry result; near/below the f64 flush floor -> bit-exact FP64 kernel
+        if (res >= 0x1p-900 && isfinite(res)) {
+          E.acc[sh.pair] = res;
+          E.status[sh.pair] = kStatusOk | kStatusRetriedF64;
+        } else {
+          append_item(E.ex64, E.ex64_count, E.list_cap, exact_slot_for(s_meta[slot * 4 + 3]),
+                      ExactItem{sh.pair, SU.read, sh.hap, 0});
         }
-        else append_item(E.ex32, E.ex32_count, E.list_cap, exact_slot_for(s_meta[slot * 4 + 3]), it);
+      } else {
+        const int n = (int)(E.hoff[sh.hap + 1] - E.hoff[sh.hap]);
+        const int sc = s_meta[slot * 4 + 1];
+        const int mm = s_meta[slot * 4 + 3];
+        const int v = stream_finish32(E, res, sh.pair, n, __int_as_float(s_meta[slot * 4 + 2]), sc);
+        if (v == 1) {
+          // guard band: queue for the bit-exact rerun this warp does after the unit
+          const ExactItem it{sh.pair, SU.read, sh.hap, sc};
+          const int c = s_nband[slot];
+          if (c < kStreamBandCap && atomicAdd(E.band_inline, 1) < E.band_budget) {
+            s_band[slot * kStreamBandCap + c] = it;
+            s_nband[slot] = c + 1;
+          } else {
+            append_item(E.ex32, E.ex32_count, E.list_cap, exact_slot_for(mm), it);
+          }
+        } else if (v == 2) {
+          if (E.r64_units && r64_geom_for(mm) >= 0) s_flag[2 * slot + L] |= 1u << hc;   // FP64 stream retry
+          else append_item(E.fx64, E.fx64_count, E.list_cap, exact_slot_for(mm), ExactItem{sh.pair, SU.read, sh.hap, 0});
+        }
       }
     };
 
     auto step = [&](const int s, auto checked) {
       constexpr bool CHECK = decltype(checked)::value;
-      float2 dgM = nbM, dgI = nbI, dgD = nbD;
+      V dgM = nbM, dgI = nbI, dgD = nbD;
       {
-        const float2 lm = M[K - 1], li = I[K - 1], ld = D[K - 1];
+        const V lm = M[K - 1], li = I[K - 1], ld = D[K - 1];
         nbM.x = __shfl_up_sync(FULL, lm.x, 1, P);
         nbM.y = __shfl_up_sync(FULL, lm.y, 1, P);
         nbI.x = __shfl_up_sync(FULL, li.x, 1, P);
@@ -836,32 +941,32 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
         if (code & (kCodeFirst << 8)) first_event(std::integral_constant<int, 1>{}, dgM, dgI, dgD);
       }
       const int cA = code & 7, cB = (code >> 8) & 7;
-      const float4* EA = Et + (cA * K4) * P + t;
-      const float4* EB = Et + (cB * K4) * P + t;
+      const EV* EA = Et + (cA * KE) * P + t;
+      const EV* EB = Et + (cB * KE) * P + t;
       // pass 1 (descending): D' from the previous row, M from the previous-row diagonal
 #pragma unroll
-      for (int k4 = K4 - 1; k4 >= 0; --k4) {
-        const float4 la = EA[k4 * P];
-        const float4 lb = EB[k4 * P];
+      for (int ke = KE - 1; ke >= 0; --ke) {
+        const EV la = EA[ke * P];
+        const EV lb = EB[ke * P];
 #pragma unroll
-        for (int kk = 3; kk >= 0; --kk) {
-          const int k = k4 * 4 + kk;
-          D[k] = fma2s(ep[k], D[k], mul2s(zp[k], M[k]));
-          const float2 pm = (k > 0) ? M[k - 1] : dgM;
-          const float2 pi = (k > 0) ? I[k - 1] : dgI;
-          const float2 pd = (k > 0) ? D[k - 1] : dgD;
-          float2 x = fma2s(be[k], pi, pd);
-          x = __fadd2_rn(pm, x);
-          M[k].x = comp(la, kk) * x.x;
-          M[k].y = comp(lb, kk) * x.y;
+        for (int kk = EW - 1; kk >= 0; --kk) {
+          const int k = ke * EW + kk;
+          D[k] = A::fma(ep[k], D[k], A::mul(zp[k], M[k]));
+          const V pm = (k > 0) ? M[k - 1] : dgM;
+          const V pi = (k > 0) ? I[k - 1] : dgI;
+          const V pd = (k > 0) ? D[k - 1] : dgD;
+          V x = A::fma(be[k], pi, pd);
+          x = A::add(pm, x);
+          M[k].x = A::comp(la, kk) * x.x;
+          M[k].y = A::comp(lb, kk) * x.y;
         }
       }
       // pass 2 (ascending): I chain along the read within the current row
       {
-        float2 lM = nbM, lI = nbI;
+        V lM = nbM, lI = nbI;
 #pragma unroll
         for (int k = 0; k < K; ++k) {
-          I[k] = fma2s(ep[k], lI, mul2s(dl[k], lM));
+          I[k] = A::fma(ep[k], lI, A::mul(dl[k], lM));
           lM = M[k];
           lI = I[k];
         }
@@ -891,17 +996,59 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
       for (; s < wend; ++s) step(s, std::true_type{});
     }
     __syncwarp();
-    // guard-band pairs found in this unit: bit-exact FP32 rerun by the same warp (same
-    // tiling; the emission-table slot is free again), overlapping other warps' work
-    const int nbd = s_nband[slot];
-    const int nbmax = __reduce_max_sync(FULL, (unsigned)nbd);
+    if constexpr (!F64) {
+      // FP32-underflowed pairs of this unit -> FP64 stream retry unit(s) for the same read
+      if (t == 0 && live && (s_flag[2 * slot] | s_flag[2 * slot + 1])) {
+        const int g64 = r64_geom_for(m);
+        const int cap = r64_cap(g64);
+        int lanes_n[2] = {0, 0}, rows_n[2] = {0, 0};
+        StreamHap buf[2][kStreamMaxLaneHaps];
+        auto emit = [&]() {
+          const int tot = lanes_n[0] + lanes_n[1];
+          if (tot == 0) return;
+          const int ui = atomicAdd(&E.r64_count[g64], 1);
+          const int hi = atomicAdd(E.r64_hap_count, tot);
+          if (ui < E.r64_unit_cap && hi + tot <= E.r64_hap_cap) {
+            for (int x = 0; x < lanes_n[0]; ++x) E.r64_haps[hi + x] = buf[0][x];
+            for (int x = 0; x < lanes_n[1]; ++x) E.r64_haps[hi + lanes_n[0] + x] = buf[1][x];
+            E.r64_units[g64][ui] = StreamUnit{r, hi, lanes_n[0], lanes_n[1], rows_n[0], rows_n[1], 0, 0};
+          } else {                                  // list overflow: per-pair FP64 kernel
+            for (int ln = 0; ln < 2; ++ln)
+              for (int x = 0; x < lanes_n[ln]; ++x)
+                append_item(E.fx64, E.fx64_count, E.list_cap, exact_slot_for(m),
+                            ExactItem{buf[ln][x].pair, r, buf[ln][x].hap, 0});
+          }
+          lanes_n[0] = lanes_n[1] = 0;
+          rows_n[0] = rows_n[1] = 0;
+        };
+        for (int ln = 0; ln < 2; ++ln) {
+          unsigned msk = s_flag[2 * slot + ln];
+          const int e0 = U.list + (ln ? U.cntA : 0);
+          while (msk) {
+            const int e = __ffs(msk) - 1;
+            msk &= msk - 1;
+            const StreamHap sh = shaps[e0 + e];
+            const int n = (int)(E.hoff[sh.hap + 1] - E.hoff[sh.hap]);
+            int l2 = rows_n[0] <= rows_n[1] ? 0 : 1;
+            if (rows_n[l2] + n > cap || lanes_n[l2] >= kStreamMaxLaneHaps) { emit(); l2 = 0; }
+            buf[l2][lanes_n[l2]++] = sh;
+            rows_n[l2] += n;
+          }
+        }
+        emit();
+      }
+      // guard-band pairs found in this unit: bit-exact FP32 rerun by the same warp (same
+      // tiling; the emission-table slot is free again), overlapping other warps' work
+      const int nbd = s_nband[slot];
+      const int nbmax = __reduce_max_sync(FULL, (unsigned)nbd);
 #pragma unroll 1
-    for (int x = 0; x < nbmax; ++x) {
-      const bool mine = x < nbd;
-      const ExactItem it = mine ? s_band[slot * kStreamBandCap + x]
-                                : ExactItem{-1, U.read, shaps[U.list].hap, 0};
-      exact_item<float, P, K>(E, it, mine, s_lut, reinterpret_cast<float*>(Et), nullptr, nullptr, 0, t);
-      __syncwarp();
+      for (int x = 0; x < nbmax; ++x) {
+        const bool mine = x < nbd;
+        const ExactItem it = mine ? s_band[slot * kStreamBandCap + x]
+                                  : ExactItem{-1, U.read, shaps[U.list].hap, 0};
+        exact_item<float, P, K>(E, it, mine, s_lut, reinterpret_cast<float*>(Et), nullptr, nullptr, 0, t);
+        __syncwarp();
+      }
     }
   }
 }
