@@ -1,0 +1,132 @@
+"""GPU parity of the read-stationary streaming kernels (k_stream FP32 + FP64 retry units)
+on inputs built to hit their edge cases: haplotypes of length 1..2 (event windows that
+overlap), one-haplotype batches (an empty lane), batches with more haplotypes than one
+unit holds (unit splitting), lanes of very different total length, every tiling width,
+degenerate reads inside streams, and units where only some lanes underflow (partial FP64
+retry units).  Checked against the C oracle (pinned bit-exactly to the reference by
+tests/test_oracle_golden.py) with the north_star bars of test_gpu_parity.py."""
+import numpy as np
+import pytest
+
+from oracle import oracle
+from paper_2411_11547_b200 import _native, default_configs
+from paper_2411_11547_b200.model import FlatBatches
+from paper_2411_11547_b200.pipeline import config_tuples
+
+pytestmark = pytest.mark.gpu
+
+REL_TOL = 1e-4
+RETRY_REL_TOL = 1e-9
+F32 = config_tuples(default_configs("f32"))
+KIND = _native.ST_KIND_MASK
+
+
+def _flat(rng, batches):
+    """batches: list of (read_lengths, hap_lengths, mode); mode 'derived' makes reads
+    substrings of the first haplotype (high likelihood), 'random' independent bases
+    (FP32 underflow for long pairs), 'degenerate' ins+del qualities that sum past 1."""
+    rb, bq, iq, dq, gq, hb = [], [], [], [], [], []
+    rlen, hlen, bro, bho = [], [], [0], [0]
+    for reads, haps, mode in batches:
+        base = rng.integers(0, 4, size=max(haps) + max(reads), dtype=np.int8)
+        for n in haps:
+            h = base[:n].copy()
+            hits = rng.random(n) < 0.01
+            h[hits] = (h[hits] + 1) % 4
+            hb.append(h)
+            hlen.append(n)
+        for m in reads:
+            if mode == "random":
+                r = rng.integers(0, 4, size=m, dtype=np.int8)
+            else:
+                start = int(rng.integers(0, max(1, min(haps) - m + 1))) if m <= min(haps) else 0
+                r = base[start:start + m].copy()
+            rb.append(r)
+            bq.append(rng.integers(10, 41, size=m).astype(np.uint8))
+            if mode == "degenerate":
+                iq.append(np.full(m, 2, np.uint8)); dq.append(np.full(m, 2, np.uint8))
+            else:
+                iq.append(rng.integers(30, 46, size=m).astype(np.uint8))
+                dq.append(rng.integers(30, 46, size=m).astype(np.uint8))
+            gq.append(np.full(m, 10, np.uint8))
+            rlen.append(m)
+        bro.append(bro[-1] + len(reads))
+        bho.append(bho[-1] + len(haps))
+    cat = np.concatenate
+    return FlatBatches(read_bases=cat(rb), bq=cat(bq), iq=cat(iq), dq=cat(dq), gq=cat(gq),
+                       read_off=np.concatenate([[0], np.cumsum(rlen)]).astype(np.int64),
+                       hap_bases=cat(hb), hap_off=np.concatenate([[0], np.cumsum(hlen)]).astype(np.int64),
+                       batch_read_off=np.asarray(bro, np.int64), batch_hap_off=np.asarray(bho, np.int64))
+
+
+def _check(engine, flat):
+    ofl = oracle.Flat(**flat.as_dict())
+    ref32, k32 = oracle.score(ofl, "f32")
+    # plain FP32 semantics: identical flag set, values within 1e-4
+    s, st, _ = engine.score(flat, F32, 0)
+    assert np.array_equal(st & KIND, k32)
+    ok = k32 == 0
+    assert np.all(np.isfinite(s[ok])) and np.all(np.isnan(s[~ok]))
+    if ok.any():
+        assert (np.abs(s[ok] - ref32[ok]) / np.abs(ref32[ok])).max() <= REL_TOL
+    # FP64 retry: exactly the reference's FP32 flag set retried, values within 1e-9
+    s, st, _ = engine.score(flat, F32, _native.FLAG_RETRY_F64)
+    flagged = k32 == 1
+    assert np.array_equal((st & _native.ST_RETRIED_F64) != 0, flagged)
+    rest = ~flagged
+    assert np.array_equal(st[rest] & KIND, k32[rest])
+    okr = rest & (k32 == 0)
+    if okr.any():
+        assert (np.abs(s[okr] - ref32[okr]) / np.abs(ref32[okr])).max() <= REL_TOL
+    if flagged.any():
+        pr, ph = flat.pair_index()
+        idx = np.flatnonzero(flagged)
+        acc64, st64 = oracle.score_raw(ofl, "f64", 0, pairs=(pr[idx], ph[idx]))
+        ref64 = oracle.finish(acc64, st64, 0)
+        assert np.array_equal(st[idx] & KIND, st64)
+        fin = st64 == 0
+        if fin.any():
+            assert (np.abs(s[idx][fin] - ref64[fin]) / np.abs(ref64[fin])).max() <= RETRY_REL_TOL
+    return k32
+
+
+def test_tiny_haplotypes_overlapping_windows(engine, rng):
+    # haplotypes of 1..3 rows: FIRST/LAST events of consecutive pairs inside one window
+    flat = _flat(rng, [([30, 31, 7], [1, 2, 3, 1, 2, 40, 1], "derived"),
+                       ([100, 1, 2], [2, 1, 1, 1, 5], "derived"),
+                       ([63, 64], [1] * 20, "random")])
+    _check(engine, flat)
+
+
+def test_single_haplotype_batches_empty_lane(engine, rng):
+    flat = _flat(rng, [([m], [n], "derived") for m, n in [(5, 9), (50, 300), (127, 128), (250, 600),
+                                                         (255, 40), (400, 450), (511, 700)]])
+    _check(engine, flat)
+
+
+def test_many_haplotypes_split_units_and_unbalanced_lanes(engine, rng):
+    # 40 haplotypes per read (> 2 x 15 per unit), lengths spread 1..600
+    haps = [int(x) for x in rng.integers(1, 601, size=40)]
+    haps[3] = 600
+    haps[7] = 1
+    flat = _flat(rng, [([60, 180, 250], haps, "derived"), ([120], [600, 5, 5, 5, 5], "derived")])
+    _check(engine, flat)
+
+
+def test_every_tiling_width(engine, rng):
+    # read lengths across all single-stripe widths W = 16 .. 512 and their edges
+    ms = [1, 14, 15, 16, 31, 32, 47, 48, 63, 64, 95, 96, 127, 128, 191, 192, 255, 256, 383, 384, 511]
+    flat = _flat(rng, [([m, max(1, m // 2)], [int(x) for x in rng.integers(50, 400, size=5)], "derived")
+                       for m in ms])
+    _check(engine, flat)
+
+
+def test_partial_underflow_units_and_degenerate_reads(engine, rng):
+    # 'random' reads underflow against long haplotypes but not short ones: FP64 retry
+    # units hold a subset of each lane; degenerate reads share batches with normal ones
+    flat = _flat(rng, [([200, 220, 90], [20, 30, 400, 500, 600, 10, 550], "random"),
+                       ([150, 150], [300, 310, 320, 330], "degenerate"),
+                       ([240, 16, 250], [250, 260, 270, 280, 290, 300], "derived"),
+                       ([180], [40, 60, 80, 590, 595, 600, 50, 70, 90, 100], "random")])
+    k32 = _check(engine, flat)
+    assert (k32 == 1).any() and (k32 == 0).any() and (k32 == 3).any()
