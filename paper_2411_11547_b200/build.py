@@ -13,7 +13,7 @@ DEPS = SOURCES + [os.path.join(HERE, "csrc", "phmm_kernels.cuh"), os.path.join(R
 OUT = os.path.join(HERE, "_lib", "libphmm.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-         "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-warn-spills"]
+         "-Xcompiler", "-fPIC", "-Xcompiler", "-pthread", "-shared", "-Xptxas", "-warn-spills"]
 
 
 def up_to_date() -> bool:

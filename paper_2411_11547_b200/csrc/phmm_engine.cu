@@ -13,6 +13,7 @@
 #include <cstring>
 #include <numeric>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/phmm.h"
@@ -47,7 +48,8 @@ const FastGeom kFastGeoms[] = {{4, 4},  {4, 8},   {4, 12},  {4, 16},  {8, 8},   
 constexpr int kNumFastGeoms = sizeof(kFastGeoms) / sizeof(kFastGeoms[0]);
 constexpr int kExactP[kNumExactP] = {4, 8, 16, 32};
 constexpr int kThreads = 128;
-constexpr int kBinCounters = 64;          // fixed counter slots before the per-bin counters
+constexpr int kBinCounters = 64;
+constexpr int kFinishThreads = 8;         // host threads finishing log10 in phmm_fetch          // fixed counter slots before the per-bin counters
 
 struct Bin {
   int geom, Q;
@@ -129,30 +131,6 @@ int stream_cap(int P) {
   return P == 4 ? StreamCap<4>::value : P == 8 ? StreamCap<8>::value : P == 16 ? StreamCap<16>::value
                                                                              : StreamCap<32>::value;
 }
-
-template <typename T, int P>
-void launch_exact(dim3 g, size_t smem, cudaStream_t s, const EngineDev& E, int slot, int* ctr, void* col,
-                  int rows) {
-  k_exact<T, P, kExactK><<<g, kThreads, smem, s>>>(E, slot, ctr, (T*)col, rows);
-}
-typedef void (*ExactLaunch)(dim3, size_t, cudaStream_t, const EngineDev&, int, int*, void*, int);
-const ExactLaunch kExact32[kNumExactP] = {launch_exact<float, 4>, launch_exact<float, 8>,
-                                          launch_exact<float, 16>, launch_exact<float, 32>};
-const ExactLaunch kExact64[kNumExactP] = {launch_exact<double, 4>, launch_exact<double, 8>,
-                                          launch_exact<double, 16>, launch_exact<double, 32>};
-const void* kExact32Fn[kNumExactP] = {(const void*)k_exact<float, 4, kExactK>, (const void*)k_exact<float, 8, kExactK>,
-                                      (const void*)k_exact<float, 16, kExactK>, (const void*)k_exact<float, 32, kExactK>};
-const void* kExact64Fn[kNumExactP] = {(const void*)k_exact<double, 4, kExactK>, (const void*)k_exact<double, 8, kExactK>,
-                                      (const void*)k_exact<double, 16, kExactK>, (const void*)k_exact<double, 32, kExactK>};
-
-template <int P>
-void launch_fast64(dim3 g, size_t smem, cudaStream_t s, const EngineDev& E, int slot, int* ctr, void* col,
-                   int rows) {
-  k_fast64<P, kExactK><<<g, kThreads, smem, s>>>(E, slot, ctr, (double*)col, rows);
-}
-const ExactLaunch kFast64[kNumExactP] = {launch_fast64<4>, launch_fast64<8>, launch_fast64<16>, launch_fast64<32>};
-const void* kFast64Fn[kNumExactP] = {(const void*)k_fast64<4, kExactK>, (const void*)k_fast64<8, kExactK>,
-                                     (const void*)k_fast64<16, kExactK>, (const void*)k_fast64<32, kExactK>};
 
 int exact_slot_host(int m) { return (m + 1 <= 32) ? 0 : (m + 1 <= 64) ? 1 : (m + 1 <= 128) ? 2 : 3; }
 
@@ -266,6 +244,9 @@ struct phmm_ctx {
   DBuf<float2> d_colf;
   DBuf<double> d_cold;
   int* h_counts = nullptr;   // pinned: initial list counts (8) + zeros for work counters
+  double* h_acc = nullptr;   // pinned result staging (phmm_fetch)
+  uint8_t* h_st = nullptr;
+  int64_t h_res_cap = 0;
 
   // plan (host)
   bool prepared = false, executed = false;
@@ -357,11 +338,12 @@ int phmm_create(phmm_ctx** out, int device, const double* phred_lut) {
     CK(cudaFuncSetAttribute(kStreamFn[g], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)stream_smem(g)));
   for (int g = 0; g < kNumR64Geoms; ++g)
     CK(cudaFuncSetAttribute(kStream64Fn[g], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)stream64_smem(g)));
-  for (int s = 0; s < kNumExactP; ++s) {
-    CK(cudaFuncSetAttribute(kExact32Fn[s], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)exact_smem(s, 4)));
-    CK(cudaFuncSetAttribute(kExact64Fn[s], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)exact_smem(s, 8)));
-    CK(cudaFuncSetAttribute(kFast64Fn[s], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)exact_smem(s, 8)));
-  }
+  CK(cudaFuncSetAttribute((const void*)k_exact_all<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)exact_smem(0, 4)));
+  CK(cudaFuncSetAttribute((const void*)k_exact_all<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)exact_smem(0, 8)));
+  CK(cudaFuncSetAttribute((const void*)k_fast64_all, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)exact_smem(0, 8)));
   return PHMM_SUCCESS;
 }
 
@@ -378,6 +360,8 @@ int phmm_destroy(phmm_ctx* ctx) {
   ctx->d_r64h.release(); ctx->d_colf.release(); ctx->d_cold.release();
   for (int s = 0; s < kNumExactP; ++s) { ctx->d_ex32[s].release(); ctx->d_ex64[s].release(); ctx->d_fx64[s].release(); }
   if (ctx->h_counts) cudaFreeHost(ctx->h_counts);
+  if (ctx->h_acc) cudaFreeHost(ctx->h_acc);
+  if (ctx->h_st) cudaFreeHost(ctx->h_st);
   ctx->h_counts = nullptr;
   if (ctx->ev_start) cudaEventDestroy(ctx->ev_start);
   if (ctx->ev_fast0) cudaEventDestroy(ctx->ev_fast0);
@@ -428,16 +412,9 @@ int phmm_prepare(phmm_ctx* ctx, const phmm_input* in, const phmm_options* opt, i
   for (int64_t h = 0; h < H; ++h)
     if (hoff[h + 1] <= hoff[h]) return ctx->fail(PHMM_ERR_INVALID, "haplotype %lld must contain at least one base", (long long)h);
   const int64_t RL = R ? roff[R] : 0, HL = H ? hoff[H] : 0;
-  {
-    uint8_t bad = 0;
-    for (int64_t i = 0; i < RL; ++i) bad |= (uint8_t)((uint8_t)in->read_bases[i] > 4);
-    for (int64_t i = 0; i < HL; ++i) bad |= (uint8_t)((uint8_t)in->hap_bases[i] > 4);
-    if (bad) return ctx->fail(PHMM_ERR_INVALID, "base code outside A,C,G,T,N (0..4)");
-    uint8_t mx = 0;
-    for (int64_t i = 0; i < RL; ++i)
-      mx |= (uint8_t)((in->base_qual[i] > 93) | (in->ins_qual[i] > 93) | (in->del_qual[i] > 93) | (in->gcp_qual[i] > 93));
-    if (mx) return ctx->fail(PHMM_ERR_INVALID, "quality values must be in [0, 93]");
-  }
+  if (RL > 0 && (!in->read_bases || !in->base_qual || !in->ins_qual || !in->del_qual || !in->gcp_qual))
+    return ctx->fail(PHMM_ERR_INVALID, "null read arrays");
+  if (HL > 0 && !in->hap_bases) return ctx->fail(PHMM_ERR_INVALID, "null haplotype bases");
   for (int c = 0; c < opt->num_configs; ++c) {
     if (opt->p[c] < 1 || opt->k[c] < 1 || (opt->precision[c] != 0 && opt->precision[c] != 1) || opt->scale_log2[c] < 0)
       return ctx->fail(PHMM_ERR_INVALID, "invalid config %d", c);
@@ -448,6 +425,25 @@ int phmm_prepare(phmm_ctx* ctx, const phmm_input* in, const phmm_options* opt, i
   ctx->batch_hap_off.assign(in->batch_hap_off, in->batch_hap_off + (B ? B + 1 : 0));
   ctx->hap_len.resize(H);
   for (int64_t h = 0; h < H; ++h) ctx->hap_len[h] = hoff[h + 1] - hoff[h];
+
+  // ---- raw inputs go to the device first (async): the copy overlaps the host planning
+  // below; their content checks run on the device (k_validate) at the end of prepare
+  int64_t bytes = 0;
+  auto up = [&](auto& buf, const auto* src, size_t n) -> cudaError_t {
+    cudaError_t e = buf.ensure(n);
+    if (e != cudaSuccess || n == 0) return e;
+    bytes += (int64_t)(n * sizeof(*src));
+    return cudaMemcpyAsync(buf.p, src, n * sizeof(*src), cudaMemcpyHostToDevice, ctx->stream);
+  };
+  CK(cudaEventRecord(ctx->ev_start, ctx->stream));
+  CK(up(ctx->d_rbases, in->read_bases, RL));
+  CK(up(ctx->d_bq, in->base_qual, RL));
+  CK(up(ctx->d_iq, in->ins_qual, RL));
+  CK(up(ctx->d_dq, in->del_qual, RL));
+  CK(up(ctx->d_gq, in->gcp_qual, RL));
+  CK(up(ctx->d_roff, roff, R ? R + 1 : 0));
+  CK(up(ctx->d_hbases, in->hap_bases, HL));
+  CK(up(ctx->d_hoff, hoff, H ? H + 1 : 0));
 
   // ---- config binding: smallest p*k >= m, ties to fewer lanes (partition.py:20-37)
   std::vector<int> order(opt->num_configs);
@@ -478,7 +474,8 @@ int phmm_prepare(phmm_ctx* ctx, const phmm_input* in, const phmm_options* opt, i
   ctx->bins.clear();
   ctx->sbins.clear();
   ctx->shaps.clear();
-  const bool use_stream = streaming_enabled();
+  // streaming units address reads/haplotypes with 32-bit offsets
+  const bool use_stream = streaming_enabled() && RL < INT32_MAX && HL < INT32_MAX;
   std::vector<int> bin_index(kNumFastGeoms * 64, -1);
   std::vector<int> sbin_index(kNumFastGeoms, -1);
   std::vector<ExactItem> host32[kNumExactP], host64[kNumExactP];
@@ -534,9 +531,11 @@ int phmm_prepare(phmm_ctx* ctx, const phmm_input* in, const phmm_options* opt, i
             su.list = (int)ctx->shaps.size();
             su.cntA = (int)lanes[0].size(); su.cntB = (int)lanes[1].size();
             su.rowsA = rows[0]; su.rowsB = rows[1];
-            su.pad0 = su.pad1 = 0;
+            su.ro = (int)roff[r];
+            su.m = m;
             for (int ln = 0; ln < 2; ++ln)
-              for (int h : lanes[ln]) ctx->shaps.push_back(StreamHap{h, (int)(gid + (h - h0))});
+              for (int h : lanes[ln])
+                ctx->shaps.push_back(StreamHap{h, (int)(gid + (h - h0)), (int)hoff[h], (int)ctx->hap_len[h]});
             sb.units.push_back(su);
             lanes[0].clear(); lanes[1].clear(); rows[0] = rows[1] = 0;
           };
@@ -592,23 +591,7 @@ int phmm_prepare(phmm_ctx* ctx, const phmm_input* in, const phmm_options* opt, i
   auto t1 = std::chrono::steady_clock::now();
   ctx->plan_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
 
-  // ---- upload
-  int64_t bytes = 0;
-  auto up = [&](auto& buf, const auto* src, size_t n) -> cudaError_t {
-    cudaError_t e = buf.ensure(n);
-    if (e != cudaSuccess || n == 0) return e;
-    bytes += (int64_t)(n * sizeof(*src));
-    return cudaMemcpyAsync(buf.p, src, n * sizeof(*src), cudaMemcpyHostToDevice, ctx->stream);
-  };
-  CK(cudaEventRecord(ctx->ev_start, ctx->stream));
-  CK(up(ctx->d_rbases, in->read_bases, RL));
-  CK(up(ctx->d_bq, in->base_qual, RL));
-  CK(up(ctx->d_iq, in->ins_qual, RL));
-  CK(up(ctx->d_dq, in->del_qual, RL));
-  CK(up(ctx->d_gq, in->gcp_qual, RL));
-  CK(up(ctx->d_roff, roff, R ? R + 1 : 0));
-  CK(up(ctx->d_hbases, in->hap_bases, HL));
-  CK(up(ctx->d_hoff, hoff, H ? H + 1 : 0));
+  // ---- plan upload
   CK(up(ctx->d_read_m, ctx->read_m.data(), R));
   CK(up(ctx->d_read_scale, ctx->read_scale.data(), R));
   CK(up(ctx->d_read_ncap, read_ncap.data(), R));
@@ -645,8 +628,23 @@ int phmm_prepare(phmm_ctx* ctx, const phmm_input* in, const phmm_options* opt, i
   if (need_col) CK(ctx->d_colf.ensure(col_elems));
   CK(ctx->d_cold.ensure(col_elems));   // exact kernels (f32 view uses half of it)
   (void)need_cold;
+  // content validation on the device (bases 0..4, qualities 0..93)
+  int* vflag = ctx->d_counters.p + kBinCounters - 1;
+  CK(cudaMemsetAsync(vflag, 0, sizeof(int), ctx->stream));
+  if (RL + HL > 0) {
+    const int64_t work = std::max<int64_t>(RL, HL) / 16 + 1;
+    const int vblocks = (int)std::min<int64_t>(ctx->num_sms * 8, (work + 255) / 256);
+    k_validate<<<vblocks, 256, 0, ctx->stream>>>((const uint8_t*)ctx->d_rbases.p, ctx->d_bq.p, ctx->d_iq.p,
+                                                 ctx->d_dq.p, ctx->d_gq.p, RL, (const uint8_t*)ctx->d_hbases.p,
+                                                 HL, vflag);
+    CK(cudaGetLastError());
+  }
+  CK(cudaMemcpyAsync(ctx->h_counts + kBinCounters - 1, vflag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaEventRecord(ctx->ev_end, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
+  const int vbad = ctx->h_counts[kBinCounters - 1];
+  if (vbad & 1) return ctx->fail(PHMM_ERR_INVALID, "base code outside A,C,G,T,N (0..4)");
+  if (vbad & 2) return ctx->fail(PHMM_ERR_INVALID, "quality values must be in [0, 93]");
   float h2d = 0.f;
   cudaEventElapsedTime(&h2d, ctx->ev_start, ctx->ev_end);
   ctx->h2d_ms = h2d;
@@ -785,15 +783,12 @@ int phmm_execute(phmm_ctx* ctx) {
   // bit-exact FP64 kernels, fed by everything before.
   CK(fork());
   used[0] = true;
-  for (int s = 0; s < kNumExactP; ++s) {
-    kExact32[s](dim3(ctx->num_sms * 2), exact_smem(s, 4), ctx->aux[0], E, s, ctx->d_counters.p + 8 + s,
-                ctx->d_cold.p, ctx->max_n + 1);
-    ++launches;
-  }
-  for (int s = 0; s < kNumExactP; ++s) {
-    if (!(ctx->flags & PHMM_FLAG_RETRY_F64)) break;
-    kFast64[s](dim3(ctx->num_sms * 2), exact_smem(s, 8), ctx->aux[0], E, s, ctx->d_counters.p + 24 + s,
-               ctx->d_cold.p, ctx->max_n + 1);
+  k_exact_all<float><<<ctx->num_sms * 2, kThreads, exact_smem(0, 4), ctx->aux[0]>>>(
+      E, ctx->d_counters.p + 8, (float*)ctx->d_cold.p, ctx->max_n + 1);
+  ++launches;
+  if (ctx->flags & PHMM_FLAG_RETRY_F64) {
+    k_fast64_all<<<ctx->num_sms * 2, kThreads, exact_smem(0, 8), ctx->aux[0]>>>(
+        E, ctx->d_counters.p + 24, ctx->d_cold.p, ctx->max_n + 1);
     ++launches;
   }
   if (ctx->r64_enabled) {
@@ -806,11 +801,9 @@ int phmm_execute(phmm_ctx* ctx) {
     }
   }
   CK(join());
-  for (int s = 0; s < kNumExactP; ++s) {
-    kExact64[s](dim3(ctx->num_sms * 2), exact_smem(s, 8), st, E, s, ctx->d_counters.p + 12 + s,
-                ctx->d_cold.p, ctx->max_n + 1);
-    ++launches;
-  }
+  k_exact_all<double><<<ctx->num_sms * 2, kThreads, exact_smem(0, 8), st>>>(
+      E, ctx->d_counters.p + 12, ctx->d_cold.p, ctx->max_n + 1);
+  ++launches;
   CK(cudaGetLastError());
   CK(cudaEventRecord(ctx->ev_end, st));
   CK(cudaEventSynchronize(ctx->ev_end));
@@ -829,55 +822,93 @@ int phmm_fetch(phmm_ctx* ctx, double* out_log10, uint8_t* out_status, phmm_stats
   if (!ctx->executed) return ctx->fail(PHMM_ERR_STATE, "phmm_fetch before phmm_execute");
   CK(cudaSetDevice(ctx->device));
   const int64_t N = ctx->num_pairs;
-  std::vector<double> acc(N);
-  std::vector<uint8_t> st(N);
+  if (N > ctx->h_res_cap) {                 // pinned staging for the D2H of acc + status
+    if (ctx->h_acc) cudaFreeHost(ctx->h_acc);
+    if (ctx->h_st) cudaFreeHost(ctx->h_st);
+    ctx->h_acc = nullptr; ctx->h_st = nullptr; ctx->h_res_cap = 0;
+    CK(cudaMallocHost(&ctx->h_acc, N * sizeof(double)));
+    CK(cudaMallocHost(&ctx->h_st, N));
+    ctx->h_res_cap = N;
+  }
+  const double* acc = ctx->h_acc;
+  const uint8_t* st = ctx->h_st;
   CK(cudaEventRecord(ctx->ev_start, ctx->stream));
   if (N > 0) {
-    CK(cudaMemcpyAsync(acc.data(), ctx->d_acc.p, N * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
-    CK(cudaMemcpyAsync(st.data(), ctx->d_status.p, N, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpyAsync(ctx->h_acc, ctx->d_acc.p, N * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpyAsync(ctx->h_st, ctx->d_status.p, N, cudaMemcpyDeviceToHost, ctx->stream));
   }
   CK(cudaEventRecord(ctx->ev_end, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
   float d2h = 0.f;
   cudaEventElapsedTime(&d2h, ctx->ev_start, ctx->ev_end);
-  int64_t total_cells = 0, fast = 0, exact = 0, f64 = 0, flagged = 0;
-  int64_t gid = 0;
-  for (int64_t b = 0; b < ctx->num_batches; ++b) {
-    const int64_t r0 = ctx->batch_read_off[b], r1 = ctx->batch_read_off[b + 1];
-    const int64_t h0 = ctx->batch_hap_off[b], h1 = ctx->batch_hap_off[b + 1];
-    for (int64_t r = r0; r < r1; ++r) {
-      const int m = ctx->read_m[r];
-      const int cfg = ctx->read_cfg[r];
-      for (int64_t h = h0; h < h1; ++h, ++gid) {
-        uint8_t s = st[gid];
-        double v = NAN;
-        if (cfg < 0) {
-          s = PHMM_ST_CONFIG_TOO_SMALL;
-        } else {
-          const int kind = s & PHMM_ST_KIND_MASK;
-          const bool retried = (s & PHMM_ST_RETRIED_F64) != 0;
-          if (kind == PHMM_ST_OK) {
-            const double a = acc[gid];
-            if (a <= 0.0 || !std::isfinite(a)) {
-              s = (uint8_t)((s & ~PHMM_ST_KIND_MASK) | PHMM_ST_NUMERIC_OVERFLOW);
-            } else {
-              const int scale = retried ? 0 : ctx->read_scale[r];
-              v = std::log10(a) - scale * kLog10_2;
+  // finishing (wavefront.py:428-434): host glibc log10 (= CPython math.log10), batches
+  // split over a few threads
+  struct Acc { int64_t cells = 0, fast = 0, exact = 0, f64 = 0, flagged = 0; };
+  const int64_t B = ctx->num_batches;
+  std::vector<int64_t> bgid(B + 1, 0);
+  for (int64_t b = 0; b < B; ++b)
+    bgid[b + 1] = bgid[b] + (ctx->batch_read_off[b + 1] - ctx->batch_read_off[b]) *
+                                (ctx->batch_hap_off[b + 1] - ctx->batch_hap_off[b]);
+  auto finish_range = [&](int64_t b0, int64_t b1, Acc* A) {
+    for (int64_t b = b0; b < b1; ++b) {
+      const int64_t r0 = ctx->batch_read_off[b], r1 = ctx->batch_read_off[b + 1];
+      const int64_t h0 = ctx->batch_hap_off[b], h1 = ctx->batch_hap_off[b + 1];
+      int64_t gid = bgid[b];
+      for (int64_t r = r0; r < r1; ++r) {
+        const int m = ctx->read_m[r];
+        const int cfg = ctx->read_cfg[r];
+        for (int64_t h = h0; h < h1; ++h, ++gid) {
+          uint8_t s = st[gid];
+          double v = NAN;
+          if (cfg < 0) {
+            s = PHMM_ST_CONFIG_TOO_SMALL;
+          } else {
+            const int kind = s & PHMM_ST_KIND_MASK;
+            const bool retried = (s & PHMM_ST_RETRIED_F64) != 0;
+            if (kind == PHMM_ST_OK) {
+              const double a = acc[gid];
+              if (a <= 0.0 || !std::isfinite(a)) {
+                s = (uint8_t)((s & ~PHMM_ST_KIND_MASK) | PHMM_ST_NUMERIC_OVERFLOW);
+              } else {
+                const int scale = retried ? 0 : ctx->read_scale[r];
+                v = std::log10(a) - scale * kLog10_2;
+              }
             }
+            const int k2 = s & PHMM_ST_KIND_MASK;
+            if (k2 == PHMM_ST_OK || k2 == PHMM_ST_NUMERIC_OVERFLOW) A->cells += (int64_t)m * ctx->hap_len[h];
+            if (k2 == PHMM_ST_OK) {
+              if (retried) ++A->f64;
+              else if (s & PHMM_ST_EXACT_F32) ++A->exact;
+              else ++A->fast;
+            }
+            if (retried || k2 == PHMM_ST_NUMERIC_OVERFLOW) ++A->flagged;
           }
-          const int k2 = s & PHMM_ST_KIND_MASK;
-          if (k2 == PHMM_ST_OK || k2 == PHMM_ST_NUMERIC_OVERFLOW) total_cells += (int64_t)m * ctx->hap_len[h];
-          if (k2 == PHMM_ST_OK) {
-            if (retried) ++f64;
-            else if (s & PHMM_ST_EXACT_F32) ++exact;
-            else ++fast;
-          }
-          if (retried || k2 == PHMM_ST_NUMERIC_OVERFLOW) ++flagged;
+          if (out_log10) out_log10[gid] = v;
+          if (out_status) out_status[gid] = s;
         }
-        if (out_log10) out_log10[gid] = v;
-        if (out_status) out_status[gid] = s;
       }
     }
+  };
+  const int nth = (int)std::max<int64_t>(1, std::min<int64_t>(kFinishThreads, N / 8192));
+  std::vector<Acc> parts(nth);
+  if (nth == 1) {
+    finish_range(0, B, &parts[0]);
+  } else {
+    std::vector<std::thread> pool;
+    int64_t b = 0;
+    for (int i = 0; i < nth; ++i) {          // equal pair counts per thread
+      const int64_t goal = N * (i + 1) / nth;
+      int64_t e = b;
+      while (e < B && bgid[e + 1] <= goal) ++e;
+      if (i == nth - 1) e = B;
+      pool.emplace_back(finish_range, b, e, &parts[i]);
+      b = e;
+    }
+    for (auto& th : pool) th.join();
+  }
+  int64_t total_cells = 0, fast = 0, exact = 0, f64 = 0, flagged = 0;
+  for (auto& A : parts) {
+    total_cells += A.cells; fast += A.fast; exact += A.exact; f64 += A.f64; flagged += A.flagged;
   }
   if (stats) {
     memset(stats, 0, sizeof(*stats));

@@ -46,9 +46,9 @@ struct StreamUnit {                       // 32 B
   int list;                               // StreamHap entries: lane A [list, list+cntA),
   int cntA, cntB;                         //                    lane B [list+cntA, +cntB)
   int rowsA, rowsB;                       // sum of the lane's haplotype lengths
-  int pad0, pad1;
+  int ro, m;                              // read offset / length (saves a dependent load)
 };
-struct StreamHap { int hap, pair; };
+struct StreamHap { int hap, pair, off, n; };   // haplotype, pair id, base offset, length
 
 struct EngineDev {
   const int8_t* rbases;
@@ -132,6 +132,36 @@ __global__ void k_precompute(EngineDev E, int num_reads) {
     E.read_gsum[r] = (float)(exp(logx) * (2.0 + sg));
     E.read_flags[r] = degen ? 1 : 0;
   }
+}
+
+// ---------------------------------------------------------------------------------
+// k_validate: input content checks of phmm_prepare on the device (model.py:14-18,47-52):
+// base codes in 0..4, Phred qualities in 0..93.  16 B per thread-iteration, byte-wise
+// SIMD compares; flag bit0 = bad base, bit1 = bad quality.
+// ---------------------------------------------------------------------------------
+__device__ __forceinline__ unsigned over4(const uint4 v, unsigned lim) {
+  return __vcmpgtu4(v.x, lim) | __vcmpgtu4(v.y, lim) | __vcmpgtu4(v.z, lim) | __vcmpgtu4(v.w, lim);
+}
+__global__ void k_validate(const uint8_t* rb, const uint8_t* bq, const uint8_t* iq, const uint8_t* dq,
+                           const uint8_t* gq, int64_t RL, const uint8_t* hb, int64_t HL, int* flag) {
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+  unsigned badb = 0, badq = 0;
+  const int64_t RV = RL / 16, HV = HL / 16;
+  for (int64_t v = tid; v < RV; v += nth) {
+    badb |= over4(reinterpret_cast<const uint4*>(rb)[v], 0x04040404u);
+    badq |= over4(reinterpret_cast<const uint4*>(bq)[v], 0x5d5d5d5du) |
+            over4(reinterpret_cast<const uint4*>(iq)[v], 0x5d5d5d5du) |
+            over4(reinterpret_cast<const uint4*>(dq)[v], 0x5d5d5d5du) |
+            over4(reinterpret_cast<const uint4*>(gq)[v], 0x5d5d5d5du);
+  }
+  for (int64_t v = tid; v < HV; v += nth) badb |= over4(reinterpret_cast<const uint4*>(hb)[v], 0x04040404u);
+  for (int64_t i = RV * 16 + tid; i < RL; i += nth) {
+    badb |= rb[i] > 4;
+    badq |= (bq[i] > 93) | (iq[i] > 93) | (dq[i] > 93) | (gq[i] > 93);
+  }
+  for (int64_t i = HV * 16 + tid; i < HL; i += nth) badb |= hb[i] > 4;
+  if (badb || badq) atomicOr(flag, (badb ? 1 : 0) | (badq ? 2 : 0));
 }
 
 // packed helpers: scalar-broadcast operand -> FFMA2 R.F32 form
@@ -719,8 +749,8 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
     const int u = g * G + sw;
     const bool has = u < num_units;
     const StreamUnit U = units[has ? u : g * G];
-    const int r = U.read, m = E.read_m[r];
-    const int64_t ro = E.roff[r];
+    const int r = U.read, m = U.m;
+    const int64_t ro = U.ro;
     const bool degen = (E.read_flags[r] & 1) != 0;
     const bool live = has && !degen;
     const int rows = live ? max(U.rowsA, U.rowsB) : 0;
@@ -802,10 +832,9 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
         int row = 1;
 #pragma unroll 1
         for (int e = 0; e < cnt; ++e) {
-          const int h = shaps[e0 + e].hap;
-          const int64_t h0 = E.hoff[h];
-          const int n = (int)(E.hoff[h + 1] - h0);
-          const int8_t* src = E.hbases + h0;
+          const StreamHap sh = shaps[e0 + e];
+          const int n = sh.n;
+          const int8_t* src = E.hbases + sh.off;
           for (int x = t; x < n; x += P)
             cd[2 * (row + x) + ln] = (unsigned char)(src[x] | (x == 0 ? kCodeFirst : 0) | (x == n - 1 ? kCodeLast : 0));
           row += n;
@@ -816,8 +845,8 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
         int* wb = s_win + slot * kStreamMaxWin;
         int ia = 0, ib = 0, ra = 1, rb = 1, nw = 0;
         const int ca = U.cntA, cbn = U.cntB;
-        auto lenA = [&](int i) { const int h = shaps[U.list + i].hap; return (int)(E.hoff[h + 1] - E.hoff[h]); };
-        auto lenB = [&](int i) { const int h = shaps[U.list + ca + i].hap; return (int)(E.hoff[h + 1] - E.hoff[h]); };
+        auto lenA = [&](int i) { return shaps[U.list + i].n; };
+        auto lenB = [&](int i) { return shaps[U.list + ca + i].n; };
         while (ia <= ca || ib <= cbn) {
           const int va = ia <= ca ? ra : 0x7fffffff, vb = ib <= cbn ? rb : 0x7fffffff;
           const int v = min(va, vb);
@@ -830,8 +859,7 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
       // per-pair boundary S'/n (FP32: scale 2^s; FP64 retry: 2^0) and read metadata
       const double sdf = (1.0 - s_lut[E.gq[ro]]) * (F64 ? 1.0 : ldexp(1.0, E.read_scale[r]));
       for (int e = t; e < U.cntA + U.cntB; e += P) {
-        const int h = shaps[U.list + e].hap;
-        s_bs[slot * 2 * kStreamMaxLaneHaps + e] = (S)(sdf / (double)(E.hoff[h + 1] - E.hoff[h]));
+        s_bs[slot * 2 * kStreamMaxLaneHaps + e] = (S)(sdf / (double)shaps[U.list + e].n);
       }
       if (t == 0) {
         s_meta[slot * 4 + 0] = Lp;
@@ -898,7 +926,7 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
                       ExactItem{sh.pair, SU.read, sh.hap, 0});
         }
       } else {
-        const int n = (int)(E.hoff[sh.hap + 1] - E.hoff[sh.hap]);
+        const int n = sh.n;
         const int sc = s_meta[slot * 4 + 1];
         const int mm = s_meta[slot * 4 + 3];
         const int v = stream_finish32(E, res, sh.pair, n, __int_as_float(s_meta[slot * 4 + 2]), sc);
@@ -988,7 +1016,7 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
       const int e_sw = wi < nwin ? wb[wi] : 0x7fffffff;
       const int e = max((int)__reduce_min_sync(FULL, (unsigned)e_sw), s);
       const int fend = min(e, steps + 1);
-#pragma unroll 1
+#pragma unroll 2
       for (; s < fend; ++s) step(s, std::false_type{});
       if (s > steps) break;
       const int wend = min(e + P, steps + 1);
@@ -1011,7 +1039,7 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
           if (ui < E.r64_unit_cap && hi + tot <= E.r64_hap_cap) {
             for (int x = 0; x < lanes_n[0]; ++x) E.r64_haps[hi + x] = buf[0][x];
             for (int x = 0; x < lanes_n[1]; ++x) E.r64_haps[hi + lanes_n[0] + x] = buf[1][x];
-            E.r64_units[g64][ui] = StreamUnit{r, hi, lanes_n[0], lanes_n[1], rows_n[0], rows_n[1], 0, 0};
+            E.r64_units[g64][ui] = StreamUnit{r, hi, lanes_n[0], lanes_n[1], rows_n[0], rows_n[1], U.ro, m};
           } else {                                  // list overflow: per-pair FP64 kernel
             for (int ln = 0; ln < 2; ++ln)
               for (int x = 0; x < lanes_n[ln]; ++x)
@@ -1028,7 +1056,7 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
             const int e = __ffs(msk) - 1;
             msk &= msk - 1;
             const StreamHap sh = shaps[e0 + e];
-            const int n = (int)(E.hoff[sh.hap + 1] - E.hoff[sh.hap]);
+            const int n = sh.n;
             int l2 = rows_n[0] <= rows_n[1] ? 0 : 1;
             if (rows_n[l2] + n > cap || lanes_n[l2] >= kStreamMaxLaneHaps) { emit(); l2 = 0; }
             buf[l2][lanes_n[l2]++] = sh;
@@ -1061,8 +1089,8 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
 // irrelevant above 2^-900, and results below that are re-run on k_exact<double>.
 // ---------------------------------------------------------------------------------
 template <int P, int K>
-__global__ void __launch_bounds__(128)
-k_fast64(const EngineDev E, int slot, int* __restrict__ counter, double* __restrict__ colbuf, int col_rows) {
+__device__ __forceinline__ void
+fast64_list(const EngineDev& E, int slot, int* __restrict__ counter, double* __restrict__ colbuf, int col_rows) {
   constexpr int W = P * K, G = 32 / P;
   constexpr unsigned FULL = 0xffffffffu;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1072,8 +1100,6 @@ k_fast64(const EngineDev E, int slot, int* __restrict__ counter, double* __restr
   const int sw = lane / P, t = lane % P;
   const int count = min(E.fx64_count[slot], E.list_cap);
   if (count == 0) return;
-  for (int i = threadIdx.x; i < 94; i += blockDim.x) s_lut[i] = E.lut[i];
-  __syncthreads();
   double* Et = s_E + (size_t)((wib * G + sw) * 5 * K) * P;   // Et[(c*K + k)*P + t]
   const int gwarp = blockIdx.x * (blockDim.x >> 5) + wib;
   double* colX = colbuf + (size_t)(gwarp * G + sw) * 2 * 3 * col_rows;
@@ -1200,8 +1226,8 @@ k_fast64(const EngineDev E, int slot, int* __restrict__ counter, double* __restr
 
 // k_exact<T, P, K>: a complete work list (host-provided + appended before launch).
 template <typename T, int P, int K>
-__global__ void __launch_bounds__(128)
-k_exact(const EngineDev E, int slot, int* __restrict__ counter, T* __restrict__ colbuf, int col_rows) {
+__device__ __forceinline__ void
+exact_list(const EngineDev& E, int slot, int* __restrict__ counter, T* __restrict__ colbuf, int col_rows) {
   constexpr int G = 32 / P;
   constexpr bool kIsF32 = sizeof(T) == 4;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1211,8 +1237,6 @@ k_exact(const EngineDev E, int slot, int* __restrict__ counter, T* __restrict__ 
   const int sw = lane / P, t = lane % P;
   const int count = min(kIsF32 ? E.ex32_count[slot] : E.ex64_count[slot], E.list_cap);
   if (count == 0) return;
-  for (int i = threadIdx.x; i < 94; i += blockDim.x) s_lut[i] = E.lut[i];
-  __syncthreads();
   T* Et = s_E + (size_t)((wib * G + sw) * 5 * K) * P;   // Et[(c*K + k)*P + t]
   const int gwarp = blockIdx.x * (blockDim.x >> 5) + wib;
   T* colX = colbuf + (size_t)(gwarp * G + sw) * 2 * 3 * col_rows;
@@ -1228,6 +1252,38 @@ k_exact(const EngineDev E, int slot, int* __restrict__ counter, T* __restrict__ 
     const ExactItem it = items[has ? u : g * G];
     exact_item<T, P, K>(E, it, has, s_lut, Et, colX, colY, col_rows, t);
   }
+}
+
+// Post-pass list kernels: one launch covers the four sub-warp widths P = 4, 8, 16, 32
+// (slot lists filled by the host and by the fast kernels); empty lists cost nothing.
+__device__ __forceinline__ bool post_lists_empty(const int* counts) {
+  return counts[0] == 0 && counts[1] == 0 && counts[2] == 0 && counts[3] == 0;
+}
+template <typename T>
+__global__ void __launch_bounds__(128)
+k_exact_all(const EngineDev E, int* __restrict__ counters, T* __restrict__ colbuf, int col_rows) {
+  constexpr bool kIsF32 = sizeof(T) == 4;
+  if (post_lists_empty(kIsF32 ? E.ex32_count : E.ex64_count)) return;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* s_lut = reinterpret_cast<double*>(smem_raw);
+  for (int i = threadIdx.x; i < 94; i += blockDim.x) s_lut[i] = E.lut[i];
+  __syncthreads();
+  exact_list<T, 4, kExactK>(E, 0, counters + 0, colbuf, col_rows);
+  exact_list<T, 8, kExactK>(E, 1, counters + 1, colbuf, col_rows);
+  exact_list<T, 16, kExactK>(E, 2, counters + 2, colbuf, col_rows);
+  exact_list<T, 32, kExactK>(E, 3, counters + 3, colbuf, col_rows);
+}
+__global__ void __launch_bounds__(128)
+k_fast64_all(const EngineDev E, int* __restrict__ counters, double* __restrict__ colbuf, int col_rows) {
+  if (post_lists_empty(E.fx64_count)) return;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* s_lut = reinterpret_cast<double*>(smem_raw);
+  for (int i = threadIdx.x; i < 94; i += blockDim.x) s_lut[i] = E.lut[i];
+  __syncthreads();
+  fast64_list<4, kExactK>(E, 0, counters + 0, colbuf, col_rows);
+  fast64_list<8, kExactK>(E, 1, counters + 1, colbuf, col_rows);
+  fast64_list<16, kExactK>(E, 2, counters + 2, colbuf, col_rows);
+  fast64_list<32, kExactK>(E, 3, counters + 3, colbuf, col_rows);
 }
 
 }  // namespace phmm
