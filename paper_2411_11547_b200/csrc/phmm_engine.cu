@@ -12,6 +12,10 @@
 #include <cstdlib>
 #include <cstring>
 #include <numeric>
+#include <condition_variable>
+#include <functional>
+#include <memory>
+#include <mutex>
 #include <string>
 #include <thread>
 #include <vector>
@@ -41,6 +45,23 @@ struct DBuf {
   void release() { if (p) cudaFree(p); p = nullptr; cap = 0; }
 };
 
+// std::vector storage in pinned host memory: plan arrays are DMA'd without staging
+template <class T>
+struct PinnedAlloc {
+  using value_type = T;
+  PinnedAlloc() = default;
+  template <class U> PinnedAlloc(const PinnedAlloc<U>&) {}
+  T* allocate(size_t n) {
+    void* p = nullptr;
+    if (cudaMallocHost(&p, n * sizeof(T)) != cudaSuccess) throw std::bad_alloc();
+    return static_cast<T*>(p);
+  }
+  void deallocate(T* p, size_t) { cudaFreeHost(p); }
+  template <class U> bool operator==(const PinnedAlloc<U>&) const { return true; }
+  template <class U> bool operator!=(const PinnedAlloc<U>&) const { return false; }
+};
+template <class T> using PinnedVec = std::vector<T, PinnedAlloc<T>>;
+
 struct FastGeom { int P, K; };
 // single-stripe widths W = P*K: 16 32 48 64 64 96 128 128 192 256 256 384 512
 const FastGeom kFastGeoms[] = {{4, 4},  {4, 8},   {4, 12},  {4, 16},  {8, 8},   {8, 12}, {8, 16},
@@ -49,7 +70,7 @@ constexpr int kNumFastGeoms = sizeof(kFastGeoms) / sizeof(kFastGeoms[0]);
 constexpr int kExactP[kNumExactP] = {4, 8, 16, 32};
 constexpr int kThreads = 128;
 constexpr int kBinCounters = 64;
-constexpr int kFinishThreads = 8;         // host threads finishing log10 in phmm_fetch          // fixed counter slots before the per-bin counters
+constexpr int kFinishThreads = 16;        // host threads finishing log10 in phmm_fetch          // fixed counter slots before the per-bin counters
 
 struct Bin {
   int geom, Q;
@@ -187,20 +208,26 @@ int choose_geom(int m, int nmax, int* Qout) {
 // Streaming tiling for a read of length m whose batch has haplotype lengths summing to
 // `total` (longest `nmax`): units of two lanes of ~total/2 rows, split when a lane would
 // exceed the geometry's row-code capacity.  -1: no single-stripe streaming geometry.
-int choose_stream_geom(int m, int64_t total, int nmax) {
+// cost of streaming a read's haplotypes (total rows, longest nmax) on tiling g (1e300:
+// infeasible or excluded by PHMM_FAST_GEOM)
+int64_t stream_geom_cost(int g, int64_t total, int nmax) {
+  constexpr int64_t kInf = INT64_MAX;
   const int fg = forced_geom();
-  double best = 1e300;
+  if (fg >= 0 && g != fg) return kInf;
+  const int64_t P = kFastGeoms[g].P, K = kFastGeoms[g].K;
+  const int64_t cap = stream_cap((int)P);
+  if (nmax > cap) return kInf;
+  const int64_t units = (total + 2 * cap - 1) / (2 * cap);
+  const int64_t rows = std::min<int64_t>(cap, (total + 2 * units - 1) / (2 * units));
+  return units * P * (2 * K + 5) * (rows + P - 1);     // 2 x (K + 2.5) per thread-row
+}
+int choose_stream_geom(int m, int64_t total, int nmax) {
+  int64_t best = INT64_MAX;
   int bi = -1;
   for (int g = 0; g < kNumFastGeoms; ++g) {
-    if (fg >= 0 && g != fg) continue;
-    const int P = kFastGeoms[g].P, K = kFastGeoms[g].K, W = P * K;
-    if (m + 1 > W) continue;
-    const int cap = stream_cap(P);
-    if (nmax > cap) continue;
-    const double units = std::ceil((double)total / (2.0 * cap));
-    const double rows = std::min<double>(cap, std::ceil((double)total / (2.0 * units)));
-    const double cost = units * P * (K + 2.5) * (rows + P - 1);
-    if (cost < best - 1e-9) { best = cost; bi = g; }
+    if (m + 1 > kFastGeoms[g].P * kFastGeoms[g].K) continue;
+    const int64_t cost = stream_geom_cost(g, total, nmax);
+    if (cost < best) { best = cost; bi = g; }
   }
   return bi;
 }
@@ -213,6 +240,94 @@ bool streaming_enabled() {
   }
   return v == 1;
 }
+
+// Small persistent worker pool for host-side data-parallel loops (result finishing).
+class WorkerPool {
+ public:
+  explicit WorkerPool(int n) {
+    for (int i = 0; i < n; ++i) workers_.emplace_back([this] { loop(); });
+  }
+  ~WorkerPool() {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    for (auto& w : workers_) w.join();
+  }
+  int size() const { return (int)workers_.size(); }
+  // runs fn(i) for i in [0, tasks) on the workers and the caller; returns when all are done
+  void run(int tasks, const std::function<void(int)>& fn) {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      fn_ = &fn;
+      tasks_ = tasks;
+      next_ = 0;
+      done_ = 0;
+      ++gen_;
+    }
+    cv_.notify_all();
+    work();
+    std::unique_lock<std::mutex> lk(mu_);
+    done_cv_.wait(lk, [this] { return done_ == tasks_; });
+    fn_ = nullptr;
+  }
+
+ private:
+  void work() {
+    for (;;) {
+      int i;
+      const std::function<void(int)>* f;
+      {
+        std::lock_guard<std::mutex> lk(mu_);
+        if (!fn_ || next_ >= tasks_) return;
+        i = next_++;
+        f = fn_;
+      }
+      (*f)(i);
+      std::lock_guard<std::mutex> lk(mu_);
+      if (++done_ == tasks_) done_cv_.notify_all();
+    }
+  }
+  void loop() {
+    uint64_t seen = 0;
+    for (;;) {
+      {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [&] { return stop_ || gen_ != seen; });
+        if (stop_) return;
+        seen = gen_;
+      }
+      work();
+    }
+  }
+  std::vector<std::thread> workers_;
+  std::mutex mu_;
+  std::condition_variable cv_, done_cv_;
+  const std::function<void(int)>* fn_ = nullptr;
+  int tasks_ = 0, next_ = 0, done_ = 0;
+  uint64_t gen_ = 0;
+  bool stop_ = false;
+};
+
+// PHMM_TRACE=1: wall-clock breakdown of the host phases on stderr
+struct Trace {
+  bool on;
+  std::chrono::steady_clock::time_point last;
+  std::string buf;
+  Trace() : on(getenv("PHMM_TRACE") != nullptr), last(std::chrono::steady_clock::now()) {}
+  void mark(const char* what) {
+    if (!on) return;
+    auto now = std::chrono::steady_clock::now();
+    char tmp[64];
+    snprintf(tmp, sizeof(tmp), " %s=%.3f", what, std::chrono::duration<double, std::milli>(now - last).count());
+    buf += tmp;
+    last = now;
+  }
+  void print(const char* phase) {
+    if (on) fprintf(stderr, "[phmm %s]%s ms\n", phase, buf.c_str());
+  }
+};
 
 }  // namespace
 
@@ -243,6 +358,7 @@ struct phmm_ctx {
   DBuf<ExactItem> d_ex32[kNumExactP], d_ex64[kNumExactP], d_fx64[kNumExactP];
   DBuf<float2> d_colf;
   DBuf<double> d_cold;
+  std::unique_ptr<WorkerPool> pool;         // host finishing threads (lazy)
   int* h_counts = nullptr;   // pinned: initial list counts (8) + zeros for work counters
   double* h_acc = nullptr;   // pinned result staging (phmm_fetch)
   uint8_t* h_st = nullptr;
@@ -258,11 +374,16 @@ struct phmm_ctx {
   std::vector<Bin> bins;
   struct SBin {
     int geom;
-    std::vector<StreamUnit> units;
-    int64_t dev_off = 0;
+    int64_t count = 0;                      // units of this tiling
+    int64_t dev_off = 0;                    // first unit in h_sunits / d_sunits
   };
   std::vector<SBin> sbins;
-  std::vector<StreamHap> shaps;
+  std::vector<StreamUnit> su_all;           // planning scratch (persistent capacity)
+  std::vector<uint8_t> su_bin;
+  std::vector<int> su_cnt;
+  PinnedVec<StreamHap> shaps;               // persistent capacity (pinned)
+  PinnedVec<StreamUnit> h_sunits;           // LPT-ordered stream units, all bins
+  PinnedVec<int> h_rmeta;                   // read m | scale | ncap
   int host_ex32[kNumExactP] = {0, 0, 0, 0}, host_ex64[kNumExactP] = {0, 0, 0, 0};
   int max_n = 1;
   int flags = 0;
@@ -379,10 +500,21 @@ int phmm_destroy(phmm_ctx* ctx) {
 
 const char* phmm_last_error(const phmm_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
 
+static int prepare_impl(phmm_ctx* ctx, const phmm_input* in, const phmm_options* opt, int64_t* num_pairs_out);
+
 int phmm_prepare(phmm_ctx* ctx, const phmm_input* in, const phmm_options* opt, int64_t* num_pairs_out) {
   if (!ctx) return PHMM_ERR_INVALID;
+  try {
+    return prepare_impl(ctx, in, opt, num_pairs_out);
+  } catch (const std::bad_alloc&) {
+    return ctx->fail(PHMM_ERR_NOMEM, "host allocation failed");
+  }
+}
+
+static int prepare_impl(phmm_ctx* ctx, const phmm_input* in, const phmm_options* opt, int64_t* num_pairs_out) {
   if (!in || !opt) return ctx->fail(PHMM_ERR_INVALID, "null input/options");
   auto t0 = std::chrono::steady_clock::now();
+  Trace trace;
   CK(cudaSetDevice(ctx->device));
   ctx->prepared = false;
   ctx->executed = false;
@@ -426,6 +558,7 @@ int phmm_prepare(phmm_ctx* ctx, const phmm_input* in, const phmm_options* opt, i
   ctx->hap_len.resize(H);
   for (int64_t h = 0; h < H; ++h) ctx->hap_len[h] = hoff[h + 1] - hoff[h];
 
+  trace.mark("validate");
   // ---- raw inputs go to the device first (async): the copy overlaps the host planning
   // below; their content checks run on the device (k_validate) at the end of prepare
   int64_t bytes = 0;
@@ -445,6 +578,7 @@ int phmm_prepare(phmm_ctx* ctx, const phmm_input* in, const phmm_options* opt, i
   CK(up(ctx->d_hbases, in->hap_bases, HL));
   CK(up(ctx->d_hoff, hoff, H ? H + 1 : 0));
 
+  trace.mark("h2d-issue");
   // ---- config binding: smallest p*k >= m, ties to fewer lanes (partition.py:20-37)
   std::vector<int> order(opt->num_configs);
   std::iota(order.begin(), order.end(), 0);
@@ -454,16 +588,22 @@ int phmm_prepare(phmm_ctx* ctx, const phmm_input* in, const phmm_options* opt, i
   });
   ctx->read_m.resize(R); ctx->read_scale.resize(R); ctx->read_cfg.resize(R);
   std::vector<int> read_ncap(R, 1);
+  int64_t memo_m = -1;
+  int memo_cfg = -1;
   for (int64_t r = 0; r < R; ++r) {
     const int64_t m = roff[r + 1] - roff[r];
     if (m > (int64_t)1 << 30) return ctx->fail(PHMM_ERR_INVALID, "read too long");
     ctx->read_m[r] = (int)m;
-    int cfg = -1;
-    for (int c : order)
-      if ((int64_t)opt->p[c] * opt->k[c] >= m) { cfg = c; break; }
-    ctx->read_cfg[r] = cfg;
-    ctx->read_scale[r] = cfg >= 0 ? opt->scale_log2[cfg] : 0;
+    if (m != memo_m) {                               // reads of a batch often share m
+      memo_cfg = -1;
+      for (int c : order)
+        if ((int64_t)opt->p[c] * opt->k[c] >= m) { memo_cfg = c; break; }
+      memo_m = m;
+    }
+    ctx->read_cfg[r] = memo_cfg;
+    ctx->read_scale[r] = memo_cfg >= 0 ? opt->scale_log2[memo_cfg] : 0;
   }
+  trace.mark("bind");
   // ---- pairs, hap pairing, units
   int64_t N = 0;
   for (int64_t b = 0; b < B; ++b)
@@ -473,6 +613,8 @@ int phmm_prepare(phmm_ctx* ctx, const phmm_input* in, const phmm_options* opt, i
   const bool exact_mode = (opt->flags & PHMM_FLAG_EXACT) != 0;
   ctx->bins.clear();
   ctx->sbins.clear();
+  ctx->su_all.clear();
+  ctx->su_bin.clear();
   ctx->shaps.clear();
   // streaming units address reads/haplotypes with 32-bit offsets
   const bool use_stream = streaming_enabled() && RL < INT32_MAX && HL < INT32_MAX;
@@ -482,6 +624,20 @@ int phmm_prepare(phmm_ctx* ctx, const phmm_input* in, const phmm_options* opt, i
   int max_n = 1;
   int64_t gid = 0;
   std::vector<int> hidx;
+  struct LaneTemplate {
+    std::vector<int> lanes[2];
+    int rows[2] = {0, 0};
+  };
+  std::vector<LaneTemplate> tmpls[kNumFastGeoms];
+  bool tvalid[kNumFastGeoms];
+  // geometries by width: choose_stream_geom(m) depends on m only through W >= m + 1
+  int wsort_idx[kNumFastGeoms], wsorted[kNumFastGeoms], best_from[kNumFastGeoms];
+  for (int g = 0; g < kNumFastGeoms; ++g) wsort_idx[g] = g;
+  std::sort(wsort_idx, wsort_idx + kNumFastGeoms, [](int a, int b) {
+    return kFastGeoms[a].P * kFastGeoms[a].K < kFastGeoms[b].P * kFastGeoms[b].K;
+  });
+  for (int i = 0; i < kNumFastGeoms; ++i) wsorted[i] = kFastGeoms[wsort_idx[i]].P * kFastGeoms[wsort_idx[i]].K;
+  if (use_stream) ctx->shaps.reserve(N);
   for (int64_t b = 0; b < B; ++b) {
     const int64_t r0 = ctx->batch_read_off[b], r1 = ctx->batch_read_off[b + 1];
     const int64_t h0 = ctx->batch_hap_off[b], h1 = ctx->batch_hap_off[b + 1];
@@ -493,6 +649,9 @@ int phmm_prepare(phmm_ctx* ctx, const phmm_input* in, const phmm_options* opt, i
       batch_total += ctx->hap_len[h];
     }
     max_n = std::max(max_n, ncap);
+    int tmpl_m = -1, tmpl_geom = -2;
+    std::fill(tvalid, tvalid + kNumFastGeoms, false);
+    std::fill(best_from, best_from + kNumFastGeoms, -2);   // per batch, filled lazily
     hidx.resize(nh);
     std::iota(hidx.begin(), hidx.end(), (int)h0);
     std::stable_sort(hidx.begin(), hidx.end(), [&](int a, int c) { return ctx->hap_len[a] > ctx->hap_len[c]; });
@@ -511,43 +670,62 @@ int phmm_prepare(phmm_ctx* ctx, const phmm_input* in, const phmm_options* opt, i
         continue;
       }
       if (use_stream) {
-        const int sg = choose_stream_geom(m, batch_total, ncap);
-        if (sg >= 0) {
-          // greedy LPT over the length-sorted haplotypes: each to the lighter lane; a new
-          // unit when the lane would exceed the geometry's row capacity
-          const int cap = stream_cap(kFastGeoms[sg].P);
-          int key = sg;
-          if (sbin_index[key] < 0) {
-            sbin_index[key] = (int)ctx->sbins.size();
-            ctx->sbins.push_back(phmm_ctx::SBin{sg, {}, 0});
+        if (m != tmpl_m) {                             // lane template per (batch, geometry)
+          tmpl_m = m;
+          int sg = -1;
+          for (int i = 0; i < kNumFastGeoms; ++i)      // best tiling of the narrowest width >= m+1
+            if (wsorted[i] >= m + 1) {
+              if (best_from[i] == -2) best_from[i] = choose_stream_geom(wsorted[i] - 1, batch_total, ncap);
+              sg = best_from[i];
+              break;
+            }
+          tmpl_geom = sg;
+          if (sg >= 0 && !tvalid[sg]) {
+            tvalid[sg] = true;
+            std::vector<LaneTemplate>& tmpl = tmpls[sg];
+            tmpl.clear();
+            {
+              // greedy LPT over the length-sorted haplotypes: each to the lighter lane; a
+              // new unit when a lane would exceed the geometry's row capacity
+              const int cap = stream_cap(kFastGeoms[sg].P);
+              tmpl.emplace_back();
+              for (int64_t x = 0; x < nh; ++x) {
+                const int h = hidx[x];
+                const int n = (int)ctx->hap_len[h];
+                LaneTemplate* t = &tmpl.back();
+                int ln = t->rows[0] <= t->rows[1] ? 0 : 1;
+                if (t->rows[ln] + n > cap || (int)t->lanes[ln].size() >= kStreamMaxLaneHaps) {
+                  tmpl.emplace_back();
+                  t = &tmpl.back();
+                  ln = 0;
+                }
+                t->lanes[ln].push_back(h);
+                t->rows[ln] += n;
+              }
+            }
           }
-          auto& sb = ctx->sbins[sbin_index[key]];
-          std::vector<int> lanes[2];
-          int rows[2] = {0, 0};
-          auto flush = [&]() {
-            if (lanes[0].empty() && lanes[1].empty()) return;
+        }
+        if (tmpl_geom >= 0) {
+          const std::vector<LaneTemplate>& tmpl = tmpls[tmpl_geom];
+          if (sbin_index[tmpl_geom] < 0) {
+            sbin_index[tmpl_geom] = (int)ctx->sbins.size();
+            ctx->sbins.push_back(phmm_ctx::SBin{tmpl_geom, 0, 0});
+          }
+          const uint8_t sbi = (uint8_t)sbin_index[tmpl_geom];
+          for (const LaneTemplate& t : tmpl) {
             StreamUnit su;
             su.read = (int)r;
             su.list = (int)ctx->shaps.size();
-            su.cntA = (int)lanes[0].size(); su.cntB = (int)lanes[1].size();
-            su.rowsA = rows[0]; su.rowsB = rows[1];
+            su.cntA = (int)t.lanes[0].size(); su.cntB = (int)t.lanes[1].size();
+            su.rowsA = t.rows[0]; su.rowsB = t.rows[1];
             su.ro = (int)roff[r];
             su.m = m;
             for (int ln = 0; ln < 2; ++ln)
-              for (int h : lanes[ln])
+              for (int h : t.lanes[ln])
                 ctx->shaps.push_back(StreamHap{h, (int)(gid + (h - h0)), (int)hoff[h], (int)ctx->hap_len[h]});
-            sb.units.push_back(su);
-            lanes[0].clear(); lanes[1].clear(); rows[0] = rows[1] = 0;
-          };
-          for (int64_t x = 0; x < nh; ++x) {
-            const int h = hidx[x];
-            const int n = (int)ctx->hap_len[h];
-            int ln = rows[0] <= rows[1] ? 0 : 1;
-            if (rows[ln] + n > cap || (int)lanes[ln].size() >= kStreamMaxLaneHaps) { flush(); ln = 0; }
-            lanes[ln].push_back(h);
-            rows[ln] += n;
+            ctx->su_all.push_back(su);
+            ctx->su_bin.push_back(sbi);
           }
-          flush();
           continue;
         }
       }
@@ -580,29 +758,45 @@ int phmm_prepare(phmm_ctx* ctx, const phmm_input* in, const phmm_options* opt, i
     bn.dev_off = nunits;
     nunits += (int64_t)bn.units.size();
   }
-  int64_t nsunits = 0;
-  for (auto& sb : ctx->sbins) {
-    std::stable_sort(sb.units.begin(), sb.units.end(), [](const StreamUnit& a, const StreamUnit& c) {
-      return std::max(a.rowsA, a.rowsB) > std::max(c.rowsA, c.rowsB);
-    });
-    sb.dev_off = nsunits;
-    nsunits += (int64_t)sb.units.size();
+  // LPT order per tiling: one stable counting sort on (bin, descending lane rows)
+  const int nsbins = (int)ctx->sbins.size();
+  const int64_t nsunits = (int64_t)ctx->su_all.size();
+  std::vector<int> bmax(nsbins, 0), bbase(nsbins + 1, 0);
+  for (int64_t i = 0; i < nsunits; ++i) {
+    const StreamUnit& u = ctx->su_all[i];
+    bmax[ctx->su_bin[i]] = std::max(bmax[ctx->su_bin[i]], std::max(u.rowsA, u.rowsB));
   }
+  for (int bi = 0; bi < nsbins; ++bi) bbase[bi + 1] = bbase[bi] + bmax[bi] + 1;
+  auto key = [&](int64_t i) {
+    const StreamUnit& u = ctx->su_all[i];
+    const int bi = ctx->su_bin[i];
+    return bbase[bi] + bmax[bi] - std::max(u.rowsA, u.rowsB);
+  };
+  ctx->su_cnt.assign(bbase[nsbins] + 1, 0);
+  for (int64_t i = 0; i < nsunits; ++i) ++ctx->su_cnt[key(i) + 1];
+  for (int k = 1; k <= bbase[nsbins]; ++k) ctx->su_cnt[k] += ctx->su_cnt[k - 1];
+  for (int bi = 0; bi < nsbins; ++bi) ctx->sbins[bi].dev_off = ctx->su_cnt[bbase[bi]];
+  for (int bi = 0; bi < nsbins; ++bi)
+    ctx->sbins[bi].count = (bi + 1 < nsbins ? ctx->su_cnt[bbase[bi + 1]] : nsunits) - ctx->sbins[bi].dev_off;
+  ctx->h_sunits.resize(nsunits);
+  for (int64_t i = 0; i < nsunits; ++i) ctx->h_sunits[ctx->su_cnt[key(i)]++] = ctx->su_all[i];
+  trace.mark("units");
   auto t1 = std::chrono::steady_clock::now();
   ctx->plan_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
 
   // ---- plan upload
-  CK(up(ctx->d_read_m, ctx->read_m.data(), R));
-  CK(up(ctx->d_read_scale, ctx->read_scale.data(), R));
-  CK(up(ctx->d_read_ncap, read_ncap.data(), R));
+  ctx->h_rmeta.resize(3 * R);
+  std::copy(ctx->read_m.begin(), ctx->read_m.end(), ctx->h_rmeta.begin());
+  std::copy(ctx->read_scale.begin(), ctx->read_scale.end(), ctx->h_rmeta.begin() + R);
+  std::copy(read_ncap.begin(), read_ncap.end(), ctx->h_rmeta.begin() + 2 * R);
+  CK(up(ctx->d_read_m, ctx->h_rmeta.data(), R));
+  CK(up(ctx->d_read_scale, ctx->h_rmeta.data() + R, R));
+  CK(up(ctx->d_read_ncap, ctx->h_rmeta.data() + 2 * R, R));
   std::vector<FastUnit> allu;
   allu.reserve(nunits);
   for (auto& bn : ctx->bins) allu.insert(allu.end(), bn.units.begin(), bn.units.end());
   CK(up(ctx->d_units, allu.data(), allu.size()));
-  std::vector<StreamUnit> alls;
-  alls.reserve(nsunits);
-  for (auto& sb : ctx->sbins) alls.insert(alls.end(), sb.units.begin(), sb.units.end());
-  CK(up(ctx->d_sunits, alls.data(), alls.size()));
+  CK(up(ctx->d_sunits, ctx->h_sunits.data(), ctx->h_sunits.size()));
   CK(up(ctx->d_shaps, ctx->shaps.data(), ctx->shaps.size()));
   CK(ctx->d_gsum.ensure(R));
   CK(ctx->d_rflags.ensure(R));
@@ -628,6 +822,7 @@ int phmm_prepare(phmm_ctx* ctx, const phmm_input* in, const phmm_options* opt, i
   if (need_col) CK(ctx->d_colf.ensure(col_elems));
   CK(ctx->d_cold.ensure(col_elems));   // exact kernels (f32 view uses half of it)
   (void)need_cold;
+  trace.mark("plan-upload");
   // content validation on the device (bases 0..4, qualities 0..93)
   int* vflag = ctx->d_counters.p + kBinCounters - 1;
   CK(cudaMemsetAsync(vflag, 0, sizeof(int), ctx->stream));
@@ -652,8 +847,7 @@ int phmm_prepare(phmm_ctx* ctx, const phmm_input* in, const phmm_options* opt, i
 
   // FP64 stream-retry lists: sized for every streamed pair (worst case: all underflow)
   int64_t streamed = 0;
-  for (auto& sb : ctx->sbins)
-    for (auto& su : sb.units) streamed += su.cntA + su.cntB;
+  for (const auto& su : ctx->h_sunits) streamed += su.cntA + su.cntB;
   const bool r64 = (opt->flags & PHMM_FLAG_RETRY_F64) && streamed > 0;
   if (r64) {
     for (int g = 0; g < kNumR64Geoms; ++g) CK(ctx->d_r64u[g].ensure(streamed));
@@ -683,6 +877,8 @@ int phmm_prepare(phmm_ctx* ctx, const phmm_input* in, const phmm_options* opt, i
   E.r64_hap_cap = r64 ? (int)streamed : 0;
   ctx->r64_enabled = r64;
 
+  trace.mark("sync");
+  trace.print("prepare");
   ctx->prepared = true;
   if (num_pairs_out) *num_pairs_out = N;
   return PHMM_SUCCESS;
@@ -755,7 +951,7 @@ int phmm_execute(phmm_ctx* ctx) {
   CK(fork());
   for (int bi = 0; bi < nsb; ++bi) {
     const auto& sb = ctx->sbins[bi];
-    const int nu = (int)sb.units.size();
+    const int nu = (int)sb.count;
     if (nu == 0) continue;
     const int G = 32 / kFastGeoms[sb.geom].P;
     const int groups = (nu + G - 1) / G;
@@ -820,6 +1016,7 @@ int phmm_execute(phmm_ctx* ctx) {
 int phmm_fetch(phmm_ctx* ctx, double* out_log10, uint8_t* out_status, phmm_stats* stats) {
   if (!ctx) return PHMM_ERR_INVALID;
   if (!ctx->executed) return ctx->fail(PHMM_ERR_STATE, "phmm_fetch before phmm_execute");
+  Trace trace;
   CK(cudaSetDevice(ctx->device));
   const int64_t N = ctx->num_pairs;
   if (N > ctx->h_res_cap) {                 // pinned staging for the D2H of acc + status
@@ -889,23 +1086,29 @@ int phmm_fetch(phmm_ctx* ctx, double* out_log10, uint8_t* out_status, phmm_stats
       }
     }
   };
-  const int nth = (int)std::max<int64_t>(1, std::min<int64_t>(kFinishThreads, N / 8192));
+  trace.mark("d2h");
+  if (!ctx->pool && N >= 16384) {
+    const int hw = (int)std::max(1u, std::thread::hardware_concurrency());
+    ctx->pool.reset(new WorkerPool(std::min(hw, kFinishThreads) - 1));
+  }
+  const int nth = ctx->pool ? (int)std::max<int64_t>(1, std::min<int64_t>(ctx->pool->size() + 1, N / 4096)) : 1;
   std::vector<Acc> parts(nth);
   if (nth == 1) {
     finish_range(0, B, &parts[0]);
   } else {
-    std::vector<std::thread> pool;
+    std::vector<int64_t> cut(nth + 1, B);      // equal pair counts per task
+    cut[0] = 0;
     int64_t b = 0;
-    for (int i = 0; i < nth; ++i) {          // equal pair counts per thread
+    for (int i = 0; i < nth - 1; ++i) {
       const int64_t goal = N * (i + 1) / nth;
-      int64_t e = b;
-      while (e < B && bgid[e + 1] <= goal) ++e;
-      if (i == nth - 1) e = B;
-      pool.emplace_back(finish_range, b, e, &parts[i]);
-      b = e;
+      while (b < B && bgid[b + 1] <= goal) ++b;
+      cut[i + 1] = b;
     }
-    for (auto& th : pool) th.join();
+    std::function<void(int)> task = [&](int i) { finish_range(cut[i], cut[i + 1], &parts[i]); };
+    ctx->pool->run(nth, task);
   }
+  trace.mark("finish");
+  trace.print("fetch");
   int64_t total_cells = 0, fast = 0, exact = 0, f64 = 0, flagged = 0;
   for (auto& A : parts) {
     total_cells += A.cells; fast += A.fast; exact += A.exact; f64 += A.f64; flagged += A.flagged;
@@ -921,7 +1124,10 @@ int phmm_fetch(phmm_ctx* ctx, double* out_log10, uint8_t* out_status, phmm_stats
     }
     for (auto& sb : ctx->sbins) {
       const FastGeom g = kFastGeoms[sb.geom];
-      for (auto& u : sb.units) comp += 2LL * g.P * g.K * (std::max(u.rowsA, u.rowsB) + g.P - 1);
+      for (int64_t i = sb.dev_off; i < sb.dev_off + sb.count; ++i) {
+        const StreamUnit& u = ctx->h_sunits[i];
+        comp += 2LL * g.P * g.K * (std::max(u.rowsA, u.rowsB) + g.P - 1);
+      }
     }
     stats->computed_cells = comp;
     stats->fast_pairs = fast;
