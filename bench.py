@@ -14,7 +14,7 @@ by a barrier + device sync and the time is the MAX over ranks.
             (CUDA events on the engine stream, phmm_execute), L2 flushed between steps.
   e2e       GCUPS through the C-ABI call phmm_score from pinned HOST buffers (H2D of the
             inputs, planning, kernels, D2H of scores + status, finishing), wall clock.
-  roofline  the dominant kernel (k_fast, FP32 fast wavefront) against the FP32-FMA
+  roofline  the dominant kernel (k_stream, FP32 streaming wavefront) against the FP32-FMA
             roofline of SURVEY.md §8(d): 148 SMs x 128 lanes x f_SM / 8 ops per cell.
   cpu_baseline  the C oracle (a port of the reference recursion, oracle/) on the host
             cores, bounded sample of the same workload, rank 0 only.
@@ -314,7 +314,7 @@ def main():
                    "mode": "fast FP32 + guard band + exact FP32 (reference f32 semantics)"},
         "roofline": {"bound": "fp32", "achieved": fast_gcups, "peak": peak, "unit": "GCUPS",
                      "frac": fast_gcups / peak, "traffic": traffic,
-                     "kernel": "k_fast (FP32 fast wavefront)",
+                     "kernel": "k_stream<FP32,16,16> (FP32 streaming wavefront)",
                      "peak_source": "SURVEY.md §8(d): %d SMs x %d FP32 lanes x sm_max_mhz %.0f (MEASURED_PEAKS.json) / %d ops per cell"
                                     % (nsm, FP32_LANES_PER_SM, sm_max, OPS_PER_CELL),
                      "frac_at_sampled_clock": (fast_gcups / (nsm * FP32_LANES_PER_SM * clk["sm_mhz"] * 1e6 / OPS_PER_CELL / 1e9)
@@ -343,8 +343,8 @@ def main():
 
 
 def profile_traffic():
-    """dram bytes per k_fast launch from the committed ncu capture, if present."""
-    path = os.path.join(ROOT, "profiles", "k_fast_traffic.json")
+    """dram bytes per k_stream launch (c2) from the committed ncu --set full capture."""
+    path = os.path.join(ROOT, "profiles", "k_stream_traffic.json")
     try:
         with open(path) as f:
             return json.load(f).get("dram_bytes_per_launch")

@@ -389,6 +389,7 @@ struct phmm_ctx {
   int flags = 0;
   int list_cap = 0;
   int64_t h2d_bytes = 0;
+  int64_t hap_bytes = 0, read_bytes = 0;
   double plan_ms = 0.0, h2d_ms = 0.0;
   int last_launches = 0;
   float last_dev_ms = 0.f, last_fast_ms = 0.f;
@@ -552,6 +553,8 @@ static int prepare_impl(phmm_ctx* ctx, const phmm_input* in, const phmm_options*
       return ctx->fail(PHMM_ERR_INVALID, "invalid config %d", c);
   }
   ctx->flags = opt->flags;
+  ctx->hap_bytes = HL;
+  ctx->read_bytes = RL;
   ctx->num_reads = R; ctx->num_haps = H; ctx->num_batches = B;
   ctx->batch_read_off.assign(in->batch_read_off, in->batch_read_off + (B ? B + 1 : 0));
   ctx->batch_hap_off.assign(in->batch_hap_off, in->batch_hap_off + (B ? B + 1 : 0));
@@ -918,7 +921,9 @@ int phmm_execute(phmm_ctx* ctx) {
   if (ctx->num_reads > 0) {
     const int threads = 128;
     const int64_t blocks_pre = (ctx->num_reads * 32 + threads - 1) / threads;
-    k_precompute<<<(unsigned)blocks_pre, threads, 0, st>>>(E, (int)ctx->num_reads);
+    k_precompute<<<(unsigned)blocks_pre, threads, 0, st>>>(
+        E, (int)ctx->num_reads, ctx->d_sunits.p, (int64_t)ctx->h_sunits.size() * (int64_t)sizeof(StreamUnit),
+        ctx->d_shaps.p, (int64_t)ctx->shaps.size() * (int64_t)sizeof(StreamHap), ctx->hap_bytes, ctx->read_bytes);
     ++launches;
   }
   CK(cudaEventRecord(ctx->ev_pre, st));

@@ -100,10 +100,27 @@ __device__ __forceinline__ void append_item(ExactItem* const* lists, int* counts
 // Flushing a value v < 2^-90 changes the final accumulator by at most v*B, so
 //   0 <= unflushed - flushed <= 2^-90 * n * Gsum        (guard band)
 // ---------------------------------------------------------------------------------
-__global__ void k_precompute(EngineDev E, int num_reads) {
+__device__ __forceinline__ void prefetch_l2(const void* base, int64_t bytes, int64_t tid, int64_t nth) {
+  const char* p = static_cast<const char*>(base);
+  for (int64_t off = tid * 128; off < bytes; off += nth * 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(p + off));
+}
+
+__global__ void k_precompute(EngineDev E, int num_reads, const void* pf0, int64_t pf0_bytes, const void* pf1,
+                             int64_t pf1_bytes, int64_t hap_bytes, int64_t read_bytes) {
   // One warp per read.  With X_i = max(B_M(i), B_I(i)) and g_i = min(n, 1/(1-eps_i)):
   //   B_D(i) <= g_i X_{i+1},  X_i <= (1 + zeta_i g_i) X_{i+1},  X_m = 1
   // so  sum_i (B_M + B_I + B_D) <= prod_{i<m}(1 + zeta_i g_i) * (2 + sum_{i<m}(2 + g_i)).
+  // The grid also pulls the inputs the fast kernels read once per unit (work units,
+  // haplotype lists and bases, read bases and base qualities) into L2.
+  {
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+    prefetch_l2(pf0, pf0_bytes, tid, nth);
+    prefetch_l2(pf1, pf1_bytes, tid, nth);
+    prefetch_l2(E.hbases, hap_bytes, tid, nth);
+    prefetch_l2(E.rbases, read_bytes, tid, nth);
+    prefetch_l2(E.bq, read_bytes, tid, nth);
+  }
   const int lane = threadIdx.x & 31;
   const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (r >= num_reads) return;
