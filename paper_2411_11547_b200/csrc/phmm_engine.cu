@@ -69,8 +69,13 @@ const FastGeom kFastGeoms[] = {{4, 4},  {4, 8},   {4, 12},  {4, 16},  {8, 8},   
 constexpr int kNumFastGeoms = sizeof(kFastGeoms) / sizeof(kFastGeoms[0]);
 constexpr int kExactP[kNumExactP] = {4, 8, 16, 32};
 constexpr int kThreads = 128;
-constexpr int kBinCounters = 64;
-constexpr int kFinishThreads = 16;        // host threads finishing log10 in phmm_fetch          // fixed counter slots before the per-bin counters
+// device counters: [0,4) ex32 counts, [4,8) ex64 counts, [8,12) ex32 work, [12,16) ex64
+// work, 16 inline guard-band pairs, [20,24) fx64 counts, [24,28) fx64 work, then the two
+// device-built stream lists (counts[8], hap count, overflow) and their work counters,
+// the validation flag (last slot), then one work counter per planned stream/legacy bin
+constexpr int kCtrR64 = 32, kCtrRX32 = 44, kCtrR64Work = 56, kCtrRX32Work = 64;
+constexpr int kBinCounters = 96;          // fixed counter slots before the per-bin counters
+constexpr int kFinishThreads = 16;        // host threads finishing log10 in phmm_fetch
 
 struct Bin {
   int geom, Q;
@@ -105,62 +110,54 @@ const void* kFastFn[2 * kNumFastGeoms] = {FASTFN(4, 4),   FASTFN(4, 8),   FASTFN
                                           FASTFN(32, 16)};
 #undef FASTFN
 
-// streaming kernel (single-stripe reads): FP32 over the k_fast geometry table, FP64 retry
-// over the r64 geometries (phmm_kernels.cuh: r64_geom_for)
-template <int P, int K>
-void launch_stream(dim3 g, size_t smem, cudaStream_t s, const EngineDev& E, const StreamUnit* u,
-                   const StreamHap* h, int nu, int* ctr) {
-  k_stream<false, P, K><<<g, kThreads, smem, s>>>(E, u, h, nu, nullptr, ctr);
+// Streaming kernel family (single-stripe reads), one tiling table per mode
+// (phmm_kernels.cuh: kFast32 / kFast64 / kExact32 / kExact64)
+struct StreamKernel {
+  int P, K, occ;
+  size_t smem;
+  const void* fn;
+  void (*launch)(dim3, size_t, cudaStream_t, const EngineDev&, const StreamUnit*, const StreamHap*, int,
+                 const int*, int*);
+};
+template <int MODE, int P, int K>
+void launch_stream_t(dim3 g, size_t smem, cudaStream_t s, const EngineDev& E, const StreamUnit* u,
+                     const StreamHap* h, int nu, const int* nud, int* ctr) {
+  k_stream<MODE, P, K><<<g, kThreads, smem, s>>>(E, u, h, nu, nud, ctr);
 }
-typedef void (*StreamLaunch)(dim3, size_t, cudaStream_t, const EngineDev&, const StreamUnit*, const StreamHap*,
-                             int, int*);
-const StreamLaunch kStreamLaunch[kNumFastGeoms] = {
-    launch_stream<4, 4>,   launch_stream<4, 8>,   launch_stream<4, 12>, launch_stream<4, 16>,
-    launch_stream<8, 8>,   launch_stream<8, 12>,  launch_stream<8, 16>, launch_stream<16, 8>,
-    launch_stream<16, 12>, launch_stream<16, 16>, launch_stream<32, 8>, launch_stream<32, 12>,
-    launch_stream<32, 16>};
-const void* kStreamFn[kNumFastGeoms] = {
-    (const void*)k_stream<false, 4, 4>,   (const void*)k_stream<false, 4, 8>,   (const void*)k_stream<false, 4, 12>,
-    (const void*)k_stream<false, 4, 16>,  (const void*)k_stream<false, 8, 8>,   (const void*)k_stream<false, 8, 12>,
-    (const void*)k_stream<false, 8, 16>,  (const void*)k_stream<false, 16, 8>,  (const void*)k_stream<false, 16, 12>,
-    (const void*)k_stream<false, 16, 16>, (const void*)k_stream<false, 32, 8>,  (const void*)k_stream<false, 32, 12>,
-    (const void*)k_stream<false, 32, 16>};
-const int kStreamOcc[kNumFastGeoms] = {StreamOcc<4>::value,  StreamOcc<8>::value,  StreamOcc<12>::value,
-                                       StreamOcc<16>::value, StreamOcc<8>::value,  StreamOcc<12>::value,
-                                       StreamOcc<16>::value, StreamOcc<8>::value,  StreamOcc<12>::value,
-                                       StreamOcc<16>::value, StreamOcc<8>::value,  StreamOcc<12>::value,
-                                       StreamOcc<16>::value};
-// FP64 retry stream geometries: W = 32, 64, 96, 128, 192, 256
-const FastGeom kR64Geoms[kNumR64Geoms] = {{8, 4}, {16, 4}, {16, 6}, {16, 8}, {32, 6}, {32, 8}};
-template <int P, int K>
-void launch_stream64(dim3 g, size_t smem, cudaStream_t s, const EngineDev& E, int geom, int* ctr) {
-  k_stream<true, P, K><<<g, kThreads, smem, s>>>(E, E.r64_units[geom], E.r64_haps, 0, E.r64_count + geom, ctr);
+template <int MODE, int P, int K>
+StreamKernel SK() {
+  const size_t elem = ModeOf<MODE>::F64 ? sizeof(double) : sizeof(float);
+  return StreamKernel{P, K, StreamOcc<MODE, K>::value,
+                      96 * sizeof(double) + (size_t)4 * (32 / P) * 5 * K * P * elem + kStreamCodeBytesPerCta,
+                      (const void*)k_stream<MODE, P, K>, launch_stream_t<MODE, P, K>};
 }
-typedef void (*Stream64Launch)(dim3, size_t, cudaStream_t, const EngineDev&, int, int*);
-const Stream64Launch kStream64Launch[kNumR64Geoms] = {launch_stream64<8, 4>,  launch_stream64<16, 4>,
-                                                      launch_stream64<16, 6>, launch_stream64<16, 8>,
-                                                      launch_stream64<32, 6>, launch_stream64<32, 8>};
-const void* kStream64Fn[kNumR64Geoms] = {(const void*)k_stream<true, 8, 4>,  (const void*)k_stream<true, 16, 4>,
-                                         (const void*)k_stream<true, 16, 6>, (const void*)k_stream<true, 16, 8>,
-                                         (const void*)k_stream<true, 32, 6>, (const void*)k_stream<true, 32, 8>};
-int stream64_occ(int g) { return kR64Geoms[g].K <= 4 ? 3 : 2; }
-size_t stream64_smem(int g) {
-  const FastGeom G = kR64Geoms[g];
-  return 96 * sizeof(double) + (size_t)4 * (32 / G.P) * 5 * G.K * G.P * sizeof(double) + kStreamCodeBytesPerCta;
-}
-int stream_cap(int P) {
-  return P == 4 ? StreamCap<4>::value : P == 8 ? StreamCap<8>::value : P == 16 ? StreamCap<16>::value
-                                                                             : StreamCap<32>::value;
-}
+// kFast32 uses the k_fast tiling table (same order as kFastGeoms)
+const StreamKernel kStreamFast32[kNumFastGeoms] = {
+    SK<kFast32, 4, 4>(),   SK<kFast32, 4, 8>(),   SK<kFast32, 4, 12>(),  SK<kFast32, 4, 16>(),
+    SK<kFast32, 8, 8>(),   SK<kFast32, 8, 12>(),  SK<kFast32, 8, 16>(),  SK<kFast32, 16, 8>(),
+    SK<kFast32, 16, 12>(), SK<kFast32, 16, 16>(), SK<kFast32, 32, 8>(),  SK<kFast32, 32, 12>(),
+    SK<kFast32, 32, 16>()};
+// FP64 tilings, indexed by r64_geom_for(m): W = 32, 64, 96, 128, 192, 256
+const StreamKernel kStreamFast64[kNumR64Geoms] = {SK<kFast64, 8, 4>(),  SK<kFast64, 16, 4>(),
+                                                  SK<kFast64, 16, 6>(), SK<kFast64, 16, 8>(),
+                                                  SK<kFast64, 32, 6>(), SK<kFast64, 32, 8>()};
+const StreamKernel kStreamExact64[kNumR64Geoms] = {SK<kExact64, 8, 4>(),  SK<kExact64, 16, 4>(),
+                                                   SK<kExact64, 16, 6>(), SK<kExact64, 16, 8>(),
+                                                   SK<kExact64, 32, 6>(), SK<kExact64, 32, 8>()};
+// exact FP32 tilings, indexed by rx32_geom_for(m): W = 32, 64, 96, 128, 192, 256, 384, 512
+const StreamKernel kStreamExact32[kNumRX32Geoms] = {
+    SK<kExact32, 8, 4>(),   SK<kExact32, 16, 4>(),  SK<kExact32, 8, 12>(), SK<kExact32, 16, 8>(),
+    SK<kExact32, 16, 12>(), SK<kExact32, 16, 16>(), SK<kExact32, 32, 12>(), SK<kExact32, 32, 16>()};
+const StreamKernel* const kStreamTab[4] = {kStreamFast32, kStreamFast64, kStreamExact32, kStreamExact64};
+const int kStreamTabN[4] = {kNumFastGeoms, kNumR64Geoms, kNumRX32Geoms, kNumR64Geoms};
+
+int stream_cap(int P) { return stream_cap_of(P); }
 
 int exact_slot_host(int m) { return (m + 1 <= 32) ? 0 : (m + 1 <= 64) ? 1 : (m + 1 <= 128) ? 2 : 3; }
 
 size_t fast_smem(int geom) {
   const FastGeom g = kFastGeoms[geom];
   return 96 * sizeof(double) + (size_t)(kThreads / 32) * (32 / g.P) * 5 * g.K * g.P * sizeof(float);
-}
-size_t stream_smem(int geom) {
-  return fast_smem(geom) + kStreamCodeBytesPerCta;
 }
 size_t exact_smem(int slot, size_t tsize) {
   const int P = kExactP[slot];
@@ -210,23 +207,23 @@ int choose_geom(int m, int nmax, int* Qout) {
 // exceed the geometry's row-code capacity.  -1: no single-stripe streaming geometry.
 // cost of streaming a read's haplotypes (total rows, longest nmax) on tiling g (1e300:
 // infeasible or excluded by PHMM_FAST_GEOM)
-int64_t stream_geom_cost(int g, int64_t total, int nmax) {
+int64_t stream_geom_cost(int mode, int g, int64_t total, int nmax) {
   constexpr int64_t kInf = INT64_MAX;
   const int fg = forced_geom();
-  if (fg >= 0 && g != fg) return kInf;
-  const int64_t P = kFastGeoms[g].P, K = kFastGeoms[g].K;
+  if (mode == kFast32 && fg >= 0 && g != fg) return kInf;
+  const int64_t P = kStreamTab[mode][g].P, K = kStreamTab[mode][g].K;
   const int64_t cap = stream_cap((int)P);
   if (nmax > cap) return kInf;
   const int64_t units = (total + 2 * cap - 1) / (2 * cap);
   const int64_t rows = std::min<int64_t>(cap, (total + 2 * units - 1) / (2 * units));
   return units * P * (2 * K + 5) * (rows + P - 1);     // 2 x (K + 2.5) per thread-row
 }
-int choose_stream_geom(int m, int64_t total, int nmax) {
+int choose_stream_geom(int mode, int m, int64_t total, int nmax) {
   int64_t best = INT64_MAX;
   int bi = -1;
-  for (int g = 0; g < kNumFastGeoms; ++g) {
-    if (m + 1 > kFastGeoms[g].P * kFastGeoms[g].K) continue;
-    const int64_t cost = stream_geom_cost(g, total, nmax);
+  for (int g = 0; g < kStreamTabN[mode]; ++g) {
+    if (m + 1 > kStreamTab[mode][g].P * kStreamTab[mode][g].K) continue;
+    const int64_t cost = stream_geom_cost(mode, g, total, nmax);
     if (cost < best) { best = cost; bi = g; }
   }
   return bi;
@@ -337,7 +334,7 @@ struct phmm_ctx {
   cudaStream_t stream = nullptr;
   cudaEvent_t ev_start = nullptr, ev_fast0 = nullptr, ev_fast1 = nullptr, ev_end = nullptr;
   cudaEvent_t ev_pre = nullptr;
-  static constexpr int kAux = 4;              // side streams: fast-kernel bins run concurrently
+  static constexpr int kAux = 8;              // side streams: kernels of a phase run concurrently
   cudaStream_t aux[kAux] = {};
   cudaEvent_t ev_join[kAux] = {};
   std::string err;
@@ -353,8 +350,8 @@ struct phmm_ctx {
   DBuf<FastUnit> d_units;
   DBuf<StreamUnit> d_sunits;
   DBuf<StreamHap> d_shaps;
-  DBuf<StreamUnit> d_r64u[kNumR64Geoms];
-  DBuf<StreamHap> d_r64h;
+  DBuf<StreamUnit> d_r64u[kNumR64Geoms], d_rx32u[kNumRX32Geoms];
+  DBuf<StreamHap> d_r64h, d_rx32h;
   DBuf<ExactItem> d_ex32[kNumExactP], d_ex64[kNumExactP], d_fx64[kNumExactP];
   DBuf<float2> d_colf;
   DBuf<double> d_cold;
@@ -366,13 +363,14 @@ struct phmm_ctx {
 
   // plan (host)
   bool prepared = false, executed = false;
-  bool r64_enabled = false;
   int64_t num_pairs = 0;
   int64_t num_reads = 0, num_haps = 0, num_batches = 0;
   std::vector<int64_t> batch_read_off, batch_hap_off, hap_len;
   std::vector<int> read_m, read_scale, read_cfg;   // read_cfg -1 = too small
   std::vector<Bin> bins;
+  unsigned r64_geoms = 0, rx32_geoms = 0;   // device-built unit tilings that can get work
   struct SBin {
+    int mode;
     int geom;
     int64_t count = 0;                      // units of this tiling
     int64_t dev_off = 0;                    // first unit in h_sunits / d_sunits
@@ -456,10 +454,10 @@ int phmm_create(phmm_ctx** out, int device, const double* phred_lut) {
   CK(cudaMemcpy(ctx->d_lut.p, ctx->lut.data(), 94 * sizeof(double), cudaMemcpyHostToDevice));
   for (int g = 0; g < 2 * kNumFastGeoms; ++g)
     CK(cudaFuncSetAttribute(kFastFn[g], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fast_smem(g / 2)));
-  for (int g = 0; g < kNumFastGeoms; ++g)
-    CK(cudaFuncSetAttribute(kStreamFn[g], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)stream_smem(g)));
-  for (int g = 0; g < kNumR64Geoms; ++g)
-    CK(cudaFuncSetAttribute(kStream64Fn[g], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)stream64_smem(g)));
+  for (int md = 0; md < 4; ++md)
+    for (int g = 0; g < kStreamTabN[md]; ++g)
+      CK(cudaFuncSetAttribute(kStreamTab[md][g].fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)kStreamTab[md][g].smem));
   CK(cudaFuncSetAttribute((const void*)k_exact_all<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (int)exact_smem(0, 4)));
   CK(cudaFuncSetAttribute((const void*)k_exact_all<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -479,7 +477,9 @@ int phmm_destroy(phmm_ctx* ctx) {
   ctx->d_read_ncap.release(); ctx->d_counters.release(); ctx->d_gsum.release(); ctx->d_lut.release();
   ctx->d_acc.release(); ctx->d_units.release(); ctx->d_sunits.release(); ctx->d_shaps.release();
   for (int g = 0; g < kNumR64Geoms; ++g) ctx->d_r64u[g].release();
-  ctx->d_r64h.release(); ctx->d_colf.release(); ctx->d_cold.release();
+  for (int g = 0; g < kNumRX32Geoms; ++g) ctx->d_rx32u[g].release();
+  ctx->d_r64h.release();
+  ctx->d_rx32h.release(); ctx->d_colf.release(); ctx->d_cold.release();
   for (int s = 0; s < kNumExactP; ++s) { ctx->d_ex32[s].release(); ctx->d_ex64[s].release(); ctx->d_fx64[s].release(); }
   if (ctx->h_counts) cudaFreeHost(ctx->h_counts);
   if (ctx->h_acc) cudaFreeHost(ctx->h_acc);
@@ -616,13 +616,15 @@ static int prepare_impl(phmm_ctx* ctx, const phmm_input* in, const phmm_options*
   const bool exact_mode = (opt->flags & PHMM_FLAG_EXACT) != 0;
   ctx->bins.clear();
   ctx->sbins.clear();
+  ctx->r64_geoms = ctx->rx32_geoms = 0;
   ctx->su_all.clear();
   ctx->su_bin.clear();
   ctx->shaps.clear();
   // streaming units address reads/haplotypes with 32-bit offsets
   const bool use_stream = streaming_enabled() && RL < INT32_MAX && HL < INT32_MAX;
   std::vector<int> bin_index(kNumFastGeoms * 64, -1);
-  std::vector<int> sbin_index(kNumFastGeoms, -1);
+  int sbin_index[4 * 16];
+  std::fill(sbin_index, sbin_index + 4 * 16, -1);
   std::vector<ExactItem> host32[kNumExactP], host64[kNumExactP];
   int max_n = 1;
   int64_t gid = 0;
@@ -631,15 +633,25 @@ static int prepare_impl(phmm_ctx* ctx, const phmm_input* in, const phmm_options*
     std::vector<int> lanes[2];
     int rows[2] = {0, 0};
   };
-  std::vector<LaneTemplate> tmpls[kNumFastGeoms];
-  bool tvalid[kNumFastGeoms];
-  // geometries by width: choose_stream_geom(m) depends on m only through W >= m + 1
-  int wsort_idx[kNumFastGeoms], wsorted[kNumFastGeoms], best_from[kNumFastGeoms];
-  for (int g = 0; g < kNumFastGeoms; ++g) wsort_idx[g] = g;
-  std::sort(wsort_idx, wsort_idx + kNumFastGeoms, [](int a, int b) {
-    return kFastGeoms[a].P * kFastGeoms[a].K < kFastGeoms[b].P * kFastGeoms[b].K;
-  });
-  for (int i = 0; i < kNumFastGeoms; ++i) wsorted[i] = kFastGeoms[wsort_idx[i]].P * kFastGeoms[wsort_idx[i]].K;
+  // per mode: tiling tables sorted by width (the choice depends on m only through
+  // W >= m + 1), best tiling per width and lane templates, both cached per batch
+  struct ModePlan {
+    int n = 0;
+    int wsort[16], wsorted[16], best_from[16];
+    bool tvalid[16];
+    std::vector<LaneTemplate> tmpls[16];
+    int tmpl_m = -1, tmpl_geom = -2;
+  };
+  ModePlan mp[4];
+  for (int md = 0; md < 4; ++md) {
+    ModePlan& M = mp[md];
+    M.n = kStreamTabN[md];
+    for (int g = 0; g < M.n; ++g) M.wsort[g] = g;
+    std::sort(M.wsort, M.wsort + M.n, [&](int x, int y) {
+      return kStreamTab[md][x].P * kStreamTab[md][x].K < kStreamTab[md][y].P * kStreamTab[md][y].K;
+    });
+    for (int i = 0; i < M.n; ++i) M.wsorted[i] = kStreamTab[md][M.wsort[i]].P * kStreamTab[md][M.wsort[i]].K;
+  }
   if (use_stream) ctx->shaps.reserve(N);
   for (int64_t b = 0; b < B; ++b) {
     const int64_t r0 = ctx->batch_read_off[b], r1 = ctx->batch_read_off[b + 1];
@@ -652,9 +664,12 @@ static int prepare_impl(phmm_ctx* ctx, const phmm_input* in, const phmm_options*
       batch_total += ctx->hap_len[h];
     }
     max_n = std::max(max_n, ncap);
-    int tmpl_m = -1, tmpl_geom = -2;
-    std::fill(tvalid, tvalid + kNumFastGeoms, false);
-    std::fill(best_from, best_from + kNumFastGeoms, -2);   // per batch, filled lazily
+    for (int md = 0; md < 4; ++md) {
+      mp[md].tmpl_m = -1;
+      mp[md].tmpl_geom = -2;
+      std::fill(mp[md].tvalid, mp[md].tvalid + 16, false);
+      std::fill(mp[md].best_from, mp[md].best_from + 16, -2);
+    }
     hidx.resize(nh);
     std::iota(hidx.begin(), hidx.end(), (int)h0);
     std::stable_sort(hidx.begin(), hidx.end(), [&](int a, int c) { return ctx->hap_len[a] > ctx->hap_len[c]; });
@@ -665,56 +680,56 @@ static int prepare_impl(phmm_ctx* ctx, const phmm_input* in, const phmm_options*
       const int m = ctx->read_m[r];
       const int scale = opt->scale_log2[cfg];
       const bool f64 = opt->precision[cfg] == 1;
-      if (f64 || exact_mode || scale > 126) {
-        for (int64_t h = h0; h < h1; ++h) {
-          ExactItem it{(int)(gid + (h - h0)), (int)r, (int)h, scale};
-          (f64 ? host64 : host32)[exact_slot_host(m)].push_back(it);
-        }
-        continue;
-      }
+      const bool exact = f64 || exact_mode || scale > 126;
+      const int mode = f64 ? kExact64 : exact ? kExact32 : kFast32;
       if (use_stream) {
-        if (m != tmpl_m) {                             // lane template per (batch, geometry)
-          tmpl_m = m;
+        ModePlan& M = mp[mode];
+        if (m != M.tmpl_m) {                           // lane template per (batch, tiling)
+          M.tmpl_m = m;
           int sg = -1;
-          for (int i = 0; i < kNumFastGeoms; ++i)      // best tiling of the narrowest width >= m+1
-            if (wsorted[i] >= m + 1) {
-              if (best_from[i] == -2) best_from[i] = choose_stream_geom(wsorted[i] - 1, batch_total, ncap);
-              sg = best_from[i];
+          for (int i = 0; i < M.n; ++i)                // best tiling of the narrowest width >= m+1
+            if (M.wsorted[i] >= m + 1) {
+              if (M.best_from[i] == -2) M.best_from[i] = choose_stream_geom(mode, M.wsorted[i] - 1, batch_total, ncap);
+              sg = M.best_from[i];
               break;
             }
-          tmpl_geom = sg;
-          if (sg >= 0 && !tvalid[sg]) {
-            tvalid[sg] = true;
-            std::vector<LaneTemplate>& tmpl = tmpls[sg];
+          M.tmpl_geom = sg;
+          if (sg >= 0 && !M.tvalid[sg]) {
+            M.tvalid[sg] = true;
+            std::vector<LaneTemplate>& tmpl = M.tmpls[sg];
             tmpl.clear();
-            {
-              // greedy LPT over the length-sorted haplotypes: each to the lighter lane; a
-              // new unit when a lane would exceed the geometry's row capacity
-              const int cap = stream_cap(kFastGeoms[sg].P);
-              tmpl.emplace_back();
-              for (int64_t x = 0; x < nh; ++x) {
-                const int h = hidx[x];
-                const int n = (int)ctx->hap_len[h];
-                LaneTemplate* t = &tmpl.back();
-                int ln = t->rows[0] <= t->rows[1] ? 0 : 1;
-                if (t->rows[ln] + n > cap || (int)t->lanes[ln].size() >= kStreamMaxLaneHaps) {
-                  tmpl.emplace_back();
-                  t = &tmpl.back();
-                  ln = 0;
-                }
-                t->lanes[ln].push_back(h);
-                t->rows[ln] += n;
+            // greedy LPT over the length-sorted haplotypes: each to the lighter lane; a
+            // new unit when a lane would exceed the tiling's row capacity
+            const int cap = stream_cap(kStreamTab[mode][sg].P);
+            tmpl.emplace_back();
+            for (int64_t x = 0; x < nh; ++x) {
+              const int h = hidx[x];
+              const int n = (int)ctx->hap_len[h];
+              LaneTemplate* t = &tmpl.back();
+              int ln = t->rows[0] <= t->rows[1] ? 0 : 1;
+              if (t->rows[ln] + n > cap || (int)t->lanes[ln].size() >= kStreamMaxLaneHaps) {
+                tmpl.emplace_back();
+                t = &tmpl.back();
+                ln = 0;
               }
+              t->lanes[ln].push_back(h);
+              t->rows[ln] += n;
             }
           }
         }
-        if (tmpl_geom >= 0) {
-          const std::vector<LaneTemplate>& tmpl = tmpls[tmpl_geom];
-          if (sbin_index[tmpl_geom] < 0) {
-            sbin_index[tmpl_geom] = (int)ctx->sbins.size();
-            ctx->sbins.push_back(phmm_ctx::SBin{tmpl_geom, 0, 0});
+        if (M.tmpl_geom >= 0) {
+          const std::vector<LaneTemplate>& tmpl = M.tmpls[M.tmpl_geom];
+          const int key = mode * 16 + M.tmpl_geom;
+          if (sbin_index[key] < 0) {
+            sbin_index[key] = (int)ctx->sbins.size();
+            ctx->sbins.push_back(phmm_ctx::SBin{mode, M.tmpl_geom, 0, 0});
           }
-          const uint8_t sbi = (uint8_t)sbin_index[tmpl_geom];
+          const uint8_t sbi = (uint8_t)sbin_index[key];
+          if (mode == kFast32) {                       // tilings its device-built units can use
+            const int g64 = r64_geom_for(m), gx = rx32_geom_for(m);
+            if (g64 >= 0) ctx->r64_geoms |= 1u << g64;
+            if (gx >= 0) ctx->rx32_geoms |= 1u << gx;
+          }
           for (const LaneTemplate& t : tmpl) {
             StreamUnit su;
             su.read = (int)r;
@@ -731,6 +746,13 @@ static int prepare_impl(phmm_ctx* ctx, const phmm_input* in, const phmm_options*
           }
           continue;
         }
+      }
+      if (exact) {                                     // per-pair bit-exact kernels
+        for (int64_t h = h0; h < h1; ++h) {
+          ExactItem it{(int)(gid + (h - h0)), (int)r, (int)h, scale};
+          (f64 ? host64 : host32)[exact_slot_host(m)].push_back(it);
+        }
+        continue;
       }
       for (int64_t x = 0; x < nh; x += 2) {
         const int ha = hidx[x], hb = (x + 1 < nh) ? hidx[x + 1] : hidx[x];
@@ -848,14 +870,23 @@ static int prepare_impl(phmm_ctx* ctx, const phmm_input* in, const phmm_options*
   ctx->h2d_ms = h2d;
   ctx->h2d_bytes = bytes;
 
-  // FP64 stream-retry lists: sized for every streamed pair (worst case: all underflow)
+  // device-built stream units (FP64 retries, exact guard-band reruns): sized for every
+  // pair of the FP32 stream units (worst case: all of them)
   int64_t streamed = 0;
-  for (const auto& su : ctx->h_sunits) streamed += su.cntA + su.cntB;
-  const bool r64 = (opt->flags & PHMM_FLAG_RETRY_F64) && streamed > 0;
-  if (r64) {
-    for (int g = 0; g < kNumR64Geoms; ++g) CK(ctx->d_r64u[g].ensure(streamed));
-    CK(ctx->d_r64h.ensure(streamed));
-  }
+  for (auto& sb : ctx->sbins)
+    if (sb.mode == kFast32)
+      for (int64_t i = sb.dev_off; i < sb.dev_off + sb.count; ++i)
+        streamed += ctx->h_sunits[i].cntA + ctx->h_sunits[i].cntB;
+  const bool r64 = (opt->flags & PHMM_FLAG_RETRY_F64) && streamed > 0 && ctx->r64_geoms;
+  const bool rx32 = streamed > 0 && ctx->rx32_geoms;
+  if (!r64) ctx->r64_geoms = 0;
+  if (!rx32) ctx->rx32_geoms = 0;
+  for (int g = 0; g < kNumR64Geoms; ++g)
+    if (ctx->r64_geoms & (1u << g)) CK(ctx->d_r64u[g].ensure(streamed));
+  for (int g = 0; g < kNumRX32Geoms; ++g)
+    if (ctx->rx32_geoms & (1u << g)) CK(ctx->d_rx32u[g].ensure(streamed));
+  if (r64) CK(ctx->d_r64h.ensure(streamed));
+  if (rx32) CK(ctx->d_rx32h.ensure(streamed));
   EngineDev& E = ctx->dev;
   E.rbases = ctx->d_rbases.p; E.bq = ctx->d_bq.p; E.iq = ctx->d_iq.p; E.dq = ctx->d_dq.p; E.gq = ctx->d_gq.p;
   E.roff = ctx->d_roff.p; E.hbases = ctx->d_hbases.p; E.hoff = ctx->d_hoff.p;
@@ -872,13 +903,19 @@ static int prepare_impl(phmm_ctx* ctx, const phmm_input* in, const phmm_options*
   E.retry_f64 = (opt->flags & PHMM_FLAG_RETRY_F64) ? 1 : 0;
   E.band_inline = ctx->d_counters.p + 16;
   E.band_budget = 2 * ctx->num_sms;
-  for (int g = 0; g < kNumR64Geoms; ++g) E.r64_units[g] = r64 ? ctx->d_r64u[g].p : nullptr;
-  E.r64_haps = r64 ? ctx->d_r64h.p : nullptr;
-  E.r64_count = ctx->d_counters.p + 32;
-  E.r64_hap_count = ctx->d_counters.p + 32 + kNumR64Geoms;
-  E.r64_unit_cap = r64 ? (int)streamed : 0;
-  E.r64_hap_cap = r64 ? (int)streamed : 0;
-  ctx->r64_enabled = r64;
+  // tilings that cannot get work (no streamed read of that width) stay null
+  auto lists = [&](RetryLists& L, DBuf<StreamUnit>* u, int ng, DBuf<StreamHap>& h, unsigned geoms, int base) {
+    for (int g = 0; g < 8; ++g) L.units[g] = (g < ng && (geoms & (1u << g))) ? u[g].p : nullptr;
+    L.enabled = geoms ? 1 : 0;
+    L.haps = geoms ? h.p : nullptr;
+    L.count = ctx->d_counters.p + base;
+    L.hap_count = ctx->d_counters.p + base + 8;
+    L.overflow = ctx->d_counters.p + base + 9;
+    L.unit_cap = geoms ? (int)streamed : 0;
+    L.hap_cap = geoms ? (int)streamed : 0;
+  };
+  lists(E.r64, ctx->d_r64u, kNumR64Geoms, ctx->d_r64h, ctx->r64_geoms, kCtrR64);
+  lists(E.rx32, ctx->d_rx32u, kNumRX32Geoms, ctx->d_rx32h, ctx->rx32_geoms, kCtrRX32);
 
   trace.mark("sync");
   trace.print("prepare");
@@ -958,12 +995,13 @@ int phmm_execute(phmm_ctx* ctx) {
     const auto& sb = ctx->sbins[bi];
     const int nu = (int)sb.count;
     if (nu == 0) continue;
-    const int G = 32 / kFastGeoms[sb.geom].P;
+    const StreamKernel& SKn = kStreamTab[sb.mode][sb.geom];
+    const int G = 32 / SKn.P;
     const int groups = (nu + G - 1) / G;
-    const int blk = std::max(1, std::min(ctx->num_sms * kStreamOcc[sb.geom], (groups + 3) / 4));
+    const int blk = std::max(1, std::min(ctx->num_sms * SKn.occ, (groups + 3) / 4));
     used[nlaunch % kStreamAux] = true;
-    kStreamLaunch[sb.geom](dim3(blk), stream_smem(sb.geom), side(nlaunch++), E, ctx->d_sunits.p + sb.dev_off,
-                           ctx->d_shaps.p, nu, bin_ctr + nb + bi);
+    SKn.launch(dim3(blk), SKn.smem, side(nlaunch++), E, ctx->d_sunits.p + sb.dev_off, ctx->d_shaps.p, nu, nullptr,
+               bin_ctr + nb + bi);
     ++launches;
   }
   for (int bi = 0; bi < nb; ++bi) {
@@ -978,30 +1016,33 @@ int phmm_execute(phmm_ctx* ctx) {
   CK(join());
   CK(cudaGetLastError());
   CK(cudaEventRecord(ctx->ev_fast1, st));
-  // Post-pass, two concurrent chains: (a) guard-band overflow on the bit-exact FP32
-  // kernels, then per-pair FP64 retries (legacy path, fed by (a) and by k_fast);
-  // (b) FP64 stream retries (FP64 pipe, overlaps (a) on the FP32 pipe).  Then the
-  // bit-exact FP64 kernels, fed by everything before.
+  // Post-pass.  (a) concurrently: device-built stream units -- bit-exact FP32 reruns of
+  // guard-band pairs and FP64 retries of FP32-underflowed pairs -- and the per-pair exact
+  // FP32 list; (b) per-pair FP64 retries (fed by (a)); (c) per-pair bit-exact FP64 (fed by
+  // everything before).  Only tilings some streamed read can use are launched.
   CK(fork());
   used[0] = true;
   k_exact_all<float><<<ctx->num_sms * 2, kThreads, exact_smem(0, 4), ctx->aux[0]>>>(
       E, ctx->d_counters.p + 8, (float*)ctx->d_cold.p, ctx->max_n + 1);
   ++launches;
+  int nside = 0;
+  auto post = [&](const StreamKernel& SKn, const RetryLists& L, int g, int* work) {
+    const int a = 1 + (nside++ % (phmm_ctx::kAux - 1));
+    used[a] = true;
+    SKn.launch(dim3(ctx->num_sms * SKn.occ), SKn.smem, ctx->aux[a], E, L.units[g], L.haps, L.unit_cap, L.count + g,
+               work);
+    ++launches;
+  };
+  for (int g = kNumR64Geoms - 1; g >= 0; --g)
+    if (ctx->r64_geoms & (1u << g)) post(kStreamFast64[g], E.r64, g, ctx->d_counters.p + kCtrR64Work + g);
+  for (int g = kNumRX32Geoms - 1; g >= 0; --g)
+    if (ctx->rx32_geoms & (1u << g)) post(kStreamExact32[g], E.rx32, g, ctx->d_counters.p + kCtrRX32Work + g);
+  CK(join());
   if (ctx->flags & PHMM_FLAG_RETRY_F64) {
-    k_fast64_all<<<ctx->num_sms * 2, kThreads, exact_smem(0, 8), ctx->aux[0]>>>(
-        E, ctx->d_counters.p + 24, ctx->d_cold.p, ctx->max_n + 1);
+    k_fast64_all<<<ctx->num_sms * 2, kThreads, exact_smem(0, 8), st>>>(E, ctx->d_counters.p + 24, ctx->d_cold.p,
+                                                                      ctx->max_n + 1);
     ++launches;
   }
-  if (ctx->r64_enabled) {
-    for (int g = kNumR64Geoms - 1; g >= 0; --g) {
-      const int a = 1 + (g % (phmm_ctx::kAux - 1));
-      used[a] = true;
-      kStream64Launch[g](dim3(ctx->num_sms * stream64_occ(g)), stream64_smem(g), ctx->aux[a], E, g,
-                         ctx->d_counters.p + 40 + g);
-      ++launches;
-    }
-  }
-  CK(join());
   k_exact_all<double><<<ctx->num_sms * 2, kThreads, exact_smem(0, 8), st>>>(
       E, ctx->d_counters.p + 12, ctx->d_cold.p, ctx->max_n + 1);
   ++launches;
@@ -1128,7 +1169,7 @@ int phmm_fetch(phmm_ctx* ctx, double* out_log10, uint8_t* out_status, phmm_stats
       for (auto& u : bn.units) comp += 2LL * bn.Q * g.P * g.K * (std::max(u.nA, u.nB) + g.P - 1);
     }
     for (auto& sb : ctx->sbins) {
-      const FastGeom g = kFastGeoms[sb.geom];
+      const StreamKernel& g = kStreamTab[sb.mode][sb.geom];
       for (int64_t i = sb.dev_off; i < sb.dev_off + sb.count; ++i) {
         const StreamUnit& u = ctx->h_sunits[i];
         comp += 2LL * g.P * g.K * (std::max(u.rowsA, u.rowsB) + g.P - 1);

@@ -50,6 +50,17 @@ struct StreamUnit {                       // 32 B
 };
 struct StreamHap { int hap, pair, off, n; };   // haplotype, pair id, base offset, length
 
+// Stream units appended on the device, one list per tiling (null units[0]: disabled)
+struct RetryLists {
+  StreamUnit* units[8];
+  int* count;                             // [8] units per tiling
+  StreamHap* haps;
+  int* hap_count;
+  int* overflow;
+  int unit_cap, hap_cap;
+  int enabled;
+};
+
 struct EngineDev {
   const int8_t* rbases;
   const uint8_t *bq, *iq, *dq, *gq;
@@ -74,12 +85,8 @@ struct EngineDev {
   int* fx64_count;                        // [kNumExactP]
   int* band_inline;                       // guard-band pairs taken inline so far
   int band_budget;
-  // FP64 stream retry units, appended by the FP32 stream kernel (one list per geometry)
-  StreamUnit* r64_units[6];
-  int* r64_count;                         // [6]
-  StreamHap* r64_haps;
-  int* r64_hap_count;
-  int r64_unit_cap, r64_hap_cap;
+  RetryLists r64;                         // FP64 retry units (built by the FP32 stream kernel)
+  RetryLists rx32;                        // bit-exact FP32 guard-band units (same)
 };
 
 __device__ __forceinline__ int exact_slot_for(int m) {
@@ -651,24 +658,47 @@ constexpr int kCodeFirst = 8, kCodeLast = 16;          // code byte: base | FIRS
 constexpr int kStreamCodeBytesPerCta = 32768;          // row-code staging, shared memory
 constexpr int kStreamMaxLaneHaps = 15;                 // haplotypes per lane of one unit
 constexpr int kStreamMaxWin = 2 * (kStreamMaxLaneHaps + 1);
-constexpr int kStreamBandCap = 8;                      // guard-band pairs rerun in-warp per unit
 template <int P> struct StreamCap {                    // max rows per lane of one unit
   static constexpr int bytes = kStreamCodeBytesPerCta / (4 * (32 / P));
   static constexpr int value = bytes / 2 - 2;
 };
-template <int K> struct StreamOcc { static constexpr int value = K <= 8 ? 4 : (K <= 12 ? 3 : 2); };
+__host__ __device__ __forceinline__ int stream_cap_of(int P) {
+  return kStreamCodeBytesPerCta / (4 * (32 / P)) / 2 - 2;
+}
 
-// FP64 retry geometries (P, K): W = 32, 64, 96, 128, 192, 256; longer reads use k_fast64
-constexpr int kNumR64Geoms = 6;
+// Kernel modes of the streaming family:
+//   kFast32   folded recurrence, FMA, packed float2 (FFMA2/FMUL2/FADD2), guard band
+//   kFast64   folded recurrence, DFMA, two lanes (FP32-underflow retries, GATK behaviour)
+//   kExact32  the reference's expressions, no FMA, per-store flush 2^-90 (packed FMUL2/FADD2
+//             round each lane like scalar FMUL/FADD): guard-band pairs, exact mode
+//   kExact64  the same in FP64 with flush 2^-970: f64 configs (bit-identical)
+enum { kFast32 = 0, kFast64 = 1, kExact32 = 2, kExact64 = 3 };
+template <int MODE> struct ModeOf {
+  static constexpr bool F64 = MODE == kFast64 || MODE == kExact64;
+  static constexpr bool EXACT = MODE == kExact32 || MODE == kExact64;
+};
+template <int MODE, int K> struct StreamOcc {
+  static constexpr int value = ModeOf<MODE>::F64 ? (K <= 4 ? 3 : 2) : (K <= 8 ? 4 : (K <= 12 ? 3 : 2));
+};
+
+// Device-built stream units (one list per tiling): FP64 retries of FP32-underflowed pairs
+// and bit-exact reruns of guard-band pairs, grouped per read by the FP32 stream kernel.
+constexpr int kNumR64Geoms = 6;     // FP64 retry:  (8,4) (16,4) (16,6) (16,8) (32,6) (32,8)
+constexpr int kNumRX32Geoms = 8;    // exact FP32:  (8,4) (16,4) (8,12) (16,8) (16,12) (16,16) (32,12) (32,16)
+// haplotypes per lane of a device-built unit: short units keep these small post-pass
+// lists parallel (their count is unknown when the grid is sized)
+constexpr int kRetryLaneHaps64 = 2, kRetryLaneHapsX32 = 1;
 __host__ __device__ __forceinline__ int r64_geom_for(int m) {
   const int w = m + 1;
   return w <= 32 ? 0 : w <= 64 ? 1 : w <= 96 ? 2 : w <= 128 ? 3 : w <= 192 ? 4 : w <= 256 ? 5 : -1;
 }
 __host__ __device__ __forceinline__ int r64_geom_P(int g) { return g == 0 ? 8 : (g <= 3 ? 16 : 32); }
-__host__ __device__ __forceinline__ int r64_cap(int g) {
-  const int P = r64_geom_P(g);
-  return kStreamCodeBytesPerCta / (4 * (32 / P)) / 2 - 2;
+__host__ __device__ __forceinline__ int rx32_geom_for(int m) {
+  const int w = m + 1;
+  return w <= 32 ? 0 : w <= 64 ? 1 : w <= 96 ? 2 : w <= 128 ? 3 : w <= 192 ? 4 : w <= 256 ? 5
+       : w <= 384 ? 6 : w <= 512 ? 7 : -1;
 }
+__host__ __device__ __forceinline__ int rx32_geom_P(int g) { return g == 0 || g == 2 ? 8 : (g <= 5 ? 16 : 32); }
 
 struct Dbl2 { double x, y; };
 
@@ -684,10 +714,17 @@ template <> struct Lanes<false> {
   static __device__ __forceinline__ V fma(S s, V a, V b) { return __ffma2_rn(make_float2(s, s), a, b); }
   static __device__ __forceinline__ V mul(S s, V a) { return __fmul2_rn(make_float2(s, s), a); }
   static __device__ __forceinline__ V add(V a, V b) { return __fadd2_rn(a, b); }
+  static __device__ __forceinline__ S mul1(S a, S b) { return __fmul_rn(a, b); }
+  // exact-mode ops: ptxas fuses packed multiplies into a following packed add (FFMA2) even
+  // from explicit mul.rn.f32x2, so products are scalar __fmul_rn (never fused) and only
+  // the adds are packed -- each lane rounds like the reference's separate mul and add
+  static __device__ __forceinline__ V xmul(S s, V a) { return make_float2(__fmul_rn(s, a.x), __fmul_rn(s, a.y)); }
+  static __device__ __forceinline__ V xadd(V a, V b) { return __fadd2_rn(a, b); }
   static __device__ __forceinline__ S comp(const EV& v, int i) {
     return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w;
   }
   static __device__ __forceinline__ EV pack(const S* l) { return make_float4(l[0], l[1], l[2], l[3]); }
+  static __device__ __forceinline__ S thr() { return 0x1p-90f; }
 };
 template <> struct Lanes<true> {
   using S = double;
@@ -696,12 +733,21 @@ template <> struct Lanes<true> {
   static constexpr int EW = 2;
   static __device__ __forceinline__ V zero() { return Dbl2{0.0, 0.0}; }
   static __device__ __forceinline__ V fma(S s, V a, V b) { return Dbl2{::fma(s, a.x, b.x), ::fma(s, a.y, b.y)}; }
-  static __device__ __forceinline__ V mul(S s, V a) { return Dbl2{s * a.x, s * a.y}; }
-  static __device__ __forceinline__ V add(V a, V b) { return Dbl2{a.x + b.x, a.y + b.y}; }
+  static __device__ __forceinline__ V mul(S s, V a) { return Dbl2{__dmul_rn(s, a.x), __dmul_rn(s, a.y)}; }
+  static __device__ __forceinline__ V add(V a, V b) { return Dbl2{__dadd_rn(a.x, b.x), __dadd_rn(a.y, b.y)}; }
+  static __device__ __forceinline__ S mul1(S a, S b) { return __dmul_rn(a, b); }
+  static __device__ __forceinline__ V xmul(S s, V a) { return mul(s, a); }    // __dmul_rn: unfused
+  static __device__ __forceinline__ V xadd(V a, V b) { return add(a, b); }
   static __device__ __forceinline__ S comp(const EV& v, int i) { return i == 0 ? v.x : v.y; }
   static __device__ __forceinline__ EV pack(const S* l) { return make_double2(l[0], l[1]); }
+  static __device__ __forceinline__ S thr() { return 0x1p-970; }
 };
 template <int L, class V> __device__ __forceinline__ auto& lane_ref(V& v) { return L == 0 ? v.x : v.y; }
+template <class V, class S> __device__ __forceinline__ V flush2(V v, S thr) {
+  v.x = v.x >= thr ? v.x : (S)0;            // reference store flush (wavefront.py:134-136)
+  v.y = v.y >= thr ? v.y : (S)0;
+  return v;
+}
 
 // Classification of a finished FP32 stream accumulator; returns 0 = written, 1 = guard
 // band (caller queues the bit-exact rerun), 2 = FP32 underflow to retry in FP64 (caller).
@@ -720,10 +766,48 @@ __device__ __forceinline__ int stream_finish32(const EngineDev& E, float a, int 
   return 0;
 }
 
-template <bool F64, int P, int K>
-__global__ void __launch_bounds__(128, F64 ? (K <= 4 ? 3 : 2) : StreamOcc<K>::value)
+// Groups the flagged entries (bit e of mask[lane]) of a finished unit into new stream
+// units of tiling g (row capacity cap) appended to L; thread-serial, rare.
+__device__ __forceinline__ void emit_retry_units(const StreamUnit& U, const StreamHap* shaps, const unsigned* mask,
+                                                 const RetryLists& L, int g, int cap, int m, int lane_haps) {
+  int lanes_n[2] = {0, 0}, rows_n[2] = {0, 0};
+  StreamHap buf[2][kStreamMaxLaneHaps];
+  auto emit = [&]() {
+    const int tot = lanes_n[0] + lanes_n[1];
+    if (tot == 0) return;
+    const int ui = atomicAdd(&L.count[g], 1);
+    const int hi = atomicAdd(L.hap_count, tot);
+    if (ui < L.unit_cap && hi + tot <= L.hap_cap) {
+      for (int x = 0; x < lanes_n[0]; ++x) L.haps[hi + x] = buf[0][x];
+      for (int x = 0; x < lanes_n[1]; ++x) L.haps[hi + lanes_n[0] + x] = buf[1][x];
+      L.units[g][ui] = StreamUnit{U.read, hi, lanes_n[0], lanes_n[1], rows_n[0], rows_n[1], U.ro, m};
+    } else {
+      atomicAdd(L.overflow, 1);                 // capacity is sized for every pair: never
+    }
+    lanes_n[0] = lanes_n[1] = 0;
+    rows_n[0] = rows_n[1] = 0;
+  };
+  for (int ln = 0; ln < 2; ++ln) {
+    unsigned msk = mask[ln];
+    const int e0 = U.list + (ln ? U.cntA : 0);
+    while (msk) {
+      const int e = __ffs(msk) - 1;
+      msk &= msk - 1;
+      const StreamHap sh = shaps[e0 + e];
+      int l2 = rows_n[0] <= rows_n[1] ? 0 : 1;
+      if (rows_n[l2] + sh.n > cap || lanes_n[l2] >= lane_haps) { emit(); l2 = 0; }
+      buf[l2][lanes_n[l2]++] = sh;
+      rows_n[l2] += sh.n;
+    }
+  }
+  emit();
+}
+
+template <int MODE, int P, int K>
+__global__ void __launch_bounds__(128, (StreamOcc<MODE, K>::value))
 k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHap* __restrict__ shaps,
          int num_units_arg, const int* __restrict__ num_units_dev, int* __restrict__ counter) {
+  constexpr bool F64 = ModeOf<MODE>::F64, EXACT = ModeOf<MODE>::EXACT;
   using A = Lanes<F64>;
   using S = typename A::S;
   using V = typename A::V;
@@ -740,7 +824,7 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int sw = lane / P, t = lane % P;
   const int slot = wib * G + sw;
-  const int num_units = num_units_dev ? min(*num_units_dev, E.r64_unit_cap) : num_units_arg;
+  const int num_units = num_units_dev ? min(*num_units_dev, num_units_arg) : num_units_arg;
   if (num_units == 0) return;
   for (int i = threadIdx.x; i < 94; i += blockDim.x) s_lut[i] = E.lut[i];
   __syncthreads();
@@ -748,15 +832,15 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
   unsigned char* cd = s_code + (size_t)slot * CB;
   const unsigned short* cd16 = reinterpret_cast<const unsigned short*>(cd);
   const V zero2 = A::zero();
+  const S thr = A::thr();
   __shared__ StreamUnit s_unit[4 * G];
   __shared__ int s_hc[2 * 128];
   __shared__ int s_win[4 * G * kStreamMaxWin];
   __shared__ S s_bs[4 * G * 2 * kStreamMaxLaneHaps];
   __shared__ int s_meta[4 * G * 4];
-  __shared__ ExactItem s_band[F64 ? 1 : 4 * G * kStreamBandCap];
-  __shared__ int s_nband[4 * G];
   __shared__ int s_nwin[4 * G];
-  __shared__ unsigned s_flag[4 * G * 2];          // FP32: per lane, entries that underflowed
+  __shared__ unsigned s_flag[4 * G * 2];          // kFast32: lane entries that underflowed
+  __shared__ unsigned s_band[4 * G * 2];          // kFast32: lane entries in the guard band
 
   for (;;) {
     int g = 0;
@@ -780,9 +864,11 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
     }
     const int Lp = W - m - 1;
 
-    // ---- coefficients + emission table, folded recurrence:
-    //   Mt(i) = alpha_{i+1} M(i), D'(i) = beta_{i+1} D(i); 7 operations per cell
-    S be[K], dl[K], ep[K], zp[K];
+    // ---- per-position coefficients + emission table.  Fast modes: folded recurrence
+    //    Mt(i) = alpha_{i+1} M(i), D'(i) = beta_{i+1} D(i), 7 ops per cell,
+    //   coefficients be, dl, ep, zt (= zeta'); exact modes: the reference's al, be, dl, ep,
+    //   zt with the f64 -> dtype casts of wavefront.py:347-355.
+    S al[K], be[K], dl[K], ep[K], zt[K];
     V M[K], I[K], D[K];
 #pragma unroll
     for (int ke = 0; ke < KE; ++ke) {
@@ -793,7 +879,7 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
         const int p = t * K + k;
         M[k] = zero2; I[k] = zero2; D[k] = zero2;
         if (p < Lp) {                                   // left padding
-          be[k] = 0; dl[k] = 0; ep[k] = 1; zp[k] = 0;
+          al[k] = 0; be[k] = 0; dl[k] = 0; ep[k] = 1; zt[k] = 0;
 #pragma unroll
           for (int c = 0; c < 5; ++c) lam[c][kk] = 0;
         } else if (p < Lp + m) {                        // real read position
@@ -802,14 +888,18 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
           const double e = s_lut[E.gq[ro + i0]], qe = s_lut[E.bq[ro + i0]];
           const int rc = E.rbases[ro + i0];
           S lm, lx;
-          if constexpr (F64) {                          // k_fast64's coefficients
+          if constexpr (EXACT) {                        // prob.py:66-112, cast per dtype
+            al[k] = (S)((1.0 - d) - z); be[k] = (S)(1.0 - e); dl[k] = (S)d; ep[k] = (S)e;
+            zt[k] = (i0 + 1 < m) ? (S)z : (S)0;         // D(m, .) never reaches the score
+            lm = (S)(1.0 - qe); lx = (S)(qe / 3.0);
+          } else if constexpr (F64) {                   // k_fast64's coefficients
             const double a = (1.0 - d) - z;
             double anext = 1.0, bnext = 0.0;
             if (i0 + 1 < m) {
               anext = (1.0 - s_lut[E.iq[ro + i0 + 1]]) - s_lut[E.dq[ro + i0 + 1]];
               bnext = 1.0 - s_lut[E.gq[ro + i0 + 1]];
             }
-            be[k] = 1.0 - e; dl[k] = d / a; ep[k] = e; zp[k] = bnext * z / anext;
+            be[k] = 1.0 - e; dl[k] = d / a; ep[k] = e; zt[k] = bnext * z / anext;
             lm = anext * (1.0 - qe); lx = anext * (qe / 3.0);
           } else {                                      // k_fast's coefficients
             const float a = (float)((1.0 - d) - z);
@@ -821,13 +911,13 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
             be[k] = (float)(1.0 - e);
             dl[k] = __fdividef((float)d, a);
             ep[k] = (float)e;
-            zp[k] = __fdividef(bnext * (float)z, anext);
+            zt[k] = __fdividef(bnext * (float)z, anext);
             lm = anext * (float)(1.0 - qe); lx = anext * ((float)qe * (1.f / 3.f));
           }
 #pragma unroll
           for (int c = 0; c < 5; ++c) lam[c][kk] = (rc == c || rc == 4 || c == 4) ? lm : lx;
         } else {                                        // accumulator position
-          be[k] = 1; dl[k] = 0; ep[k] = 1; zp[k] = 1;
+          al[k] = 1; be[k] = 1; dl[k] = 0; ep[k] = 1; zt[k] = 1;
 #pragma unroll
           for (int c = 0; c < 5; ++c) lam[c][kk] = 1;
         }
@@ -862,22 +952,21 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
         int* wb = s_win + slot * kStreamMaxWin;
         int ia = 0, ib = 0, ra = 1, rb = 1, nw = 0;
         const int ca = U.cntA, cbn = U.cntB;
-        auto lenA = [&](int i) { return shaps[U.list + i].n; };
-        auto lenB = [&](int i) { return shaps[U.list + ca + i].n; };
         while (ia <= ca || ib <= cbn) {
           const int va = ia <= ca ? ra : 0x7fffffff, vb = ib <= cbn ? rb : 0x7fffffff;
           const int v = min(va, vb);
           if (nw == 0 || wb[nw - 1] != v) wb[nw++] = v;
-          if (va == v) { if (ia < ca) ra += lenA(ia); ++ia; }
-          if (vb == v) { if (ib < cbn) rb += lenB(ib); ++ib; }
+          if (va == v) { if (ia < ca) ra += shaps[U.list + ia].n; ++ia; }
+          if (vb == v) { if (ib < cbn) rb += shaps[U.list + ca + ib].n; ++ib; }
         }
         s_nwin[slot] = nw;
       }
-      // per-pair boundary S'/n (FP32: scale 2^s; FP64 retry: 2^0) and read metadata
-      const double sdf = (1.0 - s_lut[E.gq[ro]]) * (F64 ? 1.0 : ldexp(1.0, E.read_scale[r]));
-      for (int e = t; e < U.cntA + U.cntB; e += P) {
+      // per-pair row-0 boundary: fast32 S*beta_1/n (folded), fast64 beta_1/n (scale 2^0),
+      // exact fl_dtype(S/n) (wavefront.py:405-406)
+      const double sd = ldexp(1.0, MODE == kFast64 ? 0 : E.read_scale[r]);
+      const double sdf = EXACT ? sd : (1.0 - s_lut[E.gq[ro]]) * sd;
+      for (int e = t; e < U.cntA + U.cntB; e += P)
         s_bs[slot * 2 * kStreamMaxLaneHaps + e] = (S)(sdf / (double)shaps[U.list + e].n);
-      }
       if (t == 0) {
         s_meta[slot * 4 + 0] = Lp;
         s_meta[slot * 4 + 1] = E.read_scale[r];
@@ -889,9 +978,8 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
     }
     if (t == 0) {
       s_unit[slot] = U;
-      s_nband[slot] = 0;
-      s_flag[2 * slot] = 0u;
-      s_flag[2 * slot + 1] = 0u;
+      s_flag[2 * slot] = 0u; s_flag[2 * slot + 1] = 0u;
+      s_band[2 * slot] = 0u; s_band[2 * slot + 1] = 0u;
     }
     s_hc[2 * threadIdx.x] = -1;                         // current haplotype per lane
     s_hc[2 * threadIdx.x + 1] = -1;
@@ -931,34 +1019,43 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
       const StreamUnit& SU = s_unit[slot];
       const int hc = s_hc[2 * threadIdx.x + L];
       const StreamHap sh = shaps[SU.list + (L == 0 ? 0 : SU.cntA) + hc];
-      const S res = (lane_ref<L>(D[K - 1]) + lane_ref<L>(M[K - 1])) +
-                    (lane_ref<L>(M[K - 2]) + lane_ref<L>(I[K - 2]));
-      if constexpr (F64) {
+      S res;
+      if constexpr (EXACT)                              // j-ordered sum (wavefront.py:156-160)
+        res = (lane_ref<L>(D[K - 1]) + lane_ref<L>(M[K - 1])) + (lane_ref<L>(M[K - 2]) + lane_ref<L>(I[K - 2]));
+      else
+        res = (lane_ref<L>(D[K - 1]) + lane_ref<L>(M[K - 1])) + (lane_ref<L>(M[K - 2]) + lane_ref<L>(I[K - 2]));
+      const int mm = s_meta[slot * 4 + 3];
+      if constexpr (MODE == kFast64) {
         // FP64 retry result; near/below the f64 flush floor -> bit-exact FP64 kernel
         if (res >= 0x1p-900 && isfinite(res)) {
           E.acc[sh.pair] = res;
           E.status[sh.pair] = kStatusOk | kStatusRetriedF64;
         } else {
-          append_item(E.ex64, E.ex64_count, E.list_cap, exact_slot_for(s_meta[slot * 4 + 3]),
-                      ExactItem{sh.pair, SU.read, sh.hap, 0});
+          append_item(E.ex64, E.ex64_count, E.list_cap, exact_slot_for(mm), ExactItem{sh.pair, SU.read, sh.hap, 0});
         }
+      } else if constexpr (MODE == kExact32) {
+        const bool bad = !(res > 0.f) || !isfinite(res);
+        if (bad && E.retry_f64) {
+          E.status[sh.pair] = kStatusRetriedF64;
+          append_item(E.fx64, E.fx64_count, E.list_cap, exact_slot_for(mm), ExactItem{sh.pair, SU.read, sh.hap, 0});
+        } else {
+          E.acc[sh.pair] = (double)res;
+          E.status[sh.pair] = bad ? kStatusOverflow : kStatusExactF32;
+        }
+      } else if constexpr (MODE == kExact64) {
+        const bool bad = !(res > 0.0) || !isfinite(res);
+        E.acc[sh.pair] = res;
+        const uint8_t keep = E.status[sh.pair] & kStatusRetriedF64;
+        E.status[sh.pair] = (uint8_t)((bad ? kStatusOverflow : kStatusOk) | keep);
       } else {
-        const int n = sh.n;
-        const int sc = s_meta[slot * 4 + 1];
-        const int mm = s_meta[slot * 4 + 3];
-        const int v = stream_finish32(E, res, sh.pair, n, __int_as_float(s_meta[slot * 4 + 2]), sc);
-        if (v == 1) {
-          // guard band: queue for the bit-exact rerun this warp does after the unit
-          const ExactItem it{sh.pair, SU.read, sh.hap, sc};
-          const int c = s_nband[slot];
-          if (c < kStreamBandCap && atomicAdd(E.band_inline, 1) < E.band_budget) {
-            s_band[slot * kStreamBandCap + c] = it;
-            s_nband[slot] = c + 1;
-          } else {
-            append_item(E.ex32, E.ex32_count, E.list_cap, exact_slot_for(mm), it);
-          }
-        } else if (v == 2) {
-          if (E.r64_units && r64_geom_for(mm) >= 0) s_flag[2 * slot + L] |= 1u << hc;   // FP64 stream retry
+        const int v = stream_finish32(E, res, sh.pair, sh.n, __int_as_float(s_meta[slot * 4 + 2]),
+                                      s_meta[slot * 4 + 1]);
+        if (v == 1) {                                   // guard band: exact rerun unit
+          if (E.rx32.enabled && rx32_geom_for(mm) >= 0) s_band[2 * slot + L] |= 1u << hc;
+          else append_item(E.ex32, E.ex32_count, E.list_cap, exact_slot_for(mm),
+                           ExactItem{sh.pair, SU.read, sh.hap, s_meta[slot * 4 + 1]});
+        } else if (v == 2) {                            // FP32 underflow: FP64 retry unit
+          if (E.r64.enabled && r64_geom_for(mm) >= 0) s_flag[2 * slot + L] |= 1u << hc;
           else append_item(E.fx64, E.fx64_count, E.list_cap, exact_slot_for(mm), ExactItem{sh.pair, SU.read, sh.hap, 0});
         }
       }
@@ -988,7 +1085,7 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
       const int cA = code & 7, cB = (code >> 8) & 7;
       const EV* EA = Et + (cA * KE) * P + t;
       const EV* EB = Et + (cB * KE) * P + t;
-      // pass 1 (descending): D' from the previous row, M from the previous-row diagonal
+      // pass 1 (descending): D from the previous row, M from the previous-row diagonal
 #pragma unroll
       for (int ke = KE - 1; ke >= 0; --ke) {
         const EV la = EA[ke * P];
@@ -996,14 +1093,23 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
 #pragma unroll
         for (int kk = EW - 1; kk >= 0; --kk) {
           const int k = ke * EW + kk;
-          D[k] = A::fma(ep[k], D[k], A::mul(zp[k], M[k]));
           const V pm = (k > 0) ? M[k - 1] : dgM;
           const V pi = (k > 0) ? I[k - 1] : dgI;
           const V pd = (k > 0) ? D[k - 1] : dgD;
-          V x = A::fma(be[k], pi, pd);
-          x = A::add(pm, x);
-          M[k].x = A::comp(la, kk) * x.x;
-          M[k].y = A::comp(lb, kk) * x.y;
+          if constexpr (EXACT) {
+            // D = zt*M(i,j-1) + ep*D(i,j-1); M = lam*(al*M + be*(I + D)) (reference.py:111-113)
+            D[k] = flush2(A::xadd(A::xmul(zt[k], M[k]), A::xmul(ep[k], D[k])), thr);
+            V x = A::xadd(A::xmul(al[k], pm), A::xmul(be[k], A::xadd(pi, pd)));
+            x.x = A::mul1(A::comp(la, kk), x.x);
+            x.y = A::mul1(A::comp(lb, kk), x.y);
+            M[k] = flush2(x, thr);
+          } else {
+            D[k] = A::fma(ep[k], D[k], A::mul(zt[k], M[k]));
+            V x = A::fma(be[k], pi, pd);
+            x = A::add(pm, x);
+            M[k].x = A::comp(la, kk) * x.x;
+            M[k].y = A::comp(lb, kk) * x.y;
+          }
         }
       }
       // pass 2 (ascending): I chain along the read within the current row
@@ -1011,7 +1117,8 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
         V lM = nbM, lI = nbI;
 #pragma unroll
         for (int k = 0; k < K; ++k) {
-          I[k] = A::fma(ep[k], lI, A::mul(dl[k], lM));
+          if constexpr (EXACT) I[k] = flush2(A::xadd(A::xmul(dl[k], lM), A::xmul(ep[k], lI)), thr);
+          else I[k] = A::fma(ep[k], lI, A::mul(dl[k], lM));
           lM = M[k];
           lI = I[k];
         }
@@ -1033,7 +1140,7 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
       const int e_sw = wi < nwin ? wb[wi] : 0x7fffffff;
       const int e = max((int)__reduce_min_sync(FULL, (unsigned)e_sw), s);
       const int fend = min(e, steps + 1);
-#pragma unroll 2
+#pragma unroll 1
       for (; s < fend; ++s) step(s, std::false_type{});
       if (s > steps) break;
       const int wend = min(e + P, steps + 1);
@@ -1041,58 +1148,19 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
       for (; s < wend; ++s) step(s, std::true_type{});
     }
     __syncwarp();
-    if constexpr (!F64) {
-      // FP32-underflowed pairs of this unit -> FP64 stream retry unit(s) for the same read
-      if (t == 0 && live && (s_flag[2 * slot] | s_flag[2 * slot + 1])) {
-        const int g64 = r64_geom_for(m);
-        const int cap = r64_cap(g64);
-        int lanes_n[2] = {0, 0}, rows_n[2] = {0, 0};
-        StreamHap buf[2][kStreamMaxLaneHaps];
-        auto emit = [&]() {
-          const int tot = lanes_n[0] + lanes_n[1];
-          if (tot == 0) return;
-          const int ui = atomicAdd(&E.r64_count[g64], 1);
-          const int hi = atomicAdd(E.r64_hap_count, tot);
-          if (ui < E.r64_unit_cap && hi + tot <= E.r64_hap_cap) {
-            for (int x = 0; x < lanes_n[0]; ++x) E.r64_haps[hi + x] = buf[0][x];
-            for (int x = 0; x < lanes_n[1]; ++x) E.r64_haps[hi + lanes_n[0] + x] = buf[1][x];
-            E.r64_units[g64][ui] = StreamUnit{r, hi, lanes_n[0], lanes_n[1], rows_n[0], rows_n[1], U.ro, m};
-          } else {                                  // list overflow: per-pair FP64 kernel
-            for (int ln = 0; ln < 2; ++ln)
-              for (int x = 0; x < lanes_n[ln]; ++x)
-                append_item(E.fx64, E.fx64_count, E.list_cap, exact_slot_for(m),
-                            ExactItem{buf[ln][x].pair, r, buf[ln][x].hap, 0});
-          }
-          lanes_n[0] = lanes_n[1] = 0;
-          rows_n[0] = rows_n[1] = 0;
-        };
-        for (int ln = 0; ln < 2; ++ln) {
-          unsigned msk = s_flag[2 * slot + ln];
-          const int e0 = U.list + (ln ? U.cntA : 0);
-          while (msk) {
-            const int e = __ffs(msk) - 1;
-            msk &= msk - 1;
-            const StreamHap sh = shaps[e0 + e];
-            const int n = sh.n;
-            int l2 = rows_n[0] <= rows_n[1] ? 0 : 1;
-            if (rows_n[l2] + n > cap || lanes_n[l2] >= kStreamMaxLaneHaps) { emit(); l2 = 0; }
-            buf[l2][lanes_n[l2]++] = sh;
-            rows_n[l2] += n;
-          }
+    if constexpr (MODE == kFast32) {
+      // this unit's FP32-underflowed and guard-band pairs -> device-built stream units
+      if (t == 0 && live) {
+        if (s_flag[2 * slot] | s_flag[2 * slot + 1]) {
+          const int g64 = r64_geom_for(m);
+          emit_retry_units(U, shaps, s_flag + 2 * slot, E.r64, g64, stream_cap_of(r64_geom_P(g64)), m,
+                           kRetryLaneHaps64);
         }
-        emit();
-      }
-      // guard-band pairs found in this unit: bit-exact FP32 rerun by the same warp (same
-      // tiling; the emission-table slot is free again), overlapping other warps' work
-      const int nbd = s_nband[slot];
-      const int nbmax = __reduce_max_sync(FULL, (unsigned)nbd);
-#pragma unroll 1
-      for (int x = 0; x < nbmax; ++x) {
-        const bool mine = x < nbd;
-        const ExactItem it = mine ? s_band[slot * kStreamBandCap + x]
-                                  : ExactItem{-1, U.read, shaps[U.list].hap, 0};
-        exact_item<float, P, K>(E, it, mine, s_lut, reinterpret_cast<float*>(Et), nullptr, nullptr, 0, t);
-        __syncwarp();
+        if (s_band[2 * slot] | s_band[2 * slot + 1]) {
+          const int gx = rx32_geom_for(m);
+          emit_retry_units(U, shaps, s_band + 2 * slot, E.rx32, gx, stream_cap_of(rx32_geom_P(gx)), m,
+                           kRetryLaneHapsX32);
+        }
       }
     }
   }
