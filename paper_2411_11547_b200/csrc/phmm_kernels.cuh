@@ -688,6 +688,7 @@ constexpr int kNumRX32Geoms = 8;    // exact FP32:  (8,4) (16,4) (8,12) (16,8) (
 // haplotypes per lane of a device-built unit: short units keep these small post-pass
 // lists parallel (their count is unknown when the grid is sized)
 constexpr int kRetryLaneHaps64 = 2, kRetryLaneHapsX32 = 1;
+constexpr int kInlineBand = 4;      // guard-band pairs a warp may rerun inline per unit
 __host__ __device__ __forceinline__ int r64_geom_for(int m) {
   const int w = m + 1;
   return w <= 32 ? 0 : w <= 64 ? 1 : w <= 96 ? 2 : w <= 128 ? 3 : w <= 192 ? 4 : w <= 256 ? 5 : -1;
@@ -841,6 +842,8 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
   __shared__ int s_nwin[4 * G];
   __shared__ unsigned s_flag[4 * G * 2];          // kFast32: lane entries that underflowed
   __shared__ unsigned s_band[4 * G * 2];          // kFast32: lane entries in the guard band
+  __shared__ ExactItem s_inl[MODE == kFast32 ? 4 * G * kInlineBand : 1];
+  __shared__ int s_ninl[4 * G];
 
   for (;;) {
     int g = 0;
@@ -980,6 +983,7 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
       s_unit[slot] = U;
       s_flag[2 * slot] = 0u; s_flag[2 * slot + 1] = 0u;
       s_band[2 * slot] = 0u; s_band[2 * slot + 1] = 0u;
+      s_ninl[slot] = 0;
     }
     s_hc[2 * threadIdx.x] = -1;                         // current haplotype per lane
     s_hc[2 * threadIdx.x + 1] = -1;
@@ -1050,8 +1054,14 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
       } else {
         const int v = stream_finish32(E, res, sh.pair, sh.n, __int_as_float(s_meta[slot * 4 + 2]),
                                       s_meta[slot * 4 + 1]);
-        if (v == 1) {                                   // guard band: exact rerun unit
-          if (E.rx32.enabled && rx32_geom_for(mm) >= 0) s_band[2 * slot + L] |= 1u << hc;
+        if (v == 1) {                                   // guard band: bit-exact rerun
+          const int c = s_ninl[slot];
+          if (c < kInlineBand && atomicAdd(E.band_inline, 1) < E.band_budget) {
+            // the first few per launch: rerun by this warp right after the unit (no
+            // post-pass latency when band pairs are rare)
+            s_inl[slot * kInlineBand + c] = ExactItem{sh.pair, SU.read, sh.hap, s_meta[slot * 4 + 1]};
+            s_ninl[slot] = c + 1;
+          } else if (E.rx32.enabled && rx32_geom_for(mm) >= 0) s_band[2 * slot + L] |= 1u << hc;
           else append_item(E.ex32, E.ex32_count, E.list_cap, exact_slot_for(mm),
                            ExactItem{sh.pair, SU.read, sh.hap, s_meta[slot * 4 + 1]});
         } else if (v == 2) {                            // FP32 underflow: FP64 retry unit
@@ -1161,6 +1171,16 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
           emit_retry_units(U, shaps, s_band + 2 * slot, E.rx32, gx, stream_cap_of(rx32_geom_P(gx)), m,
                            kRetryLaneHapsX32);
         }
+      }
+      // inline guard-band reruns (same tiling; the emission-table slot is free again)
+      const int nin = s_ninl[slot];
+      const int nmax = __reduce_max_sync(FULL, (unsigned)nin);
+#pragma unroll 1
+      for (int x = 0; x < nmax; ++x) {
+        const bool mine = x < nin;
+        const ExactItem it = mine ? s_inl[slot * kInlineBand + x] : ExactItem{-1, U.read, shaps[U.list].hap, 0};
+        exact_item<float, P, K>(E, it, mine, s_lut, reinterpret_cast<float*>(Et), nullptr, nullptr, 0, t);
+        __syncwarp();
       }
     }
   }
