@@ -12,7 +12,7 @@ for W in ${PROFILE_WORKLOADS:-c2}; do
      --log-file gpurun_out/launches_${W}.csv python tools/profile_run.py $W 2 --retry > gpurun_out/launches_${W}.log 2>&1
 done
 if [ -n "$NCU_FULL" ]; then
-  timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_stream -s 1 -c 1 \
+  timeout 600 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:"k_stream<.int.0," -s 1 -c 1 \
      -o gpurun_out/prof_kstream_c2 python tools/profile_run.py c2 2 > gpurun_out/prof_c2.log 2>&1
 fi
 ls gpurun_out
