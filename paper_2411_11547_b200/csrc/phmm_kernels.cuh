@@ -992,9 +992,15 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
     // ---- the stream
     V cb = zero2;                                       // thread 0: boundary D of row s
     V nbM = zero2, nbI = zero2, nbD = zero2;
+    // every thread reads its own row's code from shared memory one step ahead (row 0 is
+    // the idle code N|N: rows before, between and after this thread's stream)
+    const unsigned short* cdt = cd16 - t;
+    auto ld_code = [&](int s) -> unsigned {
+      const int i = s - t;
+      return (unsigned)cdt[(i >= 1 && i <= rows) ? s : t];
+    };
     unsigned code = 0x0404u;
-    auto ld_code = [&](int s) -> unsigned { return (t == 0 && s <= rows) ? (unsigned)cd16[s] : 0x0404u; };
-    unsigned pf1 = ld_code(1), pf2 = ld_code(2);
+    unsigned pf1 = ld_code(1);
 
     // FIRST(lane L): reset the lane to row 0 of its next haplotype (event paths only run
     // inside windows and read their inputs from shared memory)
@@ -1082,12 +1088,10 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
         nbI.y = __shfl_up_sync(FULL, li.y, 1, P);
         nbD.x = __shfl_up_sync(FULL, ld.x, 1, P);
         nbD.y = __shfl_up_sync(FULL, ld.y, 1, P);
-        const unsigned up = __shfl_up_sync(FULL, code, 1, P);
-        code = (t == 0) ? pf1 : up;
       }
       if (t == 0) { nbM = zero2; nbI = zero2; nbD = cb; }
-      pf1 = pf2;
-      pf2 = ld_code(s + 2);
+      code = pf1;
+      pf1 = ld_code(s + 1);
       if (CHECK && (code & ((kCodeFirst << 8) | kCodeFirst))) {
         if (code & kCodeFirst) first_event(std::integral_constant<int, 0>{}, dgM, dgI, dgD);
         if (code & (kCodeFirst << 8)) first_event(std::integral_constant<int, 1>{}, dgM, dgI, dgD);
