@@ -991,7 +991,8 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
 
     // ---- the stream
     V cb = zero2;                                       // thread 0: boundary D of row s
-    V nbM = zero2, nbI = zero2, nbD = zero2;
+    V xM = zero2, xI = zero2, xD = zero2;               // neighbour values of the last step
+    V yM = zero2, yI = zero2, yD = zero2;
     // every thread reads its own row's code from shared memory one step ahead (row 0 is
     // the idle code N|N: rows before, between and after this thread's stream)
     const unsigned short* cdt = cd16 - t;
@@ -1004,7 +1005,7 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
 
     // FIRST(lane L): reset the lane to row 0 of its next haplotype (event paths only run
     // inside windows and read their inputs from shared memory)
-    auto first_event = [&](auto lconst, V& dgM, V& dgI, V& dgD) {
+    auto first_event = [&](auto lconst, V& dgM, V& dgI, V& dgD, V& nbM, V& nbI, V& nbD) {
       constexpr int L = decltype(lconst)::value;
       const int hc = ++s_hc[2 * threadIdx.x + L];
       const int lp = s_meta[slot * 4 + 0];
@@ -1077,9 +1078,11 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
       }
     };
 
-    auto step = [&](const int s, auto checked) {
+    // One step; (dgM, dgI, dgD) holds the previous step's neighbour values (the diagonal
+    // input of position 0) and the shuffle writes this step's into (nbM, nbI, nbD): the
+    // caller alternates two register sets so no copy is needed between steps.
+    auto step = [&](const int s, auto checked, V& dgM, V& dgI, V& dgD, V& nbM, V& nbI, V& nbD) {
       constexpr bool CHECK = decltype(checked)::value;
-      V dgM = nbM, dgI = nbI, dgD = nbD;
       {
         const V lm = M[K - 1], li = I[K - 1], ld = D[K - 1];
         nbM.x = __shfl_up_sync(FULL, lm.x, 1, P);
@@ -1093,8 +1096,8 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
       code = pf1;
       pf1 = ld_code(s + 1);
       if (CHECK && (code & ((kCodeFirst << 8) | kCodeFirst))) {
-        if (code & kCodeFirst) first_event(std::integral_constant<int, 0>{}, dgM, dgI, dgD);
-        if (code & (kCodeFirst << 8)) first_event(std::integral_constant<int, 1>{}, dgM, dgI, dgD);
+        if (code & kCodeFirst) first_event(std::integral_constant<int, 0>{}, dgM, dgI, dgD, nbM, nbI, nbD);
+        if (code & (kCodeFirst << 8)) first_event(std::integral_constant<int, 1>{}, dgM, dgI, dgD, nbM, nbI, nbD);
       }
       const int cA = code & 7, cB = (code >> 8) & 7;
       const EV* EA = Et + (cA * KE) * P + t;
@@ -1155,11 +1158,22 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
       const int e = max((int)__reduce_min_sync(FULL, (unsigned)e_sw), s);
       const int fend = min(e, steps + 1);
 #pragma unroll 1
-      for (; s < fend; ++s) step(s, std::false_type{});
+      for (; s + 1 < fend; s += 2) {
+        step(s, std::false_type{}, xM, xI, xD, yM, yI, yD);
+        step(s + 1, std::false_type{}, yM, yI, yD, xM, xI, xD);
+      }
+      if (s < fend) {
+        step(s, std::false_type{}, xM, xI, xD, yM, yI, yD);
+        xM = yM; xI = yI; xD = yD;
+        ++s;
+      }
       if (s > steps) break;
       const int wend = min(e + P, steps + 1);
 #pragma unroll 1
-      for (; s < wend; ++s) step(s, std::true_type{});
+      for (; s < wend; ++s) {
+        step(s, std::true_type{}, xM, xI, xD, yM, yI, yD);
+        xM = yM; xI = yI; xD = yD;
+      }
     }
     __syncwarp();
     if constexpr (MODE == kFast32) {
