@@ -126,17 +126,20 @@ void launch_stream_t(dim3 g, size_t smem, cudaStream_t s, const EngineDev& E, co
 }
 template <int MODE, int P, int K>
 StreamKernel SK() {
-  const size_t elem = ModeOf<MODE>::F64 ? sizeof(double) : sizeof(float);
+  const size_t elem = ModeOf<MODE>::F64 ? sizeof(double) : sizeof(float);   // 5*K*P entries per slot
   return StreamKernel{P, K, StreamOcc<MODE, K>::value,
                       96 * sizeof(double) + (size_t)4 * (32 / P) * 5 * K * P * elem + kStreamCodeBytesPerCta,
                       (const void*)k_stream<MODE, P, K>, launch_stream_t<MODE, P, K>};
 }
-// kFast32 uses the k_fast tiling table (same order as kFastGeoms)
-const StreamKernel kStreamFast32[kNumFastGeoms] = {
+// kFast32: the k_fast tiling table (same order as kFastGeoms, so PHMM_FAST_GEOM applies),
+// then K = 10, 14 tilings (2-wide emission chunks) for widths 80 .. 448
+constexpr int kNumStreamFast32 = kNumFastGeoms + 6;
+const StreamKernel kStreamFast32[kNumStreamFast32] = {
     SK<kFast32, 4, 4>(),   SK<kFast32, 4, 8>(),   SK<kFast32, 4, 12>(),  SK<kFast32, 4, 16>(),
     SK<kFast32, 8, 8>(),   SK<kFast32, 8, 12>(),  SK<kFast32, 8, 16>(),  SK<kFast32, 16, 8>(),
     SK<kFast32, 16, 12>(), SK<kFast32, 16, 16>(), SK<kFast32, 32, 8>(),  SK<kFast32, 32, 12>(),
-    SK<kFast32, 32, 16>()};
+    SK<kFast32, 32, 16>(), SK<kFast32, 8, 10>(),  SK<kFast32, 8, 14>(),  SK<kFast32, 16, 10>(),
+    SK<kFast32, 16, 14>(), SK<kFast32, 32, 10>(), SK<kFast32, 32, 14>()};
 // FP64 tilings, indexed by r64_geom_for(m): W = 32, 64, 96, 128, 192, 256
 const StreamKernel kStreamFast64[kNumR64Geoms] = {SK<kFast64, 8, 4>(),  SK<kFast64, 16, 4>(),
                                                   SK<kFast64, 16, 6>(), SK<kFast64, 16, 8>(),
@@ -149,7 +152,9 @@ const StreamKernel kStreamExact32[kNumRX32Geoms] = {
     SK<kExact32, 8, 4>(),   SK<kExact32, 16, 4>(),  SK<kExact32, 8, 12>(), SK<kExact32, 16, 8>(),
     SK<kExact32, 16, 12>(), SK<kExact32, 16, 16>(), SK<kExact32, 32, 12>(), SK<kExact32, 32, 16>()};
 const StreamKernel* const kStreamTab[4] = {kStreamFast32, kStreamFast64, kStreamExact32, kStreamExact64};
-const int kStreamTabN[4] = {kNumFastGeoms, kNumR64Geoms, kNumRX32Geoms, kNumR64Geoms};
+const int kStreamTabN[4] = {kNumStreamFast32, kNumR64Geoms, kNumRX32Geoms, kNumR64Geoms};
+constexpr int kMaxTilings = 24;
+static_assert(kNumStreamFast32 <= kMaxTilings, "tiling table");
 
 int stream_cap(int P) { return stream_cap_of(P); }
 
@@ -623,8 +628,8 @@ static int prepare_impl(phmm_ctx* ctx, const phmm_input* in, const phmm_options*
   // streaming units address reads/haplotypes with 32-bit offsets
   const bool use_stream = streaming_enabled() && RL < INT32_MAX && HL < INT32_MAX;
   std::vector<int> bin_index(kNumFastGeoms * 64, -1);
-  int sbin_index[4 * 16];
-  std::fill(sbin_index, sbin_index + 4 * 16, -1);
+  int sbin_index[4 * kMaxTilings];
+  std::fill(sbin_index, sbin_index + 4 * kMaxTilings, -1);
   std::vector<ExactItem> host32[kNumExactP], host64[kNumExactP];
   int max_n = 1;
   int64_t gid = 0;
@@ -637,9 +642,9 @@ static int prepare_impl(phmm_ctx* ctx, const phmm_input* in, const phmm_options*
   // W >= m + 1), best tiling per width and lane templates, both cached per batch
   struct ModePlan {
     int n = 0;
-    int wsort[16], wsorted[16], best_from[16];
-    bool tvalid[16];
-    std::vector<LaneTemplate> tmpls[16];
+    int wsort[kMaxTilings], wsorted[kMaxTilings], best_from[kMaxTilings];
+    bool tvalid[kMaxTilings];
+    std::vector<LaneTemplate> tmpls[kMaxTilings];
     int tmpl_m = -1, tmpl_geom = -2;
   };
   ModePlan mp[4];
@@ -667,8 +672,8 @@ static int prepare_impl(phmm_ctx* ctx, const phmm_input* in, const phmm_options*
     for (int md = 0; md < 4; ++md) {
       mp[md].tmpl_m = -1;
       mp[md].tmpl_geom = -2;
-      std::fill(mp[md].tvalid, mp[md].tvalid + 16, false);
-      std::fill(mp[md].best_from, mp[md].best_from + 16, -2);
+      std::fill(mp[md].tvalid, mp[md].tvalid + kMaxTilings, false);
+      std::fill(mp[md].best_from, mp[md].best_from + kMaxTilings, -2);
     }
     hidx.resize(nh);
     std::iota(hidx.begin(), hidx.end(), (int)h0);
@@ -719,7 +724,7 @@ static int prepare_impl(phmm_ctx* ctx, const phmm_input* in, const phmm_options*
         }
         if (M.tmpl_geom >= 0) {
           const std::vector<LaneTemplate>& tmpl = M.tmpls[M.tmpl_geom];
-          const int key = mode * 16 + M.tmpl_geom;
+          const int key = mode * kMaxTilings + M.tmpl_geom;
           if (sbin_index[key] < 0) {
             sbin_index[key] = (int)ctx->sbins.size();
             ctx->sbins.push_back(phmm_ctx::SBin{mode, M.tmpl_geom, 0, 0});

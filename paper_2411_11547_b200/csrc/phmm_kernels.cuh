@@ -744,6 +744,18 @@ template <> struct Lanes<true> {
   static __device__ __forceinline__ S thr() { return 0x1p-970; }
 };
 template <int L, class V> __device__ __forceinline__ auto& lane_ref(V& v) { return L == 0 ? v.x : v.y; }
+// emission-table chunks: float4 (4 positions, LDS.128) when K % 4 == 0, float2 (LDS.64)
+// for K = 10, 14; double2 in FP64
+__device__ __forceinline__ float ev_comp(const float4& v, int i) { return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w; }
+__device__ __forceinline__ float ev_comp(const float2& v, int i) { return i == 0 ? v.x : v.y; }
+__device__ __forceinline__ double ev_comp(const double2& v, int i) { return i == 0 ? v.x : v.y; }
+__device__ __forceinline__ void ev_pack(float4& e, const float* l) { e = make_float4(l[0], l[1], l[2], l[3]); }
+__device__ __forceinline__ void ev_pack(float2& e, const float* l) { e = make_float2(l[0], l[1]); }
+__device__ __forceinline__ void ev_pack(double2& e, const double* l) { e = make_double2(l[0], l[1]); }
+template <bool F64, int K> struct EChunk {
+  using type = typename std::conditional<F64, double2, typename std::conditional<K % 4 == 0, float4, float2>::type>::type;
+  static constexpr int width = F64 ? 2 : (K % 4 == 0 ? 4 : 2);
+};
 template <class V, class S> __device__ __forceinline__ V flush2(V v, S thr) {
   v.x = v.x >= thr ? v.x : (S)0;            // reference store flush (wavefront.py:134-136)
   v.y = v.y >= thr ? v.y : (S)0;
@@ -812,8 +824,8 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
   using A = Lanes<F64>;
   using S = typename A::S;
   using V = typename A::V;
-  using EV = typename A::EV;
-  constexpr int EW = A::EW;
+  using EV = typename EChunk<F64, K>::type;
+  constexpr int EW = EChunk<F64, K>::width;
   constexpr int W = P * K, G = 32 / P, KE = K / EW;
   constexpr int CB = kStreamCodeBytesPerCta / (4 * G);
   static_assert(K % EW == 0 && K >= 4, "K multiple of the emission chunk");
@@ -926,7 +938,7 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
         }
       }
 #pragma unroll
-      for (int c = 0; c < 5; ++c) Et[(c * KE + ke) * P + t] = A::pack(lam[c]);
+      for (int c = 0; c < 5; ++c) ev_pack(Et[(c * KE + ke) * P + t], lam[c]);
     }
 
     // ---- row codes of both lanes into shared memory (row 0 = idle code N|N), and the
@@ -1117,15 +1129,15 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
             // D = zt*M(i,j-1) + ep*D(i,j-1); M = lam*(al*M + be*(I + D)) (reference.py:111-113)
             D[k] = flush2(A::xadd(A::xmul(zt[k], M[k]), A::xmul(ep[k], D[k])), thr);
             V x = A::xadd(A::xmul(al[k], pm), A::xmul(be[k], A::xadd(pi, pd)));
-            x.x = A::mul1(A::comp(la, kk), x.x);
-            x.y = A::mul1(A::comp(lb, kk), x.y);
+            x.x = A::mul1(ev_comp(la, kk), x.x);
+            x.y = A::mul1(ev_comp(lb, kk), x.y);
             M[k] = flush2(x, thr);
           } else {
             D[k] = A::fma(ep[k], D[k], A::mul(zt[k], M[k]));
             V x = A::fma(be[k], pi, pd);
             x = A::add(pm, x);
-            M[k].x = A::comp(la, kk) * x.x;
-            M[k].y = A::comp(lb, kk) * x.y;
+            M[k].x = ev_comp(la, kk) * x.x;
+            M[k].y = ev_comp(lb, kk) * x.y;
           }
         }
       }
