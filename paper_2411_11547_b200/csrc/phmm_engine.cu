@@ -148,9 +148,10 @@ const StreamKernel kStreamExact64[kNumR64Geoms] = {SK<kExact64, 8, 4>(),  SK<kEx
                                                    SK<kExact64, 16, 6>(), SK<kExact64, 16, 8>(),
                                                    SK<kExact64, 32, 6>(), SK<kExact64, 32, 8>()};
 // exact FP32 tilings, indexed by rx32_geom_for(m): W = 32, 64, 96, 128, 192, 256, 384, 512
+// (wide sub-warps: guard-band reruns are few and latency bound)
 const StreamKernel kStreamExact32[kNumRX32Geoms] = {
-    SK<kExact32, 8, 4>(),   SK<kExact32, 16, 4>(),  SK<kExact32, 8, 12>(), SK<kExact32, 16, 8>(),
-    SK<kExact32, 16, 12>(), SK<kExact32, 16, 16>(), SK<kExact32, 32, 12>(), SK<kExact32, 32, 16>()};
+    SK<kExact32, 8, 4>(),  SK<kExact32, 16, 4>(), SK<kExact32, 16, 6>(),  SK<kExact32, 32, 4>(),
+    SK<kExact32, 32, 6>(), SK<kExact32, 32, 8>(), SK<kExact32, 32, 12>(), SK<kExact32, 32, 16>()};
 const StreamKernel* const kStreamTab[4] = {kStreamFast32, kStreamFast64, kStreamExact32, kStreamExact64};
 const int kStreamTabN[4] = {kNumStreamFast32, kNumR64Geoms, kNumRX32Geoms, kNumR64Geoms};
 constexpr int kMaxTilings = 24;

@@ -684,7 +684,7 @@ template <int MODE, int K> struct StreamOcc {
 // Device-built stream units (one list per tiling): FP64 retries of FP32-underflowed pairs
 // and bit-exact reruns of guard-band pairs, grouped per read by the FP32 stream kernel.
 constexpr int kNumR64Geoms = 6;     // FP64 retry:  (8,4) (16,4) (16,6) (16,8) (32,6) (32,8)
-constexpr int kNumRX32Geoms = 8;    // exact FP32:  (8,4) (16,4) (8,12) (16,8) (16,12) (16,16) (32,12) (32,16)
+constexpr int kNumRX32Geoms = 8;    // exact FP32:  (8,4) (16,4) (16,6) (32,4) (32,6) (32,8) (32,12) (32,16)
 // haplotypes per lane of a device-built unit: short units keep these small post-pass
 // lists parallel (their count is unknown when the grid is sized)
 constexpr int kRetryLaneHaps64 = 2, kRetryLaneHapsX32 = 1;
@@ -699,7 +699,7 @@ __host__ __device__ __forceinline__ int rx32_geom_for(int m) {
   return w <= 32 ? 0 : w <= 64 ? 1 : w <= 96 ? 2 : w <= 128 ? 3 : w <= 192 ? 4 : w <= 256 ? 5
        : w <= 384 ? 6 : w <= 512 ? 7 : -1;
 }
-__host__ __device__ __forceinline__ int rx32_geom_P(int g) { return g == 0 || g == 2 ? 8 : (g <= 5 ? 16 : 32); }
+__host__ __device__ __forceinline__ int rx32_geom_P(int g) { return g == 0 ? 8 : (g <= 2 ? 16 : 32); }
 
 struct Dbl2 { double x, y; };
 
