@@ -235,6 +235,17 @@ int choose_stream_geom(int mode, int m, int64_t total, int nmax) {
   return bi;
 }
 
+constexpr int kScoreChunks = 4;               // phmm_score pipelining depth
+constexpr int64_t kScoreChunkMinPairs = 32768;
+bool score_chunking_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* env = getenv("PHMM_NO_CHUNK");
+    v = (env && env[0] == '1') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 bool streaming_enabled() {
   static int v = -1;
   if (v < 0) {
@@ -350,7 +361,7 @@ struct phmm_ctx {
   DBuf<int8_t> d_rbases, d_hbases;
   DBuf<uint8_t> d_bq, d_iq, d_dq, d_gq, d_status, d_rflags;
   DBuf<int64_t> d_roff, d_hoff;
-  DBuf<int> d_read_m, d_read_scale, d_read_ncap, d_counters;
+  DBuf<int> d_read_m, d_read_scale, d_read_ncap, d_counters, d_vflag;
   DBuf<float> d_gsum;
   DBuf<double> d_lut, d_acc;
   DBuf<FastUnit> d_units;
@@ -363,6 +374,11 @@ struct phmm_ctx {
   DBuf<double> d_cold;
   std::unique_ptr<WorkerPool> pool;         // host finishing threads (lazy)
   int* h_counts = nullptr;   // pinned: initial list counts (8) + zeros for work counters
+  int* h_vflag = nullptr;    // pinned: device validation flag
+  bool async = false;        // chunk contexts of phmm_score: no host syncs in prepare/execute
+  phmm_ctx* parent = nullptr;
+  std::vector<phmm_ctx*> chunks;             // chunk contexts (phmm_score pipelining), lazy
+  std::vector<int64_t> c_roff, c_hoff, c_bro, c_bho;   // chunk views: rebased offsets
   double* h_acc = nullptr;   // pinned result staging (phmm_fetch)
   uint8_t* h_st = nullptr;
   int64_t h_res_cap = 0;
@@ -423,6 +439,8 @@ extern "C" {
 
 int phmm_abi_version(void) { return PHMM_ABI_VERSION; }
 
+static int init_ctx(phmm_ctx* ctx, int device);
+
 int phmm_create(phmm_ctx** out, int device, const double* phred_lut) {
   if (!out || !phred_lut) return PHMM_ERR_INVALID;
   *out = nullptr;
@@ -439,6 +457,10 @@ int phmm_create(phmm_ctx** out, int device, const double* phred_lut) {
     return PHMM_ERR_CUDA;
   }
   *out = ctx;
+  return init_ctx(ctx, device);
+}
+
+static int init_ctx(phmm_ctx* ctx, int device) {
   CK(cudaSetDevice(device));
   cudaDeviceProp prop;
   CK(cudaGetDeviceProperties(&prop, device));
@@ -456,6 +478,7 @@ int phmm_create(phmm_ctx** out, int device, const double* phred_lut) {
   CK(cudaEventCreate(&ctx->ev_fast1));
   CK(cudaEventCreate(&ctx->ev_end));
   CK(cudaMallocHost(&ctx->h_counts, kBinCounters * sizeof(int)));
+  CK(cudaMallocHost(&ctx->h_vflag, sizeof(int)));
   CK(ctx->d_lut.ensure(94));
   CK(cudaMemcpy(ctx->d_lut.p, ctx->lut.data(), 94 * sizeof(double), cudaMemcpyHostToDevice));
   for (int g = 0; g < 2 * kNumFastGeoms; ++g)
@@ -480,14 +503,17 @@ int phmm_destroy(phmm_ctx* ctx) {
   ctx->d_rbases.release(); ctx->d_hbases.release(); ctx->d_bq.release(); ctx->d_iq.release();
   ctx->d_dq.release(); ctx->d_gq.release(); ctx->d_status.release(); ctx->d_rflags.release();
   ctx->d_roff.release(); ctx->d_hoff.release(); ctx->d_read_m.release(); ctx->d_read_scale.release();
-  ctx->d_read_ncap.release(); ctx->d_counters.release(); ctx->d_gsum.release(); ctx->d_lut.release();
+  ctx->d_read_ncap.release(); ctx->d_counters.release(); ctx->d_vflag.release(); ctx->d_gsum.release(); ctx->d_lut.release();
   ctx->d_acc.release(); ctx->d_units.release(); ctx->d_sunits.release(); ctx->d_shaps.release();
   for (int g = 0; g < kNumR64Geoms; ++g) ctx->d_r64u[g].release();
   for (int g = 0; g < kNumRX32Geoms; ++g) ctx->d_rx32u[g].release();
   ctx->d_r64h.release();
   ctx->d_rx32h.release(); ctx->d_colf.release(); ctx->d_cold.release();
   for (int s = 0; s < kNumExactP; ++s) { ctx->d_ex32[s].release(); ctx->d_ex64[s].release(); ctx->d_fx64[s].release(); }
+  for (phmm_ctx* c : ctx->chunks) phmm_destroy(c);
+  ctx->chunks.clear();
   if (ctx->h_counts) cudaFreeHost(ctx->h_counts);
+  if (ctx->h_vflag) cudaFreeHost(ctx->h_vflag);
   if (ctx->h_acc) cudaFreeHost(ctx->h_acc);
   if (ctx->h_st) cudaFreeHost(ctx->h_st);
   ctx->h_counts = nullptr;
@@ -508,6 +534,15 @@ int phmm_destroy(phmm_ctx* ctx) {
 const char* phmm_last_error(const phmm_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
 
 static int prepare_impl(phmm_ctx* ctx, const phmm_input* in, const phmm_options* opt, int64_t* num_pairs_out);
+
+// waits for the prepare's uploads and the device content checks (k_validate)
+static int check_validation(phmm_ctx* ctx) {
+  CK(cudaEventSynchronize(ctx->ev_end));
+  const int vbad = *ctx->h_vflag;
+  if (vbad & 1) return ctx->fail(PHMM_ERR_INVALID, "base code outside A,C,G,T,N (0..4)");
+  if (vbad & 2) return ctx->fail(PHMM_ERR_INVALID, "quality values must be in [0, 93]");
+  return PHMM_SUCCESS;
+}
 
 int phmm_prepare(phmm_ctx* ctx, const phmm_input* in, const phmm_options* opt, int64_t* num_pairs_out) {
   if (!ctx) return PHMM_ERR_INVALID;
@@ -855,7 +890,8 @@ static int prepare_impl(phmm_ctx* ctx, const phmm_input* in, const phmm_options*
   (void)need_cold;
   trace.mark("plan-upload");
   // content validation on the device (bases 0..4, qualities 0..93)
-  int* vflag = ctx->d_counters.p + kBinCounters - 1;
+  CK(ctx->d_vflag.ensure(1));
+  int* vflag = ctx->d_vflag.p;                 // also gates every kernel of the execute
   CK(cudaMemsetAsync(vflag, 0, sizeof(int), ctx->stream));
   if (RL + HL > 0) {
     const int64_t work = std::max<int64_t>(RL, HL) / 16 + 1;
@@ -865,16 +901,17 @@ static int prepare_impl(phmm_ctx* ctx, const phmm_input* in, const phmm_options*
                                                  HL, vflag);
     CK(cudaGetLastError());
   }
-  CK(cudaMemcpyAsync(ctx->h_counts + kBinCounters - 1, vflag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemcpyAsync(ctx->h_vflag, vflag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaEventRecord(ctx->ev_end, ctx->stream));
-  CK(cudaStreamSynchronize(ctx->stream));
-  const int vbad = ctx->h_counts[kBinCounters - 1];
-  if (vbad & 1) return ctx->fail(PHMM_ERR_INVALID, "base code outside A,C,G,T,N (0..4)");
-  if (vbad & 2) return ctx->fail(PHMM_ERR_INVALID, "quality values must be in [0, 93]");
-  float h2d = 0.f;
-  cudaEventElapsedTime(&h2d, ctx->ev_start, ctx->ev_end);
-  ctx->h2d_ms = h2d;
   ctx->h2d_bytes = bytes;
+  ctx->h2d_ms = 0.0;
+  if (!ctx->async) {
+    int rc = check_validation(ctx);
+    if (rc != PHMM_SUCCESS) return rc;
+    float h2d = 0.f;
+    cudaEventElapsedTime(&h2d, ctx->ev_start, ctx->ev_end);
+    ctx->h2d_ms = h2d;
+  }
 
   // device-built stream units (FP64 retries, exact guard-band reruns): sized for every
   // pair of the FP32 stream units (worst case: all of them)
@@ -899,6 +936,7 @@ static int prepare_impl(phmm_ctx* ctx, const phmm_input* in, const phmm_options*
   E.read_m = ctx->d_read_m.p; E.read_scale = ctx->d_read_scale.p; E.read_ncap = ctx->d_read_ncap.p;
   E.read_gsum = ctx->d_gsum.p; E.read_flags = ctx->d_rflags.p; E.lut = ctx->d_lut.p;
   E.acc = ctx->d_acc.p; E.status = ctx->d_status.p;
+  E.invalid = ctx->d_vflag.p;
   for (int s = 0; s < kNumExactP; ++s) {
     E.ex32[s] = ctx->d_ex32[s].p; E.ex64[s] = ctx->d_ex64[s].p; E.fx64[s] = ctx->d_fx64[s].p;
   }
@@ -1054,22 +1092,20 @@ int phmm_execute(phmm_ctx* ctx) {
   ++launches;
   CK(cudaGetLastError());
   CK(cudaEventRecord(ctx->ev_end, st));
+  ctx->last_launches = launches;
+  ctx->executed = true;
+  if (ctx->async) return PHMM_SUCCESS;
   CK(cudaEventSynchronize(ctx->ev_end));
   float dev = 0.f, fast = 0.f;
   CK(cudaEventElapsedTime(&dev, ctx->ev_start, ctx->ev_end));
   CK(cudaEventElapsedTime(&fast, ctx->ev_fast0, ctx->ev_fast1));
   ctx->last_dev_ms = dev;
   ctx->last_fast_ms = fast;
-  ctx->last_launches = launches;
-  ctx->executed = true;
   return PHMM_SUCCESS;
 }
 
-int phmm_fetch(phmm_ctx* ctx, double* out_log10, uint8_t* out_status, phmm_stats* stats) {
-  if (!ctx) return PHMM_ERR_INVALID;
-  if (!ctx->executed) return ctx->fail(PHMM_ERR_STATE, "phmm_fetch before phmm_execute");
-  Trace trace;
-  CK(cudaSetDevice(ctx->device));
+// D2H of the raw results into pinned staging, asynchronous on the engine stream
+static int fetch_enqueue(phmm_ctx* ctx) {
   const int64_t N = ctx->num_pairs;
   if (N > ctx->h_res_cap) {                 // pinned staging for the D2H of acc + status
     if (ctx->h_acc) cudaFreeHost(ctx->h_acc);
@@ -1079,17 +1115,34 @@ int phmm_fetch(phmm_ctx* ctx, double* out_log10, uint8_t* out_status, phmm_stats
     CK(cudaMallocHost(&ctx->h_st, N));
     ctx->h_res_cap = N;
   }
-  const double* acc = ctx->h_acc;
-  const uint8_t* st = ctx->h_st;
-  CK(cudaEventRecord(ctx->ev_start, ctx->stream));
+  CK(cudaEventRecord(ctx->ev_fast0, ctx->stream));     // (reused as the D2H start marker)
   if (N > 0) {
     CK(cudaMemcpyAsync(ctx->h_acc, ctx->d_acc.p, N * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaMemcpyAsync(ctx->h_st, ctx->d_status.p, N, cudaMemcpyDeviceToHost, ctx->stream));
   }
-  CK(cudaEventRecord(ctx->ev_end, ctx->stream));
-  CK(cudaStreamSynchronize(ctx->stream));
+  CK(cudaEventRecord(ctx->ev_fast1, ctx->stream));
+  return PHMM_SUCCESS;
+}
+
+static int fetch_complete(phmm_ctx* ctx, double* out_log10, uint8_t* out_status, phmm_stats* stats);
+
+int phmm_fetch(phmm_ctx* ctx, double* out_log10, uint8_t* out_status, phmm_stats* stats) {
+  if (!ctx) return PHMM_ERR_INVALID;
+  if (!ctx->executed) return ctx->fail(PHMM_ERR_STATE, "phmm_fetch before phmm_execute");
+  CK(cudaSetDevice(ctx->device));
+  int rc = fetch_enqueue(ctx);
+  if (rc != PHMM_SUCCESS) return rc;
+  return fetch_complete(ctx, out_log10, out_status, stats);
+}
+
+static int fetch_complete(phmm_ctx* ctx, double* out_log10, uint8_t* out_status, phmm_stats* stats) {
+  Trace trace;
+  const int64_t N = ctx->num_pairs;
+  const double* acc = ctx->h_acc;
+  const uint8_t* st = ctx->h_st;
+  CK(cudaEventSynchronize(ctx->ev_fast1));
   float d2h = 0.f;
-  cudaEventElapsedTime(&d2h, ctx->ev_start, ctx->ev_end);
+  cudaEventElapsedTime(&d2h, ctx->ev_fast0, ctx->ev_fast1);
   // finishing (wavefront.py:428-434): host glibc log10 (= CPython math.log10), batches
   // split over a few threads
   struct Acc { int64_t cells = 0, fast = 0, exact = 0, f64 = 0, flagged = 0; };
@@ -1139,11 +1192,13 @@ int phmm_fetch(phmm_ctx* ctx, double* out_log10, uint8_t* out_status, phmm_stats
     }
   };
   trace.mark("d2h");
-  if (!ctx->pool && N >= 16384) {
+  phmm_ctx* owner = ctx->parent ? ctx->parent : ctx;    // chunk contexts share one pool
+  if (!owner->pool && N >= 8192) {
     const int hw = (int)std::max(1u, std::thread::hardware_concurrency());
-    ctx->pool.reset(new WorkerPool(std::min(hw, kFinishThreads) - 1));
+    owner->pool.reset(new WorkerPool(std::min(hw, kFinishThreads) - 1));
   }
-  const int nth = ctx->pool ? (int)std::max<int64_t>(1, std::min<int64_t>(ctx->pool->size() + 1, N / 4096)) : 1;
+  WorkerPool* pool = owner->pool.get();
+  const int nth = pool ? (int)std::max<int64_t>(1, std::min<int64_t>(pool->size() + 1, N / 4096)) : 1;
   std::vector<Acc> parts(nth);
   if (nth == 1) {
     finish_range(0, B, &parts[0]);
@@ -1157,7 +1212,7 @@ int phmm_fetch(phmm_ctx* ctx, double* out_log10, uint8_t* out_status, phmm_stats
       cut[i + 1] = b;
     }
     std::function<void(int)> task = [&](int i) { finish_range(cut[i], cut[i + 1], &parts[i]); };
-    ctx->pool->run(nth, task);
+    pool->run(nth, task);
   }
   trace.mark("finish");
   trace.print("fetch");
@@ -1214,8 +1269,118 @@ int phmm_fast_geometry(int m, int n, int* P, int* K, int* Q) {
   return PHMM_SUCCESS;
 }
 
+// phmm_score pipelines large calls: the batches are cut into kScoreChunks contiguous
+// chunks of ~equal pair count, each scored by its own chunk context (device buffers,
+// streams, pinned staging).  The host plans chunk c+1 while the GPU uploads and scores
+// chunk c, and finishes chunk c while later chunks run; chunk kernels on separate
+// streams also fill each other's tails.  Results are identical to the one-pass path
+// (pairs are independent; gid order is batch-major, so a chunk owns a gid range).
+static int score_chunked(phmm_ctx* ctx, const phmm_input* in, const phmm_options* opt, double* out_log10,
+                         uint8_t* out_status, phmm_stats* stats, int nchunks) {
+  const int64_t B = in->num_batches;
+  std::vector<int64_t> pairs(B + 1, 0);
+  for (int64_t b = 0; b < B; ++b)
+    pairs[b + 1] = pairs[b] + (in->batch_read_off[b + 1] - in->batch_read_off[b]) *
+                                  (in->batch_hap_off[b + 1] - in->batch_hap_off[b]);
+  const int64_t N = pairs[B];
+  std::vector<int64_t> cut(nchunks + 1, B);
+  cut[0] = 0;
+  for (int c = 1; c < nchunks; ++c) {
+    int64_t b = cut[c - 1];
+    while (b < B && pairs[b] < N * c / nchunks) ++b;
+    cut[c] = std::max(b, cut[c - 1]);
+  }
+  while ((int)ctx->chunks.size() < nchunks) {
+    phmm_ctx* c = new (std::nothrow) phmm_ctx();
+    if (!c) return ctx->fail(PHMM_ERR_NOMEM, "chunk context");
+    c->lut = ctx->lut;
+    c->parent = ctx;
+    ctx->chunks.push_back(c);
+    const int rc = init_ctx(c, ctx->device);
+    if (rc != PHMM_SUCCESS) return ctx->fail(rc, "chunk context: %s", c->err.c_str());
+    c->async = true;
+  }
+  // enqueue every chunk (prepare + execute + D2H), planning the next one meanwhile
+  for (int c = 0; c < nchunks; ++c) {
+    phmm_ctx* cx = ctx->chunks[c];
+    const int64_t b0 = cut[c], b1 = cut[c + 1];
+    if (b1 <= b0) continue;
+    const int64_t r0 = in->batch_read_off[b0], r1 = in->batch_read_off[b1];
+    const int64_t h0 = in->batch_hap_off[b0], h1 = in->batch_hap_off[b1];
+    const int64_t ro0 = in->read_off[r0], ho0 = in->hap_off[h0];
+    cx->c_roff.resize(r1 - r0 + 1);
+    for (int64_t r = r0; r <= r1; ++r) cx->c_roff[r - r0] = in->read_off[r] - ro0;
+    cx->c_hoff.resize(h1 - h0 + 1);
+    for (int64_t h = h0; h <= h1; ++h) cx->c_hoff[h - h0] = in->hap_off[h] - ho0;
+    cx->c_bro.resize(b1 - b0 + 1);
+    cx->c_bho.resize(b1 - b0 + 1);
+    for (int64_t b = b0; b <= b1; ++b) {
+      cx->c_bro[b - b0] = in->batch_read_off[b] - r0;
+      cx->c_bho[b - b0] = in->batch_hap_off[b] - h0;
+    }
+    phmm_input sub;
+    sub.read_bases = in->read_bases + ro0;
+    sub.base_qual = in->base_qual + ro0;
+    sub.ins_qual = in->ins_qual + ro0;
+    sub.del_qual = in->del_qual + ro0;
+    sub.gcp_qual = in->gcp_qual + ro0;
+    sub.read_off = cx->c_roff.data();
+    sub.num_reads = r1 - r0;
+    sub.hap_bases = in->hap_bases + ho0;
+    sub.hap_off = cx->c_hoff.data();
+    sub.num_haps = h1 - h0;
+    sub.batch_read_off = cx->c_bro.data();
+    sub.batch_hap_off = cx->c_bho.data();
+    sub.num_batches = b1 - b0;
+    int64_t n = 0;
+    int rc = phmm_prepare(cx, &sub, opt, &n);
+    if (rc == PHMM_SUCCESS) rc = phmm_execute(cx);
+    if (rc == PHMM_SUCCESS) rc = fetch_enqueue(cx);
+    if (rc != PHMM_SUCCESS) return ctx->fail(rc, "%s", cx->err.c_str());
+  }
+  // complete in order: device validation verdict, then finishing into the caller's slice
+  phmm_stats total;
+  memset(&total, 0, sizeof(total));
+  for (int c = 0; c < nchunks; ++c) {
+    phmm_ctx* cx = ctx->chunks[c];
+    if (cut[c + 1] <= cut[c]) continue;
+    int rc = check_validation(cx);
+    if (rc != PHMM_SUCCESS) return ctx->fail(rc, "%s", cx->err.c_str());
+    phmm_stats cs;
+    const int64_t g0 = pairs[cut[c]];
+    rc = fetch_complete(cx, out_log10 ? out_log10 + g0 : nullptr, out_status ? out_status + g0 : nullptr, &cs);
+    if (rc != PHMM_SUCCESS) return ctx->fail(rc, "%s", cx->err.c_str());
+    total.num_pairs += cs.num_pairs; total.total_cells += cs.total_cells;
+    total.computed_cells += cs.computed_cells; total.fast_pairs += cs.fast_pairs;
+    total.exact_pairs += cs.exact_pairs; total.f64_pairs += cs.f64_pairs;
+    total.flagged_pairs += cs.flagged_pairs; total.h2d_bytes += cs.h2d_bytes; total.d2h_bytes += cs.d2h_bytes;
+    total.kernel_launches += cs.kernel_launches; total.plan_ms += cs.plan_ms; total.d2h_ms += cs.d2h_ms;
+  }
+  if (stats) *stats = total;
+  return PHMM_SUCCESS;
+}
+
 int phmm_score(phmm_ctx* ctx, const phmm_input* in, const phmm_options* opt, double* out_log10,
                uint8_t* out_status, phmm_stats* stats) {
+  if (!ctx) return PHMM_ERR_INVALID;
+  if (in && opt && in->num_batches >= 2 * kScoreChunks && in->batch_read_off && in->batch_hap_off &&
+      in->read_off && in->hap_off && score_chunking_enabled()) {
+    // validate the structure first (the chunk views index the offset arrays)
+    int64_t pairs = 0;
+    bool ok = in->batch_read_off[0] == 0 && in->batch_hap_off[0] == 0 &&
+              in->batch_read_off[in->num_batches] == in->num_reads &&
+              in->batch_hap_off[in->num_batches] == in->num_haps && in->read_off[0] == 0 && in->hap_off[0] == 0;
+    for (int64_t b = 0; ok && b < in->num_batches; ++b) {
+      const int64_t nr = in->batch_read_off[b + 1] - in->batch_read_off[b];
+      const int64_t nh = in->batch_hap_off[b + 1] - in->batch_hap_off[b];
+      ok = nr > 0 && nh > 0;
+      pairs += nr * nh;
+    }
+    if (ok && pairs >= kScoreChunkMinPairs) {
+      CK(cudaSetDevice(ctx->device));
+      return score_chunked(ctx, in, opt, out_log10, out_status, stats, kScoreChunks);
+    }
+  }
   int64_t n = 0;
   int rc = phmm_prepare(ctx, in, opt, &n);
   if (rc != PHMM_SUCCESS) return rc;

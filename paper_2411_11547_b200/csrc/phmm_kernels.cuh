@@ -85,6 +85,7 @@ struct EngineDev {
   int* fx64_count;                        // [kNumExactP]
   int* band_inline;                       // guard-band pairs taken inline so far
   int band_budget;
+  const int* invalid;                     // device input validation verdict: nonzero = skip
   RetryLists r64;                         // FP64 retry units (built by the FP32 stream kernel)
   RetryLists rx32;                        // bit-exact FP32 guard-band units (same)
 };
@@ -128,6 +129,7 @@ __global__ void k_precompute(EngineDev E, int num_reads, const void* pf0, int64_
     prefetch_l2(E.rbases, read_bytes, tid, nth);
     prefetch_l2(E.bq, read_bytes, tid, nth);
   }
+  if (*E.invalid) return;
   const int lane = threadIdx.x & 31;
   const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (r >= num_reads) return;
@@ -417,6 +419,7 @@ k_fast(const EngineDev E, const FastUnit* __restrict__ units, int num_units, int
   constexpr int W = P * K, G = 32 / P, K4 = K / 4;
   static_assert(K % 4 == 0 && K >= 4, "K multiple of 4");
   constexpr unsigned FULL = 0xffffffffu;
+  if (*E.invalid) return;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double* s_lut = reinterpret_cast<double*>(smem_raw);
   float4* s_E = reinterpret_cast<float4*>(smem_raw + 96 * sizeof(double));
@@ -838,7 +841,7 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
   const int sw = lane / P, t = lane % P;
   const int slot = wib * G + sw;
   const int num_units = num_units_dev ? min(*num_units_dev, num_units_arg) : num_units_arg;
-  if (num_units == 0) return;
+  if (num_units == 0 || *E.invalid) return;
   for (int i = threadIdx.x; i < 94; i += blockDim.x) s_lut[i] = E.lut[i];
   __syncthreads();
   EV* Et = s_E + (size_t)(slot * 5 * KE) * P;
@@ -1398,7 +1401,7 @@ template <typename T>
 __global__ void __launch_bounds__(128)
 k_exact_all(const EngineDev E, int* __restrict__ counters, T* __restrict__ colbuf, int col_rows) {
   constexpr bool kIsF32 = sizeof(T) == 4;
-  if (post_lists_empty(kIsF32 ? E.ex32_count : E.ex64_count)) return;
+  if (*E.invalid || post_lists_empty(kIsF32 ? E.ex32_count : E.ex64_count)) return;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double* s_lut = reinterpret_cast<double*>(smem_raw);
   for (int i = threadIdx.x; i < 94; i += blockDim.x) s_lut[i] = E.lut[i];
@@ -1410,7 +1413,7 @@ k_exact_all(const EngineDev E, int* __restrict__ counters, T* __restrict__ colbu
 }
 __global__ void __launch_bounds__(128)
 k_fast64_all(const EngineDev E, int* __restrict__ counters, double* __restrict__ colbuf, int col_rows) {
-  if (post_lists_empty(E.fx64_count)) return;
+  if (*E.invalid || post_lists_empty(E.fx64_count)) return;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double* s_lut = reinterpret_cast<double*>(smem_raw);
   for (int i = threadIdx.x; i < 94; i += blockDim.x) s_lut[i] = E.lut[i];

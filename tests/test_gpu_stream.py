@@ -130,3 +130,37 @@ def test_partial_underflow_units_and_degenerate_reads(engine, rng):
                        ([180], [40, 60, 80, 590, 595, 600, 50, 70, 90, 100], "random")])
     k32 = _check(engine, flat)
     assert (k32 == 1).any() and (k32 == 0).any() and (k32 == 3).any()
+
+
+def test_chunked_score_matches_resident_path(engine):
+    """phmm_score pipelines large calls over chunk contexts; results must equal the
+    one-pass prepare/execute/fetch path bit for bit (FP32 + guard band + FP64 retry)."""
+    from paper_2411_11547_b200 import datagen
+    flat = datagen.workload("c3", num_batches=72)            # 36,864 pairs -> 4 chunks
+    assert flat.num_pairs >= 32768
+    for flags in (0, _native.FLAG_RETRY_F64, _native.FLAG_EXACT):
+        a, sa, st = engine.score(flat, F32, flags)
+        engine.prepare(flat, F32, flags)
+        engine.execute()
+        b, sb, _ = engine.fetch()
+        assert np.array_equal(a, b, equal_nan=True) and np.array_equal(sa, sb)
+        assert st.num_pairs == flat.num_pairs
+
+
+def test_chunked_score_rejects_invalid_chunk_and_recovers(engine):
+    from paper_2411_11547_b200 import datagen
+    from paper_2411_11547_b200.errors import DataError
+    flat = datagen.workload("c3", num_batches=72)
+    bad = FlatBatches(**{f: np.array(getattr(flat, f), copy=True) for f in FlatBatches.FIELDS})
+    bad.hap_bases[-3] = 9                                     # last chunk: invalid base code
+    with pytest.raises(DataError):
+        engine.score(bad, F32, 0)
+    bad = FlatBatches(**{f: np.array(getattr(flat, f), copy=True) for f in FlatBatches.FIELDS})
+    bad.bq[5] = 200                                           # first chunk: invalid quality
+    with pytest.raises(DataError):
+        engine.score(bad, F32, 0)
+    a, sa, _ = engine.score(flat, F32, 0)                     # the context is still healthy
+    engine.prepare(flat, F32, 0)
+    engine.execute()
+    b, sb, _ = engine.fetch()
+    assert np.array_equal(a, b, equal_nan=True) and np.array_equal(sa, sb)
