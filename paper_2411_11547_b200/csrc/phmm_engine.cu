@@ -235,7 +235,15 @@ int choose_stream_geom(int mode, int m, int64_t total, int nmax) {
   return bi;
 }
 
-constexpr int kScoreChunks = 4;               // phmm_score pipelining depth
+constexpr int kMaxScoreChunks = 8;
+int score_chunks() {                          // phmm_score pipelining depth (PHMM_CHUNKS)
+  static int v = -1;
+  if (v < 0) {
+    const char* env = getenv("PHMM_CHUNKS");
+    v = env ? std::max(1, std::min(kMaxScoreChunks, atoi(env))) : 4;
+  }
+  return v;
+}
 constexpr int64_t kScoreChunkMinPairs = 32768;
 bool score_chunking_enabled() {
   static int v = -1;
@@ -377,6 +385,7 @@ struct phmm_ctx {
   int* h_vflag = nullptr;    // pinned: device validation flag
   bool async = false;        // chunk contexts of phmm_score: no host syncs in prepare/execute
   phmm_ctx* parent = nullptr;
+  int budget_div = 1;        // chunk contexts: number of chunks sharing the band budget
   std::vector<phmm_ctx*> chunks;             // chunk contexts (phmm_score pipelining), lazy
   std::vector<int64_t> c_roff, c_hoff, c_bro, c_bho;   // chunk views: rebased offsets
   double* h_acc = nullptr;   // pinned result staging (phmm_fetch)
@@ -946,7 +955,9 @@ static int prepare_impl(phmm_ctx* ctx, const phmm_input* in, const phmm_options*
   E.list_cap = ctx->list_cap;
   E.retry_f64 = (opt->flags & PHMM_FLAG_RETRY_F64) ? 1 : 0;
   E.band_inline = ctx->d_counters.p + 16;
-  E.band_budget = 2 * ctx->num_sms;
+  // inline guard-band reruns are slow per pair (scalar exact recursion inside an FP32
+  // warp): a budget per call, split between the chunk contexts of a pipelined call
+  E.band_budget = 2 * ctx->num_sms / std::max(1, ctx->budget_div);
   // tilings that cannot get work (no streamed read of that width) stay null
   auto lists = [&](RetryLists& L, DBuf<StreamUnit>* u, int ng, DBuf<StreamHap>& h, unsigned geoms, int base) {
     for (int g = 0; g < 8; ++g) L.units[g] = (g < ng && (geoms & (1u << g))) ? u[g].p : nullptr;
@@ -1333,6 +1344,7 @@ static int score_chunked(phmm_ctx* ctx, const phmm_input* in, const phmm_options
     sub.batch_hap_off = cx->c_bho.data();
     sub.num_batches = b1 - b0;
     int64_t n = 0;
+    cx->budget_div = nchunks;
     int rc = phmm_prepare(cx, &sub, opt, &n);
     if (rc == PHMM_SUCCESS) rc = phmm_execute(cx);
     if (rc == PHMM_SUCCESS) rc = fetch_enqueue(cx);
@@ -1363,7 +1375,7 @@ static int score_chunked(phmm_ctx* ctx, const phmm_input* in, const phmm_options
 int phmm_score(phmm_ctx* ctx, const phmm_input* in, const phmm_options* opt, double* out_log10,
                uint8_t* out_status, phmm_stats* stats) {
   if (!ctx) return PHMM_ERR_INVALID;
-  if (in && opt && in->num_batches >= 2 * kScoreChunks && in->batch_read_off && in->batch_hap_off &&
+  if (in && opt && in->num_batches >= 2 * score_chunks() && score_chunks() > 1 && in->batch_read_off && in->batch_hap_off &&
       in->read_off && in->hap_off && score_chunking_enabled()) {
     // validate the structure first (the chunk views index the offset arrays)
     int64_t pairs = 0;
@@ -1376,9 +1388,23 @@ int phmm_score(phmm_ctx* ctx, const phmm_input* in, const phmm_options* opt, dou
       ok = nr > 0 && nh > 0;
       pairs += nr * nh;
     }
+    // Only regular calls are pipelined: reads spanning many tiling widths split into many
+    // small per-tiling kernels per chunk, and each chunk's latency-bound post-pass (guard
+    // band, FP64 retries) then queues behind the next chunks' persistent grids.
+    if (ok && pairs >= kScoreChunkMinPairs) {
+      static const int kW[] = {16, 32, 48, 64, 80, 96, 112, 128, 160, 192, 224, 256, 320, 384, 448, 512};
+      unsigned classes = 0;
+      for (int64_t r = 0; r < in->num_reads; ++r) {
+        const int64_t m = in->read_off[r + 1] - in->read_off[r];
+        int c = 0;
+        while (c < 15 && kW[c] < m + 1) ++c;
+        classes |= 1u << c;
+      }
+      ok = __builtin_popcount(classes) <= 2;
+    }
     if (ok && pairs >= kScoreChunkMinPairs) {
       CK(cudaSetDevice(ctx->device));
-      return score_chunked(ctx, in, opt, out_log10, out_status, stats, kScoreChunks);
+      return score_chunked(ctx, in, opt, out_log10, out_status, stats, score_chunks());
     }
   }
   int64_t n = 0;

@@ -19,6 +19,7 @@ REL_TOL = 1e-4
 RETRY_REL_TOL = 1e-9
 F32 = config_tuples(default_configs("f32"))
 KIND = _native.ST_KIND_MASK
+SEED_CHUNK = 20240811 + 17
 
 
 def _flat(rng, batches):
@@ -136,9 +137,14 @@ def test_chunked_score_matches_resident_path(engine):
     """phmm_score pipelines large calls over chunk contexts; results must equal the
     one-pass prepare/execute/fetch path bit for bit (FP32 + guard band + FP64 retry)."""
     from paper_2411_11547_b200 import datagen
-    flat = datagen.workload("c3", num_batches=72)            # 36,864 pairs -> 4 chunks
-    assert flat.num_pairs >= 32768
-    for flags in (0, _native.FLAG_RETRY_F64, _native.FLAG_EXACT):
+    # regular calls (one read length, one haplotype length) are the pipelined ones
+    derived = datagen.workload("c2", num_batches=520)          # 33,280 pairs -> 4 chunks
+    indep = datagen.generate_synthetic_flat(num_batches=520, reads_per_batch=16, haps_per_batch=4,
+                                            read_len_spec=120, hap_len_spec=200, seed=SEED_CHUNK,
+                                            mode="independent")     # every pair underflows FP32
+    for flat, flags in ((derived, 0), (derived, _native.FLAG_EXACT), (indep, 0),
+                        (indep, _native.FLAG_RETRY_F64)):
+        assert flat.num_pairs >= 32768
         a, sa, st = engine.score(flat, F32, flags)
         engine.prepare(flat, F32, flags)
         engine.execute()
@@ -150,7 +156,7 @@ def test_chunked_score_matches_resident_path(engine):
 def test_chunked_score_rejects_invalid_chunk_and_recovers(engine):
     from paper_2411_11547_b200 import datagen
     from paper_2411_11547_b200.errors import DataError
-    flat = datagen.workload("c3", num_batches=72)
+    flat = datagen.workload("c2", num_batches=520)
     bad = FlatBatches(**{f: np.array(getattr(flat, f), copy=True) for f in FlatBatches.FIELDS})
     bad.hap_bases[-3] = 9                                     # last chunk: invalid base code
     with pytest.raises(DataError):
