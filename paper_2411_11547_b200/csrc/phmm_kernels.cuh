@@ -113,21 +113,34 @@ __device__ __forceinline__ void prefetch_l2(const void* base, int64_t bytes, int
   for (int64_t off = tid * 128; off < bytes; off += nth * 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(p + off));
 }
 
-__global__ void k_precompute(EngineDev E, int num_reads, const void* pf0, int64_t pf0_bytes, const void* pf1,
-                             int64_t pf1_bytes, int64_t hap_bytes, int64_t read_bytes) {
+// Pulls the inputs the stream kernels read once per unit (work units, haplotype lists
+// and bases, read bases and base qualities) into L2; runs beside k_precompute.
+__global__ void k_l2_prefetch(const void* pf0, int64_t pf0_bytes, const void* pf1, int64_t pf1_bytes,
+                              const void* pf2, int64_t pf2_bytes, const void* pf3, const void* pf4,
+                              int64_t read_bytes) {
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+  prefetch_l2(pf0, pf0_bytes, tid, nth);
+  prefetch_l2(pf1, pf1_bytes, tid, nth);
+  prefetch_l2(pf2, pf2_bytes, tid, nth);
+  prefetch_l2(pf3, read_bytes, tid, nth);
+  prefetch_l2(pf4, read_bytes, tid, nth);
+}
+
+__global__ void k_precompute(EngineDev E, int num_reads, int* counters, int ncounters, int4 host32, int4 host64,
+                             int64_t num_pairs) {
   // One warp per read.  With X_i = max(B_M(i), B_I(i)) and g_i = min(n, 1/(1-eps_i)):
   //   B_D(i) <= g_i X_{i+1},  X_i <= (1 + zeta_i g_i) X_{i+1},  X_m = 1
   // so  sum_i (B_M + B_I + B_D) <= prod_{i<m}(1 + zeta_i g_i) * (2 + sum_{i<m}(2 + g_i)).
-  // The grid also pulls the inputs the fast kernels read once per unit (work units,
-  // haplotype lists and bases, read bases and base qualities) into L2.
+  // The grid also resets the work counters (host-built list sizes first) and the status.
   {
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t nth = (int64_t)gridDim.x * blockDim.x;
-    prefetch_l2(pf0, pf0_bytes, tid, nth);
-    prefetch_l2(pf1, pf1_bytes, tid, nth);
-    prefetch_l2(E.hbases, hap_bytes, tid, nth);
-    prefetch_l2(E.rbases, read_bytes, tid, nth);
-    prefetch_l2(E.bq, read_bytes, tid, nth);
+    const int hv[8] = {host32.x, host32.y, host32.z, host32.w, host64.x, host64.y, host64.z, host64.w};
+    for (int64_t i = tid; i < ncounters; i += nth) counters[i] = i < 8 ? hv[i] : 0;
+    uint4* st4 = reinterpret_cast<uint4*>(E.status);
+    for (int64_t i = tid; i < num_pairs / 16; i += nth) st4[i] = make_uint4(0, 0, 0, 0);
+    for (int64_t i = (num_pairs / 16) * 16 + tid; i < num_pairs; i += nth) E.status[i] = 0;
   }
   if (*E.invalid) return;
   const int lane = threadIdx.x & 31;
