@@ -407,6 +407,7 @@ struct phmm_ctx {
     int64_t dev_off = 0;                    // first unit in h_sunits / d_sunits
   };
   std::vector<SBin> sbins;
+  std::vector<int> sbin_order;
   std::vector<StreamUnit> su_all;           // planning scratch (persistent capacity)
   std::vector<uint8_t> su_bin;
   std::vector<int> su_cnt;
@@ -855,6 +856,21 @@ static int prepare_impl(phmm_ctx* ctx, const phmm_input* in, const phmm_options*
     ctx->sbins[bi].count = (bi + 1 < nsbins ? ctx->su_cnt[bbase[bi + 1]] : nsunits) - ctx->sbins[bi].dev_off;
   ctx->h_sunits.resize(nsunits);
   for (int64_t i = 0; i < nsunits; ++i) ctx->h_sunits[ctx->su_cnt[key(i)]++] = ctx->su_all[i];
+  // launch order of the concurrent tiling bins: largest total work first, so the small
+  // bins fill the tails of the large ones
+  {
+    std::vector<double> work(nsbins, 0.0);
+    for (int bi = 0; bi < nsbins; ++bi) {
+      const StreamKernel& g = kStreamTab[ctx->sbins[bi].mode][ctx->sbins[bi].geom];
+      for (int64_t i = ctx->sbins[bi].dev_off; i < ctx->sbins[bi].dev_off + ctx->sbins[bi].count; ++i) {
+        const StreamUnit& u = ctx->h_sunits[i];
+        work[bi] += (double)g.P * (g.K + 2.5) * (std::max(u.rowsA, u.rowsB) + g.P - 1) / g.P * g.P;
+      }
+    }
+    ctx->sbin_order.resize(nsbins);
+    std::iota(ctx->sbin_order.begin(), ctx->sbin_order.end(), 0);
+    std::stable_sort(ctx->sbin_order.begin(), ctx->sbin_order.end(), [&](int a, int b) { return work[a] > work[b]; });
+  }
   trace.mark("units");
   auto t1 = std::chrono::steady_clock::now();
   ctx->plan_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
@@ -1053,7 +1069,8 @@ int phmm_execute(phmm_ctx* ctx) {
 #undef CKE
   CK(fork());
   used[phmm_ctx::kAux - 1] = true;                 // joins the L2 prefetch as well
-  for (int bi = 0; bi < nsb; ++bi) {
+  for (int oi = 0; oi < nsb; ++oi) {
+    const int bi = ctx->sbin_order[oi];             // costliest tiling first
     const auto& sb = ctx->sbins[bi];
     const int nu = (int)sb.count;
     if (nu == 0) continue;
