@@ -417,7 +417,7 @@ struct phmm_ctx {
   int host_ex32[kNumExactP] = {0, 0, 0, 0}, host_ex64[kNumExactP] = {0, 0, 0, 0};
   int max_n = 1;
   int flags = 0;
-  int list_cap = 0;
+  int list_cap[kNumExactP] = {0, 0, 0, 0};
   int64_t h2d_bytes = 0;
   int64_t hap_bytes = 0, read_bytes = 0;
   double plan_ms = 0.0, h2d_ms = 0.0;
@@ -677,6 +677,8 @@ static int prepare_impl(phmm_ctx* ctx, const phmm_input* in, const phmm_options*
   int sbin_index[4 * kMaxTilings];
   std::fill(sbin_index, sbin_index + 4 * kMaxTilings, -1);
   std::vector<ExactItem> host32[kNumExactP], host64[kNumExactP];
+  int64_t slot_pairs[kNumExactP] = {0, 0, 0, 0};
+  int64_t r64_pairs[8] = {0}, rx32_pairs[8] = {0};
   int max_n = 1;
   int64_t gid = 0;
   std::vector<int> hidx;
@@ -733,6 +735,7 @@ static int prepare_impl(phmm_ctx* ctx, const phmm_input* in, const phmm_options*
       const bool f64 = opt->precision[cfg] == 1;
       const bool exact = f64 || exact_mode || scale > 126;
       const int mode = f64 ? kExact64 : exact ? kExact32 : kFast32;
+      slot_pairs[exact_slot_host(m)] += nh;             // any pair may land in its slot's lists
       if (use_stream) {
         ModePlan& M = mp[mode];
         if (m != M.tmpl_m) {                           // lane template per (batch, tiling)
@@ -778,8 +781,8 @@ static int prepare_impl(phmm_ctx* ctx, const phmm_input* in, const phmm_options*
           const uint8_t sbi = (uint8_t)sbin_index[key];
           if (mode == kFast32) {                       // tilings its device-built units can use
             const int g64 = r64_geom_for(m), gx = rx32_geom_for(m);
-            if (g64 >= 0) ctx->r64_geoms |= 1u << g64;
-            if (gx >= 0) ctx->rx32_geoms |= 1u << gx;
+            if (g64 >= 0) { ctx->r64_geoms |= 1u << g64; r64_pairs[g64] += nh; }
+            if (gx >= 0) { ctx->rx32_geoms |= 1u << gx; rx32_pairs[gx] += nh; }
           }
           for (const LaneTemplate& t : tmpl) {
             StreamUnit su;
@@ -894,13 +897,13 @@ static int prepare_impl(phmm_ctx* ctx, const phmm_input* in, const phmm_options*
   CK(ctx->d_acc.ensure(N));
   CK(ctx->d_status.ensure(N));
   CK(ctx->d_counters.ensure(kBinCounters + ctx->bins.size() + ctx->sbins.size()));
-  ctx->list_cap = (int)std::max<int64_t>(N, 1);
   for (int s = 0; s < kNumExactP; ++s) {
+    ctx->list_cap[s] = (int)std::max<int64_t>(slot_pairs[s], 1);
     ctx->host_ex32[s] = (int)host32[s].size();
     ctx->host_ex64[s] = (int)host64[s].size();
-    CK(ctx->d_ex32[s].ensure(ctx->list_cap));
-    CK(ctx->d_ex64[s].ensure(ctx->list_cap));
-    CK(ctx->d_fx64[s].ensure(ctx->list_cap));
+    CK(ctx->d_ex32[s].ensure(ctx->list_cap[s]));
+    CK(ctx->d_ex64[s].ensure(ctx->list_cap[s]));
+    CK(ctx->d_fx64[s].ensure(ctx->list_cap[s]));
     if (!host32[s].empty()) CK(up(ctx->d_ex32[s], host32[s].data(), host32[s].size()));
     if (!host64[s].empty()) CK(up(ctx->d_ex64[s], host64[s].data(), host64[s].size()));
   }
@@ -950,9 +953,9 @@ static int prepare_impl(phmm_ctx* ctx, const phmm_input* in, const phmm_options*
   if (!r64) ctx->r64_geoms = 0;
   if (!rx32) ctx->rx32_geoms = 0;
   for (int g = 0; g < kNumR64Geoms; ++g)
-    if (ctx->r64_geoms & (1u << g)) CK(ctx->d_r64u[g].ensure(streamed));
+    if (ctx->r64_geoms & (1u << g)) CK(ctx->d_r64u[g].ensure(r64_pairs[g]));
   for (int g = 0; g < kNumRX32Geoms; ++g)
-    if (ctx->rx32_geoms & (1u << g)) CK(ctx->d_rx32u[g].ensure(streamed));
+    if (ctx->rx32_geoms & (1u << g)) CK(ctx->d_rx32u[g].ensure(rx32_pairs[g]));
   if (r64) CK(ctx->d_r64h.ensure(streamed));
   if (rx32) CK(ctx->d_rx32h.ensure(streamed));
   EngineDev& E = ctx->dev;
@@ -968,25 +971,26 @@ static int prepare_impl(phmm_ctx* ctx, const phmm_input* in, const phmm_options*
   E.fx64_count = ctx->d_counters.p + 20;
   E.ex32_count = ctx->d_counters.p + 0;
   E.ex64_count = ctx->d_counters.p + kNumExactP;
-  E.list_cap = ctx->list_cap;
+  for (int s = 0; s < kNumExactP; ++s) E.list_cap[s] = ctx->list_cap[s];
   E.retry_f64 = (opt->flags & PHMM_FLAG_RETRY_F64) ? 1 : 0;
   E.band_inline = ctx->d_counters.p + 16;
   // inline guard-band reruns are slow per pair (scalar exact recursion inside an FP32
   // warp): a budget per call, split between the chunk contexts of a pipelined call
   E.band_budget = 2 * ctx->num_sms / std::max(1, ctx->budget_div);
   // tilings that cannot get work (no streamed read of that width) stay null
-  auto lists = [&](RetryLists& L, DBuf<StreamUnit>* u, int ng, DBuf<StreamHap>& h, unsigned geoms, int base) {
+  auto lists = [&](RetryLists& L, DBuf<StreamUnit>* u, int ng, DBuf<StreamHap>& h, unsigned geoms, int base,
+                   const int64_t* gpairs) {
     for (int g = 0; g < 8; ++g) L.units[g] = (g < ng && (geoms & (1u << g))) ? u[g].p : nullptr;
     L.enabled = geoms ? 1 : 0;
     L.haps = geoms ? h.p : nullptr;
     L.count = ctx->d_counters.p + base;
     L.hap_count = ctx->d_counters.p + base + 8;
     L.overflow = ctx->d_counters.p + base + 9;
-    L.unit_cap = geoms ? (int)streamed : 0;
+    for (int g = 0; g < 8; ++g) L.unit_cap[g] = (g < ng && (geoms & (1u << g))) ? (int)gpairs[g] : 0;
     L.hap_cap = geoms ? (int)streamed : 0;
   };
-  lists(E.r64, ctx->d_r64u, kNumR64Geoms, ctx->d_r64h, ctx->r64_geoms, kCtrR64);
-  lists(E.rx32, ctx->d_rx32u, kNumRX32Geoms, ctx->d_rx32h, ctx->rx32_geoms, kCtrRX32);
+  lists(E.r64, ctx->d_r64u, kNumR64Geoms, ctx->d_r64h, ctx->r64_geoms, kCtrR64, r64_pairs);
+  lists(E.rx32, ctx->d_rx32u, kNumRX32Geoms, ctx->d_rx32h, ctx->rx32_geoms, kCtrRX32, rx32_pairs);
 
   trace.mark("sync");
   trace.print("prepare");
@@ -1108,7 +1112,7 @@ int phmm_execute(phmm_ctx* ctx) {
   auto post = [&](const StreamKernel& SKn, const RetryLists& L, int g, int* work) {
     const int a = 1 + (nside++ % (phmm_ctx::kAux - 1));
     used[a] = true;
-    SKn.launch(dim3(ctx->num_sms * SKn.occ), SKn.smem, ctx->aux[a], E, L.units[g], L.haps, L.unit_cap, L.count + g,
+    SKn.launch(dim3(ctx->num_sms * SKn.occ), SKn.smem, ctx->aux[a], E, L.units[g], L.haps, L.unit_cap[g], L.count + g,
                work);
     ++launches;
   };

@@ -57,7 +57,8 @@ struct RetryLists {
   StreamHap* haps;
   int* hap_count;
   int* overflow;
-  int unit_cap, hap_cap;
+  int unit_cap[8];                        // per tiling: pairs that can land there
+  int hap_cap;
   int enabled;
 };
 
@@ -79,7 +80,7 @@ struct EngineDev {
   int* ex32_count;                        // [kNumExactP]
   ExactItem* ex64[kNumExactP];            // f64 work lists
   int* ex64_count;                        // [kNumExactP]
-  int list_cap;
+  int list_cap[kNumExactP];              // per slot: pairs whose read maps to the slot
   int retry_f64;
   ExactItem* fx64[kNumExactP];            // FP64 retry lists (fast FP64 kernel)
   int* fx64_count;                        // [kNumExactP]
@@ -95,10 +96,10 @@ __device__ __forceinline__ int exact_slot_for(int m) {
   return (m + 1 <= 32) ? 0 : (m + 1 <= 64) ? 1 : (m + 1 <= 128) ? 2 : 3;
 }
 
-__device__ __forceinline__ void append_item(ExactItem* const* lists, int* counts, int cap,
+__device__ __forceinline__ void append_item(ExactItem* const* lists, int* counts, const int* caps,
                                             int slot, ExactItem it) {
   int pos = atomicAdd(&counts[slot], 1);
-  if (pos < cap) lists[slot][pos] = it;
+  if (pos < caps[slot]) lists[slot][pos] = it;
 }
 
 // ---------------------------------------------------------------------------------
@@ -806,7 +807,7 @@ __device__ __forceinline__ void emit_retry_units(const StreamUnit& U, const Stre
     if (tot == 0) return;
     const int ui = atomicAdd(&L.count[g], 1);
     const int hi = atomicAdd(L.hap_count, tot);
-    if (ui < L.unit_cap && hi + tot <= L.hap_cap) {
+    if (ui < L.unit_cap[g] && hi + tot <= L.hap_cap) {
       for (int x = 0; x < lanes_n[0]; ++x) L.haps[hi + x] = buf[0][x];
       for (int x = 0; x < lanes_n[1]; ++x) L.haps[hi + lanes_n[0] + x] = buf[1][x];
       L.units[g][ui] = StreamUnit{U.read, hi, lanes_n[0], lanes_n[1], rows_n[0], rows_n[1], U.ro, m};
@@ -1249,7 +1250,7 @@ fast64_list(const EngineDev& E, int slot, int* __restrict__ counter, double* __r
   double* s_E = reinterpret_cast<double*>(smem_raw + 96 * sizeof(double));
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int sw = lane / P, t = lane % P;
-  const int count = min(E.fx64_count[slot], E.list_cap);
+  const int count = min(E.fx64_count[slot], E.list_cap[slot]);
   if (count == 0) return;
   double* Et = s_E + (size_t)((wib * G + sw) * 5 * K) * P;   // Et[(c*K + k)*P + t]
   const int gwarp = blockIdx.x * (blockDim.x >> 5) + wib;
@@ -1386,7 +1387,7 @@ exact_list(const EngineDev& E, int slot, int* __restrict__ counter, T* __restric
   T* s_E = reinterpret_cast<T*>(smem_raw + 96 * sizeof(double));
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int sw = lane / P, t = lane % P;
-  const int count = min(kIsF32 ? E.ex32_count[slot] : E.ex64_count[slot], E.list_cap);
+  const int count = min(kIsF32 ? E.ex32_count[slot] : E.ex64_count[slot], E.list_cap[slot]);
   if (count == 0) return;
   T* Et = s_E + (size_t)((wib * G + sw) * 5 * K) * P;   // Et[(c*K + k)*P + t]
   const int gwarp = blockIdx.x * (blockDim.x >> 5) + wib;
