@@ -74,7 +74,8 @@ constexpr int kThreads = 128;
 // device-built stream lists (counts[8], hap count, overflow) and their work counters,
 // the validation flag (last slot), then one work counter per planned stream/legacy bin
 constexpr int kCtrR64 = 32, kCtrRX32 = 44, kCtrR64Work = 56, kCtrRX32Work = 64;
-constexpr int kBinCounters = 96;          // fixed counter slots before the per-bin counters
+constexpr int kBinCounters = 96;
+constexpr int64_t kBigCallPairs = 1 << 20;   // device-built retry units grow above this          // fixed counter slots before the per-bin counters
 constexpr int kFinishThreads = 16;        // host threads finishing log10 in phmm_fetch
 
 struct Bin {
@@ -988,6 +989,10 @@ static int prepare_impl(phmm_ctx* ctx, const phmm_input* in, const phmm_options*
     L.overflow = ctx->d_counters.p + base + 9;
     for (int g = 0; g < 8; ++g) L.unit_cap[g] = (g < ng && (geoms & (1u << g))) ? (int)gpairs[g] : 0;
     L.hap_cap = geoms ? (int)streamed : 0;
+    // short units keep small post-pass lists parallel (their size is unknown when the
+    // grid is sized); large calls get longer units (less fill/drain and setup per pair)
+    const bool big = streamed >= kBigCallPairs;
+    L.lane_haps = &L == &E.r64 ? (big ? 4 : kRetryLaneHaps64) : (big ? 3 : kRetryLaneHapsX32);
   };
   lists(E.r64, ctx->d_r64u, kNumR64Geoms, ctx->d_r64h, ctx->r64_geoms, kCtrR64, r64_pairs);
   lists(E.rx32, ctx->d_rx32u, kNumRX32Geoms, ctx->d_rx32h, ctx->rx32_geoms, kCtrRX32, rx32_pairs);

@@ -60,6 +60,7 @@ struct RetryLists {
   int unit_cap[8];                        // per tiling: pairs that can land there
   int hap_cap;
   int enabled;
+  int lane_haps;                          // haplotypes per lane of a built unit
 };
 
 struct EngineDev {
@@ -704,7 +705,7 @@ constexpr int kNumR64Geoms = 6;     // FP64 retry:  (8,4) (16,4) (16,6) (16,8) (
 constexpr int kNumRX32Geoms = 8;    // exact FP32:  (8,4) (16,4) (16,6) (32,4) (32,6) (32,8) (32,12) (32,16)
 // haplotypes per lane of a device-built unit: short units keep these small post-pass
 // lists parallel (their count is unknown when the grid is sized)
-constexpr int kRetryLaneHaps64 = 2, kRetryLaneHapsX32 = 1;
+constexpr int kRetryLaneHaps64 = 2, kRetryLaneHapsX32 = 1;   // defaults (RetryLists.lane_haps)
 constexpr int kInlineBand = 4;      // guard-band pairs a warp may rerun inline per unit
 __host__ __device__ __forceinline__ int r64_geom_for(int m) {
   const int w = m + 1;
@@ -1211,12 +1212,12 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
         if (s_flag[2 * slot] | s_flag[2 * slot + 1]) {
           const int g64 = r64_geom_for(m);
           emit_retry_units(U, shaps, s_flag + 2 * slot, E.r64, g64, stream_cap_of(r64_geom_P(g64)), m,
-                           kRetryLaneHaps64);
+                           E.r64.lane_haps);
         }
         if (s_band[2 * slot] | s_band[2 * slot + 1]) {
           const int gx = rx32_geom_for(m);
           emit_retry_units(U, shaps, s_band + 2 * slot, E.rx32, gx, stream_cap_of(rx32_geom_P(gx)), m,
-                           kRetryLaneHapsX32);
+                           E.rx32.lane_haps);
         }
       }
       // inline guard-band reruns (same tiling; the emission-table slot is free again)
