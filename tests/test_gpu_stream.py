@@ -170,3 +170,49 @@ def test_chunked_score_rejects_invalid_chunk_and_recovers(engine):
     engine.execute()
     b, sb, _ = engine.fetch()
     assert np.array_equal(a, b, equal_nan=True) and np.array_equal(sa, sb)
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3, 4])
+def test_random_batches_all_modes_against_oracle(engine, seed):
+    """Random batch shapes: 1-12 reads x 1-24 haplotypes, read lengths 1-520 (every
+    tiling and the striped legacy path), haplotype lengths 1-700, qualities over the full
+    0..93 range (incl. gcp 0 and degenerate indels), N bases.  Fast FP32 / retry /
+    exact / f64-config results against the oracle."""
+    rng = np.random.default_rng(1000 + seed)
+    rb, bq, iq, dq, gq, hb, rlen, hlen, bro, bho = [], [], [], [], [], [], [], [], [0], [0]
+    for _ in range(int(rng.integers(4, 9))):
+        nr, nh = int(rng.integers(1, 13)), int(rng.integers(1, 25))
+        hl = [int(x) for x in rng.integers(1, 701, size=nh)]
+        base = rng.integers(0, 5, size=max(hl) + 600, dtype=np.int8)
+        for n in hl:
+            h = base[:n].copy()
+            hit = rng.random(n) < 0.02
+            h[hit] = rng.integers(0, 5, size=int(hit.sum()))
+            hb.append(h); hlen.append(n)
+        for _ in range(nr):
+            m = int(rng.integers(1, 521)) if rng.random() < 0.8 else int(rng.integers(1, 40))
+            st = int(rng.integers(0, 300))
+            r = base[st:st + m].copy() if rng.random() < 0.7 else rng.integers(0, 5, size=m, dtype=np.int8)
+            if r.shape[0] < m:
+                r = np.concatenate([r, rng.integers(0, 5, size=m - r.shape[0], dtype=np.int8)])
+            rb.append(r); rlen.append(m)
+            bq.append(rng.integers(0, 94, size=m).astype(np.uint8))
+            low = rng.random() < 0.1
+            iq.append(rng.integers(1 if low else 20, 94, size=m).astype(np.uint8))
+            dq.append(rng.integers(1 if low else 20, 94, size=m).astype(np.uint8))
+            g = np.full(m, int(rng.choice([10, 10, 10, 3, 0, 40])), np.uint8)
+            gq.append(g)
+        bro.append(bro[-1] + nr); bho.append(bho[-1] + nh)
+    cat = np.concatenate
+    flat = FlatBatches(read_bases=cat(rb), bq=cat(bq), iq=cat(iq), dq=cat(dq), gq=cat(gq),
+                       read_off=np.concatenate([[0], np.cumsum(rlen)]).astype(np.int64),
+                       hap_bases=cat(hb), hap_off=np.concatenate([[0], np.cumsum(hlen)]).astype(np.int64),
+                       batch_read_off=np.asarray(bro, np.int64), batch_hap_off=np.asarray(bho, np.int64))
+    _check(engine, flat)
+    ofl = oracle.Flat(**flat.as_dict())
+    ref32, k32 = oracle.score(ofl, "f32")
+    s, st, _ = engine.score(flat, F32, _native.FLAG_EXACT)         # exact mode: bit-identical
+    assert np.array_equal(st & KIND, k32) and np.array_equal(s, ref32, equal_nan=True)
+    ref64, k64 = oracle.score(ofl, "f64")
+    s, st, _ = engine.score(flat, config_tuples(default_configs("f64")), 0)
+    assert np.array_equal(st & KIND, k64) and np.array_equal(s, ref64, equal_nan=True)
