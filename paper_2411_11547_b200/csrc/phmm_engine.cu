@@ -1433,7 +1433,8 @@ int phmm_score(phmm_ctx* ctx, const phmm_input* in, const phmm_options* opt, dou
         while (c < 15 && kW[c] < m + 1) ++c;
         classes |= 1u << c;
       }
-      ok = __builtin_popcount(classes) <= 2;
+      // large calls amortize the per-chunk post-pass latency: pipeline them regardless
+      ok = __builtin_popcount(classes) <= 2 || pairs >= kBigCallPairs;
     }
     if (ok && pairs >= kScoreChunkMinPairs) {
       CK(cudaSetDevice(ctx->device));
