@@ -18,6 +18,9 @@ Extra keyword-only options:
              get finite scores and are listed in report.retried instead of errors.
   exact      run every FP32 pair on the bit-exact kernel (no fast path).
   device     CUDA device ordinal.
+  devices    list of CUDA devices: the batches are sharded across them by cost with one
+             host thread (and one context) per device and gathered in global-id order
+             (shards.py; north_star multi-GPU path, no collective).
 """
 from __future__ import annotations
 
@@ -79,7 +82,7 @@ def errors_from_status(status: np.ndarray) -> list:
 
 
 def run(batches, configs=None, budget_bytes: int = DEFAULT_BUDGET_BYTES, workers: int = 1, *,
-        retry_f64: bool = False, exact: bool = False, device: int = 0):
+        retry_f64: bool = False, exact: bool = False, device: int = 0, devices=None):
     """Score every work item of ``batches`` on the GPU; see the module docstring."""
     if workers < 1:
         raise ValueError("workers must be >= 1")
@@ -89,8 +92,13 @@ def run(batches, configs=None, budget_bytes: int = DEFAULT_BUDGET_BYTES, workers
     check_budget(flat, configs, budget_bytes)
     n = flat.num_pairs
     t0 = time.perf_counter()
-    if n:
-        scores, status, stats = score_flat(flat, configs, retry_f64, exact, device)
+    if n and devices is not None and len(devices) > 1:
+        from .shards import score_sharded
+        scores, status, engine = score_sharded(flat, config_tuples(configs), engine_flags(retry_f64, exact),
+                                               devices)
+    elif n:
+        dev = devices[0] if devices else device
+        scores, status, stats = score_flat(flat, configs, retry_f64, exact, dev)
         engine = stats.as_dict()
     else:
         scores, status, engine = np.zeros(0), np.zeros(0, np.uint8), {}
