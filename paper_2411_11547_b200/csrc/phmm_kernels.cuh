@@ -343,6 +343,14 @@ __device__ __forceinline__ void exact_item(const EngineDev& E, const ExactItem& 
       else if (sact) { nbM = colPrev[0]; nbI = colPrev[col_rows]; nbD = colPrev[2 * col_rows]; }
     }
     __syncwarp();
+    // one-row-ahead prefetch of thread 0's boundary column and of every thread's
+    // haplotype character: global loads stay off the per-step dependency chain
+    T pfM = zero, pfI = zero, pfD = zero;
+    if (t == 0 && q > 0 && sact) {
+      const int jj = min(1, n);
+      pfM = colPrev[jj]; pfI = colPrev[col_rows + jj]; pfD = colPrev[2 * col_rows + jj];
+    }
+    int cpf = (sact && 1 - t >= 1 && 1 - t <= n) ? h[-t] : 0;
     for (int s = 1; s <= steps; ++s) {
       const int j = s - t;
       const T dgM = nbM, dgI = nbI, dgD = nbD;
@@ -352,12 +360,14 @@ __device__ __forceinline__ void exact_item(const EngineDev& E, const ExactItem& 
       if (t == 0) {
         if (q == 0) { nbM = zero; nbI = zero; nbD = bnd; }
         else if (sact) {
-          const int jj = min(max(j, 0), n);
-          nbM = colPrev[jj]; nbI = colPrev[col_rows + jj]; nbD = colPrev[2 * col_rows + jj];
+          nbM = pfM; nbI = pfI; nbD = pfD;
+          const int jj = min(s + 1, n);
+          pfM = colPrev[jj]; pfI = colPrev[col_rows + jj]; pfD = colPrev[2 * col_rows + jj];
         }
       }
+      const int c = cpf;
+      cpf = (sact && j + 1 >= 1 && j + 1 <= n) ? h[j] : 0;
       if (sact && j >= 1 && j <= n) {
-        const int c = h[j - 1];
         const T* Ec = Et + (c * K) * P + t;
 #pragma unroll
         for (int k = K - 1; k >= 0; --k) {
@@ -1324,6 +1334,13 @@ fast64_list(const EngineDev& E, int slot, int* __restrict__ counter, double* __r
         else if (sact) { nbM = colPrev[0]; nbI = colPrev[col_rows]; nbD = colPrev[2 * col_rows]; }
       }
       __syncwarp();
+      // one-row-ahead prefetch of the boundary column (thread 0) and the characters
+      double pfM = 0.0, pfI = 0.0, pfD = 0.0;
+      if (t == 0 && q > 0 && sact) {
+        const int jj = min(1, n);
+        pfM = colPrev[jj]; pfI = colPrev[col_rows + jj]; pfD = colPrev[2 * col_rows + jj];
+      }
+      int cpf = (sact && 1 - t >= 1 && 1 - t <= n) ? h[-t] : 0;
       for (int s = 1; s <= steps; ++s) {
         const int j = s - t;
         const double dgM = nbM, dgI = nbI, dgD = nbD;
@@ -1333,12 +1350,15 @@ fast64_list(const EngineDev& E, int slot, int* __restrict__ counter, double* __r
         if (t == 0) {
           if (q == 0) { nbM = 0.0; nbI = 0.0; nbD = bS; }
           else if (sact) {
-            const int jj = min(max(j, 0), n);
-            nbM = colPrev[jj]; nbI = colPrev[col_rows + jj]; nbD = colPrev[2 * col_rows + jj];
+            nbM = pfM; nbI = pfI; nbD = pfD;
+            const int jj = min(s + 1, n);
+            pfM = colPrev[jj]; pfI = colPrev[col_rows + jj]; pfD = colPrev[2 * col_rows + jj];
           }
         }
+        const int c = cpf;
+        cpf = (sact && j + 1 >= 1 && j + 1 <= n) ? h[j] : 0;
         if (sact && j >= 1 && j <= n) {
-          const double* Ec = Et + (h[j - 1] * K) * P + t;
+          const double* Ec = Et + (c * K) * P + t;
 #pragma unroll
           for (int k = K - 1; k >= 0; --k) {
             D[k] = fma(ep[k], D[k], zp[k] * M[k]);
