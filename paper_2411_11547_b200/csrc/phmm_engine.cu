@@ -118,19 +118,19 @@ struct StreamKernel {
   size_t smem;
   const void* fn;
   void (*launch)(dim3, size_t, cudaStream_t, const EngineDev&, const StreamUnit*, const StreamHap*, int,
-                 const int*, int*);
+                 const int*, int*, void*, int);
 };
-template <int MODE, int P, int K>
+template <int MODE, int P, int K, bool STRIPES>
 void launch_stream_t(dim3 g, size_t smem, cudaStream_t s, const EngineDev& E, const StreamUnit* u,
-                     const StreamHap* h, int nu, const int* nud, int* ctr) {
-  k_stream<MODE, P, K><<<g, kThreads, smem, s>>>(E, u, h, nu, nud, ctr);
+                     const StreamHap* h, int nu, const int* nud, int* ctr, void* col, int col_rows) {
+  k_stream<MODE, P, K, STRIPES><<<g, kThreads, smem, s>>>(E, u, h, nu, nud, ctr, col, col_rows);
 }
-template <int MODE, int P, int K>
+template <int MODE, int P, int K, bool STRIPES = false>
 StreamKernel SK() {
   const size_t elem = ModeOf<MODE>::F64 ? sizeof(double) : sizeof(float);   // 5*K*P entries per slot
   return StreamKernel{P, K, StreamOcc<MODE, K>::value,
                       96 * sizeof(double) + (size_t)4 * (32 / P) * 5 * K * P * elem + kStreamCodeBytesPerCta,
-                      (const void*)k_stream<MODE, P, K>, launch_stream_t<MODE, P, K>};
+                      (const void*)k_stream<MODE, P, K, STRIPES>, launch_stream_t<MODE, P, K, STRIPES>};
 }
 // kFast32: the k_fast tiling table (same order as kFastGeoms, so PHMM_FAST_GEOM applies),
 // then K = 10, 14 tilings (2-wide emission chunks) for widths 80 .. 448
@@ -154,6 +154,11 @@ const StreamKernel kStreamExact32[kNumRX32Geoms] = {
     SK<kExact32, 8, 4>(),  SK<kExact32, 16, 4>(), SK<kExact32, 16, 6>(),  SK<kExact32, 32, 4>(),
     SK<kExact32, 32, 6>(), SK<kExact32, 32, 8>(), SK<kExact32, 32, 12>(), SK<kExact32, 32, 16>()};
 const StreamKernel* const kStreamTab[4] = {kStreamFast32, kStreamFast64, kStreamExact32, kStreamExact64};
+// reads longer than every tiling stripe over the widest one of their mode, in a separate
+// instantiation (the column hand-off costs registers the single-stripe kernels keep)
+const StreamKernel kStripedTab[4] = {SK<kFast32, 32, 16, true>(), SK<kFast64, 32, 8, true>(),
+                                     SK<kExact32, 32, 16, true>(), SK<kExact64, 32, 8, true>()};
+const int kStripedGeom[4] = {12, kNumR64Geoms - 1, kNumRX32Geoms - 1, kNumR64Geoms - 1};
 const int kStreamTabN[4] = {kNumStreamFast32, kNumR64Geoms, kNumRX32Geoms, kNumR64Geoms};
 constexpr int kMaxTilings = 24;
 static_assert(kNumStreamFast32 <= kMaxTilings, "tiling table");
@@ -235,6 +240,13 @@ int choose_stream_geom(int mode, int m, int64_t total, int nmax) {
   }
   return bi;
 }
+constexpr int kStripedBin = 1 << 10;          // geometry code of a striped bin
+const StreamKernel& skern(int mode, int geom) {
+  return (geom & kStripedBin) ? kStripedTab[mode] : kStreamTab[mode][geom];
+}
+// column rows a striped unit of tiling P can need (its row capacity + the row-0 slot)
+int col_rows_for(int P) { return stream_cap_of(P) + 2; }
+constexpr int kR64MaxW = 256, kRX32MaxW = 512;   // widest FP64 / exact-FP32 retry tilings
 
 constexpr int kMaxScoreChunks = 8;
 int score_chunks() {                          // phmm_score pipelining depth (PHMM_CHUNKS)
@@ -406,8 +418,12 @@ struct phmm_ctx {
     int geom;
     int64_t count = 0;                      // units of this tiling
     int64_t dev_off = 0;                    // first unit in h_sunits / d_sunits
+    int64_t col_off = -1;                   // striped units: column buffer (bytes), else -1
+    int grid = 0;
   };
   std::vector<SBin> sbins;
+  DBuf<unsigned char> d_colstream;          // boundary columns of striped stream units
+  int64_t r64_col_off[8] = {-1, -1, -1, -1, -1, -1, -1, -1}, rx32_col_off[8] = {-1, -1, -1, -1, -1, -1, -1, -1};
   std::vector<int> sbin_order;
   std::vector<StreamUnit> su_all;           // planning scratch (persistent capacity)
   std::vector<uint8_t> su_bin;
@@ -494,10 +510,13 @@ static int init_ctx(phmm_ctx* ctx, int device) {
   CK(cudaMemcpy(ctx->d_lut.p, ctx->lut.data(), 94 * sizeof(double), cudaMemcpyHostToDevice));
   for (int g = 0; g < 2 * kNumFastGeoms; ++g)
     CK(cudaFuncSetAttribute(kFastFn[g], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fast_smem(g / 2)));
-  for (int md = 0; md < 4; ++md)
+  for (int md = 0; md < 4; ++md) {
     for (int g = 0; g < kStreamTabN[md]; ++g)
       CK(cudaFuncSetAttribute(kStreamTab[md][g].fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)kStreamTab[md][g].smem));
+    CK(cudaFuncSetAttribute(kStripedTab[md].fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)kStripedTab[md].smem));
+  }
   CK(cudaFuncSetAttribute((const void*)k_exact_all<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (int)exact_smem(0, 4)));
   CK(cudaFuncSetAttribute((const void*)k_exact_all<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -514,7 +533,8 @@ int phmm_destroy(phmm_ctx* ctx) {
   ctx->d_rbases.release(); ctx->d_hbases.release(); ctx->d_bq.release(); ctx->d_iq.release();
   ctx->d_dq.release(); ctx->d_gq.release(); ctx->d_status.release(); ctx->d_rflags.release();
   ctx->d_roff.release(); ctx->d_hoff.release(); ctx->d_read_m.release(); ctx->d_read_scale.release();
-  ctx->d_read_ncap.release(); ctx->d_counters.release(); ctx->d_vflag.release(); ctx->d_gsum.release(); ctx->d_lut.release();
+  ctx->d_read_ncap.release(); ctx->d_counters.release(); ctx->d_vflag.release();
+  ctx->d_colstream.release(); ctx->d_gsum.release(); ctx->d_lut.release();
   ctx->d_acc.release(); ctx->d_units.release(); ctx->d_sunits.release(); ctx->d_shaps.release();
   for (int g = 0; g < kNumR64Geoms; ++g) ctx->d_r64u[g].release();
   for (int g = 0; g < kNumRX32Geoms; ++g) ctx->d_rx32u[g].release();
@@ -680,6 +700,7 @@ static int prepare_impl(phmm_ctx* ctx, const phmm_input* in, const phmm_options*
   std::vector<ExactItem> host32[kNumExactP], host64[kNumExactP];
   int64_t slot_pairs[kNumExactP] = {0, 0, 0, 0};
   int64_t r64_pairs[8] = {0}, rx32_pairs[8] = {0};
+  bool long64 = false, long32 = false;          // streamed reads that stripe in the retry kernels
   int max_n = 1;
   int64_t gid = 0;
   std::vector<int> hidx;
@@ -748,14 +769,18 @@ static int prepare_impl(phmm_ctx* ctx, const phmm_input* in, const phmm_options*
               sg = M.best_from[i];
               break;
             }
+          if (sg < 0 && m + 1 > M.wsorted[M.n - 1] &&   // longer than every tiling: stripes
+              stream_geom_cost(mode, kStripedGeom[mode], batch_total, ncap) != INT64_MAX)
+            sg = kStripedBin | kStripedGeom[mode];
           M.tmpl_geom = sg;
-          if (sg >= 0 && !M.tvalid[sg]) {
-            M.tvalid[sg] = true;
-            std::vector<LaneTemplate>& tmpl = M.tmpls[sg];
+          const int ts = (sg & kStripedBin) ? kMaxTilings - 1 : sg;   // template cache slot
+          if (sg >= 0 && !M.tvalid[ts]) {
+            M.tvalid[ts] = true;
+            std::vector<LaneTemplate>& tmpl = M.tmpls[ts];
             tmpl.clear();
             // greedy LPT over the length-sorted haplotypes: each to the lighter lane; a
             // new unit when a lane would exceed the tiling's row capacity
-            const int cap = stream_cap(kStreamTab[mode][sg].P);
+            const int cap = stream_cap(skern(mode, sg).P);
             tmpl.emplace_back();
             for (int64_t x = 0; x < nh; ++x) {
               const int h = hidx[x];
@@ -773,8 +798,8 @@ static int prepare_impl(phmm_ctx* ctx, const phmm_input* in, const phmm_options*
           }
         }
         if (M.tmpl_geom >= 0) {
-          const std::vector<LaneTemplate>& tmpl = M.tmpls[M.tmpl_geom];
-          const int key = mode * kMaxTilings + M.tmpl_geom;
+          const std::vector<LaneTemplate>& tmpl = M.tmpls[(M.tmpl_geom & kStripedBin) ? kMaxTilings - 1 : M.tmpl_geom];
+          const int key = mode * kMaxTilings + ((M.tmpl_geom & kStripedBin) ? kMaxTilings - 1 : M.tmpl_geom);
           if (sbin_index[key] < 0) {
             sbin_index[key] = (int)ctx->sbins.size();
             ctx->sbins.push_back(phmm_ctx::SBin{mode, M.tmpl_geom, 0, 0});
@@ -782,6 +807,8 @@ static int prepare_impl(phmm_ctx* ctx, const phmm_input* in, const phmm_options*
           const uint8_t sbi = (uint8_t)sbin_index[key];
           if (mode == kFast32) {                       // tilings its device-built units can use
             const int g64 = r64_geom_for(m), gx = rx32_geom_for(m);
+            long64 |= m + 1 > kR64MaxW;
+            long32 |= m + 1 > kRX32MaxW;
             if (g64 >= 0) { ctx->r64_geoms |= 1u << g64; r64_pairs[g64] += nh; }
             if (gx >= 0) { ctx->rx32_geoms |= 1u << gx; rx32_pairs[gx] += nh; }
           }
@@ -865,7 +892,7 @@ static int prepare_impl(phmm_ctx* ctx, const phmm_input* in, const phmm_options*
   {
     std::vector<double> work(nsbins, 0.0);
     for (int bi = 0; bi < nsbins; ++bi) {
-      const StreamKernel& g = kStreamTab[ctx->sbins[bi].mode][ctx->sbins[bi].geom];
+      const StreamKernel& g = skern(ctx->sbins[bi].mode, ctx->sbins[bi].geom);
       for (int64_t i = ctx->sbins[bi].dev_off; i < ctx->sbins[bi].dev_off + ctx->sbins[bi].count; ++i) {
         const StreamUnit& u = ctx->h_sunits[i];
         work[bi] += (double)g.P * (g.K + 2.5) * (std::max(u.rowsA, u.rowsB) + g.P - 1) / g.P * g.P;
@@ -996,6 +1023,41 @@ static int prepare_impl(phmm_ctx* ctx, const phmm_input* in, const phmm_options*
   };
   lists(E.r64, ctx->d_r64u, kNumR64Geoms, ctx->d_r64h, ctx->r64_geoms, kCtrR64, r64_pairs);
   lists(E.rx32, ctx->d_rx32u, kNumRX32Geoms, ctx->d_rx32h, ctx->rx32_geoms, kCtrRX32, rx32_pairs);
+  // grids of the stream launches, and boundary-column space for the ones that can meet
+  // striped units (reads longer than the tiling width): per sub-warp slot 2 columns x
+  // 3 states x (row capacity + 1) two-lane values
+  {
+    int64_t col_total = 0;
+    auto col_bytes = [&](int mode, const StreamKernel& K, int grid) -> int64_t {
+      const int64_t v = (mode == kFast64 || mode == kExact64) ? 16 : 8;
+      return (int64_t)grid * 4 * (32 / K.P) * 6 * col_rows_for(K.P) * v;
+    };
+    for (auto& sb : ctx->sbins) {
+      const StreamKernel& K = skern(sb.mode, sb.geom);
+      const int G = 32 / K.P;
+      const int64_t groups = (sb.count + G - 1) / G;
+      sb.grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)ctx->num_sms * K.occ, (groups + 3) / 4));
+      const bool striped = (sb.geom & kStripedBin) != 0;
+      sb.col_off = striped ? col_total : -1;
+      if (striped) col_total += col_bytes(sb.mode, K, sb.grid);
+    }
+    for (int g = 0; g < 8; ++g) { ctx->r64_col_off[g] = -1; ctx->rx32_col_off[g] = -1; }
+    if (long64) {                                   // reads > 255 stripe on the widest FP64 tiling
+      const int g = kNumR64Geoms - 1;
+      if (ctx->r64_geoms & (1u << g)) {
+        ctx->r64_col_off[g] = col_total;
+        col_total += col_bytes(kFast64, kStreamFast64[g], ctx->num_sms * kStreamFast64[g].occ);
+      }
+    }
+    if (long32) {                                   // reads > 511: exact FP32 stripes
+      const int g = kNumRX32Geoms - 1;
+      if (ctx->rx32_geoms & (1u << g)) {
+        ctx->rx32_col_off[g] = col_total;
+        col_total += col_bytes(kExact32, kStreamExact32[g], ctx->num_sms * kStreamExact32[g].occ);
+      }
+    }
+    if (col_total > 0) CK(ctx->d_colstream.ensure(col_total));
+  }
 
   trace.mark("sync");
   trace.print("prepare");
@@ -1083,13 +1145,11 @@ int phmm_execute(phmm_ctx* ctx) {
     const auto& sb = ctx->sbins[bi];
     const int nu = (int)sb.count;
     if (nu == 0) continue;
-    const StreamKernel& SKn = kStreamTab[sb.mode][sb.geom];
-    const int G = 32 / SKn.P;
-    const int groups = (nu + G - 1) / G;
-    const int blk = std::max(1, std::min(ctx->num_sms * SKn.occ, (groups + 3) / 4));
+    const StreamKernel& SKn = skern(sb.mode, sb.geom);
     used[nlaunch % kStreamAux] = true;
-    SKn.launch(dim3(blk), SKn.smem, side(nlaunch++), E, ctx->d_sunits.p + sb.dev_off, ctx->d_shaps.p, nu, nullptr,
-               bin_ctr + nb + bi);
+    SKn.launch(dim3(sb.grid), SKn.smem, side(nlaunch++), E, ctx->d_sunits.p + sb.dev_off, ctx->d_shaps.p, nu, nullptr,
+               bin_ctr + nb + bi, sb.col_off >= 0 ? ctx->d_colstream.p + sb.col_off : nullptr,
+               col_rows_for(SKn.P));
     ++launches;
   }
   for (int bi = 0; bi < nb; ++bi) {
@@ -1114,17 +1174,21 @@ int phmm_execute(phmm_ctx* ctx) {
       E, ctx->d_counters.p + 8, (float*)ctx->d_cold.p, ctx->max_n + 1);
   ++launches;
   int nside = 0;
-  auto post = [&](const StreamKernel& SKn, const RetryLists& L, int g, int* work) {
+  auto post = [&](const StreamKernel& SKn, const RetryLists& L, int g, int* work, int64_t col_off) {
     const int a = 1 + (nside++ % (phmm_ctx::kAux - 1));
     used[a] = true;
     SKn.launch(dim3(ctx->num_sms * SKn.occ), SKn.smem, ctx->aux[a], E, L.units[g], L.haps, L.unit_cap[g], L.count + g,
-               work);
+               work, col_off >= 0 ? ctx->d_colstream.p + col_off : nullptr, col_rows_for(SKn.P));
     ++launches;
   };
   for (int g = kNumR64Geoms - 1; g >= 0; --g)
-    if (ctx->r64_geoms & (1u << g)) post(kStreamFast64[g], E.r64, g, ctx->d_counters.p + kCtrR64Work + g);
+    if (ctx->r64_geoms & (1u << g))
+      post(ctx->r64_col_off[g] >= 0 ? kStripedTab[kFast64] : kStreamFast64[g], E.r64, g,
+           ctx->d_counters.p + kCtrR64Work + g, ctx->r64_col_off[g]);
   for (int g = kNumRX32Geoms - 1; g >= 0; --g)
-    if (ctx->rx32_geoms & (1u << g)) post(kStreamExact32[g], E.rx32, g, ctx->d_counters.p + kCtrRX32Work + g);
+    if (ctx->rx32_geoms & (1u << g))
+      post(ctx->rx32_col_off[g] >= 0 ? kStripedTab[kExact32] : kStreamExact32[g], E.rx32, g,
+           ctx->d_counters.p + kCtrRX32Work + g, ctx->rx32_col_off[g]);
   CK(join());
   if (ctx->flags & PHMM_FLAG_RETRY_F64) {
     k_fast64_all<<<ctx->num_sms * 2, kThreads, exact_smem(0, 8), st>>>(E, ctx->d_counters.p + 24, ctx->d_cold.p,
@@ -1274,10 +1338,11 @@ static int fetch_complete(phmm_ctx* ctx, double* out_log10, uint8_t* out_status,
       for (auto& u : bn.units) comp += 2LL * bn.Q * g.P * g.K * (std::max(u.nA, u.nB) + g.P - 1);
     }
     for (auto& sb : ctx->sbins) {
-      const StreamKernel& g = kStreamTab[sb.mode][sb.geom];
+      const StreamKernel& g = skern(sb.mode, sb.geom);
       for (int64_t i = sb.dev_off; i < sb.dev_off + sb.count; ++i) {
         const StreamUnit& u = ctx->h_sunits[i];
-        comp += 2LL * g.P * g.K * (std::max(u.rowsA, u.rowsB) + g.P - 1);
+        const int64_t Q = (u.m + g.P * g.K) / (g.P * g.K);
+        comp += 2LL * Q * g.P * g.K * (std::max(u.rowsA, u.rowsB) + g.P - 1);
       }
     }
     stats->computed_cells = comp;

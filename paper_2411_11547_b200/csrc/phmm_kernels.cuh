@@ -717,15 +717,16 @@ constexpr int kNumRX32Geoms = 8;    // exact FP32:  (8,4) (16,4) (16,6) (32,4) (
 // lists parallel (their count is unknown when the grid is sized)
 constexpr int kRetryLaneHaps64 = 2, kRetryLaneHapsX32 = 1;   // defaults (RetryLists.lane_haps)
 constexpr int kInlineBand = 4;      // guard-band pairs a warp may rerun inline per unit
+// reads longer than the widest tiling stripe over it (k_stream handles Q > 1 stripes)
 __host__ __device__ __forceinline__ int r64_geom_for(int m) {
   const int w = m + 1;
-  return w <= 32 ? 0 : w <= 64 ? 1 : w <= 96 ? 2 : w <= 128 ? 3 : w <= 192 ? 4 : w <= 256 ? 5 : -1;
+  return w <= 32 ? 0 : w <= 64 ? 1 : w <= 96 ? 2 : w <= 128 ? 3 : w <= 192 ? 4 : 5;
 }
 __host__ __device__ __forceinline__ int r64_geom_P(int g) { return g == 0 ? 8 : (g <= 3 ? 16 : 32); }
 __host__ __device__ __forceinline__ int rx32_geom_for(int m) {
   const int w = m + 1;
   return w <= 32 ? 0 : w <= 64 ? 1 : w <= 96 ? 2 : w <= 128 ? 3 : w <= 192 ? 4 : w <= 256 ? 5
-       : w <= 384 ? 6 : w <= 512 ? 7 : -1;
+       : w <= 384 ? 6 : 7;
 }
 __host__ __device__ __forceinline__ int rx32_geom_P(int g) { return g == 0 ? 8 : (g <= 2 ? 16 : 32); }
 
@@ -810,7 +811,8 @@ __device__ __forceinline__ int stream_finish32(const EngineDev& E, float a, int 
 // Groups the flagged entries (bit e of mask[lane]) of a finished unit into new stream
 // units of tiling g (row capacity cap) appended to L; thread-serial, rare.
 __device__ __forceinline__ void emit_retry_units(const StreamUnit& U, const StreamHap* shaps, const unsigned* mask,
-                                                 const RetryLists& L, int g, int cap, int m, int lane_haps) {
+                                                 const RetryLists& L, int g, int cap, int m, int lane_haps,
+                                                 int cap_w = 1 << 30) {
   int lanes_n[2] = {0, 0}, rows_n[2] = {0, 0};
   StreamHap buf[2][kStreamMaxLaneHaps];
   auto emit = [&]() {
@@ -828,6 +830,7 @@ __device__ __forceinline__ void emit_retry_units(const StreamUnit& U, const Stre
     lanes_n[0] = lanes_n[1] = 0;
     rows_n[0] = rows_n[1] = 0;
   };
+  if (U.m + 1 > cap_w) lane_haps = 1;       // striped (long) reads: latency-bound, keep units short
   for (int ln = 0; ln < 2; ++ln) {
     unsigned msk = mask[ln];
     const int e0 = U.list + (ln ? U.cntA : 0);
@@ -844,10 +847,11 @@ __device__ __forceinline__ void emit_retry_units(const StreamUnit& U, const Stre
   emit();
 }
 
-template <int MODE, int P, int K>
+template <int MODE, int P, int K, bool STRIPES = false>
 __global__ void __launch_bounds__(128, (StreamOcc<MODE, K>::value))
 k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHap* __restrict__ shaps,
-         int num_units_arg, const int* __restrict__ num_units_dev, int* __restrict__ counter) {
+         int num_units_arg, const int* __restrict__ num_units_dev, int* __restrict__ counter,
+         void* __restrict__ colbuf_v, int col_rows) {
   constexpr bool F64 = ModeOf<MODE>::F64, EXACT = ModeOf<MODE>::EXACT;
   using A = Lanes<F64>;
   using S = typename A::S;
@@ -905,7 +909,30 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
         E.acc[pr] = 0.0; E.status[pr] = kStatusDegenerate;
       }
     }
-    const int Lp = W - m - 1;
+    // reads longer than W - 1 run in Q stripes of W positions: the stream is replayed per
+    // stripe; thread P-1 hands its last position's (M, I, D) per row to the next stripe
+    // through a column in global memory (L2-resident), read one row ahead by thread 0
+    const int Q = STRIPES ? (m + 1 + W - 1) / W : 1;    // single-stripe instantiations: Q = 1
+    const int Qw = STRIPES ? (int)__reduce_max_sync(FULL, (unsigned)(live ? Q : 1)) : 1;
+    const int Lp = Q * W - m - 1;
+    V* colX = nullptr;
+    V* colY = nullptr;
+    if (STRIPES && Qw > 1) {
+      const size_t gslot = ((size_t)blockIdx.x * 4 + wib) * G + sw;
+      colX = reinterpret_cast<V*>(colbuf_v) + gslot * 6 * (size_t)col_rows;
+      colY = colX + 3 * (size_t)col_rows;
+    }
+    if (t == 0) {
+      s_unit[slot] = U;
+      s_flag[2 * slot] = 0u; s_flag[2 * slot + 1] = 0u;
+      s_band[2 * slot] = 0u; s_band[2 * slot + 1] = 0u;
+      s_ninl[slot] = 0;
+    }
+#pragma unroll 1
+    for (int q = 0; q < Qw; ++q) {
+    const bool sq = live && q < Q;                      // this sub-warp has stripe q
+    const bool lastq = q == Q - 1;
+    const int rows_q = sq ? rows : 0;
 
     // ---- per-position coefficients + emission table.  Fast modes: folded recurrence
     //    Mt(i) = alpha_{i+1} M(i), D'(i) = beta_{i+1} D(i), 7 ops per cell,
@@ -919,7 +946,7 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
 #pragma unroll
       for (int kk = 0; kk < EW; ++kk) {
         const int k = ke * EW + kk;
-        const int p = t * K + k;
+        const int p = q * W + t * K + k;
         M[k] = zero2; I[k] = zero2; D[k] = zero2;
         if (p < Lp) {                                   // left padding
           al[k] = 0; be[k] = 0; dl[k] = 0; ep[k] = 1; zt[k] = 0;
@@ -972,7 +999,8 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
     // ---- row codes of both lanes into shared memory (row 0 = idle code N|N), and the
     // unit's window starts: every row where a haplotype begins in either lane, plus the
     // row after each lane's end.  Events (FIRST for thread t at step b + t, LAST for
-    // thread P-1 at step b + P - 2) fall in windows [b, b + P).
+    // thread P-1 at step b + P - 2) fall in windows [b, b + P).  Built once per unit.
+    if (q == 0) {
     if (t == 0) reinterpret_cast<unsigned short*>(cd)[0] = 0x0404;
     if (live) {
 #pragma unroll 1
@@ -1019,12 +1047,7 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
     } else if (t == 0) {
       s_nwin[slot] = 0;
     }
-    if (t == 0) {
-      s_unit[slot] = U;
-      s_flag[2 * slot] = 0u; s_flag[2 * slot + 1] = 0u;
-      s_band[2 * slot] = 0u; s_band[2 * slot + 1] = 0u;
-      s_ninl[slot] = 0;
-    }
+    }                                                   // q == 0
     s_hc[2 * threadIdx.x] = -1;                         // current haplotype per lane
     s_hc[2 * threadIdx.x + 1] = -1;
     __syncwarp();
@@ -1038,10 +1061,19 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
     const unsigned short* cdt = cd16 - t;
     auto ld_code = [&](int s) -> unsigned {
       const int i = s - t;
-      return (unsigned)cdt[(i >= 1 && i <= rows) ? s : t];
+      return (unsigned)cdt[(i >= 1 && i <= rows_q) ? s : t];
     };
     unsigned code = 0x0404u;
     unsigned pf1 = ld_code(1);
+    // stripe q > 0: thread 0's left neighbour is the previous stripe's column
+    V* colPrev = (q & 1) ? colY : colX;
+    V* colNext = (q & 1) ? colX : colY;
+    const bool from_col = STRIPES && q > 0 && t == 0 && sq;
+    const bool to_col = STRIPES && !lastq && t == P - 1 && sq;
+    V cpM = zero2, cpI = zero2, cpD = zero2;            // column prefetch (row s + 1)
+    if (from_col && rows_q >= 1) {
+      cpM = colPrev[1]; cpI = colPrev[col_rows + 1]; cpD = colPrev[2 * col_rows + 1];
+    }
 
     // FIRST(lane L): reset the lane to row 0 of its next haplotype (event paths only run
     // inside windows and read their inputs from shared memory)
@@ -1050,16 +1082,17 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
       const int hc = ++s_hc[2 * threadIdx.x + L];
       const int lp = s_meta[slot * 4 + 0];
       const S b = s_bs[slot * 2 * kStreamMaxLaneHaps + (L == 0 ? 0 : s_unit[slot].cntA) + hc];
+      const int p0 = q * W + t * K;                     // global padded position of k = 0
 #pragma unroll
       for (int k = 0; k < K; ++k) {
         lane_ref<L>(M[k]) = 0;
         lane_ref<L>(I[k]) = 0;
-        lane_ref<L>(D[k]) = (t * K + k < lp) ? b : (S)0;
+        lane_ref<L>(D[k]) = (p0 + k < lp) ? b : (S)0;
       }
       lane_ref<L>(dgM) = 0;
       lane_ref<L>(dgI) = 0;
-      lane_ref<L>(dgD) = (t == 0 || t * K - 1 < lp) ? b : (S)0;
-      if (t == 0) {
+      lane_ref<L>(dgD) = (p0 - 1 < lp) ? b : (S)0;      // (stripe 0, thread 0: the boundary)
+      if (t == 0 && q == 0) {
         lane_ref<L>(cb) = b;
         lane_ref<L>(nbM) = 0; lane_ref<L>(nbI) = 0; lane_ref<L>(nbD) = b;
       }
@@ -1103,7 +1136,7 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
                                       s_meta[slot * 4 + 1]);
         if (v == 1) {                                   // guard band: bit-exact rerun
           const int c = s_ninl[slot];
-          if (c < kInlineBand && atomicAdd(E.band_inline, 1) < E.band_budget) {
+          if (c < kInlineBand && s_meta[slot * 4 + 0] + mm + 1 <= W && atomicAdd(E.band_inline, 1) < E.band_budget) {
             // the first few per launch: rerun by this warp right after the unit (no
             // post-pass latency when band pairs are rare)
             s_inl[slot * kInlineBand + c] = ExactItem{sh.pair, SU.read, sh.hap, s_meta[slot * 4 + 1]};
@@ -1132,7 +1165,15 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
         nbD.x = __shfl_up_sync(FULL, ld.x, 1, P);
         nbD.y = __shfl_up_sync(FULL, ld.y, 1, P);
       }
-      if (t == 0) { nbM = zero2; nbI = zero2; nbD = cb; }
+      if (t == 0) {
+        if (from_col) {
+          nbM = cpM; nbI = cpI; nbD = cpD;
+          const int jn = min(s + 1, col_rows - 1);
+          cpM = colPrev[jn]; cpI = colPrev[col_rows + jn]; cpD = colPrev[2 * col_rows + jn];
+        } else {
+          nbM = zero2; nbI = zero2; nbD = cb;
+        }
+      }
       code = pf1;
       pf1 = ld_code(s + 1);
       if (CHECK && (code & ((kCodeFirst << 8) | kCodeFirst))) {
@@ -1180,7 +1221,13 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
           lI = I[k];
         }
       }
-      if (CHECK && (code & ((kCodeLast << 8) | kCodeLast)) && t == P - 1) {
+      if (to_col) {
+        const int j = s - (P - 1);
+        if (j >= 1 && j <= rows_q) {
+          colNext[j] = M[K - 1]; colNext[col_rows + j] = I[K - 1]; colNext[2 * col_rows + j] = D[K - 1];
+        }
+      }
+      if (CHECK && lastq && (code & ((kCodeLast << 8) | kCodeLast)) && t == P - 1) {
         if (code & kCodeLast) last_event(std::integral_constant<int, 0>{});
         if (code & (kCodeLast << 8)) last_event(std::integral_constant<int, 1>{});
       }
@@ -1216,18 +1263,19 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
       }
     }
     __syncwarp();
+    }                                                   // stripes
     if constexpr (MODE == kFast32) {
       // this unit's FP32-underflowed and guard-band pairs -> device-built stream units
       if (t == 0 && live) {
         if (s_flag[2 * slot] | s_flag[2 * slot + 1]) {
           const int g64 = r64_geom_for(m);
           emit_retry_units(U, shaps, s_flag + 2 * slot, E.r64, g64, stream_cap_of(r64_geom_P(g64)), m,
-                           E.r64.lane_haps);
+                           E.r64.lane_haps, 256);
         }
         if (s_band[2 * slot] | s_band[2 * slot + 1]) {
           const int gx = rx32_geom_for(m);
           emit_retry_units(U, shaps, s_band + 2 * slot, E.rx32, gx, stream_cap_of(rx32_geom_P(gx)), m,
-                           E.rx32.lane_haps);
+                           E.rx32.lane_haps, 512);
         }
       }
       // inline guard-band reruns (same tiling; the emission-table slot is free again)
