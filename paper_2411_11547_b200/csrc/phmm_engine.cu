@@ -511,9 +511,14 @@ static int init_ctx(phmm_ctx* ctx, int device) {
   for (int g = 0; g < 2 * kNumFastGeoms; ++g)
     CK(cudaFuncSetAttribute(kFastFn[g], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fast_smem(g / 2)));
   for (int md = 0; md < 4; ++md) {
-    for (int g = 0; g < kStreamTabN[md]; ++g)
+    for (int g = 0; g < kStreamTabN[md]; ++g) {
       CK(cudaFuncSetAttribute(kStreamTab[md][g].fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)kStreamTab[md][g].smem));
+      // one shared-memory carveout for every stream kernel: CTAs of different tilings can
+      // share an SM without an L1/shared reconfiguration
+      if (!getenv("PHMM_NO_CARVEOUT"))
+        CK(cudaFuncSetAttribute(kStreamTab[md][g].fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    }
     CK(cudaFuncSetAttribute(kStripedTab[md].fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)kStripedTab[md].smem));
   }
