@@ -331,7 +331,10 @@ def main():
     }
     if not args.no_secondary and ws == 1:
         try:
-            line["secondary"] = [secondary(ctx, "c3", _native.FLAG_RETRY_F64)]
+            # c3 with the GATK FP64 retry and with the reference's own FP32 semantics
+            # (flagged pairs NaN, pipeline.py has no automatic retry); c4 long pairs
+            line["secondary"] = [secondary(ctx, "c3", _native.FLAG_RETRY_F64), secondary(ctx, "c3", 0),
+                                 secondary(ctx, "c4", _native.FLAG_RETRY_F64)]
         except Exception as exc:    # reported, never fatal for the headline
             line["secondary"] = [{"error": repr(exc)}]
     if not args.no_cpu_baseline:

@@ -7,6 +7,8 @@ timeout 900 python -m pytest tests -m gpu -x -q --timeout 600 > gpurun_out/pytes
 tail -15 gpurun_out/pytest_gpu.log
 timeout 400 python bench.py --steps 10 --warmup 3 --cpu-seconds 5 > gpurun_out/bench.json 2> gpurun_out/bench.err; echo bench rc=$?
 cat gpurun_out/bench.json; tail -5 gpurun_out/bench.err
+timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; echo ref rc=$?
+cat gpurun_out/bench_ref.json
 for W in ${PROFILE_WORKLOADS:-c2}; do
   timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
      --log-file gpurun_out/launches_${W}.csv python tools/profile_run.py $W 2 --retry > gpurun_out/launches_${W}.log 2>&1
