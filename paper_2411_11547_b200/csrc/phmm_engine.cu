@@ -219,23 +219,24 @@ int choose_geom(int m, int nmax, int* Qout) {
 // exceed the geometry's row-code capacity.  -1: no single-stripe streaming geometry.
 // cost of streaming a read's haplotypes (total rows, longest nmax) on tiling g (1e300:
 // infeasible or excluded by PHMM_FAST_GEOM)
-int64_t stream_geom_cost(int mode, int g, int64_t total, int nmax) {
+// `lane_rows`: the call's lane-length budget (small calls split units further, below)
+int64_t stream_geom_cost(int mode, int g, int64_t total, int nmax, int64_t lane_rows = INT64_MAX) {
   constexpr int64_t kInf = INT64_MAX;
   const int fg = forced_geom();
   if (mode == kFast32 && fg >= 0 && g != fg) return kInf;
   const int64_t P = kStreamTab[mode][g].P, K = kStreamTab[mode][g].K;
-  const int64_t cap = stream_cap((int)P);
-  if (nmax > cap) return kInf;
+  if (nmax > stream_cap((int)P)) return kInf;
+  const int64_t cap = std::min<int64_t>(stream_cap((int)P), std::max<int64_t>(nmax, lane_rows));
   const int64_t units = (total + 2 * cap - 1) / (2 * cap);
   const int64_t rows = std::min<int64_t>(cap, (total + 2 * units - 1) / (2 * units));
   return units * P * (2 * K + 5) * (rows + P - 1);     // 2 x (K + 2.5) per thread-row
 }
-int choose_stream_geom(int mode, int m, int64_t total, int nmax) {
+int choose_stream_geom(int mode, int m, int64_t total, int nmax, int64_t lane_rows) {
   int64_t best = INT64_MAX;
   int bi = -1;
   for (int g = 0; g < kStreamTabN[mode]; ++g) {
     if (m + 1 > kStreamTab[mode][g].P * kStreamTab[mode][g].K) continue;
-    const int64_t cost = stream_geom_cost(mode, g, total, nmax);
+    const int64_t cost = stream_geom_cost(mode, g, total, nmax, lane_rows);
     if (cost < best) { best = cost; bi = g; }
   }
   return bi;
@@ -733,6 +734,20 @@ static int prepare_impl(phmm_ctx* ctx, const phmm_input* in, const phmm_options*
     for (int i = 0; i < M.n; ++i) M.wsorted[i] = kStreamTab[md][M.wsort[i]].P * kStreamTab[md][M.wsort[i]].K;
   }
   if (use_stream) ctx->shaps.reserve(N);
+  // Lane budget: a call too small to fill the GPU with long lanes (few pairs, long
+  // haplotypes: c4) splits its units until there are ~2 per sub-warp slot (#SM x 8 warps
+  // x 2 sub-warps); latency, not per-unit overhead, bounds such calls.  Large calls keep
+  // the row capacity as the only limit.
+  int64_t lane_rows = INT64_MAX;
+  {
+    int64_t all_rows = 0;
+    for (int64_t b = 0; b < B; ++b) {
+      int64_t hs = 0;
+      for (int64_t h = ctx->batch_hap_off[b]; h < ctx->batch_hap_off[b + 1]; ++h) hs += ctx->hap_len[h];
+      all_rows += hs * (ctx->batch_read_off[b + 1] - ctx->batch_read_off[b]);
+    }
+    if (!getenv("PHMM_NO_LANE_BUDGET")) lane_rows = all_rows / (2 * 2 * (int64_t)ctx->num_sms * 16);
+  }
   for (int64_t b = 0; b < B; ++b) {
     const int64_t r0 = ctx->batch_read_off[b], r1 = ctx->batch_read_off[b + 1];
     const int64_t h0 = ctx->batch_hap_off[b], h1 = ctx->batch_hap_off[b + 1];
@@ -770,7 +785,7 @@ static int prepare_impl(phmm_ctx* ctx, const phmm_input* in, const phmm_options*
           int sg = -1;
           for (int i = 0; i < M.n; ++i)                // best tiling of the narrowest width >= m+1
             if (M.wsorted[i] >= m + 1) {
-              if (M.best_from[i] == -2) M.best_from[i] = choose_stream_geom(mode, M.wsorted[i] - 1, batch_total, ncap);
+              if (M.best_from[i] == -2) M.best_from[i] = choose_stream_geom(mode, M.wsorted[i] - 1, batch_total, ncap, lane_rows);
               sg = M.best_from[i];
               break;
             }
@@ -784,15 +799,16 @@ static int prepare_impl(phmm_ctx* ctx, const phmm_input* in, const phmm_options*
             std::vector<LaneTemplate>& tmpl = M.tmpls[ts];
             tmpl.clear();
             // greedy LPT over the length-sorted haplotypes: each to the lighter lane; a
-            // new unit when a lane would exceed the tiling's row capacity
-            const int cap = stream_cap(skern(mode, sg).P);
+            // new unit when a lane would exceed the tiling's row capacity or the call's
+            // lane budget
+            const int cap = (int)std::min<int64_t>(stream_cap(skern(mode, sg).P), std::max<int64_t>(lane_rows, 1));
             tmpl.emplace_back();
             for (int64_t x = 0; x < nh; ++x) {
               const int h = hidx[x];
               const int n = (int)ctx->hap_len[h];
               LaneTemplate* t = &tmpl.back();
               int ln = t->rows[0] <= t->rows[1] ? 0 : 1;
-              if (t->rows[ln] + n > cap || (int)t->lanes[ln].size() >= kStreamMaxLaneHaps) {
+              if ((t->rows[ln] > 0 && t->rows[ln] + n > cap) || (int)t->lanes[ln].size() >= kStreamMaxLaneHaps) {
                 tmpl.emplace_back();
                 t = &tmpl.back();
                 ln = 0;
