@@ -796,6 +796,7 @@ template <class V, class S> __device__ __forceinline__ V flush2(V v, S thr) {
 __device__ __forceinline__ int stream_finish32(const EngineDev& E, float a, int pair, int n, float gsum, int scale) {
   const float bound = 0x1p-80f * (float)n * gsum;                // 2^10 * 2^-90
   const float hi = ldexpf(0.031622776f, scale);                   // 10^-1.5 * 2^scale
+  if (a != a) { E.status[pair] = kStatusExactF32; return 1; }   // beta_i = 0 (gcp q = 0): exact
   if (!(a >= 0x1p-93f)) {
     if (E.retry_f64) { E.status[pair] = kStatusRetriedF64; return 2; }
     E.acc[pair] = 0.0;
@@ -969,17 +970,19 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
               anext = (1.0 - s_lut[E.iq[ro + i0 + 1]]) - s_lut[E.dq[ro + i0 + 1]];
               bnext = 1.0 - s_lut[E.gq[ro + i0 + 1]];
             }
-            be[k] = 1.0 - e; dl[k] = d / a; ep[k] = e; zt[k] = bnext * z / anext;
+            const double bI = (i0 + 1 < m) ? bnext : 1.0;   // beta_{i+1} (accumulator: 1)
+            be[k] = bI * e / (1.0 - e); dl[k] = bI * d / a; ep[k] = e; zt[k] = bnext * z / anext;
             lm = anext * (1.0 - qe); lx = anext * (qe / 3.0);
           } else {                                      // k_fast's coefficients
-            const float a = (float)((1.0 - d) - z);
             float anext = 1.f, bnext = 0.f;
+            double bI = 1.0;                            // beta_{i+1} (accumulator: 1)
             if (i0 + 1 < m) {
               anext = (float)((1.0 - s_lut[E.iq[ro + i0 + 1]]) - s_lut[E.dq[ro + i0 + 1]]);
-              bnext = (float)(1.0 - s_lut[E.gq[ro + i0 + 1]]);
+              bI = 1.0 - s_lut[E.gq[ro + i0 + 1]];
+              bnext = (float)bI;
             }
-            be[k] = (float)(1.0 - e);
-            dl[k] = __fdividef((float)d, a);
+            be[k] = (float)(bI * e / (1.0 - e));
+            dl[k] = (float)(bI * d / ((1.0 - d) - z));
             ep[k] = (float)e;
             zt[k] = __fdividef(bnext * (float)z, anext);
             lm = anext * (float)(1.0 - qe); lx = anext * ((float)qe * (1.f / 3.f));
@@ -1203,8 +1206,7 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
             M[k] = flush2(x, thr);
           } else {
             D[k] = A::fma(ep[k], D[k], A::mul(zt[k], M[k]));
-            V x = A::fma(be[k], pi, pd);
-            x = A::add(pm, x);
+            V x = A::add(pm, A::add(pi, pd));
             M[k].x = ev_comp(la, kk) * x.x;
             M[k].y = ev_comp(lb, kk) * x.y;
           }
@@ -1216,7 +1218,7 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
 #pragma unroll
         for (int k = 0; k < K; ++k) {
           if constexpr (EXACT) I[k] = flush2(A::xadd(A::xmul(dl[k], lM), A::xmul(ep[k], lI)), thr);
-          else I[k] = A::fma(ep[k], lI, A::mul(dl[k], lM));
+          else I[k] = A::fma(be[k], lI, A::mul(dl[k], lM));
           lM = M[k];
           lI = I[k];
         }
