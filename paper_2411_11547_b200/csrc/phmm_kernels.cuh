@@ -935,12 +935,32 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
     const bool lastq = q == Q - 1;
     const int rows_q = sq ? rows : 0;
 
-    // ---- per-position coefficients + emission table.  Fast modes: folded recurrence
-    //    Mt(i) = alpha_{i+1} M(i), D'(i) = beta_{i+1} D(i), 7 ops per cell,
-    //   coefficients be, dl, ep, zt (= zeta'); exact modes: the reference's al, be, dl, ep,
-    //   zt with the f64 -> dtype casts of wavefront.py:347-355.
+    // ---- per-position coefficients + emission table.  Fast modes: scaled
+    //   state Mt(i) = alpha_{i+1} M(i), I(i) = d_i I''(i), beta_{i+1} D(i) = c_i D''(i) with
+    //   d_i = beta_{i+1} delta_i / alpha_i, c_i = beta_{i+1} zeta_i / alpha_{i+1} (position
+    //   after the read: beta = alpha = 1), so that
+    //     D'' = eps D''(up) + Mt(up),   I'' = r I''(left) + Mt(left),
+    //     Mt = lam (Mt + d_{i-1} I'' + c_{i-1} D'')(diag),   r = beta_{i+1} eps_i d_{i-1} / (beta_i d_i)
+    //   -- 6 operations per cell (4 packed FMAs + the per-lane emission product); registers
+    //   ep = eps, be = r, dl = d_{p-1}, zt = c_{p-1}.  Exact modes: the reference's al, be,
+    //   dl, ep, zt with the f64 -> dtype casts of wavefront.py:347-355.
     S al[K], be[K], dl[K], ep[K], zt[K];
     V M[K], I[K], D[K];
+    double dprev = 1.0, cprev = 1.0;                  // fast modes: d, c of position p - 1
+    if constexpr (!EXACT) {
+      const int pp = q * W + t * K - 1;
+      if (pp >= Lp && pp < Lp + m) {
+        const int i0 = pp - Lp;
+        const double d = s_lut[E.iq[ro + i0]], z = s_lut[E.dq[ro + i0]];
+        double anext = 1.0, bnext = 0.0, bI = 1.0;
+        if (i0 + 1 < m) {
+          anext = (1.0 - s_lut[E.iq[ro + i0 + 1]]) - s_lut[E.dq[ro + i0 + 1]];
+          bnext = bI = 1.0 - s_lut[E.gq[ro + i0 + 1]];
+        }
+        dprev = bI * d / ((1.0 - d) - z);
+        cprev = bnext * z / anext;
+      }
+    }
 #pragma unroll
     for (int ke = 0; ke < KE; ++ke) {
       S lam[5][EW];
@@ -950,7 +970,8 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
         const int p = q * W + t * K + k;
         M[k] = zero2; I[k] = zero2; D[k] = zero2;
         if (p < Lp) {                                   // left padding
-          al[k] = 0; be[k] = 0; dl[k] = 0; ep[k] = 1; zt[k] = 0;
+          if constexpr (EXACT) { al[k] = 0; be[k] = 0; dl[k] = 0; ep[k] = 1; zt[k] = 0; }
+          else { be[k] = 0; dl[k] = (S)dprev; zt[k] = (S)cprev; ep[k] = 1; dprev = 1.0; cprev = 1.0; }
 #pragma unroll
           for (int c = 0; c < 5; ++c) lam[c][kk] = 0;
         } else if (p < Lp + m) {                        // real read position
@@ -963,34 +984,25 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
             al[k] = (S)((1.0 - d) - z); be[k] = (S)(1.0 - e); dl[k] = (S)d; ep[k] = (S)e;
             zt[k] = (i0 + 1 < m) ? (S)z : (S)0;         // D(m, .) never reaches the score
             lm = (S)(1.0 - qe); lx = (S)(qe / 3.0);
-          } else if constexpr (F64) {                   // k_fast64's coefficients
-            const double a = (1.0 - d) - z;
-            double anext = 1.0, bnext = 0.0;
+          } else {                                      // fast modes (computed in f64)
+            double anext = 1.0, bnext = 0.0, bI = 1.0;  // alpha, beta of position i+1
             if (i0 + 1 < m) {
               anext = (1.0 - s_lut[E.iq[ro + i0 + 1]]) - s_lut[E.dq[ro + i0 + 1]];
-              bnext = 1.0 - s_lut[E.gq[ro + i0 + 1]];
+              bnext = bI = 1.0 - s_lut[E.gq[ro + i0 + 1]];
             }
-            const double bI = (i0 + 1 < m) ? bnext : 1.0;   // beta_{i+1} (accumulator: 1)
-            be[k] = bI * e / (1.0 - e); dl[k] = bI * d / a; ep[k] = e; zt[k] = bnext * z / anext;
-            lm = anext * (1.0 - qe); lx = anext * (qe / 3.0);
-          } else {                                      // k_fast's coefficients
-            float anext = 1.f, bnext = 0.f;
-            double bI = 1.0;                            // beta_{i+1} (accumulator: 1)
-            if (i0 + 1 < m) {
-              anext = (float)((1.0 - s_lut[E.iq[ro + i0 + 1]]) - s_lut[E.dq[ro + i0 + 1]]);
-              bI = 1.0 - s_lut[E.gq[ro + i0 + 1]];
-              bnext = (float)bI;
-            }
-            be[k] = (float)(bI * e / (1.0 - e));
-            dl[k] = (float)(bI * d / ((1.0 - d) - z));
-            ep[k] = (float)e;
-            zt[k] = __fdividef(bnext * (float)z, anext);
-            lm = anext * (float)(1.0 - qe); lx = anext * ((float)qe * (1.f / 3.f));
+            const double dcur = bI * d / ((1.0 - d) - z);
+            const double ccur = bnext * z / anext;      // 0 for the last position
+            // beta_i = 0 (gcp q = 0): r = inf -> NaN accumulator -> exact rerun
+            be[k] = (S)(bI * e / (1.0 - e) * dprev / dcur);
+            dl[k] = (S)dprev; zt[k] = (S)cprev; ep[k] = (S)e;
+            dprev = dcur; cprev = ccur;
+            lm = (S)(anext * (1.0 - qe)); lx = (S)(anext * (qe / 3.0));
           }
 #pragma unroll
           for (int c = 0; c < 5; ++c) lam[c][kk] = (rc == c || rc == 4 || c == 4) ? lm : lx;
         } else {                                        // accumulator position
-          al[k] = 1; be[k] = 1; dl[k] = 0; ep[k] = 1; zt[k] = 1;
+          if constexpr (EXACT) { al[k] = 1; be[k] = 1; dl[k] = 0; ep[k] = 1; zt[k] = 1; }
+          else { be[k] = 0; dl[k] = (S)dprev; zt[k] = (S)cprev; ep[k] = 1; dprev = 1.0; cprev = 1.0; }
 #pragma unroll
           for (int c = 0; c < 5; ++c) lam[c][kk] = 1;
         }
@@ -1109,8 +1121,8 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
       S res;
       if constexpr (EXACT)                              // j-ordered sum (wavefront.py:156-160)
         res = (lane_ref<L>(D[K - 1]) + lane_ref<L>(M[K - 1])) + (lane_ref<L>(M[K - 2]) + lane_ref<L>(I[K - 2]));
-      else
-        res = (lane_ref<L>(D[K - 1]) + lane_ref<L>(M[K - 1])) + (lane_ref<L>(M[K - 2]) + lane_ref<L>(I[K - 2]));
+      else                                              // I(m) = d_m I''(m); d_m = dl[K - 1]
+        res = (lane_ref<L>(D[K - 1]) + lane_ref<L>(M[K - 1])) + (lane_ref<L>(M[K - 2]) + dl[K - 1] * lane_ref<L>(I[K - 2]));
       const int mm = s_meta[slot * 4 + 3];
       if constexpr (MODE == kFast64) {
         // FP64 retry result; near/below the f64 flush floor -> bit-exact FP64 kernel
@@ -1205,8 +1217,9 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
             x.y = A::mul1(ev_comp(lb, kk), x.y);
             M[k] = flush2(x, thr);
           } else {
-            D[k] = A::fma(ep[k], D[k], A::mul(zt[k], M[k]));
-            V x = A::add(pm, A::add(pi, pd));
+            D[k] = A::fma(ep[k], D[k], M[k]);
+            V x = A::fma(dl[k], pi, pm);
+            x = A::fma(zt[k], pd, x);
             M[k].x = ev_comp(la, kk) * x.x;
             M[k].y = ev_comp(lb, kk) * x.y;
           }
@@ -1218,7 +1231,7 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
 #pragma unroll
         for (int k = 0; k < K; ++k) {
           if constexpr (EXACT) I[k] = flush2(A::xadd(A::xmul(dl[k], lM), A::xmul(ep[k], lI)), thr);
-          else I[k] = A::fma(be[k], lI, A::mul(dl[k], lM));
+          else I[k] = A::fma(be[k], lI, lM);
           lM = M[k];
           lI = I[k];
         }
