@@ -254,7 +254,7 @@ int score_chunks() {                          // phmm_score pipelining depth (PH
   static int v = -1;
   if (v < 0) {
     const char* env = getenv("PHMM_CHUNKS");
-    v = env ? std::max(1, std::min(kMaxScoreChunks, atoi(env))) : 4;
+    v = env ? std::max(1, std::min(kMaxScoreChunks, atoi(env))) : 3;
   }
   return v;
 }
