@@ -1198,42 +1198,71 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
       const int cA = code & 7, cB = (code >> 8) & 7;
       const EV* EA = Et + (cA * KE) * P + t;
       const EV* EB = Et + (cB * KE) * P + t;
-      // pass 1 (descending): D from the previous row, M from the previous-row diagonal
-#pragma unroll
-      for (int ke = KE - 1; ke >= 0; --ke) {
-        const EV la = EA[ke * P];
-        const EV lb = EB[ke * P];
-#pragma unroll
-        for (int kk = EW - 1; kk >= 0; --kk) {
-          const int k = ke * EW + kk;
-          const V pm = (k > 0) ? M[k - 1] : dgM;
-          const V pi = (k > 0) ? I[k - 1] : dgI;
-          const V pd = (k > 0) ? D[k - 1] : dgD;
-          if constexpr (EXACT) {
-            // D = zt*M(i,j-1) + ep*D(i,j-1); M = lam*(al*M + be*(I + D)) (reference.py:111-113)
-            D[k] = flush2(A::xadd(A::xmul(zt[k], M[k]), A::xmul(ep[k], D[k])), thr);
-            V x = A::xadd(A::xmul(al[k], pm), A::xmul(be[k], A::xadd(pi, pd)));
-            x.x = A::mul1(ev_comp(la, kk), x.x);
-            x.y = A::mul1(ev_comp(lb, kk), x.y);
-            M[k] = flush2(x, thr);
-          } else {
-            D[k] = A::fma(ep[k], D[k], M[k]);
-            V x = A::fma(dl[k], pi, pm);
-            x = A::fma(zt[k], pd, x);
-            M[k].x = ev_comp(la, kk) * x.x;
-            M[k].y = ev_comp(lb, kk) * x.y;
-          }
-        }
-      }
-      // pass 2 (ascending): I chain along the read within the current row
-      {
+      // fast FP32 at occupancy 2 (K = 14, 16) has the registers for the carried values
+      constexpr bool FUSED = !EXACT && !F64 && K >= 14;
+      if constexpr (FUSED) {
+        // one ascending pass: position k's D'', M~ and I'' from position k's and k-1's
+        // previous-step values (carried in pmo/pio/pdo) and k-1's new M~, I'' -- step s+1
+        // at position k needs only step s up to k, so consecutive steps overlap
+        V pmo = dgM, pio = dgI, pdo = dgD;
         V lM = nbM, lI = nbI;
 #pragma unroll
-        for (int k = 0; k < K; ++k) {
-          if constexpr (EXACT) I[k] = flush2(A::xadd(A::xmul(dl[k], lM), A::xmul(ep[k], lI)), thr);
-          else I[k] = A::fma(be[k], lI, lM);
-          lM = M[k];
-          lI = I[k];
+        for (int ke = 0; ke < KE; ++ke) {
+          const EV la = EA[ke * P];
+          const EV lb = EB[ke * P];
+#pragma unroll
+          for (int kk = 0; kk < EW; ++kk) {
+            const int k = ke * EW + kk;
+            const V mo = M[k], io = I[k], dold = D[k];
+            D[k] = A::fma(ep[k], dold, mo);
+            V x = A::fma(dl[k], pio, pmo);
+            x = A::fma(zt[k], pdo, x);
+            M[k].x = ev_comp(la, kk) * x.x;
+            M[k].y = ev_comp(lb, kk) * x.y;
+            I[k] = A::fma(be[k], lI, lM);
+            lM = M[k];
+            lI = I[k];
+            pmo = mo; pio = io; pdo = dold;
+          }
+        }
+      } else {
+        // pass 1 (descending): D from the previous row, M from the previous-row diagonal
+#pragma unroll
+        for (int ke = KE - 1; ke >= 0; --ke) {
+          const EV la = EA[ke * P];
+          const EV lb = EB[ke * P];
+#pragma unroll
+          for (int kk = EW - 1; kk >= 0; --kk) {
+            const int k = ke * EW + kk;
+            const V pm = (k > 0) ? M[k - 1] : dgM;
+            const V pi = (k > 0) ? I[k - 1] : dgI;
+            const V pd = (k > 0) ? D[k - 1] : dgD;
+            if constexpr (EXACT) {
+              // D = zt*M(i,j-1) + ep*D(i,j-1); M = lam*(al*M + be*(I + D)) (reference.py:111-113)
+              D[k] = flush2(A::xadd(A::xmul(zt[k], M[k]), A::xmul(ep[k], D[k])), thr);
+              V x = A::xadd(A::xmul(al[k], pm), A::xmul(be[k], A::xadd(pi, pd)));
+              x.x = A::mul1(ev_comp(la, kk), x.x);
+              x.y = A::mul1(ev_comp(lb, kk), x.y);
+              M[k] = flush2(x, thr);
+            } else {
+              D[k] = A::fma(ep[k], D[k], M[k]);
+              V x = A::fma(dl[k], pi, pm);
+              x = A::fma(zt[k], pd, x);
+              M[k].x = ev_comp(la, kk) * x.x;
+              M[k].y = ev_comp(lb, kk) * x.y;
+            }
+          }
+        }
+        // pass 2 (ascending): I chain along the read within the current row
+        {
+          V lM = nbM, lI = nbI;
+#pragma unroll
+          for (int k = 0; k < K; ++k) {
+            if constexpr (EXACT) I[k] = flush2(A::xadd(A::xmul(dl[k], lM), A::xmul(ep[k], lI)), thr);
+            else I[k] = A::fma(be[k], lI, lM);
+            lM = M[k];
+            lI = I[k];
+          }
         }
       }
       if (to_col) {
