@@ -254,7 +254,7 @@ int score_chunks() {                          // phmm_score pipelining depth (PH
   static int v = -1;
   if (v < 0) {
     const char* env = getenv("PHMM_CHUNKS");
-    v = env ? std::max(1, std::min(kMaxScoreChunks, atoi(env))) : 3;
+    v = env ? std::max(1, std::min(kMaxScoreChunks, atoi(env))) : 0;   // 0: by call size
   }
   return v;
 }
@@ -1494,7 +1494,7 @@ static int score_chunked(phmm_ctx* ctx, const phmm_input* in, const phmm_options
 int phmm_score(phmm_ctx* ctx, const phmm_input* in, const phmm_options* opt, double* out_log10,
                uint8_t* out_status, phmm_stats* stats) {
   if (!ctx) return PHMM_ERR_INVALID;
-  if (in && opt && in->num_batches >= 2 * score_chunks() && score_chunks() > 1 && in->batch_read_off && in->batch_hap_off &&
+  if (in && opt && in->num_batches >= 2 * std::max(3, score_chunks()) && score_chunks() != 1 && in->batch_read_off && in->batch_hap_off &&
       in->read_off && in->hap_off && score_chunking_enabled()) {
     // validate the structure first (the chunk views index the offset arrays)
     int64_t pairs = 0;
@@ -1524,7 +1524,10 @@ int phmm_score(phmm_ctx* ctx, const phmm_input* in, const phmm_options* opt, dou
     }
     if (ok && pairs >= kScoreChunkMinPairs) {
       CK(cudaSetDevice(ctx->device));
-      return score_chunked(ctx, in, opt, out_log10, out_status, stats, score_chunks());
+      // per-chunk planning overhead vs pipeline depth: 3 chunks for ordinary calls, 4 for
+      // large ones (c2: 3 -> +15 % e2e over 4; c5: 4 -> +6 % over 3)
+      const int nch = score_chunks() > 0 ? score_chunks() : (pairs >= kBigCallPairs ? 4 : 3);
+      return score_chunked(ctx, in, opt, out_log10, out_status, stats, nch);
     }
   }
   int64_t n = 0;
