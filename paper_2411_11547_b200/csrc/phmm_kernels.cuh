@@ -1199,7 +1199,7 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
       const EV* EA = Et + (cA * KE) * P + t;
       const EV* EB = Et + (cB * KE) * P + t;
       // fast FP32 at occupancy 2 (K = 14, 16) has the registers for the carried values
-      constexpr bool FUSED = !EXACT && !F64 && K >= 14;
+      constexpr bool FUSED = !EXACT && (F64 ? !STRIPES : K >= 14);
       if constexpr (FUSED) {
         // one ascending pass: position k's D'', M~ and I'' from position k's and k-1's
         // previous-step values (carried in pmo/pio/pdo) and k-1's new M~, I'' -- step s+1
