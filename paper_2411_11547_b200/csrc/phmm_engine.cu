@@ -128,8 +128,11 @@ void launch_stream_t(dim3 g, size_t smem, cudaStream_t s, const EngineDev& E, co
 template <int MODE, int P, int K, bool STRIPES = false>
 StreamKernel SK() {
   const size_t elem = ModeOf<MODE>::F64 ? sizeof(double) : sizeof(float);   // 5*K*P entries per slot
+  // striped instantiations add the boundary-column ring: per sub-warp slot 3 x kColRing
+  // two-lane values
   return StreamKernel{P, K, StreamOcc<MODE, K>::value,
-                      96 * sizeof(double) + (size_t)4 * (32 / P) * 5 * K * P * elem + kStreamCodeBytesPerCta,
+                      96 * sizeof(double) + (size_t)4 * (32 / P) * 5 * K * P * elem + kStreamCodeBytesPerCta +
+                          (STRIPES ? (size_t)4 * (32 / P) * 3 * kColRing * 2 * elem : 0),
                       (const void*)k_stream<MODE, P, K, STRIPES>, launch_stream_t<MODE, P, K, STRIPES>};
 }
 // kFast32: the k_fast tiling table (same order as kFastGeoms, so PHMM_FAST_GEOM applies),

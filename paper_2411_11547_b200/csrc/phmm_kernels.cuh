@@ -848,6 +848,15 @@ __device__ __forceinline__ void emit_retry_units(const StreamUnit& U, const Stre
   emit();
 }
 
+// cp.async (global -> shared, no registers): the striped kernels' boundary-column ring
+template <int B> __device__ __forceinline__ void cp_async(unsigned dst, const void* src) {
+  if constexpr (B == 16) asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+  else asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(dst), "l"(src), "n"(B) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+constexpr int kColRing = 64;      // rows of a striped sub-warp's boundary-column ring (x3 states)
+
 template <int MODE, int P, int K, bool STRIPES = false>
 __global__ void __launch_bounds__(128, (StreamOcc<MODE, K>::value))
 k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHap* __restrict__ shaps,
@@ -1083,12 +1092,25 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
     // stripe q > 0: thread 0's left neighbour is the previous stripe's column
     V* colPrev = (q & 1) ? colY : colX;
     V* colNext = (q & 1) ? colX : colY;
-    const bool from_col = STRIPES && q > 0 && t == 0 && sq;
+    const bool col_in = STRIPES && q > 0 && sq;        // uniform over the sub-warp
+    const bool from_col = col_in && t == 0;
     const bool to_col = STRIPES && !lastq && t == P - 1 && sq;
-    V cpM = zero2, cpI = zero2, cpD = zero2;            // column prefetch (row s + 1)
-    if (from_col && rows_q >= 1) {
-      cpM = colPrev[1]; cpI = colPrev[col_rows + 1]; cpD = colPrev[2 * col_rows + 1];
-    }
+    // The column reaches thread 0 through a shared-memory ring of kColRing rows (M, I, D)
+    // filled by the whole sub-warp with cp.async 32 rows ahead: an L2 round trip per step
+    // (one row ahead in a register) was the striped kernels' bound.  Rows r0 .. r0+31 are
+    // requested at step r0 - 32 (r0 = 1 before the stream) and waited for at step r0.
+    V* ring = STRIPES ? reinterpret_cast<V*>(s_code + kStreamCodeBytesPerCta) + (size_t)slot * 3 * kColRing : nullptr;
+    auto col_fill = [&](int r0) {
+      static_assert(!STRIPES || P == 32, "striped tilings are 32 threads wide");
+      const int r = min(r0 + t, col_rows - 1);
+      const unsigned dst = (unsigned)__cvta_generic_to_shared(ring + ((r0 + t) & (kColRing - 1)));
+      cp_async<sizeof(V)>(dst, colPrev + r);
+      cp_async<sizeof(V)>(dst + kColRing * sizeof(V), colPrev + col_rows + r);
+      cp_async<sizeof(V)>(dst + 2 * kColRing * sizeof(V), colPrev + 2 * col_rows + r);
+      cp_async_commit();
+    };
+    if constexpr (STRIPES)
+      if (col_in) col_fill(1);
 
     // FIRST(lane L): reset the lane to row 0 of its next haplotype (event paths only run
     // inside windows and read their inputs from shared memory)
@@ -1180,11 +1202,16 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
         nbD.x = __shfl_up_sync(FULL, ld.x, 1, P);
         nbD.y = __shfl_up_sync(FULL, ld.y, 1, P);
       }
+      if constexpr (STRIPES)
+        if (col_in && (s & 31) == 1) {                  // rows s .. s+31 landed; request the next 32
+          cp_async_wait_all();
+          __syncwarp();
+          col_fill(s + 32);
+        }
       if (t == 0) {
         if (from_col) {
-          nbM = cpM; nbI = cpI; nbD = cpD;
-          const int jn = min(s + 1, col_rows - 1);
-          cpM = colPrev[jn]; cpI = colPrev[col_rows + jn]; cpD = colPrev[2 * col_rows + jn];
+          const int x = s & (kColRing - 1);
+          nbM = ring[x]; nbI = ring[kColRing + x]; nbD = ring[2 * kColRing + x];
         } else {
           nbM = zero2; nbI = zero2; nbD = cb;
         }
@@ -1306,6 +1333,7 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
         xM = yM; xI = yI; xD = yD;
       }
     }
+    if constexpr (STRIPES) cp_async_wait_all();      // the ring is refilled by the next stripe
     __syncwarp();
     }                                                   // stripes
     if constexpr (MODE == kFast32) {
