@@ -74,6 +74,7 @@ constexpr int kThreads = 128;
 // device-built stream lists (counts[8], hap count, overflow) and their work counters,
 // the validation flag (last slot), then one work counter per planned stream/legacy bin
 constexpr int kCtrR64 = 32, kCtrRX32 = 44, kCtrR64Work = 56, kCtrRX32Work = 64;
+constexpr int kCtrR64b = 72, kCtrR64bWork = 80;   // second-stage striped FP64 units: counts, work
 constexpr int kBinCounters = 96;
 constexpr int64_t kBigCallPairs = 1 << 20;   // device-built retry units grow above this          // fixed counter slots before the per-bin counters
 constexpr int kFinishThreads = 16;        // host threads finishing log10 in phmm_fetch
@@ -130,7 +131,7 @@ StreamKernel SK() {
   const size_t elem = ModeOf<MODE>::F64 ? sizeof(double) : sizeof(float);   // 5*K*P entries per slot
   // striped instantiations add the boundary-column ring: per sub-warp slot 3 x kColRing
   // two-lane values
-  return StreamKernel{P, K, StreamOcc<MODE, K>::value,
+  return StreamKernel{P, K, STRIPES ? 2 : StreamOcc<MODE, K>::value,
                       96 * sizeof(double) + (size_t)4 * (32 / P) * 5 * K * P * elem + kStreamCodeBytesPerCta +
                           (STRIPES ? (size_t)4 * (32 / P) * 3 * kColRing * 2 * elem : 0),
                       (const void*)k_stream<MODE, P, K, STRIPES>, launch_stream_t<MODE, P, K, STRIPES>};
@@ -160,7 +161,7 @@ const StreamKernel* const kStreamTab[4] = {kStreamFast32, kStreamFast64, kStream
 // reads longer than every tiling stripe over the widest one of their mode, in a separate
 // instantiation (the column hand-off costs registers the single-stripe kernels keep)
 const StreamKernel kStripedTab[4] = {SK<kFast32, 32, 16, true>(), SK<kFast64, 32, 8, true>(),
-                                     SK<kExact32, 32, 16, true>(), SK<kExact64, 32, 8, true>()};
+                                     SK<kExact32, 32, 8, true>(), SK<kExact64, 32, 8, true>()};
 const int kStripedGeom[4] = {12, kNumR64Geoms - 1, kNumRX32Geoms - 1, kNumR64Geoms - 1};
 const int kStreamTabN[4] = {kNumStreamFast32, kNumR64Geoms, kNumRX32Geoms, kNumR64Geoms};
 constexpr int kMaxTilings = 24;
@@ -1005,7 +1006,8 @@ static int prepare_impl(phmm_ctx* ctx, const phmm_input* in, const phmm_options*
   if (!r64) ctx->r64_geoms = 0;
   if (!rx32) ctx->rx32_geoms = 0;
   for (int g = 0; g < kNumR64Geoms; ++g)
-    if (ctx->r64_geoms & (1u << g)) CK(ctx->d_r64u[g].ensure(r64_pairs[g]));
+    if (ctx->r64_geoms & (1u << g))   // widest tiling, long reads: a second region (r64b)
+      CK(ctx->d_r64u[g].ensure(r64_pairs[g] * (g == kNumR64Geoms - 1 && long64 && rx32 ? 2 : 1)));
   for (int g = 0; g < kNumRX32Geoms; ++g)
     if (ctx->rx32_geoms & (1u << g)) CK(ctx->d_rx32u[g].ensure(rx32_pairs[g]));
   if (r64) CK(ctx->d_r64h.ensure(streamed));
@@ -1047,6 +1049,18 @@ static int prepare_impl(phmm_ctx* ctx, const phmm_input* in, const phmm_options*
   };
   lists(E.r64, ctx->d_r64u, kNumR64Geoms, ctx->d_r64h, ctx->r64_geoms, kCtrR64, r64_pairs);
   lists(E.rx32, ctx->d_rx32u, kNumRX32Geoms, ctx->d_rx32h, ctx->rx32_geoms, kCtrRX32, rx32_pairs);
+  // second stage for long reads: guard-band pairs whose striped exact rerun underflows get
+  // striped FP64 units in the upper half of the widest FP64 list (haplotype entries share
+  // the first stage's array), run after the post-pass instead of the per-pair kernel
+  {
+    const int g = kNumR64Geoms - 1;
+    E.r64b = E.r64;
+    for (int x = 0; x < 8; ++x) E.r64b.units[x] = nullptr;
+    E.r64b.count = ctx->d_counters.p + kCtrR64b;
+    E.r64b.lane_haps = 1;
+    E.r64b.enabled = (r64 && rx32 && long64 && (ctx->r64_geoms & (1u << g))) ? 1 : 0;
+    if (E.r64b.enabled) E.r64b.units[g] = ctx->d_r64u[g].p + r64_pairs[g];
+  }
   // grids of the stream launches, and boundary-column space for the ones that can meet
   // striped units (reads longer than the tiling width): per sub-warp slot 2 columns x
   // 3 states x (row capacity + 1) two-lane values
@@ -1060,8 +1074,10 @@ static int prepare_impl(phmm_ctx* ctx, const phmm_input* in, const phmm_options*
       const StreamKernel& K = skern(sb.mode, sb.geom);
       const int G = 32 / K.P;
       const int64_t groups = (sb.count + G - 1) / G;
-      sb.grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)ctx->num_sms * K.occ, (groups + 3) / 4));
       const bool striped = (sb.geom & kStripedBin) != 0;
+      // striped bins with few units run in team mode (a CTA per unit): one CTA per unit
+      const int64_t want = striped && groups * 2 <= (int64_t)ctx->num_sms * K.occ * 4 ? groups : (groups + 3) / 4;
+      sb.grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)ctx->num_sms * K.occ, want));
       sb.col_off = striped ? col_total : -1;
       if (striped) col_total += col_bytes(sb.mode, K, sb.grid);
     }
@@ -1070,14 +1086,14 @@ static int prepare_impl(phmm_ctx* ctx, const phmm_input* in, const phmm_options*
       const int g = kNumR64Geoms - 1;
       if (ctx->r64_geoms & (1u << g)) {
         ctx->r64_col_off[g] = col_total;
-        col_total += col_bytes(kFast64, kStreamFast64[g], ctx->num_sms * kStreamFast64[g].occ);
+        col_total += col_bytes(kFast64, kStripedTab[kFast64], ctx->num_sms * kStripedTab[kFast64].occ);
       }
     }
     if (long32) {                                   // reads > 511: exact FP32 stripes
       const int g = kNumRX32Geoms - 1;
       if (ctx->rx32_geoms & (1u << g)) {
         ctx->rx32_col_off[g] = col_total;
-        col_total += col_bytes(kExact32, kStreamExact32[g], ctx->num_sms * kStreamExact32[g].occ);
+        col_total += col_bytes(kExact32, kStripedTab[kExact32], ctx->num_sms * kStripedTab[kExact32].occ);
       }
     }
     if (col_total > 0) CK(ctx->d_colstream.ensure(col_total));
@@ -1214,6 +1230,14 @@ int phmm_execute(phmm_ctx* ctx) {
       post(ctx->rx32_col_off[g] >= 0 ? kStripedTab[kExact32] : kStreamExact32[g], E.rx32, g,
            ctx->d_counters.p + kCtrRX32Work + g, ctx->rx32_col_off[g]);
   CK(join());
+  if (E.r64b.enabled) {                 // long reads: band pairs whose exact rerun underflowed
+    const int g = kNumR64Geoms - 1;
+    const StreamKernel& SKn = kStripedTab[kFast64];
+    SKn.launch(dim3(ctx->num_sms * SKn.occ), SKn.smem, st, E, E.r64b.units[g], E.r64b.haps, E.r64b.unit_cap[g],
+               E.r64b.count + g, ctx->d_counters.p + kCtrR64bWork + g, ctx->d_colstream.p + ctx->r64_col_off[g],
+               col_rows_for(SKn.P));
+    ++launches;
+  }
   if (ctx->flags & PHMM_FLAG_RETRY_F64) {
     k_fast64_all<<<ctx->num_sms * 2, kThreads, exact_smem(0, 8), st>>>(E, ctx->d_counters.p + 24, ctx->d_cold.p,
                                                                       ctx->max_n + 1);

@@ -90,6 +90,9 @@ struct EngineDev {
   const int* invalid;                     // device input validation verdict: nonzero = skip
   RetryLists r64;                         // FP64 retry units (built by the FP32 stream kernel)
   RetryLists rx32;                        // bit-exact FP32 guard-band units (same)
+  RetryLists r64b;                        // long reads: FP64 retries of guard-band pairs whose
+                                          // exact rerun underflowed (built by the exact stream
+                                          // kernel, run after the post-pass)
 };
 
 __device__ __forceinline__ int exact_slot_for(int m) {
@@ -858,7 +861,7 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 constexpr int kColRing = 64;      // rows of a striped sub-warp's boundary-column ring (x3 states)
 
 template <int MODE, int P, int K, bool STRIPES = false>
-__global__ void __launch_bounds__(128, (StreamOcc<MODE, K>::value))
+__global__ void __launch_bounds__(128, (STRIPES ? 2 : StreamOcc<MODE, K>::value))   // striped: <= 2
 k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHap* __restrict__ shaps,
          int num_units_arg, const int* __restrict__ num_units_dev, int* __restrict__ counter,
          void* __restrict__ colbuf_v, int col_rows) {
@@ -898,11 +901,27 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
   __shared__ unsigned s_band[4 * G * 2];          // kFast32: lane entries in the guard band
   __shared__ ExactItem s_inl[MODE == kFast32 ? 4 * G * kInlineBand : 1];
   __shared__ int s_ninl[4 * G];
+  // Striped tilings, few units (<= 2 per CTA, latency bound: c4 and the long-read retry
+  // lists): "team" mode -- the CTA's 4 warps share one unit, warp w running stripes
+  // w, w+4, ... concurrently; stripe q's column goes to stripe q+1 through one of 8
+  // per-CTA columns with a row-progress flag, so a unit takes ~(rows + Q x 64) steps
+  // instead of Q x rows.
+  __shared__ int s_team_unit;
+  __shared__ volatile int s_prog[STRIPES ? 8 : 1];
+  const bool team = STRIPES && num_units * 2 <= (int)gridDim.x * 4;
 
   for (;;) {
     int g = 0;
-    if (lane == 0) g = atomicAdd(counter, 1);
-    g = __shfl_sync(FULL, g, 0);
+    if (STRIPES && team) {
+      __syncthreads();                                  // every warp is done with the last unit
+      if (threadIdx.x == 0) s_team_unit = atomicAdd(counter, 1);
+      if (threadIdx.x < 8) s_prog[threadIdx.x] = 0;
+      __syncthreads();
+      g = s_team_unit;
+    } else {
+      if (lane == 0) g = atomicAdd(counter, 1);
+      g = __shfl_sync(FULL, g, 0);
+    }
     if (g * G >= num_units) break;
     const int u = g * G + sw;
     const bool has = u < num_units;
@@ -913,7 +932,7 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
     const bool live = has && !degen;
     const int rows = live ? max(U.rowsA, U.rowsB) : 0;
     const int steps = __reduce_max_sync(FULL, rows) + P - 1;
-    if (has && degen) {
+    if (has && degen && !(team && wib > 0)) {
       for (int e = t; e < U.cntA + U.cntB; e += P) {
         const int pr = shaps[U.list + e].pair;
         E.acc[pr] = 0.0; E.status[pr] = kStatusDegenerate;
@@ -927,8 +946,8 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
     const int Lp = Q * W - m - 1;
     V* colX = nullptr;
     V* colY = nullptr;
-    if (STRIPES && Qw > 1) {
-      const size_t gslot = ((size_t)blockIdx.x * 4 + wib) * G + sw;
+    if (STRIPES && Qw > 1) {                            // team mode: the CTA's 8 columns
+      const size_t gslot = ((size_t)blockIdx.x * 4 + (team ? 0 : wib)) * G + sw;
       colX = reinterpret_cast<V*>(colbuf_v) + gslot * 6 * (size_t)col_rows;
       colY = colX + 3 * (size_t)col_rows;
     }
@@ -939,8 +958,9 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
       s_ninl[slot] = 0;
     }
 #pragma unroll 1
-    for (int q = 0; q < Qw; ++q) {
+    for (int q = team ? wib : 0; q < Qw; q += team ? 4 : 1) {
     const bool sq = live && q < Q;                      // this sub-warp has stripe q
+    const bool first_q = q == (team ? wib : 0);         // this warp's first stripe of the unit
     const bool lastq = q == Q - 1;
     const int rows_q = sq ? rows : 0;
 
@@ -1024,7 +1044,7 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
     // unit's window starts: every row where a haplotype begins in either lane, plus the
     // row after each lane's end.  Events (FIRST for thread t at step b + t, LAST for
     // thread P-1 at step b + P - 2) fall in windows [b, b + P).  Built once per unit.
-    if (q == 0) {
+    if (first_q) {
     if (t == 0) reinterpret_cast<unsigned short*>(cd)[0] = 0x0404;
     if (live) {
 #pragma unroll 1
@@ -1071,7 +1091,7 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
     } else if (t == 0) {
       s_nwin[slot] = 0;
     }
-    }                                                   // q == 0
+    }                                                   // first_q
     s_hc[2 * threadIdx.x] = -1;                         // current haplotype per lane
     s_hc[2 * threadIdx.x + 1] = -1;
     __syncwarp();
@@ -1090,8 +1110,8 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
     unsigned code = 0x0404u;
     unsigned pf1 = ld_code(1);
     // stripe q > 0: thread 0's left neighbour is the previous stripe's column
-    V* colPrev = (q & 1) ? colY : colX;
-    V* colNext = (q & 1) ? colX : colY;
+    V* colPrev = team ? colX + (size_t)((q - 1) & 7) * 3 * col_rows : (q & 1) ? colY : colX;
+    V* colNext = team ? colX + (size_t)(q & 7) * 3 * col_rows : (q & 1) ? colX : colY;
     const bool col_in = STRIPES && q > 0 && sq;        // uniform over the sub-warp
     const bool from_col = col_in && t == 0;
     const bool to_col = STRIPES && !lastq && t == P - 1 && sq;
@@ -1102,6 +1122,15 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
     V* ring = STRIPES ? reinterpret_cast<V*>(s_code + kStreamCodeBytesPerCta) + (size_t)slot * 3 * kColRing : nullptr;
     auto col_fill = [&](int r0) {
       static_assert(!STRIPES || P == 32, "striped tilings are 32 threads wide");
+      if (team) {                                       // the rows must be written already
+        // flags carry (writing stripe) << 16 | rows: a column reused by stripe q + 8 never
+        // looks complete to stripe q + 9 early
+        const int need = ((q - 1) << 16) | min(r0 + 31, rows_q);
+        if (t == 0)
+          while (s_prog[(q - 1) & 7] < need) __nanosleep(64);
+        __threadfence_block();
+        __syncwarp();
+      }
       const int r = min(r0 + t, col_rows - 1);
       const unsigned dst = (unsigned)__cvta_generic_to_shared(ring + ((r0 + t) & (kColRing - 1)));
       cp_async<sizeof(V)>(dst, colPrev + r);
@@ -1158,7 +1187,8 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
         const bool bad = !(res > 0.f) || !isfinite(res);
         if (bad && E.retry_f64) {
           E.status[sh.pair] = kStatusRetriedF64;
-          append_item(E.fx64, E.fx64_count, E.list_cap, exact_slot_for(mm), ExactItem{sh.pair, SU.read, sh.hap, 0});
+          if (STRIPES && E.r64b.enabled) s_flag[2 * slot + L] |= 1u << hc;   // -> striped FP64 unit
+          else append_item(E.fx64, E.fx64_count, E.list_cap, exact_slot_for(mm), ExactItem{sh.pair, SU.read, sh.hap, 0});
         } else {
           E.acc[sh.pair] = (double)res;
           E.status[sh.pair] = bad ? kStatusOverflow : kStatusExactF32;
@@ -1296,6 +1326,10 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
         const int j = s - (P - 1);
         if (j >= 1 && j <= rows_q) {
           colNext[j] = M[K - 1]; colNext[col_rows + j] = I[K - 1]; colNext[2 * col_rows + j] = D[K - 1];
+          if (team && ((j & 31) == 0 || j == rows_q)) {   // publish the rows written so far
+            __threadfence();
+            s_prog[q & 7] = (q << 16) | j;
+          }
         }
       }
       if (CHECK && lastq && (code & ((kCodeLast << 8) | kCodeLast)) && t == P - 1) {
@@ -1336,6 +1370,11 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
     if constexpr (STRIPES) cp_async_wait_all();      // the ring is refilled by the next stripe
     __syncwarp();
     }                                                   // stripes
+    if constexpr (MODE == kExact32 && STRIPES) {
+      // long reads: guard-band pairs whose exact rerun underflowed -> striped FP64 units
+      if (t == 0 && live && (s_flag[2 * slot] | s_flag[2 * slot + 1]))
+        emit_retry_units(U, shaps, s_flag + 2 * slot, E.r64b, kNumR64Geoms - 1, stream_cap_of(32), m, 1);
+    }
     if constexpr (MODE == kFast32) {
       // this unit's FP32-underflowed and guard-band pairs -> device-built stream units
       if (t == 0 && live) {
