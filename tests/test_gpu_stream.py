@@ -122,6 +122,22 @@ def test_every_tiling_width(engine, rng):
     _check(engine, flat)
 
 
+def test_long_reads_striped_team_and_sequential_modes(engine, rng):
+    # reads past every single-stripe width (FP32 511, FP64 255, exact 511): a few units run
+    # in team mode (a CTA's warps on one unit's stripes, column progress flags), many in
+    # sequential mode; 'random' long pairs underflow (striped FP64 retries), 'derived'
+    # ones land in the guard band (striped exact reruns, second-stage FP64)
+    few = _flat(rng, [([1023, 700, 513], [1024, 1500, 37, 2000], "random"),
+                      ([600, 900], [800, 1200, 5], "derived"),
+                      ([1000], [2047, 1], "degenerate")])
+    k32 = _check(engine, few)
+    assert (k32 == 1).any() and (k32 == 0).any()
+    many = _flat(rng, [([int(m) for m in rng.integers(512, 1024, size=6)],
+                        [int(n) for n in rng.integers(100, 1600, size=5)], mode)
+                       for mode in ["random", "derived"] * 24])
+    _check(engine, many)
+
+
 def test_partial_underflow_units_and_degenerate_reads(engine, rng):
     # 'random' reads underflow against long haplotypes but not short ones: FP64 retry
     # units hold a subset of each lane; degenerate reads share batches with normal ones
