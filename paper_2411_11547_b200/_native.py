@@ -158,12 +158,18 @@ class Context:
                 raise DataError(msg)
             raise EngineError("libphmm error %d: %s" % (rc, msg))
 
-    def score(self, flat, configs, flags=0):
+    def score(self, flat, configs, flags=0, out=None, status=None):
+        """phmm_score; ``out`` (float64[N]) / ``status`` (uint8[N]) are caller-owned result
+        buffers (reused across calls by a C-ABI caller), allocated when omitted."""
         cin, keep1 = make_input(flat)
         copt, keep2 = make_options(configs, flags)
         n = flat.num_pairs
-        out = np.empty(n, np.float64)
-        st = np.empty(n, np.uint8)
+        out = np.empty(n, np.float64) if out is None else out
+        st = np.empty(n, np.uint8) if status is None else status
+        if out.shape != (n,) or out.dtype != np.float64 or not out.flags.c_contiguous:
+            raise ValueError("out must be a contiguous float64 array of %d pairs" % n)
+        if st.shape != (n,) or st.dtype != np.uint8 or not st.flags.c_contiguous:
+            raise ValueError("status must be a contiguous uint8 array of %d pairs" % n)
         stats = PhmmStats()
         self._check(self._L.phmm_score(self._h, ctypes.byref(cin), ctypes.byref(copt), _ptr(out),
                                        _ptr(st), ctypes.byref(stats)))
