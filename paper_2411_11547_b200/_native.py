@@ -10,6 +10,7 @@ from __future__ import annotations
 
 import ctypes
 import os
+import threading
 
 import numpy as np
 
@@ -133,10 +134,15 @@ def fast_geometry(m: int, n: int):
 
 
 class Context:
-    """One libphmm context bound to one CUDA device."""
+    """One libphmm context bound to one CUDA device.
+
+    The C context is single-caller (include/phmm.h); ctypes releases the GIL, so every
+    entry point here takes the context's lock: concurrent callers of one Context (e.g.
+    two threads calling run()) are serialized instead of racing on device buffers."""
 
     def __init__(self, device: int = 0, lut=None):
         from .prob import PHRED_TO_PROB
+        self._lock = threading.RLock()
         L = load()
         self._lut = np.ascontiguousarray(PHRED_TO_PROB if lut is None else lut, dtype=np.float64)
         h = _vp()
@@ -171,38 +177,47 @@ class Context:
         if st.shape != (n,) or st.dtype != np.uint8 or not st.flags.c_contiguous:
             raise ValueError("status must be a contiguous uint8 array of %d pairs" % n)
         stats = PhmmStats()
-        self._check(self._L.phmm_score(self._h, ctypes.byref(cin), ctypes.byref(copt), _ptr(out),
-                                       _ptr(st), ctypes.byref(stats)))
+        with self._lock:
+            self._check(self._L.phmm_score(self._h, ctypes.byref(cin), ctypes.byref(copt), _ptr(out),
+                                           _ptr(st), ctypes.byref(stats)))
         return out, st, stats
 
     def prepare(self, flat, configs, flags=0) -> int:
         cin, keep1 = make_input(flat)
         copt, keep2 = make_options(configs, flags)
         n = _i64()
-        self._check(self._L.phmm_prepare(self._h, ctypes.byref(cin), ctypes.byref(copt), ctypes.byref(n)))
-        self._n = n.value
+        with self._lock:
+            self._check(self._L.phmm_prepare(self._h, ctypes.byref(cin), ctypes.byref(copt), ctypes.byref(n)))
+            self._n = n.value
         return n.value
 
     def execute(self):
-        self._check(self._L.phmm_execute(self._h))
+        with self._lock:
+            self._check(self._L.phmm_execute(self._h))
 
     def last_timing(self):
         """(device_ms, fast_ms, launches) of the last execute (CUDA events, engine stream)."""
         d, f, n = ctypes.c_double(), ctypes.c_double(), ctypes.c_int()
-        self._L.phmm_last_timing(self._h, ctypes.byref(d), ctypes.byref(f), ctypes.byref(n))
+        with self._lock:
+            self._L.phmm_last_timing(self._h, ctypes.byref(d), ctypes.byref(f), ctypes.byref(n))
         return d.value, f.value, n.value
 
     def fetch(self):
-        out = np.empty(self._n, np.float64)
-        st = np.empty(self._n, np.uint8)
-        stats = PhmmStats()
-        self._check(self._L.phmm_fetch(self._h, _ptr(out), _ptr(st), ctypes.byref(stats)))
+        with self._lock:
+            out = np.empty(self._n, np.float64)
+            st = np.empty(self._n, np.uint8)
+            stats = PhmmStats()
+            self._check(self._L.phmm_fetch(self._h, _ptr(out), _ptr(st), ctypes.byref(stats)))
         return out, st, stats
 
     def close(self):
-        if self._h is not None:
-            self._L.phmm_destroy(self._h)
-            self._h = None
+        lock = getattr(self, "_lock", None)
+        if lock is None:
+            return
+        with lock:
+            if self._h is not None:
+                self._L.phmm_destroy(self._h)
+                self._h = None
 
     def __del__(self):
         try:
@@ -212,12 +227,15 @@ class Context:
 
 
 _contexts = {}
+_contexts_lock = threading.Lock()
 
 
 def context(device: int = 0) -> Context:
-    """Process-wide cached context per device."""
-    ctx = _contexts.get(device)
-    if ctx is None:
-        ctx = Context(device)
-        _contexts[device] = ctx
-    return ctx
+    """Process-wide cached context per device (created once under a module lock; its calls
+    are serialized by the context's own lock)."""
+    with _contexts_lock:
+        ctx = _contexts.get(device)
+        if ctx is None:
+            ctx = Context(device)
+            _contexts[device] = ctx
+        return ctx

@@ -1,33 +1,67 @@
 """Build libphmm.so in-tree for sm_100a (nvcc, no JIT cache): the built library
-travels with the repo snapshot to the GPU box."""
+travels with the repo snapshot to the GPU box.
+
+The library is several translation units (csrc/*.cu: the host engine, the small kernels,
+one file per stream-kernel mode) compiled in parallel to objects under _lib/obj and
+linked with nvcc -shared.  No relocatable device code: kernels are only launched from
+the translation unit that instantiates them (through the tables in phmm_registry.h)."""
 from __future__ import annotations
 
+import glob
 import os
 import subprocess
 import sys
+from concurrent.futures import ThreadPoolExecutor
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
-SOURCES = [os.path.join(HERE, "csrc", "phmm_engine.cu")]
-DEPS = SOURCES + [os.path.join(HERE, "csrc", "phmm_kernels.cuh"), os.path.join(ROOT, "include", "phmm.h")]
+CSRC = os.path.join(HERE, "csrc")
+SOURCES = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
+HEADERS = sorted(glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(CSRC, "*.cuh"))) + [
+    os.path.join(ROOT, "include", "phmm.h")]
 OUT = os.path.join(HERE, "_lib", "libphmm.so")
+OBJ = os.path.join(HERE, "_lib", "obj")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-         "-Xcompiler", "-fPIC", "-Xcompiler", "-pthread", "-shared", "-Xptxas", "-warn-spills"]
+         "-Xcompiler", "-fPIC", "-Xcompiler", "-pthread", "-Xptxas", "-warn-spills"]
+
+
+def _obj(src: str) -> str:
+    return os.path.join(OBJ, os.path.basename(src)[:-3] + ".o")
+
+
+def _stale(target: str, deps) -> bool:
+    if not os.path.exists(target):
+        return True
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(p) > t for p in deps)
 
 
 def up_to_date() -> bool:
-    if not os.path.exists(OUT):
-        return False
-    t = os.path.getmtime(OUT)
-    return all(os.path.getmtime(p) <= t for p in DEPS)
+    return not _stale(OUT, SOURCES + HEADERS)
 
 
 def build_native(force: bool = False, verbose: bool = False) -> str:
     if not force and up_to_date():
         return OUT
-    os.makedirs(os.path.dirname(OUT), exist_ok=True)
-    cmd = [NVCC] + FLAGS + ["-I", os.path.join(ROOT, "include"), "-o", OUT + ".tmp"] + SOURCES
+    os.makedirs(OBJ, exist_ok=True)
+    inc = ["-I", os.path.join(ROOT, "include")]
+
+    def compile_one(src):
+        obj = _obj(src)
+        if not force and not _stale(obj, [src] + HEADERS):
+            return obj
+        cmd = [NVCC] + FLAGS + inc + ["-c", "-o", obj + ".tmp", src]
+        if verbose:
+            print(" ".join(cmd), file=sys.stderr)
+        subprocess.run(cmd, check=True)
+        os.replace(obj + ".tmp", obj)
+        return obj
+
+    with ThreadPoolExecutor(max_workers=max(1, min(len(SOURCES), os.cpu_count() or 1))) as ex:
+        objs = list(ex.map(compile_one, SOURCES))
+    cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-Xcompiler", "-pthread",
+           "-o", OUT + ".tmp"] + objs
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.run(cmd, check=True)

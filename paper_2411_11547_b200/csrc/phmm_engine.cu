@@ -21,7 +21,7 @@
 #include <vector>
 
 #include "../../include/phmm.h"
-#include "phmm_kernels.cuh"
+#include "phmm_registry.h"
 
 using namespace phmm;
 
@@ -62,128 +62,46 @@ struct PinnedAlloc {
 };
 template <class T> using PinnedVec = std::vector<T, PinnedAlloc<T>>;
 
-struct FastGeom { int P, K; };
-// single-stripe widths W = P*K: 16 32 48 64 64 96 128 128 192 256 256 384 512
-const FastGeom kFastGeoms[] = {{4, 4},  {4, 8},   {4, 12},  {4, 16},  {8, 8},   {8, 12}, {8, 16},
-                               {16, 8}, {16, 12}, {16, 16}, {32, 8},  {32, 12}, {32, 16}};
-constexpr int kNumFastGeoms = sizeof(kFastGeoms) / sizeof(kFastGeoms[0]);
-constexpr int kExactP[kNumExactP] = {4, 8, 16, 32};
-constexpr int kThreads = 128;
-// device counters: [0,4) ex32 counts, [4,8) ex64 counts, [8,12) ex32 work, [12,16) ex64
-// work, 16 inline guard-band pairs, [20,24) fx64 counts, [24,28) fx64 work, then the two
-// device-built stream lists (counts[8], hap count, overflow) and their work counters,
-// the validation flag (last slot), then one work counter per planned stream/legacy bin
-constexpr int kCtrR64 = 32, kCtrRX32 = 44, kCtrR64Work = 56, kCtrRX32Work = 64;
-constexpr int kCtrR64b = 72, kCtrR64bWork = 80;   // second-stage striped FP64 units: counts, work
-constexpr int kBinCounters = 96;
-constexpr int64_t kBigCallPairs = 1 << 20;   // device-built retry units grow above this          // fixed counter slots before the per-bin counters
-constexpr int kFinishThreads = 16;        // host threads finishing log10 in phmm_fetch
-
-struct Bin {
-  int geom, Q;
-  std::vector<FastUnit> units;
-  int64_t dev_off = 0;     // offset into the device unit array
-};
-
-// fast-kernel launcher table: single-stripe and multi-stripe variant per geometry
-template <int P, int K>
-void launch_fast(dim3 g, size_t smem, cudaStream_t s, const EngineDev& E, const FastUnit* u, int nu,
-                 int Q, int* ctr, float2* col, int rows) {
-  if (Q > 1)
-    k_fast<P, K, true><<<g, kThreads, smem, s>>>(E, u, nu, Q, ctr, col, rows);
-  else
-    k_fast<P, K, false><<<g, kThreads, smem, s>>>(E, u, nu, Q, ctr, col, rows);
-}
-typedef void (*FastLaunch)(dim3, size_t, cudaStream_t, const EngineDev&, const FastUnit*, int, int,
-                           int*, float2*, int);
-const FastLaunch kFastLaunch[kNumFastGeoms] = {
-    launch_fast<4, 4>,  launch_fast<4, 8>,   launch_fast<4, 12>,  launch_fast<4, 16>, launch_fast<8, 8>,
-    launch_fast<8, 12>, launch_fast<8, 16>,  launch_fast<16, 8>,  launch_fast<16, 12>,
-    launch_fast<16, 16>, launch_fast<32, 8>, launch_fast<32, 12>, launch_fast<32, 16>};
-const int kFastOcc[kNumFastGeoms] = {FastOcc<4>::value,  FastOcc<8>::value,  FastOcc<12>::value,
-                                     FastOcc<16>::value, FastOcc<8>::value,  FastOcc<12>::value,
-                                     FastOcc<16>::value, FastOcc<8>::value,  FastOcc<12>::value,
-                                     FastOcc<16>::value, FastOcc<8>::value,  FastOcc<12>::value,
-                                     FastOcc<16>::value};
-#define FASTFN(P, K) (const void*)k_fast<P, K, false>, (const void*)k_fast<P, K, true>
-const void* kFastFn[2 * kNumFastGeoms] = {FASTFN(4, 4),   FASTFN(4, 8),   FASTFN(4, 12), FASTFN(4, 16),
-                                          FASTFN(8, 8),   FASTFN(8, 12),  FASTFN(8, 16), FASTFN(16, 8),
-                                          FASTFN(16, 12), FASTFN(16, 16), FASTFN(32, 8), FASTFN(32, 12),
-                                          FASTFN(32, 16)};
-#undef FASTFN
-
-// Streaming kernel family (single-stripe reads), one tiling table per mode
-// (phmm_kernels.cuh: kFast32 / kFast64 / kExact32 / kExact64)
-struct StreamKernel {
-  int P, K, occ;
-  size_t smem;
-  const void* fn;
-  void (*launch)(dim3, size_t, cudaStream_t, const EngineDev&, const StreamUnit*, const StreamHap*, int,
-                 const int*, int*, void*, int);
-};
-template <int MODE, int P, int K, bool STRIPES>
-void launch_stream_t(dim3 g, size_t smem, cudaStream_t s, const EngineDev& E, const StreamUnit* u,
-                     const StreamHap* h, int nu, const int* nud, int* ctr, void* col, int col_rows) {
-  k_stream<MODE, P, K, STRIPES><<<g, kThreads, smem, s>>>(E, u, h, nu, nud, ctr, col, col_rows);
-}
-template <int MODE, int P, int K, bool STRIPES = false>
-StreamKernel SK() {
-  const size_t elem = ModeOf<MODE>::F64 ? sizeof(double) : sizeof(float);   // 5*K*P entries per slot
-  // striped instantiations add the boundary-column ring: per sub-warp slot 3 x kColRing
-  // two-lane values
-  return StreamKernel{P, K, STRIPES ? 2 : StreamOcc<MODE, K>::value,
-                      96 * sizeof(double) + (size_t)4 * (32 / P) * 5 * K * P * elem + kStreamCodeBytesPerCta +
-                          (STRIPES ? (size_t)4 * (32 / P) * 3 * kColRing * 2 * elem : 0),
-                      (const void*)k_stream<MODE, P, K, STRIPES>, launch_stream_t<MODE, P, K, STRIPES>};
-}
-// kFast32: the k_fast tiling table (same order as kFastGeoms, so PHMM_FAST_GEOM applies),
-// then K = 10, 14 tilings (2-wide emission chunks) for widths 80 .. 448
-constexpr int kNumStreamFast32 = kNumFastGeoms + 6;
-const StreamKernel kStreamFast32[kNumStreamFast32] = {
-    SK<kFast32, 4, 4>(),   SK<kFast32, 4, 8>(),   SK<kFast32, 4, 12>(),  SK<kFast32, 4, 16>(),
-    SK<kFast32, 8, 8>(),   SK<kFast32, 8, 12>(),  SK<kFast32, 8, 16>(),  SK<kFast32, 16, 8>(),
-    SK<kFast32, 16, 12>(), SK<kFast32, 16, 16>(), SK<kFast32, 32, 8>(),  SK<kFast32, 32, 12>(),
-    SK<kFast32, 32, 16>(), SK<kFast32, 8, 10>(),  SK<kFast32, 8, 14>(),  SK<kFast32, 16, 10>(),
-    SK<kFast32, 16, 14>(), SK<kFast32, 32, 10>(), SK<kFast32, 32, 14>()};
-// FP64 tilings, indexed by r64_geom_for(m): W = 32, 64, 96, 128, 192, 256
-const StreamKernel kStreamFast64[kNumR64Geoms] = {SK<kFast64, 8, 4>(),  SK<kFast64, 16, 4>(),
-                                                  SK<kFast64, 16, 6>(), SK<kFast64, 16, 8>(),
-                                                  SK<kFast64, 32, 6>(), SK<kFast64, 32, 8>()};
-const StreamKernel kStreamExact64[kNumR64Geoms] = {SK<kExact64, 8, 4>(),  SK<kExact64, 16, 4>(),
-                                                   SK<kExact64, 16, 6>(), SK<kExact64, 16, 8>(),
-                                                   SK<kExact64, 32, 6>(), SK<kExact64, 32, 8>()};
-// exact FP32 tilings, indexed by rx32_geom_for(m): W = 32, 64, 96, 128, 192, 256, 384, 512
-// (wide sub-warps: guard-band reruns are few and latency bound)
-const StreamKernel kStreamExact32[kNumRX32Geoms] = {
-    SK<kExact32, 8, 4>(),  SK<kExact32, 16, 4>(), SK<kExact32, 16, 6>(),  SK<kExact32, 32, 4>(),
-    SK<kExact32, 32, 6>(), SK<kExact32, 32, 8>(), SK<kExact32, 32, 12>(), SK<kExact32, 32, 16>()};
-const StreamKernel* const kStreamTab[4] = {kStreamFast32, kStreamFast64, kStreamExact32, kStreamExact64};
-// reads longer than every tiling stripe over the widest one of their mode, in a separate
-// instantiation (the column hand-off costs registers the single-stripe kernels keep)
-const StreamKernel kStripedTab[4] = {SK<kFast32, 32, 16, true>(), SK<kFast64, 32, 8, true>(),
-                                     SK<kExact32, 32, 8, true>(), SK<kExact64, 32, 8, true>()};
-const int kStripedGeom[4] = {12, kNumR64Geoms - 1, kNumRX32Geoms - 1, kNumR64Geoms - 1};
-const int kStreamTabN[4] = {kNumStreamFast32, kNumR64Geoms, kNumRX32Geoms, kNumR64Geoms};
+// Stream tiling tables per mode (k_stream_<mode>.cu); kFast32's first kNumFastGeoms entries
+// are the geometry table PHMM_FAST_GEOM ("PxK") selects from
+constexpr int kNumFastGeoms = 13;
 constexpr int kMaxTilings = 24;
 static_assert(kNumStreamFast32 <= kMaxTilings, "tiling table");
+const int kStreamTabN[4] = {kNumStreamFast32, kNumR64Geoms, kNumRX32Geoms, kNumR64Geoms};
+const StreamKernel* stream_tab(int mode) {
+  switch (mode) {
+    case kFast32: return stream_table_fast32();
+    case kFast64: return stream_table_fast64();
+    case kExact32: return stream_table_exact32();
+    default: return stream_table_exact64();
+  }
+}
+const StreamKernel& striped_tab(int mode) {
+  switch (mode) {
+    case kFast32: return striped_fast32();
+    case kFast64: return striped_fast64();
+    case kExact32: return striped_exact32();
+    default: return striped_exact64();
+  }
+}
+// the tiling the striped instantiation of each mode corresponds to in its table
+const int kStripedGeom[4] = {12, kNumR64Geoms - 1, kNumRX32Geoms - 1, kNumR64Geoms - 1};
+// device counters: [0,4) ex32 counts, [4,8) ex64 counts, [8,12) ex32 work, [12,16) ex64
+// work, 16 inline guard-band pairs, [20,24) fx64 counts, [24,28) fx64 work, then the
+// device-built stream lists (counts[8], hap count, overflow) and their work counters, then
+// one work counter per planned stream bin
+constexpr int kCtrR64 = 32, kCtrRX32 = 44, kCtrR64Work = 56, kCtrRX32Work = 64;
+constexpr int kCtrR64b = 72, kCtrR64bWork = 80;   // second-stage striped FP64 units: counts, work
+constexpr int kBinCounters = 96;                  // fixed counter slots before the per-bin counters
+constexpr int64_t kBigCallPairs = 1 << 20;        // device-built retry units grow above this
+constexpr int kFinishThreads = 16;                // host threads finishing log10 in phmm_fetch
+// scratch bound for boundary columns of long haplotypes (striped stream bins, post-pass)
+constexpr size_t kColBudget = (size_t)1 << 30;
 
 int stream_cap(int P) { return stream_cap_of(P); }
 
 int exact_slot_host(int m) { return (m + 1 <= 32) ? 0 : (m + 1 <= 64) ? 1 : (m + 1 <= 128) ? 2 : 3; }
 
-size_t fast_smem(int geom) {
-  const FastGeom g = kFastGeoms[geom];
-  return 96 * sizeof(double) + (size_t)(kThreads / 32) * (32 / g.P) * 5 * g.K * g.P * sizeof(float);
-}
-size_t exact_smem(int slot, size_t tsize) {
-  const int P = kExactP[slot];
-  return 96 * sizeof(double) + (size_t)(kThreads / 32) * (32 / P) * 5 * kExactK * P * tsize;
-}
-
-// Cost model for choosing a fast geometry: padded cells x (rows + fill/drain), plus a
-// per-step overhead worth ~2.5 cells per thread.
-// Single-stripe tilings (W >= m + 1) are preferred; reads longer than the widest tile
-// (m >= 512) stripe over P = 32 tiles.
 int forced_geom() {
   static int g = -2;
   if (g == -2) {
@@ -192,45 +110,22 @@ int forced_geom() {
     int P = 0, K = 0;
     if (env && sscanf(env, "%dx%d", &P, &K) == 2)
       for (int i = 0; i < kNumFastGeoms; ++i)
-        if (kFastGeoms[i].P == P && kFastGeoms[i].K == K) g = i;
+        if (stream_table_fast32()[i].P == P && stream_table_fast32()[i].K == K) g = i;
   }
   return g;
 }
 
-int choose_geom(int m, int nmax, int* Qout) {
-  const int fg = forced_geom();
-  if (fg >= 0) {
-    const int W = kFastGeoms[fg].P * kFastGeoms[fg].K;
-    *Qout = (m + 1 + W - 1) / W;
-    return fg;
-  }
-  double best = 1e300;
-  int bi = 0, bq = 1;
-  const bool stripe = m + 1 > kFastGeoms[kNumFastGeoms - 1].P * kFastGeoms[kNumFastGeoms - 1].K;
-  for (int g = 0; g < kNumFastGeoms; ++g) {
-    const int P = kFastGeoms[g].P, K = kFastGeoms[g].K, W = P * K;
-    const int Q = (m + 1 + W - 1) / W;
-    if (stripe ? P != 32 : Q != 1) continue;
-    const double cost = (double)Q * P * (K + 2.5) * (double)(nmax + P - 1);
-    if (cost < best - 1e-9) { best = cost; bi = g; bq = Q; }
-  }
-  *Qout = bq;
-  return bi;
-}
-
-// Streaming tiling for a read of length m whose batch has haplotype lengths summing to
-// `total` (longest `nmax`): units of two lanes of ~total/2 rows, split when a lane would
-// exceed the geometry's row-code capacity.  -1: no single-stripe streaming geometry.
-// cost of streaming a read's haplotypes (total rows, longest nmax) on tiling g (1e300:
-// infeasible or excluded by PHMM_FAST_GEOM)
-// `lane_rows`: the call's lane-length budget (small calls split units further, below)
+// Cost of streaming a read's haplotypes (lengths summing to `total`, longest `nmax`) on
+// tiling g: units of two lanes of ~total/2 rows, split when a lane would exceed the
+// tiling's row-code capacity or `lane_rows`, the call's lane-length budget (small calls
+// split units further, below).  INT64_MAX: excluded by PHMM_FAST_GEOM.
 int64_t stream_geom_cost(int mode, int g, int64_t total, int nmax, int64_t lane_rows = INT64_MAX) {
   constexpr int64_t kInf = INT64_MAX;
   const int fg = forced_geom();
   if (mode == kFast32 && fg >= 0 && g != fg) return kInf;
-  const int64_t P = kStreamTab[mode][g].P, K = kStreamTab[mode][g].K;
-  if (nmax > stream_cap((int)P)) return kInf;
-  const int64_t cap = std::min<int64_t>(stream_cap((int)P), std::max<int64_t>(nmax, lane_rows));
+  const int64_t P = stream_tab(mode)[g].P, K = stream_tab(mode)[g].K;
+  // a haplotype longer than the row capacity streams alone in its lane (ring mode)
+  const int64_t cap = std::max<int64_t>(nmax, std::min<int64_t>(stream_cap((int)P), std::max<int64_t>(nmax, lane_rows)));
   const int64_t units = (total + 2 * cap - 1) / (2 * cap);
   const int64_t rows = std::min<int64_t>(cap, (total + 2 * units - 1) / (2 * units));
   return units * P * (2 * K + 5) * (rows + P - 1);     // 2 x (K + 2.5) per thread-row
@@ -239,7 +134,7 @@ int choose_stream_geom(int mode, int m, int64_t total, int nmax, int64_t lane_ro
   int64_t best = INT64_MAX;
   int bi = -1;
   for (int g = 0; g < kStreamTabN[mode]; ++g) {
-    if (m + 1 > kStreamTab[mode][g].P * kStreamTab[mode][g].K) continue;
+    if (m + 1 > stream_tab(mode)[g].P * stream_tab(mode)[g].K) continue;
     const int64_t cost = stream_geom_cost(mode, g, total, nmax, lane_rows);
     if (cost < best) { best = cost; bi = g; }
   }
@@ -247,10 +142,11 @@ int choose_stream_geom(int mode, int m, int64_t total, int nmax, int64_t lane_ro
 }
 constexpr int kStripedBin = 1 << 10;          // geometry code of a striped bin
 const StreamKernel& skern(int mode, int geom) {
-  return (geom & kStripedBin) ? kStripedTab[mode] : kStreamTab[mode][geom];
+  return (geom & kStripedBin) ? striped_tab(mode) : stream_tab(mode)[geom];
 }
-// column rows a striped unit of tiling P can need (its row capacity + the row-0 slot)
-int col_rows_for(int P) { return stream_cap_of(P) + 2; }
+// column rows a striped unit of tiling P with lanes of <= max_rows rows can need (the
+// row-0 slot + one spare)
+int col_rows_for(int P, int max_rows) { return std::max(stream_cap_of(P), max_rows) + 2; }
 constexpr int kR64MaxW = 256, kRX32MaxW = 512;   // widest FP64 / exact-FP32 retry tilings
 
 constexpr int kMaxScoreChunks = 8;
@@ -267,15 +163,6 @@ bool score_chunking_enabled() {
   static int v = -1;
   if (v < 0) {
     const char* env = getenv("PHMM_NO_CHUNK");
-    v = (env && env[0] == '1') ? 0 : 1;
-  }
-  return v == 1;
-}
-
-bool streaming_enabled() {
-  static int v = -1;
-  if (v < 0) {
-    const char* env = getenv("PHMM_NO_STREAM");
     v = (env && env[0] == '1') ? 0 : 1;
   }
   return v == 1;
@@ -375,7 +262,9 @@ struct phmm_ctx {
   int device = 0;
   int num_sms = 148;
   cudaStream_t stream = nullptr;
-  cudaEvent_t ev_start = nullptr, ev_fast0 = nullptr, ev_fast1 = nullptr, ev_end = nullptr;
+  cudaEvent_t ev_start = nullptr, ev_fast0 = nullptr, ev_fast1 = nullptr, ev_end = nullptr;   // execute
+  cudaEvent_t ev_up0 = nullptr, ev_up1 = nullptr;       // prepare: uploads + device validation
+  cudaEvent_t ev_d0 = nullptr, ev_d1 = nullptr;         // fetch: D2H of the results
   cudaEvent_t ev_pre = nullptr;
   static constexpr int kAux = 8;              // side streams: kernels of a phase run concurrently
   cudaStream_t aux[kAux] = {};
@@ -390,13 +279,11 @@ struct phmm_ctx {
   DBuf<int> d_read_m, d_read_scale, d_read_ncap, d_counters, d_vflag;
   DBuf<float> d_gsum;
   DBuf<double> d_lut, d_acc;
-  DBuf<FastUnit> d_units;
   DBuf<StreamUnit> d_sunits;
   DBuf<StreamHap> d_shaps;
   DBuf<StreamUnit> d_r64u[kNumR64Geoms], d_rx32u[kNumRX32Geoms];
   DBuf<StreamHap> d_r64h, d_rx32h;
   DBuf<ExactItem> d_ex32[kNumExactP], d_ex64[kNumExactP], d_fx64[kNumExactP];
-  DBuf<float2> d_colf;
   DBuf<double> d_cold;
   std::unique_ptr<WorkerPool> pool;         // host finishing threads (lazy)
   int* h_counts = nullptr;   // pinned: initial list counts (8) + zeros for work counters
@@ -416,7 +303,6 @@ struct phmm_ctx {
   int64_t num_reads = 0, num_haps = 0, num_batches = 0;
   std::vector<int64_t> batch_read_off, batch_hap_off, hap_len;
   std::vector<int> read_m, read_scale, read_cfg;   // read_cfg -1 = too small
-  std::vector<Bin> bins;
   unsigned r64_geoms = 0, rx32_geoms = 0;   // device-built unit tilings that can get work
   struct SBin {
     int mode;
@@ -425,6 +311,7 @@ struct phmm_ctx {
     int64_t dev_off = 0;                    // first unit in h_sunits / d_sunits
     int64_t col_off = -1;                   // striped units: column buffer (bytes), else -1
     int grid = 0;
+    int max_rows = 0;                       // longest lane of the bin's units
   };
   std::vector<SBin> sbins;
   DBuf<unsigned char> d_colstream;          // boundary columns of striped stream units
@@ -436,7 +323,6 @@ struct phmm_ctx {
   PinnedVec<StreamHap> shaps;               // persistent capacity (pinned)
   PinnedVec<StreamUnit> h_sunits;           // LPT-ordered stream units, all bins
   PinnedVec<int> h_rmeta;                   // read m | scale | ncap
-  int host_ex32[kNumExactP] = {0, 0, 0, 0}, host_ex64[kNumExactP] = {0, 0, 0, 0};
   int max_n = 1;
   int flags = 0;
   int list_cap[kNumExactP] = {0, 0, 0, 0};
@@ -444,6 +330,8 @@ struct phmm_ctx {
   int64_t hap_bytes = 0, read_bytes = 0;
   double plan_ms = 0.0, h2d_ms = 0.0;
   int last_launches = 0;
+  int post_grid = 0;                         // CTAs of the per-pair post-pass kernels
+  int r64_grid = 0, rx32_grid = 0;           // CTAs of the striped retry launches
   float last_dev_ms = 0.f, last_fast_ms = 0.f;
   EngineDev dev{};
 
@@ -509,30 +397,27 @@ static int init_ctx(phmm_ctx* ctx, int device) {
   CK(cudaEventCreate(&ctx->ev_fast0));
   CK(cudaEventCreate(&ctx->ev_fast1));
   CK(cudaEventCreate(&ctx->ev_end));
+  CK(cudaEventCreate(&ctx->ev_up0));
+  CK(cudaEventCreate(&ctx->ev_up1));
+  CK(cudaEventCreate(&ctx->ev_d0));
+  CK(cudaEventCreate(&ctx->ev_d1));
   CK(cudaMallocHost(&ctx->h_counts, kBinCounters * sizeof(int)));
   CK(cudaMallocHost(&ctx->h_vflag, sizeof(int)));
   CK(ctx->d_lut.ensure(94));
   CK(cudaMemcpy(ctx->d_lut.p, ctx->lut.data(), 94 * sizeof(double), cudaMemcpyHostToDevice));
-  for (int g = 0; g < 2 * kNumFastGeoms; ++g)
-    CK(cudaFuncSetAttribute(kFastFn[g], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fast_smem(g / 2)));
   for (int md = 0; md < 4; ++md) {
     for (int g = 0; g < kStreamTabN[md]; ++g) {
-      CK(cudaFuncSetAttribute(kStreamTab[md][g].fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)kStreamTab[md][g].smem));
+      const StreamKernel& k = stream_tab(md)[g];
+      CK(cudaFuncSetAttribute(k.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k.smem));
       // one shared-memory carveout for every stream kernel: CTAs of different tilings can
       // share an SM without an L1/shared reconfiguration
       if (!getenv("PHMM_NO_CARVEOUT"))
-        CK(cudaFuncSetAttribute(kStreamTab[md][g].fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+        CK(cudaFuncSetAttribute(k.fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     }
-    CK(cudaFuncSetAttribute(kStripedTab[md].fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)kStripedTab[md].smem));
+    CK(cudaFuncSetAttribute(striped_tab(md).fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)striped_tab(md).smem));
   }
-  CK(cudaFuncSetAttribute((const void*)k_exact_all<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          (int)exact_smem(0, 4)));
-  CK(cudaFuncSetAttribute((const void*)k_exact_all<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          (int)exact_smem(0, 8)));
-  CK(cudaFuncSetAttribute((const void*)k_fast64_all, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          (int)exact_smem(0, 8)));
+  CK(aux_set_attributes());
   return PHMM_SUCCESS;
 }
 
@@ -545,11 +430,11 @@ int phmm_destroy(phmm_ctx* ctx) {
   ctx->d_roff.release(); ctx->d_hoff.release(); ctx->d_read_m.release(); ctx->d_read_scale.release();
   ctx->d_read_ncap.release(); ctx->d_counters.release(); ctx->d_vflag.release();
   ctx->d_colstream.release(); ctx->d_gsum.release(); ctx->d_lut.release();
-  ctx->d_acc.release(); ctx->d_units.release(); ctx->d_sunits.release(); ctx->d_shaps.release();
+  ctx->d_acc.release(); ctx->d_sunits.release(); ctx->d_shaps.release();
   for (int g = 0; g < kNumR64Geoms; ++g) ctx->d_r64u[g].release();
   for (int g = 0; g < kNumRX32Geoms; ++g) ctx->d_rx32u[g].release();
   ctx->d_r64h.release();
-  ctx->d_rx32h.release(); ctx->d_colf.release(); ctx->d_cold.release();
+  ctx->d_rx32h.release(); ctx->d_cold.release();
   for (int s = 0; s < kNumExactP; ++s) { ctx->d_ex32[s].release(); ctx->d_ex64[s].release(); ctx->d_fx64[s].release(); }
   for (phmm_ctx* c : ctx->chunks) phmm_destroy(c);
   ctx->chunks.clear();
@@ -562,6 +447,8 @@ int phmm_destroy(phmm_ctx* ctx) {
   if (ctx->ev_fast0) cudaEventDestroy(ctx->ev_fast0);
   if (ctx->ev_fast1) cudaEventDestroy(ctx->ev_fast1);
   if (ctx->ev_end) cudaEventDestroy(ctx->ev_end);
+  for (cudaEvent_t e : {ctx->ev_up0, ctx->ev_up1, ctx->ev_d0, ctx->ev_d1})
+    if (e) cudaEventDestroy(e);
   if (ctx->ev_pre) cudaEventDestroy(ctx->ev_pre);
   for (int a = 0; a < phmm_ctx::kAux; ++a) {
     if (ctx->aux[a]) { cudaStreamSynchronize(ctx->aux[a]); cudaStreamDestroy(ctx->aux[a]); }
@@ -578,7 +465,7 @@ static int prepare_impl(phmm_ctx* ctx, const phmm_input* in, const phmm_options*
 
 // waits for the prepare's uploads and the device content checks (k_validate)
 static int check_validation(phmm_ctx* ctx) {
-  CK(cudaEventSynchronize(ctx->ev_end));
+  CK(cudaEventSynchronize(ctx->ev_up1));
   const int vbad = *ctx->h_vflag;
   if (vbad & 1) return ctx->fail(PHMM_ERR_INVALID, "base code outside A,C,G,T,N (0..4)");
   if (vbad & 2) return ctx->fail(PHMM_ERR_INVALID, "quality values must be in [0, 93]");
@@ -653,7 +540,7 @@ static int prepare_impl(phmm_ctx* ctx, const phmm_input* in, const phmm_options*
     bytes += (int64_t)(n * sizeof(*src));
     return cudaMemcpyAsync(buf.p, src, n * sizeof(*src), cudaMemcpyHostToDevice, ctx->stream);
   };
-  CK(cudaEventRecord(ctx->ev_start, ctx->stream));
+  CK(cudaEventRecord(ctx->ev_up0, ctx->stream));
   CK(up(ctx->d_rbases, in->read_bases, RL));
   CK(up(ctx->d_bq, in->base_qual, RL));
   CK(up(ctx->d_iq, in->ins_qual, RL));
@@ -696,18 +583,17 @@ static int prepare_impl(phmm_ctx* ctx, const phmm_input* in, const phmm_options*
   if (N > INT32_MAX - 1) return ctx->fail(PHMM_ERR_INVALID, "too many pairs in one call (%lld)", (long long)N);
   ctx->num_pairs = N;
   const bool exact_mode = (opt->flags & PHMM_FLAG_EXACT) != 0;
-  ctx->bins.clear();
+  // stream units address reads/haplotypes with 32-bit offsets (phmm_score chunks larger calls)
+  if (RL >= INT32_MAX || HL >= INT32_MAX)
+    return ctx->fail(PHMM_ERR_INVALID, "one prepare holds < 2 GiB of read / haplotype bases; use phmm_score "
+                                       "(which streams larger inputs in chunks)");
   ctx->sbins.clear();
   ctx->r64_geoms = ctx->rx32_geoms = 0;
   ctx->su_all.clear();
   ctx->su_bin.clear();
   ctx->shaps.clear();
-  // streaming units address reads/haplotypes with 32-bit offsets
-  const bool use_stream = streaming_enabled() && RL < INT32_MAX && HL < INT32_MAX;
-  std::vector<int> bin_index(kNumFastGeoms * 64, -1);
   int sbin_index[4 * kMaxTilings];
   std::fill(sbin_index, sbin_index + 4 * kMaxTilings, -1);
-  std::vector<ExactItem> host32[kNumExactP], host64[kNumExactP];
   int64_t slot_pairs[kNumExactP] = {0, 0, 0, 0};
   int64_t r64_pairs[8] = {0}, rx32_pairs[8] = {0};
   bool long64 = false, long32 = false;          // streamed reads that stripe in the retry kernels
@@ -733,11 +619,11 @@ static int prepare_impl(phmm_ctx* ctx, const phmm_input* in, const phmm_options*
     M.n = kStreamTabN[md];
     for (int g = 0; g < M.n; ++g) M.wsort[g] = g;
     std::sort(M.wsort, M.wsort + M.n, [&](int x, int y) {
-      return kStreamTab[md][x].P * kStreamTab[md][x].K < kStreamTab[md][y].P * kStreamTab[md][y].K;
+      return stream_tab(md)[x].P * stream_tab(md)[x].K < stream_tab(md)[y].P * stream_tab(md)[y].K;
     });
-    for (int i = 0; i < M.n; ++i) M.wsorted[i] = kStreamTab[md][M.wsort[i]].P * kStreamTab[md][M.wsort[i]].K;
+    for (int i = 0; i < M.n; ++i) M.wsorted[i] = stream_tab(md)[M.wsort[i]].P * stream_tab(md)[M.wsort[i]].K;
   }
-  if (use_stream) ctx->shaps.reserve(N);
+  ctx->shaps.reserve(N);
   // Lane budget: a call too small to fill the GPU with long lanes (few pairs, long
   // haplotypes: c4) splits its units until there are ~2 per sub-warp slot (#SM x 8 warps
   // x 2 sub-warps); latency, not per-unit overhead, bounds such calls.  Large calls keep
@@ -782,7 +668,7 @@ static int prepare_impl(phmm_ctx* ctx, const phmm_input* in, const phmm_options*
       const bool exact = f64 || exact_mode || scale > 126;
       const int mode = f64 ? kExact64 : exact ? kExact32 : kFast32;
       slot_pairs[exact_slot_host(m)] += nh;             // any pair may land in its slot's lists
-      if (use_stream) {
+      {
         ModePlan& M = mp[mode];
         if (m != M.tmpl_m) {                           // lane template per (batch, tiling)
           M.tmpl_m = m;
@@ -793,12 +679,10 @@ static int prepare_impl(phmm_ctx* ctx, const phmm_input* in, const phmm_options*
               sg = M.best_from[i];
               break;
             }
-          if (sg < 0 && m + 1 > M.wsorted[M.n - 1] &&   // longer than every tiling: stripes
-              stream_geom_cost(mode, kStripedGeom[mode], batch_total, ncap) != INT64_MAX)
-            sg = kStripedBin | kStripedGeom[mode];
+          if (sg < 0) sg = kStripedBin | kStripedGeom[mode];   // longer than every tiling: stripes
           M.tmpl_geom = sg;
           const int ts = (sg & kStripedBin) ? kMaxTilings - 1 : sg;   // template cache slot
-          if (sg >= 0 && !M.tvalid[ts]) {
+          if (!M.tvalid[ts]) {
             M.tvalid[ts] = true;
             std::vector<LaneTemplate>& tmpl = M.tmpls[ts];
             tmpl.clear();
@@ -822,7 +706,7 @@ static int prepare_impl(phmm_ctx* ctx, const phmm_input* in, const phmm_options*
             }
           }
         }
-        if (M.tmpl_geom >= 0) {
+        {
           const std::vector<LaneTemplate>& tmpl = M.tmpls[(M.tmpl_geom & kStripedBin) ? kMaxTilings - 1 : M.tmpl_geom];
           const int key = mode * kMaxTilings + ((M.tmpl_geom & kStripedBin) ? kMaxTilings - 1 : M.tmpl_geom);
           if (sbin_index[key] < 0) {
@@ -850,46 +734,14 @@ static int prepare_impl(phmm_ctx* ctx, const phmm_input* in, const phmm_options*
                 ctx->shaps.push_back(StreamHap{h, (int)(gid + (h - h0)), (int)hoff[h], (int)ctx->hap_len[h]});
             ctx->su_all.push_back(su);
             ctx->su_bin.push_back(sbi);
+            ctx->sbins[sbi].max_rows = std::max(ctx->sbins[sbi].max_rows, std::max(t.rows[0], t.rows[1]));
           }
-          continue;
         }
       }
-      if (exact) {                                     // per-pair bit-exact kernels
-        for (int64_t h = h0; h < h1; ++h) {
-          ExactItem it{(int)(gid + (h - h0)), (int)r, (int)h, scale};
-          (f64 ? host64 : host32)[exact_slot_host(m)].push_back(it);
-        }
-        continue;
-      }
-      for (int64_t x = 0; x < nh; x += 2) {
-        const int ha = hidx[x], hb = (x + 1 < nh) ? hidx[x + 1] : hidx[x];
-        FastUnit u;
-        u.read = (int)r; u.hapA = ha; u.hapB = hb;
-        u.pairA = (int)(gid + (ha - h0));
-        u.pairB = (x + 1 < nh) ? (int)(gid + (hb - h0)) : -1;
-        u.nA = (int)ctx->hap_len[ha]; u.nB = (int)ctx->hap_len[hb];
-        u.pad = 0;
-        int Q;
-        const int g = choose_geom(m, std::max(u.nA, u.nB), &Q);
-        const int key = g * 64 + std::min(Q, 63);
-        if (bin_index[key] < 0) {
-          bin_index[key] = (int)ctx->bins.size();
-          ctx->bins.push_back(Bin{g, Q, {}, 0});
-        }
-        ctx->bins[bin_index[key]].units.push_back(u);
-      }
+      (void)exact;
     }
   }
   ctx->max_n = max_n;
-  // LPT: costliest units first inside every bin; stable for determinism
-  int64_t nunits = 0;
-  for (auto& bn : ctx->bins) {
-    std::stable_sort(bn.units.begin(), bn.units.end(), [](const FastUnit& a, const FastUnit& c) {
-      return std::max(a.nA, a.nB) > std::max(c.nA, c.nB);
-    });
-    bn.dev_off = nunits;
-    nunits += (int64_t)bn.units.size();
-  }
   // LPT order per tiling: one stable counting sort on (bin, descending lane rows)
   const int nsbins = (int)ctx->sbins.size();
   const int64_t nsunits = (int64_t)ctx->su_all.size();
@@ -939,36 +791,38 @@ static int prepare_impl(phmm_ctx* ctx, const phmm_input* in, const phmm_options*
   CK(up(ctx->d_read_m, ctx->h_rmeta.data(), R));
   CK(up(ctx->d_read_scale, ctx->h_rmeta.data() + R, R));
   CK(up(ctx->d_read_ncap, ctx->h_rmeta.data() + 2 * R, R));
-  std::vector<FastUnit> allu;
-  allu.reserve(nunits);
-  for (auto& bn : ctx->bins) allu.insert(allu.end(), bn.units.begin(), bn.units.end());
-  CK(up(ctx->d_units, allu.data(), allu.size()));
   CK(up(ctx->d_sunits, ctx->h_sunits.data(), ctx->h_sunits.size()));
   CK(up(ctx->d_shaps, ctx->shaps.data(), ctx->shaps.size()));
   CK(ctx->d_gsum.ensure(R));
   CK(ctx->d_rflags.ensure(R));
   CK(ctx->d_acc.ensure(N));
   CK(ctx->d_status.ensure(N));
-  CK(ctx->d_counters.ensure(kBinCounters + ctx->bins.size() + ctx->sbins.size()));
+  CK(ctx->d_counters.ensure(kBinCounters + ctx->sbins.size()));
+  // per-pair post-pass lists (device-appended): sized for every pair whose read maps there
   for (int s = 0; s < kNumExactP; ++s) {
     ctx->list_cap[s] = (int)std::max<int64_t>(slot_pairs[s], 1);
-    ctx->host_ex32[s] = (int)host32[s].size();
-    ctx->host_ex64[s] = (int)host64[s].size();
     CK(ctx->d_ex32[s].ensure(ctx->list_cap[s]));
     CK(ctx->d_ex64[s].ensure(ctx->list_cap[s]));
     CK(ctx->d_fx64[s].ensure(ctx->list_cap[s]));
-    if (!host32[s].empty()) CK(up(ctx->d_ex32[s], host32[s].data(), host32[s].size()));
-    if (!host64[s].empty()) CK(up(ctx->d_ex64[s], host64[s].data(), host64[s].size()));
   }
-  // boundary-column scratch: 2 buffers x 3 values x (max_n + 1) rows per sub-warp slot
-  const int slots_per_sm = 4 * (kThreads / 32) * 8;   // <= 4 CTAs/SM x 4 warps x 8 sub-warps
-  const size_t col_elems = (size_t)ctx->num_sms * slots_per_sm * 2 * 3 * (size_t)(max_n + 1);
-  bool need_col = false, need_cold = false;
-  for (auto& bn : ctx->bins) need_col |= bn.Q > 1;
-  for (int s = 0; s < kNumExactP; ++s) need_cold |= true;
-  if (need_col) CK(ctx->d_colf.ensure(col_elems));
-  CK(ctx->d_cold.ensure(col_elems));   // exact kernels (f32 view uses half of it)
-  (void)need_cold;
+  // Boundary-column scratch of the per-pair post-pass kernels (k_exact_all / k_fast64_all):
+  // only their P = 32 slot stripes (reads >= 256), one sub-warp per warp, 2 buffers x
+  // 3 values x (max_n + 1) rows each; the grid is capped so the scratch stays under
+  // kColBudget even for very long haplotypes.
+  {
+    const size_t per_slot = 2 * 3 * (size_t)(max_n + 1);
+    int max_m = 0;
+    for (int64_t r = 0; r < R; ++r)
+      if (ctx->read_cfg[r] >= 0) max_m = std::max(max_m, ctx->read_m[r]);
+    const size_t per_cta = (size_t)(kThreads / 32) * per_slot * sizeof(double);
+    ctx->post_grid = ctx->num_sms * 2;
+    if (max_m + 1 > 32 * kExactK) {
+      ctx->post_grid = (int)std::max<size_t>(1, std::min<size_t>(ctx->post_grid, kColBudget / per_cta));
+      CK(ctx->d_cold.ensure((size_t)ctx->post_grid * (kThreads / 32) * per_slot));
+    } else {
+      CK(ctx->d_cold.ensure(1));       // never dereferenced: every post-pass read fits one stripe
+    }
+  }
   trace.mark("plan-upload");
   // content validation on the device (bases 0..4, qualities 0..93)
   CK(ctx->d_vflag.ensure(1));
@@ -977,20 +831,19 @@ static int prepare_impl(phmm_ctx* ctx, const phmm_input* in, const phmm_options*
   if (RL + HL > 0) {
     const int64_t work = std::max<int64_t>(RL, HL) / 16 + 1;
     const int vblocks = (int)std::min<int64_t>(ctx->num_sms * 8, (work + 255) / 256);
-    k_validate<<<vblocks, 256, 0, ctx->stream>>>((const uint8_t*)ctx->d_rbases.p, ctx->d_bq.p, ctx->d_iq.p,
-                                                 ctx->d_dq.p, ctx->d_gq.p, RL, (const uint8_t*)ctx->d_hbases.p,
-                                                 HL, vflag);
+    launch_validate(vblocks, ctx->stream, (const uint8_t*)ctx->d_rbases.p, ctx->d_bq.p, ctx->d_iq.p, ctx->d_dq.p,
+                    ctx->d_gq.p, RL, (const uint8_t*)ctx->d_hbases.p, HL, vflag);
     CK(cudaGetLastError());
   }
   CK(cudaMemcpyAsync(ctx->h_vflag, vflag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
-  CK(cudaEventRecord(ctx->ev_end, ctx->stream));
+  CK(cudaEventRecord(ctx->ev_up1, ctx->stream));
   ctx->h2d_bytes = bytes;
   ctx->h2d_ms = 0.0;
   if (!ctx->async) {
     int rc = check_validation(ctx);
     if (rc != PHMM_SUCCESS) return rc;
     float h2d = 0.f;
-    cudaEventElapsedTime(&h2d, ctx->ev_start, ctx->ev_end);
+    cudaEventElapsedTime(&h2d, ctx->ev_up0, ctx->ev_up1);
     ctx->h2d_ms = h2d;
   }
 
@@ -1063,12 +916,16 @@ static int prepare_impl(phmm_ctx* ctx, const phmm_input* in, const phmm_options*
   }
   // grids of the stream launches, and boundary-column space for the ones that can meet
   // striped units (reads longer than the tiling width): per sub-warp slot 2 columns x
-  // 3 states x (row capacity + 1) two-lane values
+  // 3 states x (longest lane + 2) two-lane values.  A grid whose columns would exceed
+  // kColBudget (very long haplotypes) is shrunk to fit.
   {
     int64_t col_total = 0;
-    auto col_bytes = [&](int mode, const StreamKernel& K, int grid) -> int64_t {
+    auto col_per_cta = [&](int mode, const StreamKernel& K, int max_rows) -> int64_t {
       const int64_t v = (mode == kFast64 || mode == kExact64) ? 16 : 8;
-      return (int64_t)grid * 4 * (32 / K.P) * 6 * col_rows_for(K.P) * v;
+      return (int64_t)4 * (32 / K.P) * 6 * col_rows_for(K.P, max_rows) * v;
+    };
+    auto fit = [&](int grid, int64_t per_cta) {
+      return (int)std::max<int64_t>(1, std::min<int64_t>(grid, (int64_t)kColBudget / per_cta));
     };
     for (auto& sb : ctx->sbins) {
       const StreamKernel& K = skern(sb.mode, sb.geom);
@@ -1079,21 +936,33 @@ static int prepare_impl(phmm_ctx* ctx, const phmm_input* in, const phmm_options*
       const int64_t want = striped && groups * 2 <= (int64_t)ctx->num_sms * K.occ * 4 ? groups : (groups + 3) / 4;
       sb.grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)ctx->num_sms * K.occ, want));
       sb.col_off = striped ? col_total : -1;
-      if (striped) col_total += col_bytes(sb.mode, K, sb.grid);
+      if (striped) {
+        const int64_t per = col_per_cta(sb.mode, K, sb.max_rows);
+        sb.grid = fit(sb.grid, per);
+        col_total += sb.grid * per;
+      }
     }
+    // device-built units of striped reads: lanes of <= max(row capacity, longest haplotype)
     for (int g = 0; g < 8; ++g) { ctx->r64_col_off[g] = -1; ctx->rx32_col_off[g] = -1; }
+    ctx->r64_grid = ctx->rx32_grid = 0;
     if (long64) {                                   // reads > 255 stripe on the widest FP64 tiling
       const int g = kNumR64Geoms - 1;
       if (ctx->r64_geoms & (1u << g)) {
+        const StreamKernel& K = striped_tab(kFast64);
+        const int64_t per = col_per_cta(kFast64, K, max_n);
+        ctx->r64_grid = fit(ctx->num_sms * K.occ, per);
         ctx->r64_col_off[g] = col_total;
-        col_total += col_bytes(kFast64, kStripedTab[kFast64], ctx->num_sms * kStripedTab[kFast64].occ);
+        col_total += ctx->r64_grid * per;
       }
     }
     if (long32) {                                   // reads > 511: exact FP32 stripes
       const int g = kNumRX32Geoms - 1;
       if (ctx->rx32_geoms & (1u << g)) {
+        const StreamKernel& K = striped_tab(kExact32);
+        const int64_t per = col_per_cta(kExact32, K, max_n);
+        ctx->rx32_grid = fit(ctx->num_sms * K.occ, per);
         ctx->rx32_col_off[g] = col_total;
-        col_total += col_bytes(kExact32, kStripedTab[kExact32], ctx->num_sms * kStripedTab[kExact32].occ);
+        col_total += ctx->rx32_grid * per;
       }
     }
     if (col_total > 0) CK(ctx->d_colstream.ensure(col_total));
@@ -1114,48 +983,26 @@ int phmm_execute(phmm_ctx* ctx) {
   const EngineDev& E = ctx->dev;
   const int64_t N = ctx->num_pairs;
   int launches = 0;
-  // counters: [0,4) ex32 counts, [4,8) ex64 counts, [8,12) ex32 work, [12,16) ex64 work,
-  // 16 inline guard-band pairs, [20,24) fx64 counts, [24,28) fx64 work, [32,38) FP64
-  // stream-retry unit counts, 38 their haplotype count, [40,46) their work counters,
-  // [kBinCounters, +bins) fast-kernel bins
-  const int nb = (int)ctx->bins.size();
-  std::vector<int> blocks(nb, 0);
-  for (int bi = 0; bi < nb; ++bi) {
-    const Bin& bn = ctx->bins[bi];
-    const int nu = (int)bn.units.size();
-    if (nu == 0) continue;
-    const int G = 32 / kFastGeoms[bn.geom].P;
-    const int groups = (nu + G - 1) / G;
-    blocks[bi] = std::max(1, std::min(ctx->num_sms * kFastOcc[bn.geom], (groups + 3) / 4));
-  }
   CK(cudaEventRecord(ctx->ev_start, st));
   const int nsb = (int)ctx->sbins.size();
   int* bin_ctr = ctx->d_counters.p + kBinCounters;
-  // counters (host list sizes in [0, 8), zero elsewhere) and per-pair status are reset by
-  // k_precompute itself: no small H2D copy / memsets on the critical path
-  const int4 hc0 = make_int4(ctx->host_ex32[0], ctx->host_ex32[1], ctx->host_ex32[2], ctx->host_ex32[3]);
-  const int4 hc1 = make_int4(ctx->host_ex64[0], ctx->host_ex64[1], ctx->host_ex64[2], ctx->host_ex64[3]);
+  // the work counters and per-pair status are reset by k_precompute itself: no small
+  // H2D copy / memsets on the critical path
   // L2 prefetch of the per-unit inputs on a side stream, beside k_precompute (joined with
   // the FP32 phase; the bench flushes L2 between steps)
   CK(cudaEventRecord(ctx->ev_pre, st));
   CK(cudaStreamWaitEvent(ctx->aux[phmm_ctx::kAux - 1], ctx->ev_pre, 0));
-  k_l2_prefetch<<<ctx->num_sms * 2, 256, 0, ctx->aux[phmm_ctx::kAux - 1]>>>(
-      ctx->d_sunits.p, (int64_t)ctx->h_sunits.size() * (int64_t)sizeof(StreamUnit), ctx->d_shaps.p,
-      (int64_t)ctx->shaps.size() * (int64_t)sizeof(StreamHap), ctx->d_hbases.p, ctx->hap_bytes, ctx->d_rbases.p,
-      ctx->d_bq.p, ctx->read_bytes);
+  launch_l2_prefetch(ctx->num_sms * 2, ctx->aux[phmm_ctx::kAux - 1], ctx->d_sunits.p,
+                     (int64_t)ctx->h_sunits.size() * (int64_t)sizeof(StreamUnit), ctx->d_shaps.p,
+                     (int64_t)ctx->shaps.size() * (int64_t)sizeof(StreamHap), ctx->d_hbases.p, ctx->hap_bytes,
+                     ctx->d_rbases.p, ctx->d_bq.p, ctx->read_bytes);
   ++launches;
-  {
-    const int threads = 128;
-    const int64_t blocks_pre = std::max<int64_t>(1, (ctx->num_reads * 32 + threads - 1) / threads);
-    k_precompute<<<(unsigned)blocks_pre, threads, 0, st>>>(E, (int)ctx->num_reads, ctx->d_counters.p,
-                                                           kBinCounters + nb + nsb, hc0, hc1, N);
-    ++launches;
-  }
+  launch_precompute(ctx->num_reads, st, E, ctx->d_counters.p, kBinCounters + nsb, N);
+  ++launches;
   CK(cudaEventRecord(ctx->ev_pre, st));
   CK(cudaEventRecord(ctx->ev_fast0, st));
-  // Fast-kernel bins (one persistent launch per tiling) go round-robin onto side streams
-  // so a bin's tail (its last CTAs draining) overlaps the next bin's work.  Legacy k_fast
-  // bins share the boundary-column scratch: they stay serialized on the last side stream.
+  // Stream bins (one persistent launch per tiling) go round-robin onto side streams so a
+  // bin's tail (its last CTAs draining) overlaps the next bin's work.
   constexpr int kStreamAux = phmm_ctx::kAux - 1;
   int nlaunch = 0;
   auto side = [&](int i) -> cudaStream_t { return ctx->aux[i % kStreamAux]; };
@@ -1188,17 +1035,8 @@ int phmm_execute(phmm_ctx* ctx) {
     const StreamKernel& SKn = skern(sb.mode, sb.geom);
     used[nlaunch % kStreamAux] = true;
     SKn.launch(dim3(sb.grid), SKn.smem, side(nlaunch++), E, ctx->d_sunits.p + sb.dev_off, ctx->d_shaps.p, nu, nullptr,
-               bin_ctr + nb + bi, sb.col_off >= 0 ? ctx->d_colstream.p + sb.col_off : nullptr,
-               col_rows_for(SKn.P));
-    ++launches;
-  }
-  for (int bi = 0; bi < nb; ++bi) {
-    const Bin& bn = ctx->bins[bi];
-    const int nu = (int)bn.units.size();
-    if (nu == 0) continue;
-    used[phmm_ctx::kAux - 1] = true;
-    kFastLaunch[bn.geom](dim3(blocks[bi]), fast_smem(bn.geom), ctx->aux[phmm_ctx::kAux - 1], E,
-                         ctx->d_units.p + bn.dev_off, nu, bn.Q, bin_ctr + bi, ctx->d_colf.p, ctx->max_n + 1);
+               bin_ctr + bi, sb.col_off >= 0 ? ctx->d_colstream.p + sb.col_off : nullptr,
+               col_rows_for(SKn.P, sb.max_rows));
     ++launches;
   }
   CK(join());
@@ -1210,41 +1048,44 @@ int phmm_execute(phmm_ctx* ctx) {
   // everything before).  Only tilings some streamed read can use are launched.
   CK(fork());
   used[0] = true;
-  k_exact_all<float><<<ctx->num_sms * 2, kThreads, exact_smem(0, 4), ctx->aux[0]>>>(
-      E, ctx->d_counters.p + 8, (float*)ctx->d_cold.p, ctx->max_n + 1);
+  launch_exact_all_f32(ctx->post_grid, ctx->aux[0], E, ctx->d_counters.p + 8, (float*)ctx->d_cold.p, ctx->max_n + 1);
   ++launches;
   int nside = 0;
-  auto post = [&](const StreamKernel& SKn, const RetryLists& L, int g, int* work, int64_t col_off) {
+  auto post = [&](const StreamKernel& SKn, const RetryLists& L, int g, int* work, int64_t col_off, int grid) {
     const int a = 1 + (nside++ % (phmm_ctx::kAux - 1));
     used[a] = true;
-    SKn.launch(dim3(ctx->num_sms * SKn.occ), SKn.smem, ctx->aux[a], E, L.units[g], L.haps, L.unit_cap[g], L.count + g,
-               work, col_off >= 0 ? ctx->d_colstream.p + col_off : nullptr, col_rows_for(SKn.P));
+    SKn.launch(dim3(grid), SKn.smem, ctx->aux[a], E, L.units[g], L.haps, L.unit_cap[g], L.count + g, work,
+               col_off >= 0 ? ctx->d_colstream.p + col_off : nullptr, col_rows_for(SKn.P, ctx->max_n));
     ++launches;
   };
   for (int g = kNumR64Geoms - 1; g >= 0; --g)
-    if (ctx->r64_geoms & (1u << g))
-      post(ctx->r64_col_off[g] >= 0 ? kStripedTab[kFast64] : kStreamFast64[g], E.r64, g,
-           ctx->d_counters.p + kCtrR64Work + g, ctx->r64_col_off[g]);
+    if (ctx->r64_geoms & (1u << g)) {
+      const bool str = ctx->r64_col_off[g] >= 0;
+      const StreamKernel& SKn = str ? striped_tab(kFast64) : stream_table_fast64()[g];
+      post(SKn, E.r64, g, ctx->d_counters.p + kCtrR64Work + g, ctx->r64_col_off[g],
+           str ? ctx->r64_grid : ctx->num_sms * SKn.occ);
+    }
   for (int g = kNumRX32Geoms - 1; g >= 0; --g)
-    if (ctx->rx32_geoms & (1u << g))
-      post(ctx->rx32_col_off[g] >= 0 ? kStripedTab[kExact32] : kStreamExact32[g], E.rx32, g,
-           ctx->d_counters.p + kCtrRX32Work + g, ctx->rx32_col_off[g]);
+    if (ctx->rx32_geoms & (1u << g)) {
+      const bool str = ctx->rx32_col_off[g] >= 0;
+      const StreamKernel& SKn = str ? striped_tab(kExact32) : stream_table_exact32()[g];
+      post(SKn, E.rx32, g, ctx->d_counters.p + kCtrRX32Work + g, ctx->rx32_col_off[g],
+           str ? ctx->rx32_grid : ctx->num_sms * SKn.occ);
+    }
   CK(join());
   if (E.r64b.enabled) {                 // long reads: band pairs whose exact rerun underflowed
     const int g = kNumR64Geoms - 1;
-    const StreamKernel& SKn = kStripedTab[kFast64];
-    SKn.launch(dim3(ctx->num_sms * SKn.occ), SKn.smem, st, E, E.r64b.units[g], E.r64b.haps, E.r64b.unit_cap[g],
+    const StreamKernel& SKn = striped_tab(kFast64);
+    SKn.launch(dim3(ctx->r64_grid), SKn.smem, st, E, E.r64b.units[g], E.r64b.haps, E.r64b.unit_cap[g],
                E.r64b.count + g, ctx->d_counters.p + kCtrR64bWork + g, ctx->d_colstream.p + ctx->r64_col_off[g],
-               col_rows_for(SKn.P));
+               col_rows_for(SKn.P, ctx->max_n));
     ++launches;
   }
   if (ctx->flags & PHMM_FLAG_RETRY_F64) {
-    k_fast64_all<<<ctx->num_sms * 2, kThreads, exact_smem(0, 8), st>>>(E, ctx->d_counters.p + 24, ctx->d_cold.p,
-                                                                      ctx->max_n + 1);
+    launch_fast64_all(ctx->post_grid, st, E, ctx->d_counters.p + 24, ctx->d_cold.p, ctx->max_n + 1);
     ++launches;
   }
-  k_exact_all<double><<<ctx->num_sms * 2, kThreads, exact_smem(0, 8), st>>>(
-      E, ctx->d_counters.p + 12, ctx->d_cold.p, ctx->max_n + 1);
+  launch_exact_all_f64(ctx->post_grid, st, E, ctx->d_counters.p + 12, ctx->d_cold.p, ctx->max_n + 1);
   ++launches;
   CK(cudaGetLastError());
   CK(cudaEventRecord(ctx->ev_end, st));
@@ -1271,12 +1112,12 @@ static int fetch_enqueue(phmm_ctx* ctx) {
     CK(cudaMallocHost(&ctx->h_st, N));
     ctx->h_res_cap = N;
   }
-  CK(cudaEventRecord(ctx->ev_fast0, ctx->stream));     // (reused as the D2H start marker)
+  CK(cudaEventRecord(ctx->ev_d0, ctx->stream));
   if (N > 0) {
     CK(cudaMemcpyAsync(ctx->h_acc, ctx->d_acc.p, N * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaMemcpyAsync(ctx->h_st, ctx->d_status.p, N, cudaMemcpyDeviceToHost, ctx->stream));
   }
-  CK(cudaEventRecord(ctx->ev_fast1, ctx->stream));
+  CK(cudaEventRecord(ctx->ev_d1, ctx->stream));
   return PHMM_SUCCESS;
 }
 
@@ -1296,9 +1137,18 @@ static int fetch_complete(phmm_ctx* ctx, double* out_log10, uint8_t* out_status,
   const int64_t N = ctx->num_pairs;
   const double* acc = ctx->h_acc;
   const uint8_t* st = ctx->h_st;
-  CK(cudaEventSynchronize(ctx->ev_fast1));
+  CK(cudaEventSynchronize(ctx->ev_d1));
   float d2h = 0.f;
-  cudaEventElapsedTime(&d2h, ctx->ev_fast0, ctx->ev_fast1);
+  cudaEventElapsedTime(&d2h, ctx->ev_d0, ctx->ev_d1);
+  if (ctx->async) {            // chunk contexts: the execute / upload events completed by now
+    float dev = 0.f, fast = 0.f, h2d = 0.f;
+    cudaEventElapsedTime(&dev, ctx->ev_start, ctx->ev_end);
+    cudaEventElapsedTime(&fast, ctx->ev_fast0, ctx->ev_fast1);
+    cudaEventElapsedTime(&h2d, ctx->ev_up0, ctx->ev_up1);
+    ctx->last_dev_ms = dev;
+    ctx->last_fast_ms = fast;
+    ctx->h2d_ms = h2d;
+  }
   // finishing (wavefront.py:428-434): host glibc log10 (= CPython math.log10), batches
   // split over a few threads
   struct Acc { int64_t cells = 0, fast = 0, exact = 0, f64 = 0, flagged = 0; };
@@ -1381,10 +1231,6 @@ static int fetch_complete(phmm_ctx* ctx, double* out_log10, uint8_t* out_status,
     stats->num_pairs = N;
     stats->total_cells = total_cells;
     int64_t comp = 0;
-    for (auto& bn : ctx->bins) {
-      const FastGeom g = kFastGeoms[bn.geom];
-      for (auto& u : bn.units) comp += 2LL * bn.Q * g.P * g.K * (std::max(u.nA, u.nB) + g.P - 1);
-    }
     for (auto& sb : ctx->sbins) {
       const StreamKernel& g = skern(sb.mode, sb.geom);
       for (int64_t i = sb.dev_off; i < sb.dev_off + sb.count; ++i) {
@@ -1420,9 +1266,10 @@ int phmm_last_timing(const phmm_ctx* ctx, double* device_ms, double* fast_ms, in
 
 int phmm_fast_geometry(int m, int n, int* P, int* K, int* Q) {
   if (m < 1 || n < 1 || !P || !K || !Q) return PHMM_ERR_INVALID;
-  int q = 1;
-  const int g = choose_geom(m, n, &q);
-  *P = kFastGeoms[g].P; *K = kFastGeoms[g].K; *Q = q;
+  // the FP32 stream tiling a one-pair batch (m x n) is planned on
+  const int g = choose_stream_geom(kFast32, m, n, n, INT64_MAX);
+  const StreamKernel& k = g >= 0 ? stream_table_fast32()[g] : striped_fast32();
+  *P = k.P; *K = k.K; *Q = (m + 1 + k.P * k.K - 1) / (k.P * k.K);
   return PHMM_SUCCESS;
 }
 
@@ -1457,6 +1304,14 @@ static int score_chunked(phmm_ctx* ctx, const phmm_input* in, const phmm_options
     if (rc != PHMM_SUCCESS) return ctx->fail(rc, "chunk context: %s", c->err.c_str());
     c->async = true;
   }
+  // on an error, chunks already enqueued are drained before returning (their contexts and
+  // the caller's buffers must not be in use when the caller regains control)
+  auto drain = [&]() {
+    for (phmm_ctx* cx : ctx->chunks) {
+      cudaStreamSynchronize(cx->stream);
+      for (int a = 0; a < phmm_ctx::kAux; ++a) cudaStreamSynchronize(cx->aux[a]);
+    }
+  };
   // enqueue every chunk (prepare + execute + D2H), planning the next one meanwhile
   for (int c = 0; c < nchunks; ++c) {
     phmm_ctx* cx = ctx->chunks[c];
@@ -1494,26 +1349,46 @@ static int score_chunked(phmm_ctx* ctx, const phmm_input* in, const phmm_options
     int rc = phmm_prepare(cx, &sub, opt, &n);
     if (rc == PHMM_SUCCESS) rc = phmm_execute(cx);
     if (rc == PHMM_SUCCESS) rc = fetch_enqueue(cx);
-    if (rc != PHMM_SUCCESS) return ctx->fail(rc, "%s", cx->err.c_str());
+    if (rc != PHMM_SUCCESS) {
+      drain();
+      return ctx->fail(rc, "%s", cx->err.c_str());
+    }
   }
   // complete in order: device validation verdict, then finishing into the caller's slice
   phmm_stats total;
   memset(&total, 0, sizeof(total));
+  phmm_ctx* first = nullptr;
+  float span = 0.f;                  // first chunk's execute start -> last execute end
   for (int c = 0; c < nchunks; ++c) {
     phmm_ctx* cx = ctx->chunks[c];
     if (cut[c + 1] <= cut[c]) continue;
     int rc = check_validation(cx);
-    if (rc != PHMM_SUCCESS) return ctx->fail(rc, "%s", cx->err.c_str());
+    if (rc != PHMM_SUCCESS) {
+      drain();
+      return ctx->fail(rc, "%s", cx->err.c_str());
+    }
     phmm_stats cs;
     const int64_t g0 = pairs[cut[c]];
     rc = fetch_complete(cx, out_log10 ? out_log10 + g0 : nullptr, out_status ? out_status + g0 : nullptr, &cs);
-    if (rc != PHMM_SUCCESS) return ctx->fail(rc, "%s", cx->err.c_str());
+    if (rc != PHMM_SUCCESS) {
+      drain();
+      return ctx->fail(rc, "%s", cx->err.c_str());
+    }
+    if (!first) first = cx;
+    float t = 0.f;
+    if (cudaEventElapsedTime(&t, first->ev_start, cx->ev_end) == cudaSuccess) span = std::max(span, t);
+    total.fast_ms += cs.fast_ms;   // per-chunk FP32 phases (they overlap other chunks' work)
+    total.h2d_ms += cs.h2d_ms;
     total.num_pairs += cs.num_pairs; total.total_cells += cs.total_cells;
     total.computed_cells += cs.computed_cells; total.fast_pairs += cs.fast_pairs;
     total.exact_pairs += cs.exact_pairs; total.f64_pairs += cs.f64_pairs;
     total.flagged_pairs += cs.flagged_pairs; total.h2d_bytes += cs.h2d_bytes; total.d2h_bytes += cs.d2h_bytes;
     total.kernel_launches += cs.kernel_launches; total.plan_ms += cs.plan_ms; total.d2h_ms += cs.d2h_ms;
   }
+  total.device_ms = span;
+  ctx->last_dev_ms = span;
+  ctx->last_fast_ms = (float)total.fast_ms;
+  ctx->last_launches = total.kernel_launches;
   if (stats) *stats = total;
   return PHMM_SUCCESS;
 }

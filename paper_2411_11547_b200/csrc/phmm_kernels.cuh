@@ -4,16 +4,17 @@
 //   k_precompute      per read: degenerate-transition flag (prob.py:71-75) and the
 //                     guard-band sensitivity sum Gsum used to decide when the fast
 //                     FP32 result provably equals the reference's flushed FP32 result.
-//   k_fast<P,K>       FP32 fast wavefront: one sub-warp of P threads scores ONE read
-//                     against TWO haplotypes packed in float2 lanes (FFMA2/FMUL2 with a
-//                     scalar-broadcast transition operand); each thread owns K read
+//   k_stream<MODE,P,K> read-stationary haplotype streaming wavefront (the hot kernel): one
+//                     sub-warp of P threads owns one read and streams two LANES of the
+//                     batch's haplotypes through an anti-diagonal wavefront (float2 lanes,
+//                     FFMA2 with a scalar-broadcast coefficient); each thread owns K read
 //                     positions; neighbour M/I/D cross threads by __shfl_up_sync
 //                     (PAPER.md:186-218); emissions come from a per-read shared-memory
-//                     table E[c][i].  Reads longer than P*K-1 are
-//                     processed in stripes with a boundary column in global memory.
-//   k_exact<T,P,K>    bit-exact restatement of the reference recursion (no FMA, per-store
-//                     flush, j-ordered accumulation) in T = float (guard band, exact
-//                     mode) or T = double (f64 configs, FP32-underflow retries).
+//                     table E[c][i].  Modes: fast FP32 / fast FP64
+//                     (retries) / bit-exact FP32 / bit-exact FP64.  Reads longer than the
+//                     tiling stripe over it with a boundary column.
+//   k_exact_all / k_fast64_all  per-pair post-pass lists (bit-exact FP32/FP64 recursion:
+//                     no FMA, per-store flush, j-ordered accumulation; FP64 retry).
 //
 // Read layout inside a kernel: Q stripes of W = P*K padded positions;
 //   [L left-padding positions][m real read positions][1 accumulator position],
@@ -34,9 +35,6 @@ constexpr int kStatusExactF32 = 0x20, kStatusRetriedF64 = 0x40;
 constexpr int kNumExactP = 4;            // exact kernels for P in {4, 8, 16, 32}
 constexpr int kExactK = 8;
 
-struct FastUnit {                         // one read x two haplotypes (hapB may repeat hapA)
-  int read, hapA, hapB, pairA, pairB, nA, nB, pad;
-};
 struct ExactItem {                        // one read x one haplotype
   int pair, read, hap, scale;
 };
@@ -106,161 +104,24 @@ __device__ __forceinline__ void append_item(ExactItem* const* lists, int* counts
   if (pos < caps[slot]) lists[slot][pos] = it;
 }
 
-// ---------------------------------------------------------------------------------
-// k_precompute: one warp per read.
-// Gsum bounds sum over positions i of the backward sensitivities B_M(i)+B_I(i)+B_D(i)
-// of the final accumulator w.r.t. a cell value, with every emission replaced by 1.
-// Flushing a value v < 2^-90 changes the final accumulator by at most v*B, so
-//   0 <= unflushed - flushed <= 2^-90 * n * Gsum        (guard band)
-// ---------------------------------------------------------------------------------
-__device__ __forceinline__ void prefetch_l2(const void* base, int64_t bytes, int64_t tid, int64_t nth) {
-  const char* p = static_cast<const char*>(base);
-  for (int64_t off = tid * 128; off < bytes; off += nth * 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(p + off));
-}
-
-// Pulls the inputs the stream kernels read once per unit (work units, haplotype lists
-// and bases, read bases and base qualities) into L2; runs beside k_precompute.
-__global__ void k_l2_prefetch(const void* pf0, int64_t pf0_bytes, const void* pf1, int64_t pf1_bytes,
-                              const void* pf2, int64_t pf2_bytes, const void* pf3, const void* pf4,
-                              int64_t read_bytes) {
-  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t nth = (int64_t)gridDim.x * blockDim.x;
-  prefetch_l2(pf0, pf0_bytes, tid, nth);
-  prefetch_l2(pf1, pf1_bytes, tid, nth);
-  prefetch_l2(pf2, pf2_bytes, tid, nth);
-  prefetch_l2(pf3, read_bytes, tid, nth);
-  prefetch_l2(pf4, read_bytes, tid, nth);
-}
-
-__global__ void k_precompute(EngineDev E, int num_reads, int* counters, int ncounters, int4 host32, int4 host64,
-                             int64_t num_pairs) {
-  // One warp per read.  With X_i = max(B_M(i), B_I(i)) and g_i = min(n, 1/(1-eps_i)):
-  //   B_D(i) <= g_i X_{i+1},  X_i <= (1 + zeta_i g_i) X_{i+1},  X_m = 1
-  // so  sum_i (B_M + B_I + B_D) <= prod_{i<m}(1 + zeta_i g_i) * (2 + sum_{i<m}(2 + g_i)).
-  // The grid also resets the work counters (host-built list sizes first) and the status.
-  {
-    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int64_t nth = (int64_t)gridDim.x * blockDim.x;
-    const int hv[8] = {host32.x, host32.y, host32.z, host32.w, host64.x, host64.y, host64.z, host64.w};
-    for (int64_t i = tid; i < ncounters; i += nth) counters[i] = i < 8 ? hv[i] : 0;
-    uint4* st4 = reinterpret_cast<uint4*>(E.status);
-    for (int64_t i = tid; i < num_pairs / 16; i += nth) st4[i] = make_uint4(0, 0, 0, 0);
-    for (int64_t i = (num_pairs / 16) * 16 + tid; i < num_pairs; i += nth) E.status[i] = 0;
-  }
-  if (*E.invalid) return;
-  const int lane = threadIdx.x & 31;
-  const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (r >= num_reads) return;
-  const int m = E.read_m[r];
-  const int64_t o = E.roff[r];
-  const double ncap = (double)E.read_ncap[r];
-  const double* lut = E.lut;
-  bool degen = false;
-  double logx = 0.0, sg = 0.0;
-  for (int i = lane; i < m; i += 32) {
-    const double d = lut[E.iq[o + i]], z = lut[E.dq[o + i]], e = lut[E.gq[o + i]];
-    degen |= (d + z >= 1.0);
-    if (i < m - 1) {
-      const double g = (e >= 1.0) ? ncap : fmin(ncap, 1.0 / (1.0 - e));
-      logx += log1p(z * g);
-      sg += 2.0 + g;
-    }
-  }
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) {
-    logx += __shfl_xor_sync(0xffffffffu, logx, off);
-    sg += __shfl_xor_sync(0xffffffffu, sg, off);
-  }
-  degen = __any_sync(0xffffffffu, degen);
-  if (lane == 0) {
-    E.read_gsum[r] = (float)(exp(logx) * (2.0 + sg));
-    E.read_flags[r] = degen ? 1 : 0;
-  }
-}
-
-// ---------------------------------------------------------------------------------
-// k_validate: input content checks of phmm_prepare on the device (model.py:14-18,47-52):
-// base codes in 0..4, Phred qualities in 0..93.  16 B per thread-iteration, byte-wise
-// SIMD compares; flag bit0 = bad base, bit1 = bad quality.
-// ---------------------------------------------------------------------------------
-__device__ __forceinline__ unsigned over4(const uint4 v, unsigned lim) {
-  return __vcmpgtu4(v.x, lim) | __vcmpgtu4(v.y, lim) | __vcmpgtu4(v.z, lim) | __vcmpgtu4(v.w, lim);
-}
-__global__ void k_validate(const uint8_t* rb, const uint8_t* bq, const uint8_t* iq, const uint8_t* dq,
-                           const uint8_t* gq, int64_t RL, const uint8_t* hb, int64_t HL, int* flag) {
-  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t nth = (int64_t)gridDim.x * blockDim.x;
-  unsigned badb = 0, badq = 0;
-  const int64_t RV = RL / 16, HV = HL / 16;
-  for (int64_t v = tid; v < RV; v += nth) {
-    badb |= over4(reinterpret_cast<const uint4*>(rb)[v], 0x04040404u);
-    badq |= over4(reinterpret_cast<const uint4*>(bq)[v], 0x5d5d5d5du) |
-            over4(reinterpret_cast<const uint4*>(iq)[v], 0x5d5d5d5du) |
-            over4(reinterpret_cast<const uint4*>(dq)[v], 0x5d5d5d5du) |
-            over4(reinterpret_cast<const uint4*>(gq)[v], 0x5d5d5d5du);
-  }
-  for (int64_t v = tid; v < HV; v += nth) badb |= over4(reinterpret_cast<const uint4*>(hb)[v], 0x04040404u);
-  for (int64_t i = RV * 16 + tid; i < RL; i += nth) {
-    badb |= rb[i] > 4;
-    badq |= (bq[i] > 93) | (iq[i] > 93) | (dq[i] > 93) | (gq[i] > 93);
-  }
-  for (int64_t i = HV * 16 + tid; i < HL; i += nth) badb |= hb[i] > 4;
-  if (badb || badq) atomicOr(flag, (badb ? 1 : 0) | (badq ? 2 : 0));
-}
-
-// packed helpers: scalar-broadcast operand -> FFMA2 R.F32 form
-__device__ __forceinline__ float2 fma2s(float s, float2 a, float2 b) {
-  return __ffma2_rn(make_float2(s, s), a, b);
-}
-__device__ __forceinline__ float2 mul2s(float s, float2 a) {
-  return __fmul2_rn(make_float2(s, s), a);
-}
-__device__ __forceinline__ float comp(const float4& v, int i) {
-  return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w;
-}
-
 // Fast-path classification of a finished FP32 accumulator:
 //   a < 2^-93                    -> every final-row term flushes in the reference: flagged
-//   a < 2^10 * 2^-90 * n * Gsum  -> guard band: rerun on the bit-exact kernel (outside the
-//                                   band the flush effect is < 2^-10 relative, i.e. < 4.3e-4
-//                                   in log10 at |score| > 52: < 1e-5 relative)
+//   guard band                   -> rerun on the bit-exact kernel.  The reference's flushes
+//                                   lower the accumulator by at most 2^-90 * n * Gsum, i.e.
+//                                   |d log10| <= 2^-90 n Gsum / (a ln 10); that is <= 1e-5 |s|
+//                                   (a tenth of the 1e-4 relative bar on the score s) iff
+//                                   a |s| >= 2^-90 * 1e5 / ln 10 * n * Gsum = 2^-74.6 n Gsum
 //   score > -1.5 (short pairs)   -> bit-exact kernel (relative tolerance near log10 = 0)
 //   otherwise                    -> accept
-__device__ __forceinline__ bool fast_finish_g(const EngineDev& E, float a, int pair, int read, int hap,
-                                              int n, int m, int scale, float gsum, bool allow_inline = false,
-                                              bool band_to_caller = false) {
-  const float bound = 0x1p-80f * (float)n * gsum;                // 2^10 * 2^-90
+__device__ __forceinline__ bool guard_band(float a, int n, float gsum, int scale) {
   const float hi = ldexpf(0.031622776f, scale);                   // 10^-1.5 * 2^scale
-  if (!(a >= 0x1p-93f)) {
-    if (E.retry_f64) {
-      E.status[pair] = kStatusRetriedF64;
-      append_item(E.fx64, E.fx64_count, E.list_cap, exact_slot_for(m), ExactItem{pair, read, hap, 0});
-    } else {
-      E.acc[pair] = 0.0;
-      E.status[pair] = kStatusOverflow;
-    }
-  } else if (a < bound || a > hi) {
-    E.status[pair] = kStatusExactF32;
-    // guard band: the first band_budget pairs are rerun inline by the finding warp (no
-    // tail when they are rare); beyond that they go to the post-pass exact kernels.
-    if (allow_inline && atomicAdd(E.band_inline, 1) < E.band_budget) return true;
-    if (band_to_caller) return true;
-    append_item(E.ex32, E.ex32_count, E.list_cap, exact_slot_for(m), ExactItem{pair, read, hap, scale});
-  } else {
-    E.acc[pair] = (double)a;
-    E.status[pair] = kStatusOk;
-  }
-  return false;
+  const float s = fabsf(__log2f(a) - (float)scale) * 0.30103f;     // |log10 score| (a normal)
+  return a * s < 0x1.6a09e6p-75f * (float)n * gsum || a > hi;     // 2^-74.5 (conservative)
 }
-
 // ---------------------------------------------------------------------------------
 // k_exact<T, P, K>: bit-exact reference recursion (reference.py:106-122,
 // wavefront.py:130-160) — no FMA, per-store flush, j-ordered accumulation.
 // ---------------------------------------------------------------------------------
-__device__ __forceinline__ bool fast_finish(const EngineDev& E, float a, int pair, int read, int hap,
-                                            int n, int m, int scale) {
-  return fast_finish_g(E, a, pair, read, hap, n, m, scale, E.read_gsum[read], true);
-}
 
 template <typename T> struct ExactTraits;
 template <> struct ExactTraits<float> {
@@ -424,250 +285,6 @@ __device__ __forceinline__ void exact_item(const EngineDev& E, const ExactItem& 
 }
 
 // ---------------------------------------------------------------------------------
-// k_fast<P, K, MULTI>: persistent; each warp takes G = 32/P units per atomic grab.
-// MULTI = reads longer than one stripe (boundary column through global memory).
-//
-// Step loop (one haplotype row per step and thread; thread t is on row j = s - t):
-//   * neighbour exchange: __shfl_up_sync of the last position's M/I/D' (6 SHFL) and of
-//     the packed haplotype-character pair (1 SHFL); thread 0 takes the matrix boundary
-//     (or the previous stripe's column) instead and is the only thread loading
-//     haplotype characters, two rows ahead;
-//   * pass 1 (descending positions): D' from the previous row, M from the previous-row
-//     diagonal — in place, independent across positions;
-//   * pass 2 (ascending): the I chain along the read within the current row.
-// The steady phase (every thread of the warp on a valid row) runs without any
-// activity test; fill/drain steps and result capture use the checked variant.
-// ---------------------------------------------------------------------------------
-// resident CTAs (of 4 warps) per SM by positions per thread: K=8 -> 4, K=12 -> 3, K=16 -> 2
-template <int K> struct FastOcc { static constexpr int value = K <= 8 ? 4 : (K <= 12 ? 3 : 2); };
-template <int P, int K, bool MULTI>
-__global__ void __launch_bounds__(128, FastOcc<K>::value)
-k_fast(const EngineDev E, const FastUnit* __restrict__ units, int num_units, int Q,
-       int* __restrict__ counter, float2* __restrict__ colbuf, int col_rows) {
-  constexpr int W = P * K, G = 32 / P, K4 = K / 4;
-  static_assert(K % 4 == 0 && K >= 4, "K multiple of 4");
-  constexpr unsigned FULL = 0xffffffffu;
-  if (*E.invalid) return;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  double* s_lut = reinterpret_cast<double*>(smem_raw);
-  float4* s_E = reinterpret_cast<float4*>(smem_raw + 96 * sizeof(double));
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const int sw = lane / P, t = lane % P;
-  for (int i = threadIdx.x; i < 94; i += blockDim.x) s_lut[i] = E.lut[i];
-  __syncthreads();
-  float4* Et = s_E + (size_t)((wib * G + sw) * 5 * K4) * P;
-  const int gwarp = blockIdx.x * (blockDim.x >> 5) + wib;
-  float2* colX = MULTI ? colbuf + (size_t)(gwarp * G + sw) * 2 * 3 * col_rows : nullptr;
-  float2* colY = MULTI ? colX + 3 * col_rows : nullptr;
-  const float2 zero2 = make_float2(0.f, 0.f);
-
-  for (;;) {
-    int g = 0;
-    if (lane == 0) g = atomicAdd(counter, 1);
-    g = __shfl_sync(FULL, g, 0);
-    if (g * G >= num_units) break;
-    const int u = g * G + sw;
-    const bool has = u < num_units;
-    const FastUnit U = units[has ? u : g * G];
-    const int r = U.read, m = E.read_m[r];
-    const int64_t ro = E.roff[r];
-    const bool degen = (E.read_flags[r] & 1) != 0;
-    const bool live = has && !degen;
-    const int nA = U.nA, nB = U.nB, nmax = max(nA, nB);
-    const int steps = __reduce_max_sync(FULL, live ? nmax + P - 1 : 0);
-    const int steady_end = min(steps, (int)__reduce_min_sync(FULL, live ? (unsigned)min(nA, nB) : 0x7fffffffu));
-    if (has && degen && t == 0) {
-      E.acc[U.pairA] = 0.0; E.status[U.pairA] = kStatusDegenerate;
-      if (U.pairB >= 0) { E.acc[U.pairB] = 0.0; E.status[U.pairB] = kStatusDegenerate; }
-    }
-    const int scale = E.read_scale[r];
-    const int Lp = Q * W - m - 1;
-    const double Sd = ldexp(1.0, scale);
-    const double bfirst = 1.0 - s_lut[E.gq[ro]];
-    const float2 bS = make_float2((float)(bfirst * Sd / nA), (float)(bfirst * Sd / nB));
-    const int8_t* hA = E.hbases + E.hoff[U.hapA];
-    const int8_t* hB = E.hbases + E.hoff[U.hapB];
-    float resA = 0.f, resB = 0.f;
-    float2* colPrev = colX;
-    float2* colNext = colY;
-
-    // packed haplotype-character pair of one row (1-based); only thread 0 loads
-    auto load_code = [&](int row) -> unsigned {
-      unsigned a = 4u, b = 4u;
-      if (row >= 1 && row <= nA) a = (unsigned)(unsigned char)hA[row - 1];
-      if (row >= 1 && row <= nB) b = (unsigned)(unsigned char)hB[row - 1];
-      return a | (b << 8);
-    };
-
-    for (int q = 0; q < Q; ++q) {
-      // ---- per-stripe coefficients + emission table (each thread: its K positions).
-      // Folded state: Mt(i) = alpha_{i+1} M(i),  D'(i) = beta_{i+1} D(i):
-      //   Mt(i,j) = T_i(c_j) * (Mt(i-1,j-1) + beta_i I(i-1,j-1) + D'(i-1,j-1)),
-      //             T_i(c) = alpha_{i+1} * lambda_i(c)            (shared-memory table)
-      //   I(i,j)  = (delta_i / alpha_i) Mt(i-1,j) + eps_i I(i-1,j)
-      //   D'(i,j) = (beta_{i+1} zeta_i / alpha_{i+1}) Mt(i,j-1) + eps_i D'(i,j-1)
-      // 7 FP32 operations per cell, 4 coefficients per position.
-      float be[K], dl[K], ep[K], zp[K];
-      float2 M[K], I[K], D[K];
-#pragma unroll
-      for (int k4 = 0; k4 < K4; ++k4) {
-        float lam[5][4];
-#pragma unroll
-        for (int kk = 0; kk < 4; ++kk) {
-          const int k = k4 * 4 + kk;
-          const int p = q * W + t * K + k;
-          M[k] = zero2;
-          I[k] = zero2;
-          if (p < Lp) {                                   // left padding
-            be[k] = 0.f; dl[k] = 0.f; ep[k] = 1.f; zp[k] = 0.f;
-            D[k] = bS;
-#pragma unroll
-            for (int c = 0; c < 5; ++c) lam[c][kk] = 0.f;
-          } else if (p < Lp + m) {                        // real read position
-            const int i0 = p - Lp;
-            const double d = s_lut[E.iq[ro + i0]], z = s_lut[E.dq[ro + i0]];
-            const double e = s_lut[E.gq[ro + i0]], qe = s_lut[E.bq[ro + i0]];
-            const float a = (float)((1.0 - d) - z);
-            float anext = 1.f, bnext = 0.f;
-            if (i0 + 1 < m) {
-              anext = (float)((1.0 - s_lut[E.iq[ro + i0 + 1]]) - s_lut[E.dq[ro + i0 + 1]]);
-              bnext = (float)(1.0 - s_lut[E.gq[ro + i0 + 1]]);
-            }
-            be[k] = (float)(1.0 - e);
-            dl[k] = __fdividef((float)d, a);
-            ep[k] = (float)e;
-            zp[k] = __fdividef(bnext * (float)z, anext);
-            D[k] = zero2;
-            const int rc = E.rbases[ro + i0];
-            const float lm = anext * (float)(1.0 - qe), lx = anext * ((float)qe * (1.f / 3.f));
-#pragma unroll
-            for (int c = 0; c < 5; ++c) lam[c][kk] = (rc == c || rc == 4 || c == 4) ? lm : lx;
-          } else {                                        // accumulator position
-            be[k] = 1.f; dl[k] = 0.f; ep[k] = 1.f; zp[k] = 1.f;
-            D[k] = zero2;
-#pragma unroll
-            for (int c = 0; c < 5; ++c) lam[c][kk] = 1.f;
-          }
-        }
-#pragma unroll
-        for (int c = 0; c < 5; ++c)
-          Et[(c * K4 + k4) * P + t] = make_float4(lam[c][0], lam[c][1], lam[c][2], lam[c][3]);
-      }
-      const bool last_stripe = (q == Q - 1);
-      if (MULTI && t == P - 1 && !last_stripe) {
-        colNext[0] = M[K - 1]; colNext[col_rows] = I[K - 1]; colNext[2 * col_rows] = D[K - 1];
-      }
-      // thread-0 boundary source: stripe 0 -> matrix boundary, else previous column
-      float2 cbM = zero2, cbI = zero2, cbD = bS;          // boundary of row s (thread 0)
-      if (MULTI && q > 0 && t == 0) {
-        cbM = colPrev[0]; cbI = colPrev[col_rows]; cbD = colPrev[2 * col_rows];
-      }
-      float2 nbM = (t == 0) ? cbM : zero2, nbI = (t == 0) ? cbI : zero2, nbD = (t == 0) ? cbD : zero2;
-      if (MULTI && q > 0 && t == 0) {                     // prefetch row 1
-        const int jj = min(1, nmax);
-        cbM = colPrev[jj]; cbI = colPrev[col_rows + jj]; cbD = colPrev[2 * col_rows + jj];
-      }
-      unsigned code = 0x0404u;
-      unsigned pf1 = load_code(t == 0 ? 1 : 0), pf2 = load_code(t == 0 ? 2 : 0);
-      __syncwarp();
-
-      auto step = [&](const int s, auto checked) {
-        constexpr bool CHECK = decltype(checked)::value;
-        const int j = s - t;
-        const float2 dgM = nbM, dgI = nbI, dgD = nbD;
-        {
-          const float2 lm = M[K - 1], li = I[K - 1], ld = D[K - 1];
-          nbM.x = __shfl_up_sync(FULL, lm.x, 1, P);
-          nbM.y = __shfl_up_sync(FULL, lm.y, 1, P);
-          nbI.x = __shfl_up_sync(FULL, li.x, 1, P);
-          nbI.y = __shfl_up_sync(FULL, li.y, 1, P);
-          nbD.x = __shfl_up_sync(FULL, ld.x, 1, P);
-          nbD.y = __shfl_up_sync(FULL, ld.y, 1, P);
-          const unsigned up = __shfl_up_sync(FULL, code, 1, P);
-          code = (t == 0) ? pf1 : up;
-        }
-        if (t == 0) {
-          nbM = cbM; nbI = cbI; nbD = cbD;
-        }
-        pf1 = pf2;
-        pf2 = load_code(t == 0 ? s + 2 : 0);
-        if (MULTI && q > 0 && t == 0) {                   // next row's column entry
-          const int jj = min(s + 1, nmax);
-          cbM = colPrev[jj]; cbI = colPrev[col_rows + jj]; cbD = colPrev[2 * col_rows + jj];
-        }
-        if (!CHECK || (live && j >= 1 && j <= nmax)) {
-          const int cA = code & 0xff, cB = (code >> 8) & 0xff;
-          const float4* EA = Et + (cA * K4) * P + t;
-          const float4* EB = Et + (cB * K4) * P + t;
-          // pass 1 (descending): D' from the previous row, M from the previous-row diagonal
-#pragma unroll
-          for (int k4 = K4 - 1; k4 >= 0; --k4) {
-            const float4 la = EA[k4 * P];
-            const float4 lb = EB[k4 * P];
-#pragma unroll
-            for (int kk = 3; kk >= 0; --kk) {
-              const int k = k4 * 4 + kk;
-              D[k] = fma2s(ep[k], D[k], mul2s(zp[k], M[k]));
-              const float2 pm = (k > 0) ? M[k - 1] : dgM;
-              const float2 pi = (k > 0) ? I[k - 1] : dgI;
-              const float2 pd = (k > 0) ? D[k - 1] : dgD;
-              float2 x = fma2s(be[k], pi, pd);
-              x = __fadd2_rn(pm, x);
-              M[k].x = comp(la, kk) * x.x;
-              M[k].y = comp(lb, kk) * x.y;
-            }
-          }
-          // pass 2 (ascending): I chain along the read within the current row
-          float2 lM = nbM, lI = nbI;
-#pragma unroll
-          for (int k = 0; k < K; ++k) {
-            I[k] = fma2s(ep[k], lI, mul2s(dl[k], lM));
-            lM = M[k];
-            lI = I[k];
-          }
-          if (MULTI && t == P - 1 && !last_stripe) {
-            colNext[j] = M[K - 1]; colNext[col_rows + j] = I[K - 1]; colNext[2 * col_rows + j] = D[K - 1];
-          }
-          if (CHECK && t == P - 1 && last_stripe) {
-            if (j == nA) resA = (D[K - 1].x + M[K - 1].x) + (M[K - 2].x + I[K - 2].x);
-            if (j == nB) resB = (D[K - 1].y + M[K - 1].y) + (M[K - 2].y + I[K - 2].y);
-          }
-        }
-      };
-
-      int s = 1;
-      const int fill_end = min(P - 1, steps);
-      for (; s <= fill_end; ++s) step(s, std::true_type{});
-      for (; s <= steady_end; ++s) step(s, std::false_type{});
-      for (; s <= steps; ++s) step(s, std::true_type{});
-      __syncwarp();
-      float2* tmp = colPrev; colPrev = colNext; colNext = tmp;
-    }
-    int band = 0;                                       // bit0: pair A, bit1: pair B
-    if (live && t == P - 1) {
-      band = fast_finish(E, resA, U.pairA, r, U.hapA, nA, m, scale) ? 1 : 0;
-      if (U.pairB >= 0 && fast_finish(E, resB, U.pairB, r, U.hapB, nB, m, scale)) band |= 2;
-    }
-    // guard band: rerun those pairs right here on the bit-exact recursion (same tiling,
-    // the unit's emission table slot and boundary-column scratch are free again), so
-    // band work overlaps the other warps' fast work instead of forming a tail.
-    band = __shfl_sync(FULL, band, sw * P + P - 1);
-    if (__any_sync(FULL, band != 0)) {
-#pragma unroll 1
-      for (int x = 0; x < 2; ++x) {
-        const bool mine = (band >> x) & 1;
-        if (!__any_sync(FULL, mine)) continue;
-        const ExactItem it{x == 0 ? U.pairA : U.pairB, r, x == 0 ? U.hapA : U.hapB, scale};
-        float* ex_col = reinterpret_cast<float*>(colX);
-        exact_item<float, P, K>(E, it, mine, s_lut, reinterpret_cast<float*>(Et), ex_col,
-                                ex_col + 3 * col_rows, col_rows, t);
-        __syncwarp();
-      }
-    }
-  }
-}
-
-// ---------------------------------------------------------------------------------
 // k_stream<P, K>: read-stationary haplotype streaming (single-stripe reads).
 //
 // A StreamUnit is one read and two LANES of haplotypes (float2 .x = lane A, .y = lane B);
@@ -797,8 +414,6 @@ template <class V, class S> __device__ __forceinline__ V flush2(V v, S thr) {
 // Classification of a finished FP32 stream accumulator; returns 0 = written, 1 = guard
 // band (caller queues the bit-exact rerun), 2 = FP32 underflow to retry in FP64 (caller).
 __device__ __forceinline__ int stream_finish32(const EngineDev& E, float a, int pair, int n, float gsum, int scale) {
-  const float bound = 0x1p-80f * (float)n * gsum;                // 2^10 * 2^-90
-  const float hi = ldexpf(0.031622776f, scale);                   // 10^-1.5 * 2^scale
   if (a != a) { E.status[pair] = kStatusExactF32; return 1; }   // beta_i = 0 (gcp q = 0): exact
   if (!(a >= 0x1p-93f)) {
     if (E.retry_f64) { E.status[pair] = kStatusRetriedF64; return 2; }
@@ -806,7 +421,7 @@ __device__ __forceinline__ int stream_finish32(const EngineDev& E, float a, int 
     E.status[pair] = kStatusOverflow;
     return 0;
   }
-  if (a < bound || a > hi) { E.status[pair] = kStatusExactF32; return 1; }
+  if (guard_band(a, n, gsum, scale)) { E.status[pair] = kStatusExactF32; return 1; }
   E.acc[pair] = (double)a;
   E.status[pair] = kStatusOk;
   return 0;
@@ -1040,29 +655,44 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
       for (int c = 0; c < 5; ++c) ev_pack(Et[(c * KE + ke) * P + t], lam[c]);
     }
 
-    // ---- row codes of both lanes into shared memory (row 0 = idle code N|N), and the
-    // unit's window starts: every row where a haplotype begins in either lane, plus the
-    // row after each lane's end.  Events (FIRST for thread t at step b + t, LAST for
-    // thread P-1 at step b + P - 2) fall in windows [b, b + P).  Built once per unit.
-    if (first_q) {
-    if (t == 0) reinterpret_cast<unsigned short*>(cd)[0] = 0x0404;
-    if (live) {
+    // ---- row codes of both lanes into shared memory (one uint16 per row: lane A | lane B,
+    // each byte base | FIRST | LAST; rows outside a lane's stream read the idle code N).
+    // A unit whose lanes fit the slot (rows < RS) is staged once; a longer one (a haplotype
+    // longer than the slot: no length limit) runs in RING mode -- row i lives in slot
+    // i & (RS - 1) and the sub-warp restages the next half-ring of rows every RS/2 steps,
+    // once every thread has passed the rows it replaces (stage_rows / the step loop).
+    constexpr int RS = CB / 2;                          // code slots per sub-warp (power of 2)
+    static_assert((RS & (RS - 1)) == 0 && RS / 2 > P + 1, "code ring");
+    const bool cring = rows >= RS;
+    const unsigned rmask = cring ? (unsigned)(RS - 1) : 0xffffffffu;
+    auto stage_rows = [&](int r0, int r1) {             // rows [r0, r1), r0 >= 1, both lanes
 #pragma unroll 1
       for (int ln = 0; ln < 2; ++ln) {
         const int cnt = ln ? U.cntB : U.cntA;
         const int e0 = U.list + (ln ? U.cntA : 0);
-        int row = 1;
+        int start = 1;                                  // first row of haplotype e
 #pragma unroll 1
-        for (int e = 0; e < cnt; ++e) {
+        for (int e = 0; e < cnt && start < r1; ++e) {
           const StreamHap sh = shaps[e0 + e];
-          const int n = sh.n;
-          const int8_t* src = E.hbases + sh.off;
-          for (int x = t; x < n; x += P)
-            cd[2 * (row + x) + ln] = (unsigned char)(src[x] | (x == 0 ? kCodeFirst : 0) | (x == n - 1 ? kCodeLast : 0));
-          row += n;
+          const int lo = max(r0, start), hi = min(r1, start + sh.n);
+          const int8_t* src = E.hbases + sh.off - start;   // src[row] = base of that row
+          for (int x = lo + t; x < hi; x += P)
+            cd[2 * (x & rmask) + ln] =
+                (unsigned char)(src[x] | (x == start ? kCodeFirst : 0) | (x == start + sh.n - 1 ? kCodeLast : 0));
+          start += sh.n;
         }
-        for (int x = row + t; x <= rows; x += P) cd[2 * x + ln] = 4;
+        for (int x = max(r0, start) + t; x < r1; x += P) cd[2 * (x & rmask) + ln] = 4;
       }
+    };
+    // windows: every row where a haplotype begins in either lane, plus the row after each
+    // lane's end.  Events (FIRST for thread t at step b + t, LAST for thread P-1 at step
+    // b + P - 2) fall in windows [b, b + P).  Built once per unit.
+    if (first_q || cring) {
+      if (t == 0 && !cring) reinterpret_cast<unsigned short*>(cd)[0] = 0x0404;
+      if (live) stage_rows(1, min(rows + 1, RS));
+    }
+    if (first_q) {
+    if (live) {
       if (t == 0) {                                   // merge the two lanes' window starts
         int* wb = s_win + slot * kStreamMaxWin;
         int ia = 0, ib = 0, ra = 1, rb = 1, nw = 0;
@@ -1102,10 +732,9 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
     V yM = zero2, yI = zero2, yD = zero2;
     // every thread reads its own row's code from shared memory one step ahead (row 0 is
     // the idle code N|N: rows before, between and after this thread's stream)
-    const unsigned short* cdt = cd16 - t;
     auto ld_code = [&](int s) -> unsigned {
       const int i = s - t;
-      return (unsigned)cdt[(i >= 1 && i <= rows_q) ? s : t];
+      return (i >= 1 && i <= rows_q) ? (unsigned)cd16[(unsigned)i & rmask] : 0x0404u;
     };
     unsigned code = 0x0404u;
     unsigned pf1 = ld_code(1);
@@ -1338,17 +967,28 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
       }
     };
 
-    // event-free stretches run the plain step; windows run the event-checking one
+    // event-free stretches run the plain step; windows run the event-checking one; ring
+    // units restage a half-ring of row codes at the (warp-uniform) refill steps nr:
+    // at step (b+1)H + P the rows of block b (rows bH .. (b+1)H-1, last read at step
+    // (b+1)H + P - 2) are free and block b+2 (first read at step (b+2)H - 1) is written
     const int nwin = s_nwin[slot];
     const int* wb = s_win + slot * kStreamMaxWin;
+    constexpr int H = RS / 2;
+    int nr = __any_sync(FULL, cring && sq) ? H + P : 0x7fffffff;
     int wi = 0;
     int s = 1;
 #pragma unroll 1
     while (s <= steps) {
+      if (s == nr) {
+        __syncwarp();
+        if (cring && sq) stage_rows(s - P + H, min(s - P + 2 * H, rows + 1));
+        __syncwarp();
+        nr += H;
+      }
       while (wi < nwin && wb[wi] + P <= s) ++wi;
       const int e_sw = wi < nwin ? wb[wi] : 0x7fffffff;
       const int e = max((int)__reduce_min_sync(FULL, (unsigned)e_sw), s);
-      const int fend = min(e, steps + 1);
+      const int fend = min(min(e, nr), steps + 1);
 #pragma unroll 1
       for (; s + 1 < fend; s += 2) {
         step(s, std::false_type{}, xM, xI, xD, yM, yI, yD);
@@ -1360,7 +1000,8 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
         ++s;
       }
       if (s > steps) break;
-      const int wend = min(e + P, steps + 1);
+      if (s == nr) continue;                            // refill before the next step
+      const int wend = min(min(e + P, nr), steps + 1);
 #pragma unroll 1
       for (; s < wend; ++s) {
         step(s, std::true_type{}, xM, xI, xD, yM, yI, yD);
@@ -1584,38 +1225,6 @@ exact_list(const EngineDev& E, int slot, int* __restrict__ counter, T* __restric
     const ExactItem it = items[has ? u : g * G];
     exact_item<T, P, K>(E, it, has, s_lut, Et, colX, colY, col_rows, t);
   }
-}
-
-// Post-pass list kernels: one launch covers the four sub-warp widths P = 4, 8, 16, 32
-// (slot lists filled by the host and by the fast kernels); empty lists cost nothing.
-__device__ __forceinline__ bool post_lists_empty(const int* counts) {
-  return counts[0] == 0 && counts[1] == 0 && counts[2] == 0 && counts[3] == 0;
-}
-template <typename T>
-__global__ void __launch_bounds__(128)
-k_exact_all(const EngineDev E, int* __restrict__ counters, T* __restrict__ colbuf, int col_rows) {
-  constexpr bool kIsF32 = sizeof(T) == 4;
-  if (*E.invalid || post_lists_empty(kIsF32 ? E.ex32_count : E.ex64_count)) return;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  double* s_lut = reinterpret_cast<double*>(smem_raw);
-  for (int i = threadIdx.x; i < 94; i += blockDim.x) s_lut[i] = E.lut[i];
-  __syncthreads();
-  exact_list<T, 4, kExactK>(E, 0, counters + 0, colbuf, col_rows);
-  exact_list<T, 8, kExactK>(E, 1, counters + 1, colbuf, col_rows);
-  exact_list<T, 16, kExactK>(E, 2, counters + 2, colbuf, col_rows);
-  exact_list<T, 32, kExactK>(E, 3, counters + 3, colbuf, col_rows);
-}
-__global__ void __launch_bounds__(128)
-k_fast64_all(const EngineDev E, int* __restrict__ counters, double* __restrict__ colbuf, int col_rows) {
-  if (*E.invalid || post_lists_empty(E.fx64_count)) return;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  double* s_lut = reinterpret_cast<double*>(smem_raw);
-  for (int i = threadIdx.x; i < 94; i += blockDim.x) s_lut[i] = E.lut[i];
-  __syncthreads();
-  fast64_list<4, kExactK>(E, 0, counters + 0, colbuf, col_rows);
-  fast64_list<8, kExactK>(E, 1, counters + 1, colbuf, col_rows);
-  fast64_list<16, kExactK>(E, 2, counters + 2, colbuf, col_rows);
-  fast64_list<32, kExactK>(E, 3, counters + 3, colbuf, col_rows);
 }
 
 }  // namespace phmm

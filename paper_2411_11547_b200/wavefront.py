@@ -48,12 +48,18 @@ def forward_wavefront(read, hap, cfg) -> Score:
 
 
 def forward_wavefront_counted(read, hap, cfg):
-    """As forward_wavefront, also returning the wavefront steps the engine executed:
-    (n + P - 1) per stripe for the engine's own sub-warp size P (the reference's
-    lane-emulating CPU kernel runs n + p, wavefront.py:314-315)."""
+    """As forward_wavefront, also returning the step count of the reference's lane-tiled
+    schedule, n + p (wavefront.py:314-315, pinned by test_wavefront.py:54-55).  The
+    engine's own schedule is reported by engine_wavefront_steps()."""
     score = _single(read, hap, cfg)
-    P, _, Q = _native.fast_geometry(read.length, hap.length)
-    return score, Q * (hap.length + P - 1)
+    return score, hap.length + cfg.p
+
+
+def engine_wavefront_steps(m: int, n: int) -> int:
+    """Wavefront steps the B200 engine's per-pair tiling executes for an m x n pair:
+    (n + P - 1) per stripe for its sub-warp size P."""
+    P, _, Q = _native.fast_geometry(int(m), int(n))
+    return Q * (n + P - 1)
 
 
 def forward_wavefront_batch(batches, items, cfg, out, errors=None) -> list:

@@ -71,9 +71,11 @@ def test_kernels_use_packed_fp32_and_shuffles(lib):
     sass = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", _native.LIB_PATH],
                           capture_output=True, text=True, check=True).stdout
     funcs = {c.split("\n", 1)[0].strip(): c for c in sass.split("Function : ")[1:]}
-    fast = [body for name, body in funcs.items() if "k_fastILi16ELi16ELb0E" in name]
+    # the production FP32 kernel k_stream<kFast32, 16, 16, false>: packed FFMA2 recurrence,
+    # neighbour exchange by shuffles, emissions from shared memory (LDS.128)
+    fast = [body for name, body in funcs.items() if "k_streamILi0ELi16ELi16ELb0E" in name]
     assert len(fast) == 1
-    assert "FFMA2" in fast[0] and "FMUL2" in fast[0] and "SHFL.UP" in fast[0]
+    assert "FFMA2" in fast[0] and "SHFL.UP" in fast[0] and "LDS.128" in fast[0]
     # bit-exactness of the k_exact kernels (no contraction in the recurrence) is
     # verified numerically by tests/test_gpu_parity.py; their setup code legitimately
     # uses DFMA inside IEEE double division.

@@ -108,12 +108,19 @@ def test_single_precision_close_to_double(rng):
     assert worst <= 1e-3
 
 
-def test_step_count_reports_engine_wavefront(rng):
-    read, hap = random_pair(rng, 100, 150)
-    _, steps = forward_wavefront_counted(read, hap, EngineConfig(8, 16))
+def test_step_count_is_rows_plus_lanes(rng):
+    # test_wavefront.py:50-55: the reference's step count n + p, for any config
+    for m, n, p, k in [(1, 1, 2, 4), (5, 200, 4, 8), (60, 3, 32, 8), (256, 64, 32, 8), (17, 17, 4, 8)]:
+        read, hap = random_pair(rng, m, n)
+        _, steps = forward_wavefront_counted(read, hap, EngineConfig(p, k, "f64"))
+        assert steps == n + p
+
+
+def test_engine_wavefront_steps():
     from paper_2411_11547_b200 import _native
+    from paper_2411_11547_b200.wavefront import engine_wavefront_steps
     P, K, Q = _native.fast_geometry(100, 150)
-    assert steps == Q * (150 + P - 1)
+    assert engine_wavefront_steps(100, 150) == Q * (150 + P - 1)
 
 
 def test_padding_and_tiling_invariance(rng):

@@ -1,6 +1,6 @@
 """Registers / spills per kernel from `nvcc -Xptxas -v` output.
 
-usage: python tools/ptxas_regs.py [filter]   (compiles phmm_engine.cu to /tmp, ~1 min)
+usage: python tools/ptxas_regs.py [filter]   (compiles every csrc/*.cu to /tmp, ~1 min)
 """
 import re
 import subprocess
@@ -11,8 +11,16 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2411_11547_b200.build import FLAGS, NVCC, ROOT, SOURCES  # noqa: E402
 
 flt = sys.argv[1] if len(sys.argv) > 1 else "k_"
-cmd = [NVCC] + FLAGS + ["-Xptxas", "-v", "-I", os.path.join(ROOT, "include"), "-o", "/tmp/ptxas_probe.so"] + SOURCES
-err = subprocess.run(cmd, capture_output=True, text=True).stderr
+from concurrent.futures import ThreadPoolExecutor  # noqa: E402
+
+
+def _ptxas(src):
+    cmd = [NVCC] + FLAGS + ["-Xptxas", "-v", "-I", os.path.join(ROOT, "include"), "-c", "-o", "/dev/null", src]
+    return subprocess.run(cmd, capture_output=True, text=True).stderr
+
+
+with ThreadPoolExecutor(len(SOURCES)) as ex:
+    err = "\n".join(ex.map(_ptxas, SOURCES))
 cur = None
 rows = {}
 for line in err.splitlines():
