@@ -20,6 +20,8 @@ SOURCES = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
 HEADERS = sorted(glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(CSRC, "*.cuh"))) + [
     os.path.join(ROOT, "include", "phmm.h")]
 OUT = os.path.join(HERE, "_lib", "libphmm.so")
+GEN_SRC = os.path.join(CSRC, "datagen.cpp")
+GEN_OUT = os.path.join(HERE, "_lib", "libphmm_datagen.so")   # host-only input generator
 OBJ = os.path.join(HERE, "_lib", "obj")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
@@ -41,7 +43,21 @@ def up_to_date() -> bool:
     return not _stale(OUT, SOURCES + HEADERS)
 
 
+def build_datagen(force: bool = False, verbose: bool = False) -> str:
+    """g++ -> libphmm_datagen.so (no CUDA: also used by the CPU tests)."""
+    if not force and not _stale(GEN_OUT, [GEN_SRC]):
+        return GEN_OUT
+    os.makedirs(os.path.dirname(GEN_OUT), exist_ok=True)
+    cmd = ["g++", "-O2", "-std=c++17", "-shared", "-fPIC", "-o", GEN_OUT + ".tmp", GEN_SRC]
+    if verbose:
+        print(" ".join(cmd), file=sys.stderr)
+    subprocess.run(cmd, check=True)
+    os.replace(GEN_OUT + ".tmp", GEN_OUT)
+    return GEN_OUT
+
+
 def build_native(force: bool = False, verbose: bool = False) -> str:
+    build_datagen(force, verbose)
     if not force and up_to_date():
         return OUT
     os.makedirs(OBJ, exist_ok=True)

@@ -52,3 +52,40 @@ def test_workload_shapes():
     c2 = datagen.workload("c2", num_batches=4)
     assert c2.num_pairs == 4 * 16 * 4
     assert set(np.unique(c2.read_len)) == {250} and set(np.unique(c2.hap_len)) == {250}
+
+
+@pytest.fixture(scope="module")
+def native_gen():
+    from paper_2411_11547_b200.build import build_datagen
+    build_datagen()
+
+
+@pytest.mark.parametrize("name", SYNTH)
+def test_native_generator_matches_reference_fixture(native_gen, name):
+    """csrc/datagen.cpp (PCG64 + numpy's bounded-integer algorithms) draws the reference
+    generator's stream element for element."""
+    z = load_golden(name)
+    params = json.loads(str(z["params"]))
+    flat = datagen._native_flat(*(params["args"] + [params["kw"].get(k, d) for k, d in (
+        ("mode", "independent"), ("mutation_rate", datagen.DEFAULT_MUTATION_RATE),
+        ("base_qual", datagen.DEFAULT_BASE_QUAL), ("indel_qual", datagen.DEFAULT_INDEL_QUAL),
+        ("gcp_qual", datagen.DEFAULT_GCP_QUAL))]))
+    assert flat is not None
+    _same(flat, golden_flat(z))
+
+
+@pytest.mark.parametrize("kw", [
+    dict(num_batches=40, reads_per_batch=7, haps_per_batch=3, read_len_spec=(1, 300),
+         hap_len_spec=(1, 200), seed=5, mode="derived", mutation_rate=0.2),
+    dict(num_batches=30, reads_per_batch=3, haps_per_batch=5, read_len_spec=(1, 40),
+         hap_len_spec=(1, 40), seed=6, mode="independent", base_qual=(0, 93), indel_qual=(0, 93),
+         gcp_qual=(0, 5)),
+    dict(num_batches=25, reads_per_batch=4, haps_per_batch=2, read_len_spec=60, hap_len_spec=60,
+         seed=7, mode="derived", base_qual=17, indel_qual=(44, 45), gcp_qual=(9, 11)),
+    dict(num_batches=300, reads_per_batch=64, haps_per_batch=8, read_len_spec=(50, 250),
+         hap_len_spec=(100, 600), seed=datagen.SEED + 4, mode="derived")])
+def test_native_generator_matches_numpy_stream(native_gen, kw):
+    """Edge shapes (reads longer than the shortest haplotype, equal lengths -> empty start
+    range, full quality range, fixed specs, c5's first 300 batches) against the numpy
+    restatement."""
+    _same(datagen.generate_synthetic_flat(**kw, native=True), datagen.generate_synthetic_flat(**kw, native=False))

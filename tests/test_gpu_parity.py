@@ -157,3 +157,29 @@ def test_prepare_execute_fetch_is_rerunnable(engine):
     c, sc, _ = engine.score(flat, F32, 0)
     assert np.array_equal(a, c)
     assert st2.device_ms > 0 and st2.fast_ms > 0 and st2.kernel_launches >= 2
+
+
+def test_million_pair_gatk_call_against_oracle(engine):
+    """A >= 1M-pair GATK-shaped call (the c5 prefix of 2,048 batches = 1,048,576 pairs)
+    with the FP64 retry: the big-call branches (4 pipelined chunk contexts, longer
+    device-built retry units) against the oracle -- f32 for every pair, f64 on the
+    flagged subset; chunked-call stats are filled (device time span, FP32 phases)."""
+    flat = datagen.workload("c5", num_batches=2048)
+    assert flat.num_pairs >= 1 << 20
+    ofl = oracle.Flat(**flat.as_dict())
+    ref32, k32 = oracle.score(ofl, "f32")
+    scores, status, stats = engine.score(flat, F32, _native.FLAG_RETRY_F64)
+    flagged = k32 == 1
+    assert flagged.mean() > 0.1
+    assert np.array_equal((status & _native.ST_RETRIED_F64) != 0, flagged)
+    rest = ~flagged
+    _check_fast(scores[rest], status[rest], ref32[rest], k32[rest], "c5[:2048]")
+    pr, ph = flat.pair_index()
+    idx = np.flatnonzero(flagged)
+    acc64, st64 = oracle.score_raw(ofl, "f64", 0, pairs=(pr[idx], ph[idx]))
+    ref64 = oracle.finish(acc64, st64, 0)
+    assert np.array_equal(status[idx] & KIND, st64)
+    fin = st64 == 0
+    assert _rel(scores[idx][fin], ref64[fin]).max() <= RETRY_REL_TOL
+    assert stats.num_pairs == flat.num_pairs
+    assert stats.device_ms > 0 and stats.fast_ms > 0 and stats.h2d_ms > 0

@@ -232,3 +232,68 @@ def test_random_batches_all_modes_against_oracle(engine, seed):
     ref64, k64 = oracle.score(ofl, "f64")
     s, st, _ = engine.score(flat, config_tuples(default_configs("f64")), 0)
     assert np.array_equal(st & KIND, k64) and np.array_equal(s, ref64, equal_nan=True)
+
+
+def test_long_haplotypes_ring_mode_all_modes(engine, rng):
+    """Haplotypes longer than a sub-warp slot's row-code capacity (P=4: 510, P=16: 2046,
+    P=32: 4094 rows) stream in ring mode (row codes restaged every half ring): short
+    reads x haplotypes of 511-8000 bases, and long (striped) reads x 4095-6000-base
+    haplotypes; fast FP32, FP64 retry, exact mode and f64 configurations."""
+    flat = _flat(rng, [([60, 14, 250], [511, 512, 1100, 2047, 2048, 2049], "derived"),
+                       ([120, 255], [4095, 4096, 4097, 8000], "derived"),
+                       ([90, 200], [5000, 3, 600], "random"),
+                       ([700, 1023], [4095, 6000], "derived"),
+                       ([600], [4500, 10], "random")])
+    k32 = _check(engine, flat)
+    assert (k32 == 0).any()
+    ofl = oracle.Flat(**flat.as_dict())
+    ref32, _ = oracle.score(ofl, "f32")
+    s, st, _ = engine.score(flat, F32, _native.FLAG_EXACT)
+    assert np.array_equal(st & KIND, k32) and np.array_equal(s, ref32, equal_nan=True)
+    ref64, k64 = oracle.score(ofl, "f64")
+    s, st, _ = engine.score(flat, config_tuples(default_configs("f64")), 0)
+    assert np.array_equal(st & KIND, k64) and np.array_equal(s, ref64, equal_nan=True)
+
+
+@pytest.mark.parametrize("scale", [0, 24, 120])
+def test_guard_band_adversarial_qualities(engine, scale):
+    """Adversarial transition qualities for the guard band: low gap-
+    continuation (eps near 1: g_i up to n) and low deletion / insertion qualities make
+    n*Gsum huge, and small boundary scales put short, high-likelihood pairs (|score| of a
+    few units) near the band.  Flag sets must equal the reference's and values stay
+    within 1e-4 relative."""
+    from paper_2411_11547_b200 import EngineConfig
+    rng = np.random.default_rng(4242 + scale)
+    rb, bq, iq, dq, gq, hb, rlen, hlen, bro, bho = [], [], [], [], [], [], [], [], [0], [0]
+    for _ in range(40):
+        nr, nh = int(rng.integers(1, 6)), int(rng.integers(1, 8))
+        hl = [int(x) for x in rng.integers(1, 400, size=nh)]
+        base = rng.integers(0, 4, size=max(hl) + 300, dtype=np.int8)
+        for n in hl:
+            hb.append(base[:n].copy()); hlen.append(n)
+        for _ in range(nr):
+            m = int(rng.integers(1, 120))
+            st0 = int(rng.integers(0, 200))
+            rb.append(base[st0:st0 + m].copy()); rlen.append(m)
+            bq.append(rng.integers(20, 94, size=m).astype(np.uint8))
+            iq.append(rng.integers(4, 12, size=m).astype(np.uint8))    # delta + zeta < 1
+            dq.append(rng.integers(4, 12, size=m).astype(np.uint8))
+            gq.append(rng.integers(1, 4, size=m).astype(np.uint8))
+        bro.append(bro[-1] + nr); bho.append(bho[-1] + nh)
+    cat = np.concatenate
+    flat = FlatBatches(read_bases=cat(rb), bq=cat(bq), iq=cat(iq), dq=cat(dq), gq=cat(gq),
+                       read_off=np.concatenate([[0], np.cumsum(rlen)]).astype(np.int64),
+                       hap_bases=cat(hb), hap_off=np.concatenate([[0], np.cumsum(hlen)]).astype(np.int64),
+                       batch_read_off=np.asarray(bro, np.int64), batch_hap_off=np.asarray(bho, np.int64))
+    cfg = config_tuples([EngineConfig(32, 32, "f32", scale_log2=scale)])
+    ofl = oracle.Flat(**flat.as_dict())
+    pr, ph = flat.pair_index()
+    acc, kind = oracle.score_raw(ofl, "f32", scale)
+    ref = oracle.finish(acc, kind, scale)
+    # the (one) config binds reads <= 1024: every pair is scored
+    s, st, _ = engine.score(flat, cfg, 0)
+    assert np.array_equal(st & KIND, kind)
+    ok = kind == 0
+    assert ok.sum() > 100
+    rel = np.abs(s[ok] - ref[ok]) / np.maximum(np.abs(ref[ok]), 1e-300)
+    assert rel.max() <= REL_TOL, rel.max()
