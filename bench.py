@@ -2,24 +2,32 @@
 """Benchmark of the Pair-HMM forward hot path (BASELINE.json metric: GCUPS).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload c2] [--cpu-seconds 10] [--no-secondary]
+                    [--workload c5] [--cpu-seconds 10] [--no-secondary]
 
-One step = one pass of the engine over the whole workload (default c2 =
-BASELINE.json configs[1]: 65,536 pairs 250x250, FP32, 1 B200).  Under torchrun
-each rank scores its own seeded copy of the workload on its GPU (weak scaling;
-pairs are independent, no data-path collective); the timed region is bracketed
-by a barrier + device sync and the time is the MAX over ranks.
+Workload (default c5 = BASELINE.json configs[4], the config the 1/2/4/8-GPU metric is
+quoted on; it fits one B200): ONE batch list of 10,000,384 GATK-shaped pairs (reads
+50-250 x haplotypes 100-600, derived, seed 20240811+4), scored with the GATK FP64 retry
+(FP32 fast path + guard band + bit-exact FP32 reruns + FP64 retry of FP32-underflowed
+pairs).  One step = one pass of the engine over the whole batch list.
 
-  value     GCUPS with inputs resident in HBM: true cells / engine device time
-            (CUDA events on the engine stream, phmm_execute), L2 flushed between steps.
+Under torchrun the batch list is SHARDED: every rank draws the same list, takes its
+cost-balanced, bin-stratified share of the reads (shards.plan_shards: one read with all
+of its batch's haplotypes is the planning unit) and scores it on its GPU; results are
+gathered on the host into global-id order through shared memory (shards.HostGather).
+No collective on the data path — NCCL only carries the max-over-ranks timing.
+
+  value     GCUPS with inputs resident in HBM: true cells (all ranks) / max over ranks of
+            the engine device time per step (CUDA events on the engine stream, phmm_execute).
   e2e       GCUPS through the C-ABI call phmm_score from pinned HOST buffers (H2D of the
-            inputs, planning, kernels, D2H of scores + status, finishing), wall clock.
-  roofline  the dominant kernel (k_stream, FP32 streaming wavefront) against the FP32-FMA
-            roofline of SURVEY.md §8(d): 148 SMs x 128 lanes x f_SM / 8 ops per cell.
+            inputs, planning, kernels, D2H of scores + status, finishing) plus the host
+            gather into the global result arrays, wall clock, max over ranks.
+  roofline  the dominant kernel (k_stream FP32 streaming wavefront, all tiling bins of the
+            FP32 phase) against the FP32-FMA roofline of SURVEY.md §8(d): 148 SMs x 128
+            lanes x f_SM / 8 ops per cell; plus the whole step and a per-phase breakdown.
   cpu_baseline  the C oracle (a port of the reference recursion, oracle/) on the host
             cores, bounded sample of the same workload, rank 0 only.
---impl reference times that CPU port alone (the reference package itself is not
-installable on the GPU box: it is numba-based and absent there).
+--impl reference times that CPU port alone (the reference package itself is numba-based and
+absent on the GPU box).
 """
 from __future__ import annotations
 
@@ -38,14 +46,19 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 WORKLOAD_TEXT = {
+    "c5": "c5: 10,000,384-pair GATK-shaped batch list (19,532 batches x 64 reads x 8 haps; reads 50-250 x "
+          "haps 100-600, derived, seed 20240811+4), FP64 retry of FP32-underflowed pairs",
     "c2": "c2: 65,536 uniform pairs 250x250 FP32 on 1xB200 (peak-kernel microbench), derived, seed 20240811+1",
     "c3": "c3: GATK-shaped 65,536 pairs, reads 50-250 x haps 100-600, derived, seed 20240811+2",
     "c1": "c1: 1,000 pairs 100x150, fixed qualities",
     "c4": "c4: 2,048 long pairs, reads 512-1024 x haps 1024-2048",
-    "c5": "c5: 10M-pair mixed-length batch (reads 50-250, haps 100-600)",
 }
-FP32_LANES_PER_SM = 128          # tools/microbench/pipes.cu: FFMA 113/clk/SM of 128 nominal
+# headline flags per workload: c5/c3/c4 GATK FP64 retry; c1/c2 the reference's FP32 semantics
+RETRY_WORKLOADS = ("c5", "c3", "c4")
+FP32_LANES_PER_SM = 128          # tools/microbench/pipes.cu: FFMA 128 lanes/clk/SM
+FP64_LANES_PER_SM = 64           # tools/microbench/pipes.cu: DFMA 64 lanes/clk/SM
 OPS_PER_CELL = 8                 # 1 FADD + 4 FMUL + 3 FFMA per cell
+PHASES = ("precompute", "fp32_stream", "post_a_exact32_and_fp64_units", "post_bc_fp64_per_pair")
 
 
 def dist_env():
@@ -132,26 +145,51 @@ def pinned_copy(flat):
     return out
 
 
-def cpu_baseline(flat, seconds):
-    """Time the C oracle (reference recursion port) on a bounded prefix of the workload."""
+def pair_cells(flat):
+    pr, ph = flat.pair_index()
+    return flat.read_len[pr] * flat.hap_len[ph]
+
+
+def cpu_baseline(flat, seconds, flags_retry=False):
+    """Time the C oracle (reference recursion port) on a bounded prefix of the workload:
+    FP32 on every pair of the prefix, plus (GATK semantics) FP64 on its FP32-flagged pairs."""
     from oracle import oracle
     oracle.build()
     ofl = oracle.Flat(**flat.as_dict())
     pr, ph = flat.pair_index()
     cores = os.cpu_count() or 1
-    done = cells = 0
+    done = cells = retried = 0
     t0 = time.perf_counter()
     chunk = 256
     while done < pr.shape[0] and time.perf_counter() - t0 < seconds:
         sl = slice(done, min(done + chunk, pr.shape[0]))
-        oracle.score_raw(ofl, "f32", 120, threads=cores, pairs=(pr[sl], ph[sl]))
+        acc, st = oracle.score_raw(ofl, "f32", 120, threads=cores, pairs=(pr[sl], ph[sl]))
+        if flags_retry:
+            bad = np.flatnonzero(st == oracle.OVERFLOW)
+            if bad.size:
+                oracle.score_raw(ofl, "f64", 0, threads=cores, pairs=(pr[sl][bad], ph[sl][bad]))
+                retried += int(bad.size)
         cells += int((flat.read_len[pr[sl]] * flat.hap_len[ph[sl]]).sum())
         done = sl.stop
-        chunk = min(chunk * 2, 8192)
+        chunk = min(chunk * 2, 65536)
     dt = time.perf_counter() - t0
     return {"value": cells / dt / 1e9, "unit": "GCUPS", "cores": cores, "kind": "port",
-            "sample": "first %d of %d pairs (%.3g cells) of the same workload, FP32, oracle/phmm_oracle.c "
-                      "with %d threads, %.1f s" % (done, pr.shape[0], cells, cores, dt)}
+            "cpu_model": cpu_model(),
+            "sample": "first %d of %d pairs (%.3g cells) of the same workload, FP32%s, oracle/phmm_oracle.c "
+                      "with %d threads, %.1f s" % (done, pr.shape[0], cells,
+                                                    " + FP64 on its %d FP32-flagged pairs" % retried
+                                                    if flags_retry else "", cores, dt)}
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
 
 
 def run_reference(args, ws, rank):
@@ -163,7 +201,7 @@ def run_reference(args, ws, rank):
     per_step = []
     base = None
     for i in range(args.warmup + args.steps):
-        b = cpu_baseline(flat, args.cpu_seconds / max(1, args.steps))
+        b = cpu_baseline(flat, args.cpu_seconds / max(1, args.steps), args.workload in RETRY_WORKLOADS)
         if i >= args.warmup:
             per_step.append(b["value"])
             base = b
@@ -171,7 +209,8 @@ def run_reference(args, ws, rank):
     base = dict(base, value=v)
     line = {"impl": "reference", "metric": "GCUPS (cell updates/s)", "value": v, "unit": "GCUPS",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "higher_is_better": True, "scaling": "weak" if args.workload != "c5" else "strong",
+            "vs_baseline": None, "dtype": "f32",
             "data": "synthetic", "config": {"workload": WORKLOAD_TEXT.get(args.workload, args.workload)},
             "cpu_baseline": base,
             "e2e": {"value": v, "unit": "GCUPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -192,9 +231,17 @@ def reduce_time_cells(seconds, cells, ws, device):
     return float(t.item()), float(c.item())
 
 
-def shard_seed_offset(rank):
-    """Weak scaling: rank r scores its own copy of the workload drawn with seed + r."""
-    return int(rank)
+def shard_for_rank(flat, ws, rank):
+    """This rank's share of the ONE batch list (shards.plan_shards); ws == 1: all of it."""
+    from paper_2411_11547_b200.shards import Shard, make_shard, plan_shards, read_costs
+    if ws == 1:
+        return Shard(flat, np.arange(flat.num_pairs, dtype=np.int64), 0.0)
+    owner = plan_shards(flat, ws)
+    return make_shard(flat, owner, rank, read_costs(flat)[0])
+
+
+def gather_name():
+    return "phmm_bench_%s_%s" % (os.environ.get("MASTER_PORT", "0"), os.environ.get("TORCHELASTIC_RUN_ID", "x"))
 
 
 def secondary(ctx, name, flags, steps=3):
@@ -205,28 +252,48 @@ def secondary(ctx, name, flags, steps=3):
     cfg = config_tuples(default_configs("f32"))
     ctx.prepare(flat, cfg, flags)
     ctx.execute()
-    ms, fast = [], []
+    ms, fast, ph = [], [], []
     for _ in range(steps):
         ctx.execute()
         d, f, _n = ctx.last_timing()
         ms.append(d)
         fast.append(f)
+        ph.append(ctx.last_phases())
     _, _, st = ctx.fetch()
     cells = st.total_cells
     return {"workload": WORKLOAD_TEXT.get(name, name), "gcups": cells / (np.mean(ms) * 1e-3) / 1e9,
             "pairs": st.num_pairs, "cells": cells, "fast_pairs": st.fast_pairs,
             "exact_pairs": st.exact_pairs, "f64_retry_pairs": st.f64_pairs,
             "device_ms": float(np.mean(ms)), "fast_ms": float(np.mean(fast)),
+            "fp32_phase_gcups": cells / (np.mean(fast) * 1e-3) / 1e9,
+            "phases_ms": dict(zip(PHASES, np.mean(ph, axis=0).tolist())),
             "flags": "retry_f64" if flags & 1 else "reference-f32"}
+
+
+def e2e_run(name, steps=3):
+    """Wall GCUPS of the drop-in API pipeline.run(batches) from reference-style Batch
+    objects (flatten + budget check + engine call + report), c2/c3-sized."""
+    from paper_2411_11547_b200 import datagen, default_configs, run
+    kw = dict(datagen.WORKLOADS[name])
+    batches = datagen.generate_synthetic(**kw)
+    cfg = default_configs("f32")
+    run(batches, cfg)
+    vals = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        _, rep = run(batches, cfg)
+        vals.append(rep.total_cells / (time.perf_counter() - t0) / 1e9)
+    return {"workload": WORKLOAD_TEXT.get(name, name), "api": "pipeline.run(list[Batch])",
+            "gcups": float(np.median(vals))}
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="c2")
+    ap.add_argument("--workload", default="c5")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-secondary", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -240,18 +307,21 @@ def main():
     from paper_2411_11547_b200 import _native, datagen, default_configs
     from paper_2411_11547_b200.build import build_native
     from paper_2411_11547_b200.pipeline import config_tuples
+    from paper_2411_11547_b200.shards import HostGather
 
     build_native()
+    # PHMM_BENCH_SHARE_DEVICE=1 (testing the N>1 path on a 1-GPU box): every rank on cuda:0,
+    # timing reductions over gloo
+    share = os.environ.get("PHMM_BENCH_SHARE_DEVICE") == "1"
+    if share:
+        local = 0
     torch.cuda.set_device(local)
+    red_dev = "cpu" if share else "cuda"
     if ws > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-
-    flat = datagen.workload(args.workload, seed_offset=shard_seed_offset(rank))
-    cfg = config_tuples(default_configs("f32"))
-    flags = 0                                        # reference f32 semantics (c2 has no underflow)
-    ctx = _native.Context(local)
-    n_pairs = ctx.prepare(flat, cfg, flags)
-    l2_flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     def barrier():
         torch.cuda.synchronize()
@@ -259,10 +329,22 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
+    full = datagen.workload(args.workload)
+    t_plan = time.perf_counter()
+    shard = shard_for_rank(full, ws, rank)
+    t_plan = time.perf_counter() - t_plan
+    flat = shard.flat
+    n_total = full.num_pairs
+    cfg = config_tuples(default_configs("f32"))
+    flags = _native.FLAG_RETRY_F64 if args.workload in RETRY_WORKLOADS else 0
+    ctx = _native.Context(local)
+    n_pairs = ctx.prepare(flat, cfg, flags)
+    l2_flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+
     for _ in range(args.warmup):
         ctx.execute()
     barrier()
-    dev_ms, fast_ms = [], []
+    dev_ms, fast_ms, phases = [], [], []
     launches = 0
     with ClockSampler(local) as clocks:
         for _ in range(args.steps):
@@ -272,27 +354,49 @@ def main():
             d, f, n = ctx.last_timing()          # CUDA events on the engine stream
             dev_ms.append(d)
             fast_ms.append(f)
+            phases.append(ctx.last_phases())
             launches += n
         barrier()
     scores, status, st = ctx.fetch()
     cells = st.total_cells
-    t_max, total_cells = reduce_time_cells(float(np.sum(dev_ms)) * 1e-3, cells, ws, "cuda")
+    t_max, total_cells = reduce_time_cells(float(np.sum(dev_ms)) * 1e-3, cells, ws, red_dev)
     value = total_cells * args.steps / t_max / 1e9
+    fast_max, _ = reduce_time_cells(float(np.sum(fast_ms)) * 1e-3, 0, ws, red_dev)
+    retried = (status & _native.ST_RETRIED_F64) != 0
+    retry_cells = int(pair_cells(flat)[retried].sum()) if retried.any() else 0
 
-    # ---- e2e through the C-ABI from pinned host buffers (phmm_score)
+    # ---- e2e through the C-ABI from pinned host buffers (phmm_score) + host gather
     # (caller-owned result buffers, reused across calls like any C-ABI caller's)
     pflat = pinned_copy(flat)
     res = np.empty(pflat.num_pairs, np.float64)
     res_st = np.empty(pflat.num_pairs, np.uint8)
+    gather = None
+    if ws > 1:
+        if rank == 0:
+            gather = HostGather(gather_name(), n_total, create=True)
+        dist.barrier()
+        if rank != 0:
+            gather = HostGather(gather_name(), n_total, create=False)
     for _ in range(2):
         ctx.score(pflat, cfg, flags, out=res, status=res_st)
     barrier()
     t0 = time.perf_counter()
     for _ in range(args.steps):
         out, ost, est = ctx.score(pflat, cfg, flags, out=res, status=res_st)
+        if gather is not None:
+            gather.put(shard.gids, out, ost)
+    if ws > 1:
+        dist.barrier()
     torch.cuda.synchronize()
-    e2e_max, _ = reduce_time_cells(time.perf_counter() - t0, 0, ws, "cuda")
+    e2e_max, _ = reduce_time_cells(time.perf_counter() - t0, 0, ws, red_dev)
     e2e_value = total_cells * args.steps / e2e_max / 1e9
+    gathered_ok = None
+    if gather is not None:
+        dist.barrier()
+        if rank == 0:   # every global id was written by exactly one rank, statuses consistent
+            gathered_ok = bool(np.array_equal(np.isnan(gather.scores), (gather.status & 0x0F) != 0))
+        dist.barrier()
+        gather.close()
 
     if rank != 0:
         dist.destroy_process_group() if ws > 1 else None
@@ -304,58 +408,81 @@ def main():
     props = torch.cuda.get_device_properties(local)
     nsm = props.multi_processor_count
     peak = nsm * FP32_LANES_PER_SM * sm_max * 1e6 / OPS_PER_CELL / 1e9
+    peak64 = nsm * FP64_LANES_PER_SM * sm_max * 1e6 / OPS_PER_CELL / 1e9
     fast_gcups = cells / (float(np.mean(fast_ms)) * 1e-3) / 1e9
-    traffic = profile_traffic()
+    ph_mean = np.mean(phases, axis=0)
+    traffic = profile_traffic(args.workload)
     line = {
         "metric": "GCUPS (cell updates/s)", "value": value, "unit": "GCUPS", "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_max / args.steps * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "higher_is_better": True, "scaling": "strong" if args.workload == "c5" else "weak",
+        "vs_baseline": None, "dtype": "f32",
         "data": "synthetic",
-        "config": {"workload": WORKLOAD_TEXT.get(args.workload, args.workload), "pairs_per_gpu": n_pairs,
-                   "cells_per_step_per_gpu": cells, "l2": "flushed between timed steps (256 MiB write)",
-                   "parallelism": "dp%d: independent per-GPU shards, no collective" % ws,
-                   "mode": "fast FP32 + guard band + exact FP32 (reference f32 semantics)"},
+        "config": {"workload": WORKLOAD_TEXT.get(args.workload, args.workload), "pairs_total": n_total,
+                   "pairs_rank0": n_pairs, "cells_per_step_total": int(total_cells),
+                   "l2": "inputs (%.2f GB) larger than L2, and L2 flushed between timed steps (256 MiB write)"
+                         % (flat.nbytes() / 1e9),
+                   "parallelism": ("dp%d: one batch list sharded by cost-balanced length bins "
+                                   "(shards.plan_shards), host gather, no collective" % ws) if ws > 1 else "1 GPU",
+                   "mode": ("fast FP32 + guard band (bit-exact FP32 reruns) + FP64 retry of FP32-underflowed pairs"
+                            if flags & _native.FLAG_RETRY_F64 else "fast FP32 + guard band (reference f32 semantics)")},
         "roofline": {"bound": "fp32", "achieved": fast_gcups, "peak": peak, "unit": "GCUPS",
                      "frac": fast_gcups / peak, "traffic": traffic,
-                     "kernel": "k_stream<FP32,16,16> (FP32 streaming wavefront)",
+                     "kernel": "k_stream<kFast32,P,K> FP32 streaming wavefront (all tiling bins of the FP32 phase)",
+                     "algorithmic_units": "every pair's true m*n cells once (SURVEY §8(d): 8 FP32-pipe ops/cell)",
                      "peak_source": "SURVEY.md §8(d): %d SMs x %d FP32 lanes x sm_max_mhz %.0f (MEASURED_PEAKS.json) / %d ops per cell"
                                     % (nsm, FP32_LANES_PER_SM, sm_max, OPS_PER_CELL),
                      "frac_at_sampled_clock": (fast_gcups / (nsm * FP32_LANES_PER_SM * clk["sm_mhz"] * 1e6 / OPS_PER_CELL / 1e9)
                                                if clk.get("sm_mhz") else None),
-                     "fast_share_of_step": float(np.mean(fast_ms) / np.mean(dev_ms))},
-        "e2e": {"value": e2e_value, "unit": "GCUPS", "h2d_bytes_per_step": int(est.h2d_bytes),
-                "d2h_bytes_per_step": int(est.d2h_bytes)},
+                     "whole_step_frac": value / ws / peak,
+                     "fast_share_of_step": float(np.mean(fast_ms) / np.mean(dev_ms)),
+                     "phases_ms": dict(zip(PHASES, ph_mean.tolist())),
+                     "fp64_retry": {"pairs": int(retried.sum()), "cells": retry_cells,
+                                    "gcups_in_post_pass_a": (retry_cells / (ph_mean[2] * 1e-3) / 1e9) if ph_mean[2] > 0 else None,
+                                    "peak_fp64_gcups": peak64}},
+        "e2e": {"value": e2e_value, "unit": "GCUPS", "h2d_bytes_per_step": int(est.h2d_bytes) * ws,
+                "d2h_bytes_per_step": int(est.d2h_bytes) * ws,
+                "api": "phmm_score (C-ABI) from pinned host buffers" + (" + shared-memory host gather" if ws > 1 else "")},
         "clocks": clk,
         "gpu_launches": int(launches),
         "engine": {"device_ms_mean": float(np.mean(dev_ms)), "fast_ms_mean": float(np.mean(fast_ms)),
+                   "fast_ms_max_over_ranks": fast_max / args.steps * 1e3,
                    "fast_pairs": int(st.fast_pairs), "exact_pairs": int(st.exact_pairs),
                    "f64_pairs": int(st.f64_pairs), "plan_ms": float(est.plan_ms),
-                   "h2d_ms": float(est.h2d_ms), "d2h_ms": float(est.d2h_ms)},
+                   "h2d_ms": float(est.h2d_ms), "d2h_ms": float(est.d2h_ms), "shard_plan_s": t_plan,
+                   "gather_complete": gathered_ok},
     }
     if not args.no_secondary and ws == 1:
+        sec = []
+        for name, fl in (("c2", 0), ("c3", _native.FLAG_RETRY_F64), ("c3", 0), ("c4", _native.FLAG_RETRY_F64)):
+            try:
+                sec.append(secondary(ctx, name, fl))
+            except Exception as exc:    # reported, never fatal for the headline
+                sec.append({"workload": name, "error": repr(exc)})
+        line["secondary"] = sec
         try:
-            # c3 with the GATK FP64 retry and with the reference's own FP32 semantics
-            # (flagged pairs NaN, pipeline.py has no automatic retry); c4 long pairs
-            line["secondary"] = [secondary(ctx, "c3", _native.FLAG_RETRY_F64), secondary(ctx, "c3", 0),
-                                 secondary(ctx, "c4", _native.FLAG_RETRY_F64)]
-        except Exception as exc:    # reported, never fatal for the headline
-            line["secondary"] = [{"error": repr(exc)}]
+            line["e2e_run"] = [e2e_run("c2"), e2e_run("c3")]
+        except Exception as exc:
+            line["e2e_run"] = [{"error": repr(exc)}]
     if not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(flat, args.cpu_seconds)
+        line["cpu_baseline"] = cpu_baseline(full, args.cpu_seconds, bool(flags & _native.FLAG_RETRY_F64))
     print(json.dumps(line))
     if ws > 1:
         dist.destroy_process_group()
     return 0
 
 
-def profile_traffic():
-    """dram bytes per k_stream launch (c2) from the committed ncu --set full capture."""
+def profile_traffic(workload):
+    """dram bytes per launch of the dominant k_stream launch from the committed ncu
+    --set full capture of this workload (profiles/k_stream_traffic.json)."""
     path = os.path.join(ROOT, "profiles", "k_stream_traffic.json")
     try:
         with open(path) as f:
-            return json.load(f).get("dram_bytes_per_launch")
+            d = json.load(f)
     except OSError:
         return None
+    d = d.get(workload, d) if isinstance(d, dict) else {}
+    return d.get("dram_bytes_per_launch") if isinstance(d, dict) else None
 
 
 if __name__ == "__main__":

@@ -132,6 +132,13 @@ int phmm_execute(phmm_ctx* ctx);
 /* CUDA-event timings of the last phmm_execute (engine stream): whole execute, the
  * FP32 fast kernels alone, and the number of engine kernels launched. */
 int phmm_last_timing(const phmm_ctx* ctx, double* device_ms, double* fast_ms, int* launches);
+/* Per-phase CUDA-event timings of the last phmm_execute (engine stream), 4 doubles (ms):
+ * [0] k_precompute (+ L2 prefetch), [1] FP32 stream phase (all tiling bins, concurrent),
+ * [2] post-pass (a): device-built exact-FP32 guard-band reruns and FP64 retry units,
+ * concurrent, [3] post-pass (b)+(c): second-stage FP64 units, per-pair FP64 retries and
+ * bit-exact FP64.  Replaces nothing in the reference (its RunReport.per_config holds
+ * wall seconds per config, pipeline.py:116-124); measurement only. */
+int phmm_last_phases(const phmm_ctx* ctx, double* phase_ms);
 /* Download and finish the last execute's results. */
 int phmm_fetch(phmm_ctx* ctx, double* out_log10, uint8_t* out_status, phmm_stats* stats);
 

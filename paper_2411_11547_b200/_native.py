@@ -61,7 +61,8 @@ class PhmmStats(ctypes.Structure):
 
 # every symbol include/phmm.h declares (tests/test_abi.py checks the .so exports them)
 EXPORTS = ("phmm_abi_version", "phmm_create", "phmm_destroy", "phmm_last_error", "phmm_score",
-           "phmm_prepare", "phmm_execute", "phmm_fetch", "phmm_fast_geometry", "phmm_last_timing")
+           "phmm_prepare", "phmm_execute", "phmm_fetch", "phmm_fast_geometry", "phmm_last_timing",
+           "phmm_last_phases")
 
 _lib = None
 
@@ -99,6 +100,8 @@ def load():
     L.phmm_last_timing.argtypes = [_vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double),
                                    ctypes.POINTER(ctypes.c_int)]
     L.phmm_last_timing.restype = ctypes.c_int
+    L.phmm_last_phases.argtypes = [_vp, _vp]
+    L.phmm_last_phases.restype = ctypes.c_int
     if L.phmm_abi_version() != 1:
         raise EngineUnavailableError("libphmm ABI version mismatch")
     _lib = L
@@ -201,6 +204,13 @@ class Context:
         with self._lock:
             self._L.phmm_last_timing(self._h, ctypes.byref(d), ctypes.byref(f), ctypes.byref(n))
         return d.value, f.value, n.value
+
+    def last_phases(self):
+        """[precompute, FP32 stream, post-pass (a), post-pass (b)+(c)] ms of the last execute."""
+        out = np.zeros(4, np.float64)
+        with self._lock:
+            self._L.phmm_last_phases(self._h, _ptr(out))
+        return out.tolist()
 
     def fetch(self):
         with self._lock:

@@ -263,6 +263,7 @@ struct phmm_ctx {
   int num_sms = 148;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev_start = nullptr, ev_fast0 = nullptr, ev_fast1 = nullptr, ev_end = nullptr;   // execute
+  cudaEvent_t ev_post1 = nullptr;                       // execute: end of the concurrent post-pass
   cudaEvent_t ev_up0 = nullptr, ev_up1 = nullptr;       // prepare: uploads + device validation
   cudaEvent_t ev_d0 = nullptr, ev_d1 = nullptr;         // fetch: D2H of the results
   cudaEvent_t ev_pre = nullptr;
@@ -333,6 +334,7 @@ struct phmm_ctx {
   int post_grid = 0;                         // CTAs of the per-pair post-pass kernels
   int r64_grid = 0, rx32_grid = 0;           // CTAs of the striped retry launches
   float last_dev_ms = 0.f, last_fast_ms = 0.f;
+  float last_phase_ms[4] = {0.f, 0.f, 0.f, 0.f};   // precompute, FP32 stream, post-pass (a), (b)+(c)
   EngineDev dev{};
 
   int fail(int code, const char* fmt, ...) {
@@ -397,6 +399,7 @@ static int init_ctx(phmm_ctx* ctx, int device) {
   CK(cudaEventCreate(&ctx->ev_fast0));
   CK(cudaEventCreate(&ctx->ev_fast1));
   CK(cudaEventCreate(&ctx->ev_end));
+  CK(cudaEventCreate(&ctx->ev_post1));
   CK(cudaEventCreate(&ctx->ev_up0));
   CK(cudaEventCreate(&ctx->ev_up1));
   CK(cudaEventCreate(&ctx->ev_d0));
@@ -447,7 +450,7 @@ int phmm_destroy(phmm_ctx* ctx) {
   if (ctx->ev_fast0) cudaEventDestroy(ctx->ev_fast0);
   if (ctx->ev_fast1) cudaEventDestroy(ctx->ev_fast1);
   if (ctx->ev_end) cudaEventDestroy(ctx->ev_end);
-  for (cudaEvent_t e : {ctx->ev_up0, ctx->ev_up1, ctx->ev_d0, ctx->ev_d1})
+  for (cudaEvent_t e : {ctx->ev_up0, ctx->ev_up1, ctx->ev_d0, ctx->ev_d1, ctx->ev_post1})
     if (e) cudaEventDestroy(e);
   if (ctx->ev_pre) cudaEventDestroy(ctx->ev_pre);
   for (int a = 0; a < phmm_ctx::kAux; ++a) {
@@ -975,6 +978,21 @@ static int prepare_impl(phmm_ctx* ctx, const phmm_input* in, const phmm_options*
   return PHMM_SUCCESS;
 }
 
+// CUDA-event timings of a completed execute: whole, FP32 stream phase, and the four phases
+static int record_timing(phmm_ctx* ctx) {
+  float dev = 0.f, fast = 0.f, ph[4] = {0.f, 0.f, 0.f, 0.f};
+  CK(cudaEventElapsedTime(&dev, ctx->ev_start, ctx->ev_end));
+  CK(cudaEventElapsedTime(&fast, ctx->ev_fast0, ctx->ev_fast1));
+  CK(cudaEventElapsedTime(&ph[0], ctx->ev_start, ctx->ev_fast0));
+  CK(cudaEventElapsedTime(&ph[2], ctx->ev_fast1, ctx->ev_post1));
+  CK(cudaEventElapsedTime(&ph[3], ctx->ev_post1, ctx->ev_end));
+  ph[1] = fast;
+  ctx->last_dev_ms = dev;
+  ctx->last_fast_ms = fast;
+  for (int i = 0; i < 4; ++i) ctx->last_phase_ms[i] = ph[i];
+  return PHMM_SUCCESS;
+}
+
 int phmm_execute(phmm_ctx* ctx) {
   if (!ctx) return PHMM_ERR_INVALID;
   if (!ctx->prepared) return ctx->fail(PHMM_ERR_STATE, "phmm_execute before phmm_prepare");
@@ -1073,6 +1091,7 @@ int phmm_execute(phmm_ctx* ctx) {
            str ? ctx->rx32_grid : ctx->num_sms * SKn.occ);
     }
   CK(join());
+  CK(cudaEventRecord(ctx->ev_post1, st));
   if (E.r64b.enabled) {                 // long reads: band pairs whose exact rerun underflowed
     const int g = kNumR64Geoms - 1;
     const StreamKernel& SKn = striped_tab(kFast64);
@@ -1093,12 +1112,7 @@ int phmm_execute(phmm_ctx* ctx) {
   ctx->executed = true;
   if (ctx->async) return PHMM_SUCCESS;
   CK(cudaEventSynchronize(ctx->ev_end));
-  float dev = 0.f, fast = 0.f;
-  CK(cudaEventElapsedTime(&dev, ctx->ev_start, ctx->ev_end));
-  CK(cudaEventElapsedTime(&fast, ctx->ev_fast0, ctx->ev_fast1));
-  ctx->last_dev_ms = dev;
-  ctx->last_fast_ms = fast;
-  return PHMM_SUCCESS;
+  return record_timing(ctx);
 }
 
 // D2H of the raw results into pinned staging, asynchronous on the engine stream
@@ -1141,12 +1155,9 @@ static int fetch_complete(phmm_ctx* ctx, double* out_log10, uint8_t* out_status,
   float d2h = 0.f;
   cudaEventElapsedTime(&d2h, ctx->ev_d0, ctx->ev_d1);
   if (ctx->async) {            // chunk contexts: the execute / upload events completed by now
-    float dev = 0.f, fast = 0.f, h2d = 0.f;
-    cudaEventElapsedTime(&dev, ctx->ev_start, ctx->ev_end);
-    cudaEventElapsedTime(&fast, ctx->ev_fast0, ctx->ev_fast1);
+    float h2d = 0.f;
+    record_timing(ctx);
     cudaEventElapsedTime(&h2d, ctx->ev_up0, ctx->ev_up1);
-    ctx->last_dev_ms = dev;
-    ctx->last_fast_ms = fast;
     ctx->h2d_ms = h2d;
   }
   // finishing (wavefront.py:428-434): host glibc log10 (= CPython math.log10), batches
@@ -1261,6 +1272,12 @@ int phmm_last_timing(const phmm_ctx* ctx, double* device_ms, double* fast_ms, in
   if (device_ms) *device_ms = ctx->last_dev_ms;
   if (fast_ms) *fast_ms = ctx->last_fast_ms;
   if (launches) *launches = ctx->last_launches;
+  return PHMM_SUCCESS;
+}
+
+int phmm_last_phases(const phmm_ctx* ctx, double* phase_ms) {
+  if (!ctx || !phase_ms) return PHMM_ERR_INVALID;
+  for (int i = 0; i < 4; ++i) phase_ms[i] = ctx->last_phase_ms[i];
   return PHMM_SUCCESS;
 }
 

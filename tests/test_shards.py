@@ -1,38 +1,90 @@
-"""Multi-GPU sharding host logic (shards.py) on CPU: cost-balanced contiguous cuts and
-rebased sub-batches; the GPU test runs two shard contexts on one device."""
+"""Multi-GPU sharding host logic (shards.py) on CPU: bin-stratified cost-balanced read
+deal, shard extraction with global ids, and the gather; the GPU test runs three shard
+contexts on one device."""
 import numpy as np
 import pytest
 
 from paper_2411_11547_b200 import datagen
-from paper_2411_11547_b200.shards import batch_costs, cut_points, sub_flat
+from paper_2411_11547_b200.shards import (TILING_WIDTHS, make_shard, plan_shards, read_costs,
+                                          shards)
 
 
-def test_cut_points_balance_cost_and_cover_all_batches():
-    flat = datagen.workload("c3", num_batches=40)
-    costs = batch_costs(flat)
-    assert costs.shape == (40,) and np.all(costs > 0)
-    for parts in (1, 2, 3, 4, 8):
-        cuts = cut_points(costs, parts)
-        assert cuts[0] == 0 and cuts[-1] == 40 and np.all(np.diff(cuts) >= 0)
-        shares = np.array([costs[a:b].sum() for a, b in zip(cuts[:-1], cuts[1:])])
-        assert shares.sum() == pytest.approx(costs.sum())
-        assert shares.max() <= costs.sum() / parts + costs.max() + 1e-9
-
-
-def test_sub_flat_rebases_and_preserves_pairs():
-    flat = datagen.workload("c3", num_batches=12)
+def _pairs(flat):
     pr, ph = flat.pair_index()
-    cuts = cut_points(batch_costs(flat), 3)
-    got = []
-    for a, b in zip(cuts[:-1], cuts[1:]):
-        s = sub_flat(flat, int(a), int(b))
-        assert s.read_off[0] == 0 and s.hap_off[0] == 0 and s.batch_read_off[0] == 0
-        spr, sph = s.pair_index()
-        got.append((s.read_len[spr], s.hap_len[sph],
-                    [bytes(s.read_bases[s.read_off[r]:s.read_off[r + 1]]) for r in spr[:5]]))
-    m = np.concatenate([g[0] for g in got])
-    n = np.concatenate([g[1] for g in got])
-    assert np.array_equal(m, flat.read_len[pr]) and np.array_equal(n, flat.hap_len[ph])
+    return pr, ph
+
+
+@pytest.mark.parametrize("parts", [1, 2, 3, 4, 8])
+def test_plan_balances_cost_and_bins(parts):
+    flat = datagen.workload("c3", num_batches=64)
+    cost, key = read_costs(flat)
+    owner = plan_shards(flat, parts)
+    assert owner.shape == (flat.num_reads,) and owner.min() >= 0 and owner.max() < parts
+    loads = np.bincount(owner, weights=cost, minlength=parts)
+    assert loads.sum() == pytest.approx(cost.sum())
+    # within about one read per bin of the mean
+    nbins = np.unique(key).shape[0]
+    assert loads.max() - loads.min() <= cost.max() * max(2, nbins // parts + 2)
+    assert loads.max() <= cost.sum() / parts * 1.05
+    # every GPU gets the same mix of tiling-width classes (within one read per bin)
+    for k in np.unique(key):
+        cnt = np.bincount(owner[key == k], minlength=parts)
+        assert cnt.max() - cnt.min() <= 1
+
+
+def test_cost_counts_padding_to_the_tiling_width():
+    flat = datagen.workload("c3", num_batches=4)
+    cost, _ = read_costs(flat)
+    m = flat.read_len
+    W = TILING_WIDTHS[np.searchsorted(TILING_WIDTHS, m + 1)]
+    rb = np.repeat(np.arange(flat.num_batches), np.diff(flat.batch_read_off))
+    hsum = np.add.reduceat(flat.hap_len, flat.batch_hap_off[:-1])[rb]
+    assert np.all(cost >= W * hsum) and np.all(cost < W * (hsum + 64))
+
+
+@pytest.mark.parametrize("parts", [2, 3, 5])
+def test_shards_partition_the_pairs_and_keep_contents(parts):
+    flat = datagen.workload("c3", num_batches=20)
+    pr, ph = _pairs(flat)
+    got = shards(flat, parts)
+    gids = np.concatenate([s.gids for s in got])
+    assert np.array_equal(np.sort(gids), np.arange(flat.num_pairs))
+    for s in got:
+        f = s.flat
+        assert f.read_off[0] == 0 and f.hap_off[0] == 0 and f.batch_read_off[0] == 0
+        spr, sph = f.pair_index()
+        assert np.array_equal(f.read_len[spr], flat.read_len[pr[s.gids]])
+        assert np.array_equal(f.hap_len[sph], flat.hap_len[ph[s.gids]])
+        # same bases and qualities for a sample of pairs
+        for i in range(0, f.num_pairs, max(1, f.num_pairs // 7)):
+            gr, gh, lr, lh = pr[s.gids[i]], ph[s.gids[i]], spr[i], sph[i]
+            for a, b in ((f.read_bases, flat.read_bases), (f.bq, flat.bq), (f.gq, flat.gq)):
+                assert np.array_equal(a[f.read_off[lr]:f.read_off[lr + 1]],
+                                      b[flat.read_off[gr]:flat.read_off[gr + 1]])
+            assert np.array_equal(f.hap_bases[f.hap_off[lh]:f.hap_off[lh + 1]],
+                                  flat.hap_bases[flat.hap_off[gh]:flat.hap_off[gh + 1]])
+
+
+def test_sharded_oracle_scores_gather_bit_identical():
+    """Shard, score every shard with the CPU oracle, gather by global id: bitwise equal to
+    scoring the unsharded batch list (pairs are independent)."""
+    from oracle import oracle
+    flat = datagen.workload("c3", num_batches=6)
+    ref, kind = oracle.score(oracle.Flat(**flat.as_dict()), "f32")
+    out = np.full(flat.num_pairs, -1.0)
+    ok = np.zeros(flat.num_pairs, np.int64)
+    for s in shards(flat, 3):
+        v, k = oracle.score(oracle.Flat(**s.flat.as_dict()), "f32")
+        out[s.gids] = v
+        ok[s.gids] = k
+    assert np.array_equal(out, ref, equal_nan=True) and np.array_equal(ok, kind)
+
+
+def test_empty_shard_when_more_gpus_than_reads():
+    flat = datagen.workload("c1", num_batches=1)          # 25 reads
+    owner = plan_shards(flat, 32)
+    s = make_shard(flat, owner, 31)
+    assert s.flat.num_pairs == 0 and s.gids.shape == (0,)
 
 
 @pytest.mark.gpu
