@@ -11,6 +11,7 @@ import glob
 import os
 import subprocess
 import sys
+import sysconfig
 from concurrent.futures import ThreadPoolExecutor
 
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -20,8 +21,10 @@ SOURCES = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
 HEADERS = sorted(glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(CSRC, "*.cuh"))) + [
     os.path.join(ROOT, "include", "phmm.h")]
 OUT = os.path.join(HERE, "_lib", "libphmm.so")
-GEN_SRC = os.path.join(CSRC, "datagen.cpp")
-GEN_OUT = os.path.join(HERE, "_lib", "libphmm_datagen.so")   # host-only input generator
+HOST_SRC = [os.path.join(CSRC, "datagen.cpp"), os.path.join(CSRC, "batchio.cpp")]
+HOST_OUT = os.path.join(HERE, "_lib", "libphmm_host.so")   # host-only: input generator, batch text I/O
+FLAT_SRC = os.path.join(CSRC, "flatten.cpp")                # CPython extension: Batch list -> flat arrays
+FLAT_OUT = os.path.join(HERE, "_lib", "_phmm_flatten" + (sysconfig.get_config_var("EXT_SUFFIX") or ".so"))
 OBJ = os.path.join(HERE, "_lib", "obj")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
@@ -43,21 +46,37 @@ def up_to_date() -> bool:
     return not _stale(OUT, SOURCES + HEADERS)
 
 
-def build_datagen(force: bool = False, verbose: bool = False) -> str:
-    """g++ -> libphmm_datagen.so (no CUDA: also used by the CPU tests)."""
-    if not force and not _stale(GEN_OUT, [GEN_SRC]):
-        return GEN_OUT
-    os.makedirs(os.path.dirname(GEN_OUT), exist_ok=True)
-    cmd = ["g++", "-O2", "-std=c++17", "-shared", "-fPIC", "-o", GEN_OUT + ".tmp", GEN_SRC]
+def build_host(force: bool = False, verbose: bool = False) -> str:
+    """g++ -> libphmm_host.so (no CUDA: also used by the CPU tests)."""
+    if not force and not _stale(HOST_OUT, HOST_SRC):
+        return HOST_OUT
+    os.makedirs(os.path.dirname(HOST_OUT), exist_ok=True)
+    cmd = ["g++", "-O2", "-std=c++17", "-shared", "-fPIC", "-o", HOST_OUT + ".tmp"] + HOST_SRC
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.run(cmd, check=True)
-    os.replace(GEN_OUT + ".tmp", GEN_OUT)
-    return GEN_OUT
+    os.replace(HOST_OUT + ".tmp", HOST_OUT)
+    return HOST_OUT
+
+
+def build_flatten(force: bool = False, verbose: bool = False) -> str:
+    """g++ -> the _phmm_flatten CPython extension (Python.h of this interpreter)."""
+    if not force and not _stale(FLAT_OUT, [FLAT_SRC]):
+        return FLAT_OUT
+    os.makedirs(os.path.dirname(FLAT_OUT), exist_ok=True)
+    import numpy
+    cmd = ["g++", "-O2", "-std=c++17", "-shared", "-fPIC", "-I", sysconfig.get_paths()["include"],
+           "-I", numpy.get_include(), "-o", FLAT_OUT + ".tmp", FLAT_SRC]
+    if verbose:
+        print(" ".join(cmd), file=sys.stderr)
+    subprocess.run(cmd, check=True)
+    os.replace(FLAT_OUT + ".tmp", FLAT_OUT)
+    return FLAT_OUT
 
 
 def build_native(force: bool = False, verbose: bool = False) -> str:
-    build_datagen(force, verbose)
+    build_host(force, verbose)
+    build_flatten(force, verbose)
     if not force and up_to_date():
         return OUT
     os.makedirs(OBJ, exist_ok=True)

@@ -1,4 +1,4 @@
-// datagen.cpp — host-only synthetic input generator (libphmm_datagen.so).
+// datagen.cpp — host-only synthetic input generator (libphmm_host.so).
 //
 // Re-implements, draw for draw, the numpy Generator stream that the reference's
 // synthetic generator consumes (pkg/src/pairhmm/datagen.py:78-121, restated in

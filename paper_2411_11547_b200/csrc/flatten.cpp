@@ -1,0 +1,201 @@
+// flatten.cpp — CPython extension _phmm_flatten: Batch objects -> flat C-ABI arrays.
+//
+// The drop-in API takes the reference's list[Batch] (model.py:55-136: ReadRecord with
+// int8 bases + four uint8 Phred tracks, Haplotype bases).  FlatBatches.from_batches must
+// copy every read's five arrays and every haplotype into contiguous buffers; done per
+// read in Python (attribute lookups + np.concatenate of 16k-1M small arrays) that cost
+// ~100 ms per 65k pairs, on the run() path.  This walks the list once in C through the
+// buffer protocol and memcpy's each array into its slot (two passes: sizes, then copy).
+//
+//   flatten(batches) -> (read_bases, base_qual, ins_qual, del_qual, gcp_qual, read_len,
+//                        hap_bases, hap_len, batch_reads, batch_haps)
+// as bytearrays (int8/uint8 data, int64 lengths/counts) that numpy wraps without a copy.
+// The arrays are located with the numpy C API (PyArray_DATA), other buffers through the
+// buffer protocol.
+// Tracks must be C-contiguous 1-byte arrays of the read's length (ReadRecord guarantees
+// it; anything else raises ValueError and the caller falls back to numpy).
+#define PY_SSIZE_T_CLEAN
+#include <Python.h>
+#define NPY_NO_DEPRECATED_API NPY_2_0_API_VERSION
+#include <numpy/arrayobject.h>
+
+#include <cstdint>
+#include <cstring>
+#include <vector>
+
+namespace {
+
+// Source spans of the arrays to copy.  numpy arrays are read through the numpy C API
+// (data pointer + size: no buffer export, which costs ~0.7 us per array); other objects
+// through the buffer protocol, whose views are held until the copy is done.
+struct Spans {
+  std::vector<const char*> p;
+  std::vector<Py_ssize_t> n;
+  std::vector<Py_buffer> views;
+  size_t nviews = 0;
+  explicit Spans(size_t cap) : views(cap) {
+    p.reserve(cap);
+    n.reserve(cap);
+  }
+  ~Spans() {
+    for (size_t i = 0; i < nviews; ++i) PyBuffer_Release(&views[i]);
+  }
+  bool get(PyObject* obj, PyObject* name, const char* attr) {
+    PyObject* a = PyObject_GetAttr(obj, name);
+    if (!a) return false;
+    const bool ok = take(a, attr);
+    Py_DECREF(a);          // the owning record keeps the array alive
+    return ok;
+  }
+  // a: borrowed reference to the attribute value
+  bool take(PyObject* a, const char* attr) {
+    if (PyArray_Check(a)) {
+      PyArrayObject* arr = reinterpret_cast<PyArrayObject*>(a);
+      const bool ok = PyArray_NDIM(arr) == 1 && PyArray_ITEMSIZE(arr) == 1 && PyArray_IS_C_CONTIGUOUS(arr);
+      if (ok) {
+        p.push_back(static_cast<const char*>(PyArray_DATA(arr)));
+        n.push_back(PyArray_DIM(arr, 0));
+      }
+      if (!ok) PyErr_Format(PyExc_ValueError, "%s must be a contiguous 1-D array of 1-byte elements", attr);
+      return ok;
+    }
+    Py_buffer& b = views[nviews];
+    if (PyObject_GetBuffer(a, &b, PyBUF_C_CONTIGUOUS | PyBUF_FORMAT) != 0) return false;
+    ++nviews;
+    if (b.itemsize != 1 || b.ndim != 1) {
+      PyErr_Format(PyExc_ValueError, "%s must be a 1-D array of 1-byte elements", attr);
+      return false;
+    }
+    p.push_back(static_cast<const char*>(b.buf));
+    n.push_back(b.len);
+    return true;
+  }
+};
+
+PyObject* new_bytes(const void* src, Py_ssize_t n) {
+  return PyByteArray_FromStringAndSize(static_cast<const char*>(src), n);
+}
+
+PyObject* flatten(PyObject*, PyObject* arg) {
+  PyObject* seq = PySequence_Fast(arg, "batches must be a sequence");
+  if (!seq) return nullptr;
+  const Py_ssize_t B = PySequence_Fast_GET_SIZE(seq);
+  static const char* kTracks[5] = {"bases", "base_qual", "ins_qual", "del_qual", "gcp_qual"};
+  static PyObject* kNames[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+  static PyObject *kReads = nullptr, *kHaps = nullptr;
+  if (!kReads) {                      // interned attribute names (GetAttrString builds a str per call)
+    for (int x = 0; x < 5; ++x) kNames[x] = PyUnicode_InternFromString(kTracks[x]);
+    kReads = PyUnicode_InternFromString("reads");
+    kHaps = PyUnicode_InternFromString("haps");
+  }
+  std::vector<int64_t> bre(B), bha(B), rlen, hlen;
+  int64_t RL = 0, HL = 0;
+  bool ok = true;
+  std::vector<PyObject*> keep;   // the reads / haps sequences of each batch
+  // pass 1: the batches' read / haplotype sequences and counts
+  size_t nreads = 0, nhaps = 0;
+  for (Py_ssize_t b = 0; ok && b < B; ++b) {
+    PyObject* batch = PySequence_Fast_GET_ITEM(seq, b);
+    PyObject* reads = PyObject_GetAttr(batch, kReads);
+    PyObject* haps = reads ? PyObject_GetAttr(batch, kHaps) : nullptr;
+    PyObject* rs = reads ? PySequence_Fast(reads, "reads must be a sequence") : nullptr;
+    PyObject* hs = haps ? PySequence_Fast(haps, "haps must be a sequence") : nullptr;
+    Py_XDECREF(reads);
+    Py_XDECREF(haps);
+    if (!rs || !hs) { Py_XDECREF(rs); Py_XDECREF(hs); ok = false; break; }
+    keep.push_back(rs);
+    keep.push_back(hs);
+    bre[b] = PySequence_Fast_GET_SIZE(rs);
+    bha[b] = PySequence_Fast_GET_SIZE(hs);
+    nreads += (size_t)bre[b];
+    nhaps += (size_t)bha[b];
+  }
+  // pass 2: buffer views and lengths
+  Spans rv(ok ? 5 * nreads : 0), hv(ok ? nhaps : 0);
+  rlen.reserve(nreads);
+  hlen.reserve(nhaps);
+  for (Py_ssize_t b = 0; ok && b < B; ++b) {
+    PyObject* rs = keep[2 * b];
+    PyObject* hs = keep[2 * b + 1];
+    for (Py_ssize_t r = 0; ok && r < bre[b]; ++r) {
+      PyObject* rd = PySequence_Fast_GET_ITEM(rs, r);
+      const size_t first = rv.n.size();
+      // instance __dict__ lookups (a frozen dataclass stores its fields there) instead of
+      // five generic attribute lookups; anything else -> getattr
+      PyObject* dict = PyObject_GenericGetDict(rd, nullptr);
+      if (!dict) PyErr_Clear();
+      for (int x = 0; ok && x < 5; ++x) {
+        PyObject* a = dict ? PyDict_GetItemWithError(dict, kNames[x]) : nullptr;
+        ok = a ? rv.take(a, kTracks[x]) : (!PyErr_Occurred() && rv.get(rd, kNames[x], kTracks[x]));
+      }
+      Py_XDECREF(dict);
+      if (!ok) break;
+      const Py_ssize_t m = rv.n[first];
+      for (int x = 1; ok && x < 5; ++x)
+        if (rv.n[first + x] != m) {
+          PyErr_Format(PyExc_ValueError, "%s track has length %zd, expected %zd", kTracks[x],
+                       rv.n[first + x], m);
+          ok = false;
+        }
+      rlen.push_back(m);
+      RL += m;
+    }
+    for (Py_ssize_t h = 0; ok && h < bha[b]; ++h) {
+      ok = hv.get(PySequence_Fast_GET_ITEM(hs, h), kNames[0], kTracks[0]);
+      if (ok) {
+        hlen.push_back(hv.n.back());
+        HL += hlen.back();
+      }
+    }
+  }
+  PyObject* out = nullptr;
+  if (ok) {
+    PyObject* tr[5];
+    for (int x = 0; x < 5; ++x) tr[x] = PyByteArray_FromStringAndSize(nullptr, RL);
+    PyObject* hb = PyByteArray_FromStringAndSize(nullptr, HL);
+    bool alloc = hb != nullptr;
+    for (int x = 0; x < 5; ++x) alloc = alloc && tr[x] != nullptr;
+    if (alloc) {
+      char* d[5];
+      for (int x = 0; x < 5; ++x) d[x] = PyByteArray_AS_STRING(tr[x]);
+      const size_t R = rlen.size();
+      Py_BEGIN_ALLOW_THREADS
+      for (size_t r = 0; r < R; ++r)
+        for (int x = 0; x < 5; ++x) {
+          memcpy(d[x], rv.p[5 * r + x], (size_t)rlen[r]);
+          d[x] += rlen[r];
+        }
+      char* dh = PyByteArray_AS_STRING(hb);
+      for (size_t h = 0; h < hlen.size(); ++h) {
+        memcpy(dh, hv.p[h], (size_t)hlen[h]);
+        dh += hlen[h];
+      }
+      Py_END_ALLOW_THREADS
+      out = Py_BuildValue("(NNNNNNNNNN)", tr[0], tr[1], tr[2], tr[3], tr[4],
+                          new_bytes(rlen.data(), (Py_ssize_t)(rlen.size() * 8)), hb,
+                          new_bytes(hlen.data(), (Py_ssize_t)(hlen.size() * 8)),
+                          new_bytes(bre.data(), (Py_ssize_t)(bre.size() * 8)),
+                          new_bytes(bha.data(), (Py_ssize_t)(bha.size() * 8)));
+    } else {
+      for (int x = 0; x < 5; ++x) Py_XDECREF(tr[x]);
+      Py_XDECREF(hb);
+      if (!PyErr_Occurred()) PyErr_NoMemory();
+    }
+  }
+  for (PyObject* o : keep) Py_DECREF(o);
+  Py_DECREF(seq);
+  return out;
+}
+
+PyMethodDef kMethods[] = {
+    {"flatten", flatten, METH_O, "flatten(batches) -> 10 bytearrays (see flatten.cpp)"},
+    {nullptr, nullptr, 0, nullptr}};
+
+PyModuleDef kModule = {PyModuleDef_HEAD_INIT, "_phmm_flatten", "Batch list -> flat arrays", -1, kMethods};
+
+}  // namespace
+
+PyMODINIT_FUNC PyInit__phmm_flatten(void) {
+  import_array();
+  return PyModule_Create(&kModule);
+}

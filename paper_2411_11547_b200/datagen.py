@@ -130,11 +130,11 @@ def _spec3(spec, what, is_len):
 
 def _native_flat(num_batches, reads_per_batch, haps_per_batch, read_len_spec, hap_len_spec, seed,
                  mode, mutation_rate, base_qual, indel_qual, gcp_qual):
-    """The same stream drawn by csrc/datagen.cpp (libphmm_datagen.so), or None when the
+    """The same stream drawn by csrc/datagen.cpp (libphmm_host.so), or None when the
     library is not built.  Ranges must fit the 32-bit bounded draw (always true here)."""
     import ctypes
     import os
-    lib_path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libphmm_datagen.so")
+    lib_path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libphmm_host.so")
     if not os.path.exists(lib_path) or num_batches < 1:
         return None
     if mode not in ("independent", "derived"):
@@ -189,7 +189,7 @@ def generate_synthetic_flat(num_batches, reads_per_batch, haps_per_batch, read_l
                             indel_qual=DEFAULT_INDEL_QUAL, gcp_qual=DEFAULT_GCP_QUAL,
                             native=True) -> FlatBatches:
     """Same stream as generate_synthetic, returned as FlatBatches (no per-read objects).
-    ``native``: draw it with libphmm_datagen.so (csrc/datagen.cpp, identical arrays, ~100x
+    ``native``: draw it with libphmm_host.so (csrc/datagen.cpp, identical arrays, ~100x
     faster) when that library is built; otherwise the numpy restatement below."""
     if native:
         out = _native_flat(num_batches, reads_per_batch, haps_per_batch, read_len_spec, hap_len_spec,

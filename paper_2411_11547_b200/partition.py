@@ -82,14 +82,36 @@ def item_bytes(flat: FlatBatches, configs):
 
 
 def check_budget(flat: FlatBatches, configs, budget_bytes: int):
-    """Raise BudgetError for the first item (global_id order) over the budget."""
-    est, _ = item_bytes(flat, configs)
-    over = np.flatnonzero(est > budget_bytes)
+    """Raise BudgetError for the first item (global_id order) over the budget.
+
+    O(reads + haplotypes): an item's estimate grows with its haplotype length, so a read
+    has an item over budget iff its batch's longest haplotype exceeds the read's slack
+    (budget - the read's part of the estimate); only that read's items are expanded."""
+    R = flat.num_reads
+    if R == 0:
+        return
+    cidx = config_index(flat.read_len, configs)
+    ok = cidx >= 0
+    if not ok.any():
+        return
+    mmax = np.array([c.m_max for c in configs], np.int64)
+    real = np.array([np.dtype(c.dtype).itemsize for c in configs], np.int64)
+    ci = np.where(ok, cidx, 0)
+    base = mmax[ci] + 4 * flat.read_len + 10 * mmax[ci] * real[ci] + 8
+    rb = np.repeat(np.arange(flat.num_batches), np.diff(flat.batch_read_off))
+    hmax = np.maximum.reduceat(flat.hap_len, flat.batch_hap_off[:-1]) if flat.num_haps else np.zeros(0, np.int64)
+    over = np.flatnonzero(ok & (base + hmax[rb] > budget_bytes))
     if over.size:
-        gid = int(over[0])
+        r = int(over[0])
+        b = int(rb[r])
+        h0, h1 = int(flat.batch_hap_off[b]), int(flat.batch_hap_off[b + 1])
+        est = base[r] + flat.hap_len[h0:h1]
+        k = int(np.flatnonzero(est > budget_bytes)[0])
+        H = h1 - h0
+        gid = int((np.diff(flat.batch_read_off) * np.diff(flat.batch_hap_off))[:b].sum()
+                  + (r - int(flat.batch_read_off[b])) * H + k)
         raise BudgetError("work item %d alone needs ~%d bytes, over the %d-byte budget"
-                          % (gid, int(est[gid]), budget_bytes))
-    return est
+                          % (gid, int(est[k]), budget_bytes))
 
 
 def cut_chunks(est: np.ndarray, budget_bytes: int) -> tuple:
@@ -131,5 +153,6 @@ def build_plan(batches, configs, budget_bytes: int = DEFAULT_BUDGET_BYTES) -> Pa
     by_config = {}
     for i, cfg in enumerate(configs):
         by_config.setdefault(cfg, []).extend(np.flatnonzero(cidx == i).tolist())
-    est = check_budget(flat, configs, budget_bytes)
+    check_budget(flat, configs, budget_bytes)
+    est, _ = item_bytes(flat, configs)
     return PartitionPlan(tuple(items), by_config, cut_chunks(est, budget_bytes))

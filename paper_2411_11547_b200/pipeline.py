@@ -81,6 +81,32 @@ def errors_from_status(status: np.ndarray) -> list:
     return [(int(g), _native.KIND_NAMES[int(kinds[g])]) for g in bad]
 
 
+def _config_cells(flat: FlatBatches, configs, status: np.ndarray, device_s: float):
+    """({geometry: ConfigStats}, total executed cells) in O(reads)."""
+    H = np.diff(flat.batch_hap_off)
+    rb = np.repeat(np.arange(flat.num_batches), np.diff(flat.batch_read_off))
+    pair_base = np.concatenate([[0], np.cumsum(np.diff(flat.batch_read_off) * H)])
+    first = pair_base[rb] + (np.arange(flat.num_reads) - flat.batch_read_off[rb]) * H[rb]
+    kinds = status[first] & _native.ST_KIND_MASK
+    executed = (kinds == _native.ST_OK) | (kinds == _native.ST_OVERFLOW)
+    hsum = np.add.reduceat(flat.hap_len, flat.batch_hap_off[:-1])
+    cells = flat.read_len * hsum[rb]
+    cidx = config_index(flat.read_len, configs)
+    sel = executed & (cidx >= 0)
+    per = np.bincount(cidx[sel], weights=cells[sel].astype(np.float64), minlength=len(configs))
+    exact = np.zeros(len(configs), np.int64)
+    np.add.at(exact, cidx[sel], cells[sel])
+    total = int(exact.sum())
+    per_config = {}
+    for i in np.flatnonzero(per > 0).tolist():
+        geo = configs[i].geometry
+        c = int(exact[i])
+        sec = device_s * c / total if total else 0.0
+        prev = per_config.get(geo)
+        per_config[geo] = ConfigStats(c + (prev.cells if prev else 0), sec + (prev.seconds if prev else 0.0))
+    return per_config, total
+
+
 def run(batches, configs=None, budget_bytes: int = DEFAULT_BUDGET_BYTES, workers: int = 1, *,
         retry_f64: bool = False, exact: bool = False, device: int = 0, devices=None):
     """Score every work item of ``batches`` on the GPU; see the module docstring."""
@@ -106,23 +132,13 @@ def run(batches, configs=None, budget_bytes: int = DEFAULT_BUDGET_BYTES, workers
     errors = errors_from_status(status)
     retried = np.flatnonzero((status & _native.ST_RETRIED_F64) != 0).tolist()
 
-    # per-config accounting keyed like the reference (geometry of the bound config)
+    # per-config accounting keyed like the reference (geometry of the bound config), per
+    # READ: a read's items are all executed or none (config-too-small and
+    # degenerate-transition are properties of the read; numeric-overflow items count)
     per_config = {}
     total_cells = 0
     if n:
-        pr, ph = flat.pair_index()
-        kinds = status & _native.ST_KIND_MASK
-        executed = (kinds == _native.ST_OK) | (kinds == _native.ST_OVERFLOW)
-        cells = flat.read_len[pr] * flat.hap_len[ph]
-        cidx = config_index(flat.read_len, configs)[pr]
-        total_cells = int(cells[executed].sum())
-        dev_s = engine.get("device_ms", 0.0) * 1e-3
-        for i in np.unique(cidx[executed]).tolist():
-            c = int(cells[executed & (cidx == i)].sum())
-            geo = configs[i].geometry
-            prev = per_config.get(geo)
-            sec = dev_s * c / total_cells if total_cells else 0.0
-            per_config[geo] = ConfigStats(c + (prev.cells if prev else 0), sec + (prev.seconds if prev else 0.0))
+        per_config, total_cells = _config_cells(flat, configs, status, engine.get("device_ms", 0.0) * 1e-3)
     report = RunReport(total_cells, wall, throughput(total_cells, wall), per_config, errors,
                        retried, engine)
     return scores, report

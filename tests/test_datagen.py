@@ -56,8 +56,8 @@ def test_workload_shapes():
 
 @pytest.fixture(scope="module")
 def native_gen():
-    from paper_2411_11547_b200.build import build_datagen
-    build_datagen()
+    from paper_2411_11547_b200.build import build_host
+    build_host()
 
 
 @pytest.mark.parametrize("name", SYNTH)

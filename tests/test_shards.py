@@ -95,3 +95,23 @@ def test_sharded_run_equals_single_device():
     b, rb = run(flat, default_configs("f32"), retry_f64=True, devices=[0, 0, 0])
     assert np.array_equal(a, b, equal_nan=True)
     assert ra.total_cells == rb.total_cells and ra.errors == rb.errors and ra.retried == rb.retried
+
+
+def test_check_budget_first_item_matches_per_item_definition():
+    """partition.check_budget (O(reads)) raises for the same first item, with the same
+    estimate, as the per-item definition (partition.py:40-45 / item_bytes)."""
+    from paper_2411_11547_b200 import default_configs
+    from paper_2411_11547_b200.errors import BudgetError
+    from paper_2411_11547_b200.partition import check_budget, item_bytes
+    flat = datagen.workload("c3", num_batches=30)
+    cfgs = default_configs("f32")
+    est, _ = item_bytes(flat, cfgs)
+    for budget in (int(est.max()), int(np.percentile(est, 99.9)), int(np.percentile(est, 50)), 100):
+        over = np.flatnonzero(est > budget)
+        if over.size == 0:
+            check_budget(flat, cfgs, budget)
+            continue
+        with pytest.raises(BudgetError) as err:
+            check_budget(flat, cfgs, budget)
+        assert str(err.value) == ("work item %d alone needs ~%d bytes, over the %d-byte budget"
+                                  % (over[0], est[over[0]], budget))
