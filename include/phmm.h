@@ -124,6 +124,17 @@ const char* phmm_last_error(const phmm_ctx* ctx);
 int phmm_score(phmm_ctx* ctx, const phmm_input* in, const phmm_options* opt,
                double* out_log10, uint8_t* out_status, phmm_stats* stats);
 
+/* Bound the device working set of phmm_score (bytes; 0 = no bound, the default).  A call
+ * whose estimated footprint exceeds the bound streams through at most three chunk
+ * contexts reused round-robin, each chunk within a third of the bound (a single batch
+ * larger than that is one chunk); without a bound the same happens automatically when a
+ * call would not fit the free device memory.  Replaces the reference's chunk budget
+ * (partition.py:88-119, pipeline.py:116-136: contiguous global-id chunks, each within the
+ * budget, the next staged while the current one computes) for inputs larger than HBM. */
+int phmm_set_device_budget(phmm_ctx* ctx, int64_t bytes);
+/* Device bytes currently allocated by the context and its chunk contexts. */
+int phmm_device_bytes(const phmm_ctx* ctx, int64_t* bytes);
+
 /* Upload inputs and build the work plan; returns the pair count in *num_pairs. */
 int phmm_prepare(phmm_ctx* ctx, const phmm_input* in, const phmm_options* opt,
                  int64_t* num_pairs);
@@ -141,6 +152,15 @@ int phmm_last_timing(const phmm_ctx* ctx, double* device_ms, double* fast_ms, in
 int phmm_last_phases(const phmm_ctx* ctx, double* phase_ms);
 /* Download and finish the last execute's results. */
 int phmm_fetch(phmm_ctx* ctx, double* out_log10, uint8_t* out_status, phmm_stats* stats);
+
+/* The complete (m+1) x (n+1) FP64 dynamic-programming matrices M, I, D of ONE pair
+ * (row-major, boundaries included), bit-identical to the reference's debugging oracle
+ * forward_matrices (reference.py:150-156, _full_kernel reference.py:36-75) with boundary
+ * 2^scale_log2 / n and the f64 flush (prob.py:39).  Caller-owned outputs of (m+1)*(n+1)
+ * doubles each; the GPU kernel k_matrices computes them (debugging path, one CTA). */
+int phmm_forward_matrices(phmm_ctx* ctx, const int8_t* read_bases, const uint8_t* base_qual,
+                          const uint8_t* ins_qual, const uint8_t* del_qual, const uint8_t* gcp_qual, int32_t m,
+                          const int8_t* hap_bases, int32_t n, int32_t scale_log2, double* M, double* I, double* D);
 
 /* The fast kernel's tiling for a read of length m against haplotypes of length <= n:
  * P threads per sub-warp, K read positions per thread, Q stripes (no device needed).

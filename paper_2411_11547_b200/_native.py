@@ -62,7 +62,7 @@ class PhmmStats(ctypes.Structure):
 # every symbol include/phmm.h declares (tests/test_abi.py checks the .so exports them)
 EXPORTS = ("phmm_abi_version", "phmm_create", "phmm_destroy", "phmm_last_error", "phmm_score",
            "phmm_prepare", "phmm_execute", "phmm_fetch", "phmm_fast_geometry", "phmm_last_timing",
-           "phmm_last_phases")
+           "phmm_last_phases", "phmm_forward_matrices", "phmm_set_device_budget", "phmm_device_bytes")
 
 _lib = None
 
@@ -102,6 +102,12 @@ def load():
     L.phmm_last_timing.restype = ctypes.c_int
     L.phmm_last_phases.argtypes = [_vp, _vp]
     L.phmm_last_phases.restype = ctypes.c_int
+    L.phmm_forward_matrices.argtypes = [_vp] * 6 + [_i32, _vp, _i32, _i32, _vp, _vp, _vp]
+    L.phmm_forward_matrices.restype = ctypes.c_int
+    L.phmm_set_device_budget.argtypes = [_vp, _i64]
+    L.phmm_set_device_budget.restype = ctypes.c_int
+    L.phmm_device_bytes.argtypes = [_vp, ctypes.POINTER(_i64)]
+    L.phmm_device_bytes.restype = ctypes.c_int
     if L.phmm_abi_version() != 1:
         raise EngineUnavailableError("libphmm ABI version mismatch")
     _lib = L
@@ -219,6 +225,28 @@ class Context:
             stats = PhmmStats()
             self._check(self._L.phmm_fetch(self._h, _ptr(out), _ptr(st), ctypes.byref(stats)))
         return out, st, stats
+
+    def set_device_budget(self, nbytes: int):
+        """Bound the device working set of score() (0: none; see phmm_set_device_budget)."""
+        with self._lock:
+            self._check(self._L.phmm_set_device_budget(self._h, int(nbytes)))
+
+    def device_bytes(self) -> int:
+        v = _i64()
+        with self._lock:
+            self._check(self._L.phmm_device_bytes(self._h, ctypes.byref(v)))
+        return v.value
+
+    def forward_matrices(self, read, hap, scale_log2: int = 0):
+        """(M, I, D) float64 (m+1, n+1) of one ReadRecord / Haplotype pair (k_matrices)."""
+        m, n = int(read.length), int(hap.length)
+        arrs = [np.ascontiguousarray(a) for a in (read.bases, read.base_qual, read.ins_qual, read.del_qual,
+                                                   read.gcp_qual, hap.bases)]
+        out = [np.empty((m + 1, n + 1), np.float64) for _ in range(3)]
+        with self._lock:
+            self._check(self._L.phmm_forward_matrices(self._h, *[_ptr(a) for a in arrs[:5]], m, _ptr(arrs[5]), n,
+                                                      int(scale_log2), *[_ptr(o) for o in out]))
+        return out
 
     def close(self):
         lock = getattr(self, "_lock", None)

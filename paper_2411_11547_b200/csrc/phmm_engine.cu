@@ -95,8 +95,12 @@ constexpr int kCtrR64b = 72, kCtrR64bWork = 80;   // second-stage striped FP64 u
 constexpr int kBinCounters = 96;                  // fixed counter slots before the per-bin counters
 constexpr int64_t kBigCallPairs = 1 << 20;        // device-built retry units grow above this
 constexpr int kFinishThreads = 16;                // host threads finishing log10 in phmm_fetch
-// scratch bound for boundary columns of long haplotypes (striped stream bins, post-pass)
+// scratch bound for boundary columns of long haplotypes (striped stream bins, post-pass);
+// contexts of a budgeted phmm_score use an eighth of their chunk budget instead
 constexpr size_t kColBudget = (size_t)1 << 30;
+// device bytes per pair a prepare can allocate (acc, status, stream entry, the device-built
+// retry units / entries and per-pair lists, each sized for every pair), for chunk budgets
+constexpr int64_t kDevBytesPerPair = 200;
 
 int stream_cap(int P) { return stream_cap_of(P); }
 
@@ -264,6 +268,7 @@ struct phmm_ctx {
   cudaStream_t stream = nullptr;
   cudaEvent_t ev_start = nullptr, ev_fast0 = nullptr, ev_fast1 = nullptr, ev_end = nullptr;   // execute
   cudaEvent_t ev_post1 = nullptr;                       // execute: end of the concurrent post-pass
+  cudaEvent_t ev_span0 = nullptr;                       // phmm_score chunked: first chunk's execute start
   cudaEvent_t ev_up0 = nullptr, ev_up1 = nullptr;       // prepare: uploads + device validation
   cudaEvent_t ev_d0 = nullptr, ev_d1 = nullptr;         // fetch: D2H of the results
   cudaEvent_t ev_pre = nullptr;
@@ -292,6 +297,8 @@ struct phmm_ctx {
   bool async = false;        // chunk contexts of phmm_score: no host syncs in prepare/execute
   phmm_ctx* parent = nullptr;
   int budget_div = 1;        // chunk contexts: number of chunks sharing the band budget
+  int64_t device_budget = 0; // phmm_set_device_budget: bound on the device working set of phmm_score (0: none)
+  size_t col_budget = kColBudget;        // boundary-column scratch bound of this context
   std::vector<phmm_ctx*> chunks;             // chunk contexts (phmm_score pipelining), lazy
   std::vector<int64_t> c_roff, c_hoff, c_bro, c_bho;   // chunk views: rebased offsets
   double* h_acc = nullptr;   // pinned result staging (phmm_fetch)
@@ -400,6 +407,7 @@ static int init_ctx(phmm_ctx* ctx, int device) {
   CK(cudaEventCreate(&ctx->ev_fast1));
   CK(cudaEventCreate(&ctx->ev_end));
   CK(cudaEventCreate(&ctx->ev_post1));
+  CK(cudaEventCreate(&ctx->ev_span0));
   CK(cudaEventCreate(&ctx->ev_up0));
   CK(cudaEventCreate(&ctx->ev_up1));
   CK(cudaEventCreate(&ctx->ev_d0));
@@ -450,7 +458,7 @@ int phmm_destroy(phmm_ctx* ctx) {
   if (ctx->ev_fast0) cudaEventDestroy(ctx->ev_fast0);
   if (ctx->ev_fast1) cudaEventDestroy(ctx->ev_fast1);
   if (ctx->ev_end) cudaEventDestroy(ctx->ev_end);
-  for (cudaEvent_t e : {ctx->ev_up0, ctx->ev_up1, ctx->ev_d0, ctx->ev_d1, ctx->ev_post1})
+  for (cudaEvent_t e : {ctx->ev_up0, ctx->ev_up1, ctx->ev_d0, ctx->ev_d1, ctx->ev_post1, ctx->ev_span0})
     if (e) cudaEventDestroy(e);
   if (ctx->ev_pre) cudaEventDestroy(ctx->ev_pre);
   for (int a = 0; a < phmm_ctx::kAux; ++a) {
@@ -820,7 +828,7 @@ static int prepare_impl(phmm_ctx* ctx, const phmm_input* in, const phmm_options*
     const size_t per_cta = (size_t)(kThreads / 32) * per_slot * sizeof(double);
     ctx->post_grid = ctx->num_sms * 2;
     if (max_m + 1 > 32 * kExactK) {
-      ctx->post_grid = (int)std::max<size_t>(1, std::min<size_t>(ctx->post_grid, kColBudget / per_cta));
+      ctx->post_grid = (int)std::max<size_t>(1, std::min<size_t>(ctx->post_grid, ctx->col_budget / per_cta));
       CK(ctx->d_cold.ensure((size_t)ctx->post_grid * (kThreads / 32) * per_slot));
     } else {
       CK(ctx->d_cold.ensure(1));       // never dereferenced: every post-pass read fits one stripe
@@ -928,7 +936,7 @@ static int prepare_impl(phmm_ctx* ctx, const phmm_input* in, const phmm_options*
       return (int64_t)4 * (32 / K.P) * 6 * col_rows_for(K.P, max_rows) * v;
     };
     auto fit = [&](int grid, int64_t per_cta) {
-      return (int)std::max<int64_t>(1, std::min<int64_t>(grid, (int64_t)kColBudget / per_cta));
+      return (int)std::max<int64_t>(1, std::min<int64_t>(grid, (int64_t)ctx->col_budget / per_cta));
     };
     for (auto& sb : ctx->sbins) {
       const StreamKernel& K = skern(sb.mode, sb.geom);
@@ -1281,6 +1289,56 @@ int phmm_last_phases(const phmm_ctx* ctx, double* phase_ms) {
   return PHMM_SUCCESS;
 }
 
+int phmm_forward_matrices(phmm_ctx* ctx, const int8_t* read_bases, const uint8_t* base_qual,
+                          const uint8_t* ins_qual, const uint8_t* del_qual, const uint8_t* gcp_qual, int32_t m,
+                          const int8_t* hap_bases, int32_t n, int32_t scale_log2, double* M, double* I, double* D) {
+  if (!ctx) return PHMM_ERR_INVALID;
+  if (m < 1 || n < 1) return ctx->fail(PHMM_ERR_INVALID, "read and haplotype must contain at least one base");
+  if (!read_bases || !base_qual || !ins_qual || !del_qual || !gcp_qual || !hap_bases || !M || !I || !D)
+    return ctx->fail(PHMM_ERR_INVALID, "null argument");
+  if ((int64_t)(m + 1) * (n + 1) > ((int64_t)1 << 28)) return ctx->fail(PHMM_ERR_INVALID, "matrices too large");
+  for (int i = 0; i < m; ++i) {
+    if ((uint8_t)read_bases[i] > 4) return ctx->fail(PHMM_ERR_INVALID, "base code outside A,C,G,T,N (0..4)");
+    if (base_qual[i] > 93 || ins_qual[i] > 93 || del_qual[i] > 93 || gcp_qual[i] > 93)
+      return ctx->fail(PHMM_ERR_INVALID, "quality values must be in [0, 93]");
+  }
+  for (int j = 0; j < n; ++j)
+    if ((uint8_t)hap_bases[j] > 4) return ctx->fail(PHMM_ERR_INVALID, "base code outside A,C,G,T,N (0..4)");
+  CK(cudaSetDevice(ctx->device));
+  const size_t cells = (size_t)(m + 1) * (n + 1);
+  const size_t in_bytes = 5 * (size_t)m + (size_t)n;
+  unsigned char* d_in = nullptr;
+  double* d_mat = nullptr;
+  cudaError_t e = cudaMalloc(&d_in, in_bytes);
+  if (e == cudaSuccess) e = cudaMalloc(&d_mat, 3 * cells * sizeof(double));
+  if (e == cudaSuccess) {
+    const void* src[6] = {read_bases, base_qual, ins_qual, del_qual, gcp_qual, hap_bases};
+    size_t off = 0;
+    for (int x = 0; x < 6 && e == cudaSuccess; ++x) {
+      const size_t len = x < 5 ? (size_t)m : (size_t)n;
+      e = cudaMemcpyAsync(d_in + off, src[x], len, cudaMemcpyHostToDevice, ctx->stream);
+      off += len;
+    }
+  }
+  if (e == cudaSuccess) {
+    // prob.py / reference.py:138: boundary 2.0 ** scale_log2 / n in f64
+    const double boundary = ldexp(1.0, scale_log2) / (double)n;
+    launch_matrices(ctx->stream, (const int8_t*)d_in, d_in + m, d_in + 2 * (size_t)m, d_in + 3 * (size_t)m,
+                    d_in + 4 * (size_t)m, m, (const int8_t*)(d_in + 5 * (size_t)m), n, boundary, ctx->d_lut.p,
+                    d_mat, d_mat + cells, d_mat + 2 * cells);
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) e = cudaMemcpyAsync(M, d_mat, cells * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(I, d_mat + cells, cells * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(D, d_mat + 2 * cells, cells * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+  cudaStreamSynchronize(ctx->stream);
+  if (d_in) cudaFree(d_in);
+  if (d_mat) cudaFree(d_mat);
+  if (e != cudaSuccess) return ctx->cuda_fail(e, "phmm_forward_matrices");
+  return PHMM_SUCCESS;
+}
+
 int phmm_fast_geometry(int m, int n, int* P, int* K, int* Q) {
   if (m < 1 || n < 1 || !P || !K || !Q) return PHMM_ERR_INVALID;
   // the FP32 stream tiling a one-pair batch (m x n) is planned on
@@ -1290,28 +1348,24 @@ int phmm_fast_geometry(int m, int n, int* P, int* K, int* Q) {
   return PHMM_SUCCESS;
 }
 
-// phmm_score pipelines large calls: the batches are cut into kScoreChunks contiguous
-// chunks of ~equal pair count, each scored by its own chunk context (device buffers,
-// streams, pinned staging).  The host plans chunk c+1 while the GPU uploads and scores
-// chunk c, and finishes chunk c while later chunks run; chunk kernels on separate
-// streams also fill each other's tails.  Results are identical to the one-pass path
-// (pairs are independent; gid order is batch-major, so a chunk owns a gid range).
+// phmm_score pipelines large calls: the batches are cut into contiguous chunks (cut[c] ..
+// cut[c+1]), each scored by one of `nctx` chunk contexts (device buffers, streams, pinned
+// staging) used round-robin.  The host plans chunk c+1 while the GPU uploads and scores
+// chunk c, and finishes chunk c while later chunks run; chunk kernels on separate streams
+// also fill each other's tails.  A context is reused for chunk c + nctx only after chunk c
+// is complete, so the device working set is bounded by nctx chunks (phmm_set_device_budget
+// sizes the chunks for that).  Results are identical to the one-pass path (pairs are
+// independent; gid order is batch-major, so a chunk owns a gid range).
 static int score_chunked(phmm_ctx* ctx, const phmm_input* in, const phmm_options* opt, double* out_log10,
-                         uint8_t* out_status, phmm_stats* stats, int nchunks) {
+                         uint8_t* out_status, phmm_stats* stats, const std::vector<int64_t>& cut, int nctx,
+                         size_t col_budget) {
   const int64_t B = in->num_batches;
+  const int nchunks = (int)cut.size() - 1;
   std::vector<int64_t> pairs(B + 1, 0);
   for (int64_t b = 0; b < B; ++b)
     pairs[b + 1] = pairs[b] + (in->batch_read_off[b + 1] - in->batch_read_off[b]) *
                                   (in->batch_hap_off[b + 1] - in->batch_hap_off[b]);
-  const int64_t N = pairs[B];
-  std::vector<int64_t> cut(nchunks + 1, B);
-  cut[0] = 0;
-  for (int c = 1; c < nchunks; ++c) {
-    int64_t b = cut[c - 1];
-    while (b < B && pairs[b] < N * c / nchunks) ++b;
-    cut[c] = std::max(b, cut[c - 1]);
-  }
-  while ((int)ctx->chunks.size() < nchunks) {
+  while ((int)ctx->chunks.size() < nctx) {
     phmm_ctx* c = new (std::nothrow) phmm_ctx();
     if (!c) return ctx->fail(PHMM_ERR_NOMEM, "chunk context");
     c->lut = ctx->lut;
@@ -1329,9 +1383,40 @@ static int score_chunked(phmm_ctx* ctx, const phmm_input* in, const phmm_options
       for (int a = 0; a < phmm_ctx::kAux; ++a) cudaStreamSynchronize(cx->aux[a]);
     }
   };
-  // enqueue every chunk (prepare + execute + D2H), planning the next one meanwhile
+  phmm_stats total;
+  memset(&total, 0, sizeof(total));
+  float span = 0.f;                  // first chunk's execute start -> last execute end
+  bool span_set = false;
+  // complete chunk c: device validation verdict, then finishing into the caller's slice
+  auto complete = [&](int c) -> int {
+    if (cut[c + 1] <= cut[c]) return PHMM_SUCCESS;
+    phmm_ctx* cx = ctx->chunks[c % nctx];
+    int rc = check_validation(cx);
+    if (rc != PHMM_SUCCESS) return rc;
+    phmm_stats cs;
+    const int64_t g0 = pairs[cut[c]];
+    rc = fetch_complete(cx, out_log10 ? out_log10 + g0 : nullptr, out_status ? out_status + g0 : nullptr, &cs);
+    if (rc != PHMM_SUCCESS) return rc;
+    float t = 0.f;
+    if (span_set && cudaEventElapsedTime(&t, ctx->ev_span0, cx->ev_end) == cudaSuccess) span = std::max(span, t);
+    total.fast_ms += cs.fast_ms;   // per-chunk FP32 phases (they overlap other chunks' work)
+    total.h2d_ms += cs.h2d_ms;
+    total.num_pairs += cs.num_pairs; total.total_cells += cs.total_cells;
+    total.computed_cells += cs.computed_cells; total.fast_pairs += cs.fast_pairs;
+    total.exact_pairs += cs.exact_pairs; total.f64_pairs += cs.f64_pairs;
+    total.flagged_pairs += cs.flagged_pairs; total.h2d_bytes += cs.h2d_bytes; total.d2h_bytes += cs.d2h_bytes;
+    total.kernel_launches += cs.kernel_launches; total.plan_ms += cs.plan_ms; total.d2h_ms += cs.d2h_ms;
+    return PHMM_SUCCESS;
+  };
   for (int c = 0; c < nchunks; ++c) {
-    phmm_ctx* cx = ctx->chunks[c];
+    phmm_ctx* cx = ctx->chunks[c % nctx];
+    if (c >= nctx) {
+      const int rc = complete(c - nctx);
+      if (rc != PHMM_SUCCESS) {
+        drain();
+        return ctx->fail(rc, "%s", ctx->chunks[(c - nctx) % nctx]->err.c_str());
+      }
+    }
     const int64_t b0 = cut[c], b1 = cut[c + 1];
     if (b1 <= b0) continue;
     const int64_t r0 = in->batch_read_off[b0], r1 = in->batch_read_off[b1];
@@ -1362,8 +1447,13 @@ static int score_chunked(phmm_ctx* ctx, const phmm_input* in, const phmm_options
     sub.batch_hap_off = cx->c_bho.data();
     sub.num_batches = b1 - b0;
     int64_t n = 0;
-    cx->budget_div = nchunks;
+    cx->budget_div = std::min(nchunks, nctx);
+    cx->col_budget = col_budget;
     int rc = phmm_prepare(cx, &sub, opt, &n);
+    if (rc == PHMM_SUCCESS && !span_set) {     // timing origin: the first execute's start
+      rc = cudaEventRecord(ctx->ev_span0, cx->stream) == cudaSuccess ? PHMM_SUCCESS : PHMM_ERR_CUDA;
+      span_set = rc == PHMM_SUCCESS;
+    }
     if (rc == PHMM_SUCCESS) rc = phmm_execute(cx);
     if (rc == PHMM_SUCCESS) rc = fetch_enqueue(cx);
     if (rc != PHMM_SUCCESS) {
@@ -1371,36 +1461,12 @@ static int score_chunked(phmm_ctx* ctx, const phmm_input* in, const phmm_options
       return ctx->fail(rc, "%s", cx->err.c_str());
     }
   }
-  // complete in order: device validation verdict, then finishing into the caller's slice
-  phmm_stats total;
-  memset(&total, 0, sizeof(total));
-  phmm_ctx* first = nullptr;
-  float span = 0.f;                  // first chunk's execute start -> last execute end
-  for (int c = 0; c < nchunks; ++c) {
-    phmm_ctx* cx = ctx->chunks[c];
-    if (cut[c + 1] <= cut[c]) continue;
-    int rc = check_validation(cx);
+  for (int c = std::max(0, nchunks - nctx); c < nchunks; ++c) {
+    const int rc = complete(c);
     if (rc != PHMM_SUCCESS) {
       drain();
-      return ctx->fail(rc, "%s", cx->err.c_str());
+      return ctx->fail(rc, "%s", ctx->chunks[c % nctx]->err.c_str());
     }
-    phmm_stats cs;
-    const int64_t g0 = pairs[cut[c]];
-    rc = fetch_complete(cx, out_log10 ? out_log10 + g0 : nullptr, out_status ? out_status + g0 : nullptr, &cs);
-    if (rc != PHMM_SUCCESS) {
-      drain();
-      return ctx->fail(rc, "%s", cx->err.c_str());
-    }
-    if (!first) first = cx;
-    float t = 0.f;
-    if (cudaEventElapsedTime(&t, first->ev_start, cx->ev_end) == cudaSuccess) span = std::max(span, t);
-    total.fast_ms += cs.fast_ms;   // per-chunk FP32 phases (they overlap other chunks' work)
-    total.h2d_ms += cs.h2d_ms;
-    total.num_pairs += cs.num_pairs; total.total_cells += cs.total_cells;
-    total.computed_cells += cs.computed_cells; total.fast_pairs += cs.fast_pairs;
-    total.exact_pairs += cs.exact_pairs; total.f64_pairs += cs.f64_pairs;
-    total.flagged_pairs += cs.flagged_pairs; total.h2d_bytes += cs.h2d_bytes; total.d2h_bytes += cs.d2h_bytes;
-    total.kernel_launches += cs.kernel_launches; total.plan_ms += cs.plan_ms; total.d2h_ms += cs.d2h_ms;
   }
   total.device_ms = span;
   ctx->last_dev_ms = span;
@@ -1410,43 +1476,127 @@ static int score_chunked(phmm_ctx* ctx, const phmm_input* in, const phmm_options
   return PHMM_SUCCESS;
 }
 
+// estimated device bytes of batch b in one prepare (see kDevBytesPerPair)
+static int64_t batch_device_bytes(const phmm_input* in, int64_t b) {
+  const int64_t r0 = in->batch_read_off[b], r1 = in->batch_read_off[b + 1];
+  const int64_t h0 = in->batch_hap_off[b], h1 = in->batch_hap_off[b + 1];
+  const int64_t rbytes = in->read_off[r1] - in->read_off[r0], hbytes = in->hap_off[h1] - in->hap_off[h0];
+  return 5 * rbytes + hbytes + 48 * (r1 - r0) + 16 * (h1 - h0) + kDevBytesPerPair * (r1 - r0) * (h1 - h0);
+}
+
+// equal-pair-count cut of the batches into nch contiguous chunks
+static std::vector<int64_t> equal_pair_cut(const phmm_input* in, int nch) {
+  const int64_t B = in->num_batches;
+  std::vector<int64_t> pairs(B + 1, 0);
+  for (int64_t b = 0; b < B; ++b)
+    pairs[b + 1] = pairs[b] + (in->batch_read_off[b + 1] - in->batch_read_off[b]) *
+                                  (in->batch_hap_off[b + 1] - in->batch_hap_off[b]);
+  std::vector<int64_t> cut(nch + 1, B);
+  cut[0] = 0;
+  for (int c = 1; c < nch; ++c) {
+    int64_t b = cut[c - 1];
+    while (b < B && pairs[b] < pairs[B] * c / nch) ++b;
+    cut[c] = std::max(b, cut[c - 1]);
+  }
+  return cut;
+}
+
+int phmm_set_device_budget(phmm_ctx* ctx, int64_t bytes) {
+  if (!ctx) return PHMM_ERR_INVALID;
+  if (bytes < 0) return ctx->fail(PHMM_ERR_INVALID, "negative device budget");
+  ctx->device_budget = bytes;
+  return PHMM_SUCCESS;
+}
+
+int phmm_device_bytes(const phmm_ctx* ctx, int64_t* bytes) {
+  if (!ctx || !bytes) return PHMM_ERR_INVALID;
+  auto one = [](const phmm_ctx* c) -> int64_t {
+    int64_t t = 0;
+    auto add = [&](const auto& buf) { t += (int64_t)(buf.cap * sizeof(*buf.p)); };
+    add(c->d_rbases); add(c->d_hbases); add(c->d_bq); add(c->d_iq); add(c->d_dq); add(c->d_gq);
+    add(c->d_status); add(c->d_rflags); add(c->d_roff); add(c->d_hoff); add(c->d_read_m); add(c->d_read_scale);
+    add(c->d_read_ncap); add(c->d_counters); add(c->d_vflag); add(c->d_gsum); add(c->d_lut); add(c->d_acc);
+    add(c->d_sunits); add(c->d_shaps); add(c->d_r64h); add(c->d_rx32h); add(c->d_cold); add(c->d_colstream);
+    for (int g = 0; g < kNumR64Geoms; ++g) add(c->d_r64u[g]);
+    for (int g = 0; g < kNumRX32Geoms; ++g) add(c->d_rx32u[g]);
+    for (int x = 0; x < kNumExactP; ++x) { add(c->d_ex32[x]); add(c->d_ex64[x]); add(c->d_fx64[x]); }
+    return t;
+  };
+  int64_t t = one(ctx);
+  for (const phmm_ctx* c : ctx->chunks) t += one(c);
+  *bytes = t;
+  return PHMM_SUCCESS;
+}
+
 int phmm_score(phmm_ctx* ctx, const phmm_input* in, const phmm_options* opt, double* out_log10,
                uint8_t* out_status, phmm_stats* stats) {
   if (!ctx) return PHMM_ERR_INVALID;
-  if (in && opt && in->num_batches >= 2 * std::max(3, score_chunks()) && score_chunks() != 1 && in->batch_read_off && in->batch_hap_off &&
-      in->read_off && in->hap_off && score_chunking_enabled()) {
-    // validate the structure first (the chunk views index the offset arrays)
-    int64_t pairs = 0;
-    bool ok = in->batch_read_off[0] == 0 && in->batch_hap_off[0] == 0 &&
-              in->batch_read_off[in->num_batches] == in->num_reads &&
-              in->batch_hap_off[in->num_batches] == in->num_haps && in->read_off[0] == 0 && in->hap_off[0] == 0;
-    for (int64_t b = 0; ok && b < in->num_batches; ++b) {
-      const int64_t nr = in->batch_read_off[b + 1] - in->batch_read_off[b];
-      const int64_t nh = in->batch_hap_off[b + 1] - in->batch_hap_off[b];
-      ok = nr > 0 && nh > 0;
-      pairs += nr * nh;
+  const bool structure = in && opt && in->batch_read_off && in->batch_hap_off && in->read_off && in->hap_off &&
+                         in->num_batches > 0;
+  // validate the structure first (the chunk views index the offset arrays)
+  int64_t pairs = 0;
+  bool ok = structure && in->batch_read_off[0] == 0 && in->batch_hap_off[0] == 0 &&
+            in->batch_read_off[in->num_batches] == in->num_reads && in->batch_hap_off[in->num_batches] == in->num_haps &&
+            in->read_off[0] == 0 && in->hap_off[0] == 0;
+  for (int64_t b = 0; ok && b < in->num_batches; ++b) {
+    const int64_t nr = in->batch_read_off[b + 1] - in->batch_read_off[b];
+    const int64_t nh = in->batch_hap_off[b + 1] - in->batch_hap_off[b];
+    ok = nr > 0 && nh > 0;
+    pairs += nr * nh;
+  }
+  // Device working-set bound: the caller's budget, or -- when the call would not fit the
+  // free device memory -- half of that.  Over budget, the call streams through chunk
+  // contexts reused round-robin, each chunk within budget / kBudgetCtx.
+  constexpr int kBudgetCtx = 3;
+  if (ok) {
+    int64_t budget = ctx->device_budget;
+    int64_t est = 0;
+    std::vector<int64_t> best(in->num_batches);
+    for (int64_t b = 0; b < in->num_batches; ++b) est += (best[b] = batch_device_bytes(in, b));
+    if (budget == 0) {
+      size_t free_b = 0, total_b = 0;
+      CK(cudaSetDevice(ctx->device));
+      if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess && est > (int64_t)(free_b * 0.6))
+        budget = (int64_t)(free_b / 2);
     }
+    if (budget > 0 && est > budget) {
+      CK(cudaSetDevice(ctx->device));
+      const int64_t per = std::max<int64_t>(1, budget / kBudgetCtx);
+      std::vector<int64_t> cut{0};
+      int64_t acc = 0;
+      for (int64_t b = 0; b < in->num_batches; ++b) {
+        if (acc > 0 && acc + best[b] > per) {
+          cut.push_back(b);
+          acc = 0;
+        }
+        acc += best[b];
+      }
+      cut.push_back(in->num_batches);
+      const size_t col = (size_t)std::max<int64_t>(1 << 20, std::min<int64_t>(kColBudget, per / 8));
+      return score_chunked(ctx, in, opt, out_log10, out_status, stats, cut,
+                           std::min<int>(kBudgetCtx, (int)cut.size() - 1), col);
+    }
+  }
+  if (ok && in->num_batches >= 2 * std::max(3, score_chunks()) && score_chunks() != 1 && score_chunking_enabled() &&
+      pairs >= kScoreChunkMinPairs) {
     // Only regular calls are pipelined: reads spanning many tiling widths split into many
     // small per-tiling kernels per chunk, and each chunk's latency-bound post-pass (guard
     // band, FP64 retries) then queues behind the next chunks' persistent grids.
-    if (ok && pairs >= kScoreChunkMinPairs) {
-      static const int kW[] = {16, 32, 48, 64, 80, 96, 112, 128, 160, 192, 224, 256, 320, 384, 448, 512};
-      unsigned classes = 0;
-      for (int64_t r = 0; r < in->num_reads; ++r) {
-        const int64_t m = in->read_off[r + 1] - in->read_off[r];
-        int c = 0;
-        while (c < 15 && kW[c] < m + 1) ++c;
-        classes |= 1u << c;
-      }
-      // large calls amortize the per-chunk post-pass latency: pipeline them regardless
-      ok = __builtin_popcount(classes) <= 2 || pairs >= kBigCallPairs;
+    static const int kW[] = {16, 32, 48, 64, 80, 96, 112, 128, 160, 192, 224, 256, 320, 384, 448, 512};
+    unsigned classes = 0;
+    for (int64_t r = 0; r < in->num_reads; ++r) {
+      const int64_t m = in->read_off[r + 1] - in->read_off[r];
+      int c = 0;
+      while (c < 15 && kW[c] < m + 1) ++c;
+      classes |= 1u << c;
     }
-    if (ok && pairs >= kScoreChunkMinPairs) {
+    // large calls amortize the per-chunk post-pass latency: pipeline them regardless
+    if (__builtin_popcount(classes) <= 2 || pairs >= kBigCallPairs) {
       CK(cudaSetDevice(ctx->device));
       // per-chunk planning overhead vs pipeline depth: 3 chunks for ordinary calls, 4 for
       // large ones (c2: 3 -> +15 % e2e over 4; c5: 4 -> +6 % over 3)
       const int nch = score_chunks() > 0 ? score_chunks() : (pairs >= kBigCallPairs ? 4 : 3);
-      return score_chunked(ctx, in, opt, out_log10, out_status, stats, nch);
+      return score_chunked(ctx, in, opt, out_log10, out_status, stats, equal_pair_cut(in, nch), nch, kColBudget);
     }
   }
   int64_t n = 0;

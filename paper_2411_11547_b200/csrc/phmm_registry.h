@@ -64,6 +64,10 @@ void launch_validate(int grid, cudaStream_t st, const uint8_t* rb, const uint8_t
                      const uint8_t* dq, const uint8_t* gq, int64_t RL, const uint8_t* hb, int64_t HL, int* flag);
 void launch_exact_all_f32(int grid, cudaStream_t st, const EngineDev& E, int* counters, float* col, int col_rows);
 void launch_exact_all_f64(int grid, cudaStream_t st, const EngineDev& E, int* counters, double* col, int col_rows);
+// phmm_matrices.cu
+void launch_matrices(cudaStream_t st, const int8_t* rb, const uint8_t* bq, const uint8_t* iq, const uint8_t* dq,
+                     const uint8_t* gq, int m, const int8_t* hb, int n, double boundary, const double* lut,
+                     double* M, double* I, double* D);
 void launch_fast64_all(int grid, cudaStream_t st, const EngineDev& E, int* counters, double* col, int col_rows);
 
 }  // namespace phmm

@@ -21,6 +21,12 @@ Extra keyword-only options:
   devices    list of CUDA devices: the batches are sharded across them by cost with one
              host thread (and one context) per device and gathered in global-id order
              (shards.py; north_star multi-GPU path, no collective).
+  device_budget_bytes  bound on the engine's device working set: a larger batch list
+             streams through three chunk contexts in budget-sized chunks (the reference's
+             chunk budget, partition.py:88-119, for inputs larger than HBM); without it the
+             engine streams automatically only when a call would not fit free memory.
+``budget_bytes`` keeps the reference's meaning: one item estimated over it raises
+BudgetError (partition.py:104-112).
 """
 from __future__ import annotations
 
@@ -69,10 +75,17 @@ def engine_flags(retry_f64: bool = False, exact: bool = False) -> int:
     return (_native.FLAG_RETRY_F64 if retry_f64 else 0) | (_native.FLAG_EXACT if exact else 0)
 
 
-def score_flat(flat: FlatBatches, configs, retry_f64=False, exact=False, device=0):
+def score_flat(flat: FlatBatches, configs, retry_f64=False, exact=False, device=0, device_budget_bytes=None):
     """Engine call on flat arrays -> (scores, status, stats)."""
     ctx = _native.context(device)
-    return ctx.score(flat, config_tuples(configs), engine_flags(retry_f64, exact))
+    if device_budget_bytes is None:
+        return ctx.score(flat, config_tuples(configs), engine_flags(retry_f64, exact))
+    with ctx._lock:
+        ctx.set_device_budget(device_budget_bytes)
+        try:
+            return ctx.score(flat, config_tuples(configs), engine_flags(retry_f64, exact))
+        finally:
+            ctx.set_device_budget(0)
 
 
 def errors_from_status(status: np.ndarray) -> list:
@@ -108,7 +121,8 @@ def _config_cells(flat: FlatBatches, configs, status: np.ndarray, device_s: floa
 
 
 def run(batches, configs=None, budget_bytes: int = DEFAULT_BUDGET_BYTES, workers: int = 1, *,
-        retry_f64: bool = False, exact: bool = False, device: int = 0, devices=None):
+        retry_f64: bool = False, exact: bool = False, device: int = 0, devices=None,
+        device_budget_bytes=None):
     """Score every work item of ``batches`` on the GPU; see the module docstring."""
     if workers < 1:
         raise ValueError("workers must be >= 1")
@@ -124,7 +138,7 @@ def run(batches, configs=None, budget_bytes: int = DEFAULT_BUDGET_BYTES, workers
                                                devices)
     elif n:
         dev = devices[0] if devices else device
-        scores, status, stats = score_flat(flat, configs, retry_f64, exact, dev)
+        scores, status, stats = score_flat(flat, configs, retry_f64, exact, dev, device_budget_bytes)
         engine = stats.as_dict()
     else:
         scores, status, engine = np.zeros(0), np.zeros(0, np.uint8), {}

@@ -234,3 +234,33 @@ def test_scale_invariance():
         a = forward_reference_linear_space(read, hap, scale_log2=0).log10_likelihood
         b = forward_reference_linear_space(read, hap, scale_log2=120).log10_likelihood
         assert abs(a - b) < 1e-12
+
+
+def test_forward_matrices_bit_identical_to_reference():
+    """forward_matrices (GPU k_matrices) against the reference's own forward_matrices on the
+    fixtures tests/golden/make_matrices_golden.py produced: every M, I, D entry bitwise."""
+    import os
+    from conftest import ROOT
+    from paper_2411_11547_b200 import DpMatrices, forward_matrices
+    z = np.load(os.path.join(ROOT, "tests", "golden", "matrices.npz"))
+    for i in range(int(z["count"])):
+        read = ReadRecord(z["%d_bases" % i], z["%d_bq" % i], z["%d_iq" % i], z["%d_dq" % i], z["%d_gq" % i])
+        hap = Haplotype(z["%d_hap" % i])
+        mats = forward_matrices(read, hap, int(z["%d_scale" % i]))
+        assert isinstance(mats, DpMatrices)
+        for k in ("M", "I", "D"):
+            want = z["%d_%s" % (i, k)]
+            got = getattr(mats, k)
+            assert got.shape == want.shape and np.array_equal(got.view(np.uint64), want.view(np.uint64)), (i, k)
+
+
+def test_forward_matrices_score_matches_forward_reference(rng):
+    from paper_2411_11547_b200 import forward_matrices
+    read, hap = random_pair(rng, 40, 55)
+    mats = forward_matrices(read, hap)
+    acc = 0.0
+    for j in range(1, hap.length + 1):
+        acc = acc + (mats.M[read.length, j] + mats.I[read.length, j])
+    assert math.log10(acc) == forward_reference(read, hap).log10_likelihood
+    with pytest.raises(DegenerateTransitionError):
+        forward_matrices(make_read("A", base_q=10, ins_q=0, del_q=0, gcp_q=10), make_hap("A"))

@@ -9,7 +9,8 @@ import numpy as np
 import pytest
 
 from oracle import oracle
-from paper_2411_11547_b200 import _native, default_configs
+from paper_2411_11547_b200 import _native, datagen, default_configs
+from paper_2411_11547_b200.errors import DataError
 from paper_2411_11547_b200.model import FlatBatches
 from paper_2411_11547_b200.pipeline import config_tuples
 
@@ -297,3 +298,36 @@ def test_guard_band_adversarial_qualities(engine, scale):
     assert ok.sum() > 100
     rel = np.abs(s[ok] - ref[ok]) / np.maximum(np.abs(ref[ok]), 1e-300)
     assert rel.max() <= REL_TOL, rel.max()
+
+
+def test_device_budget_streams_in_bounded_chunks(engine):
+    """phmm_set_device_budget: a call ~4x over the bound streams through three chunk
+    contexts reused round-robin (many chunks); results equal the resident path bitwise and
+    the device working set stays within the bound (+ fixed per-context scratch)."""
+    flat = datagen.workload("c3", num_batches=48)
+    want, wst, _ = engine.score(flat, F32, _native.FLAG_RETRY_F64)
+    ctx = _native.Context(0)
+    budget = 6 << 20
+    ctx.set_device_budget(budget)
+    got, gst, stats = ctx.score(flat, F32, _native.FLAG_RETRY_F64)
+    assert np.array_equal(got, want, equal_nan=True) and np.array_equal(gst, wst)
+    assert stats.num_pairs == flat.num_pairs and stats.device_ms > 0
+    assert ctx.device_bytes() <= budget * 1.25 + (8 << 20), ctx.device_bytes()
+    # an invalid chunk in the middle is reported and the context recovers
+    bad = datagen.workload("c3", num_batches=48)
+    bad.bq = bad.bq.copy()
+    bad.bq[bad.read_off[bad.batch_read_off[30]]] = 200
+    with pytest.raises(DataError):
+        ctx.score(bad, F32, _native.FLAG_RETRY_F64)
+    again, _, _ = ctx.score(flat, F32, _native.FLAG_RETRY_F64)
+    assert np.array_equal(again, want, equal_nan=True)
+    ctx.close()
+
+
+def test_run_device_budget_matches_unbounded():
+    from paper_2411_11547_b200 import default_configs, run
+    flat = datagen.workload("c3", num_batches=24)
+    a, ra = run(flat, default_configs("f32"), retry_f64=True)
+    b, rb = run(flat, default_configs("f32"), retry_f64=True, device_budget_bytes=2 << 20)
+    assert np.array_equal(a, b, equal_nan=True) and ra.total_cells == rb.total_cells
+    assert ra.errors == rb.errors and ra.retried == rb.retried
