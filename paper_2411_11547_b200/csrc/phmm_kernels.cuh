@@ -572,6 +572,7 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
       s_band[2 * slot] = 0u; s_band[2 * slot + 1] = 0u;
       s_ninl[slot] = 0;
     }
+    __syncwarp();          // a team warp without a stripe of this unit reads these right away
 #pragma unroll 1
     for (int q = team ? wib : 0; q < Qw; q += team ? 4 : 1) {
     const bool sq = live && q < Q;                      // this sub-warp has stripe q
