@@ -522,7 +522,7 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
   // per-CTA columns with a row-progress flag, so a unit takes ~(rows + Q x 64) steps
   // instead of Q x rows.
   __shared__ int s_team_unit;
-  __shared__ volatile int s_prog[STRIPES ? 8 : 1];
+  __shared__ int s_prog[STRIPES ? 8 : 1];          // team mode: column progress flags (atomics)
   const bool team = STRIPES && num_units * 2 <= (int)gridDim.x * 4;
 
   for (;;) {
@@ -757,7 +757,7 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
         // looks complete to stripe q + 9 early
         const int need = ((q - 1) << 16) | min(r0 + 31, rows_q);
         if (t == 0)
-          while (s_prog[(q - 1) & 7] < need) __nanosleep(64);
+          while (atomicAdd(&s_prog[(q - 1) & 7], 0) < need) __nanosleep(64);   // acquire: + fence below
         __threadfence_block();
         __syncwarp();
       }
@@ -958,7 +958,7 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
           colNext[j] = M[K - 1]; colNext[col_rows + j] = I[K - 1]; colNext[2 * col_rows + j] = D[K - 1];
           if (team && ((j & 31) == 0 || j == rows_q)) {   // publish the rows written so far
             __threadfence();
-            s_prog[q & 7] = (q << 16) | j;
+            atomicExch(&s_prog[q & 7], (q << 16) | j);   // release: after the fence above
           }
         }
       }
