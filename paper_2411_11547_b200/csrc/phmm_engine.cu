@@ -104,6 +104,16 @@ constexpr int64_t kDevBytesPerPair = 200;
 
 int stream_cap(int P) { return stream_cap_of(P); }
 
+// PHMM_OCC_CAP=n (experiments): at most n CTAs per SM for every stream-kernel grid
+int occ_cap(int occ) {
+  static int v = -1;
+  if (v < 0) {
+    const char* env = getenv("PHMM_OCC_CAP");
+    v = env ? std::max(1, atoi(env)) : 1 << 20;
+  }
+  return std::min(occ, v);
+}
+
 int exact_slot_host(int m) { return (m + 1 <= 32) ? 0 : (m + 1 <= 64) ? 1 : (m + 1 <= 128) ? 2 : 3; }
 
 int forced_geom() {
@@ -945,7 +955,7 @@ static int prepare_impl(phmm_ctx* ctx, const phmm_input* in, const phmm_options*
       const bool striped = (sb.geom & kStripedBin) != 0;
       // striped bins with few units run in team mode (a CTA per unit): one CTA per unit
       const int64_t want = striped && groups * 2 <= (int64_t)ctx->num_sms * K.occ * 4 ? groups : (groups + 3) / 4;
-      sb.grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)ctx->num_sms * K.occ, want));
+      sb.grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)ctx->num_sms * occ_cap(K.occ), want));
       sb.col_off = striped ? col_total : -1;
       if (striped) {
         const int64_t per = col_per_cta(sb.mode, K, sb.max_rows);
@@ -961,7 +971,7 @@ static int prepare_impl(phmm_ctx* ctx, const phmm_input* in, const phmm_options*
       if (ctx->r64_geoms & (1u << g)) {
         const StreamKernel& K = striped_tab(kFast64);
         const int64_t per = col_per_cta(kFast64, K, max_n);
-        ctx->r64_grid = fit(ctx->num_sms * K.occ, per);
+        ctx->r64_grid = fit(ctx->num_sms * occ_cap(K.occ), per);
         ctx->r64_col_off[g] = col_total;
         col_total += ctx->r64_grid * per;
       }
@@ -971,7 +981,7 @@ static int prepare_impl(phmm_ctx* ctx, const phmm_input* in, const phmm_options*
       if (ctx->rx32_geoms & (1u << g)) {
         const StreamKernel& K = striped_tab(kExact32);
         const int64_t per = col_per_cta(kExact32, K, max_n);
-        ctx->rx32_grid = fit(ctx->num_sms * K.occ, per);
+        ctx->rx32_grid = fit(ctx->num_sms * occ_cap(K.occ), per);
         ctx->rx32_col_off[g] = col_total;
         col_total += ctx->rx32_grid * per;
       }
@@ -1089,14 +1099,14 @@ int phmm_execute(phmm_ctx* ctx) {
       const bool str = ctx->r64_col_off[g] >= 0;
       const StreamKernel& SKn = str ? striped_tab(kFast64) : stream_table_fast64()[g];
       post(SKn, E.r64, g, ctx->d_counters.p + kCtrR64Work + g, ctx->r64_col_off[g],
-           str ? ctx->r64_grid : ctx->num_sms * SKn.occ);
+           str ? ctx->r64_grid : ctx->num_sms * occ_cap(SKn.occ));
     }
   for (int g = kNumRX32Geoms - 1; g >= 0; --g)
     if (ctx->rx32_geoms & (1u << g)) {
       const bool str = ctx->rx32_col_off[g] >= 0;
       const StreamKernel& SKn = str ? striped_tab(kExact32) : stream_table_exact32()[g];
       post(SKn, E.rx32, g, ctx->d_counters.p + kCtrRX32Work + g, ctx->rx32_col_off[g],
-           str ? ctx->rx32_grid : ctx->num_sms * SKn.occ);
+           str ? ctx->rx32_grid : ctx->num_sms * occ_cap(SKn.occ));
     }
   CK(join());
   CK(cudaEventRecord(ctx->ev_post1, st));

@@ -303,6 +303,15 @@ __device__ __forceinline__ void exact_item(const EngineDev& E, const ExactItem& 
 // ---------------------------------------------------------------------------------
 
 constexpr int kCodeFirst = 8, kCodeLast = 16;          // code byte: base | FIRST | LAST
+// Row code of the rows before a thread's first row (the wavefront fill): emission 0 at
+// every position, so a fill step maps the row-0 state onto itself (M stays 0, I stays 0,
+// D keeps the boundary in the left padding and 0 elsewhere) -- every lane starts from its
+// pre-initialised row 0 with no per-thread FIRST event.
+constexpr int kCodeIdle = 5;
+constexpr unsigned kIdle2 = kCodeIdle | (kCodeIdle << 8);
+// window list entries: start row | kWinShort (a one-step window: the LAST event of a lane's
+// final haplotype) -- otherwise P steps (the FIRST events of a haplotype boundary)
+constexpr int kWinShort = 1 << 30;
 constexpr int kStreamCodeBytesPerCta = 32768;          // row-code staging, shared memory
 constexpr int kStreamMaxLaneHaps = 15;                 // haplotypes per lane of one unit
 constexpr int kStreamMaxWin = 2 * (kStreamMaxLaneHaps + 1);
@@ -499,7 +508,10 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
   const int slot = wib * G + sw;
   const int num_units = num_units_dev ? min(*num_units_dev, num_units_arg) : num_units_arg;
   if (num_units == 0 || *E.invalid) return;
+  __shared__ EV s_zero[KE * P];                   // emission row of kCodeIdle (all 0)
   for (int i = threadIdx.x; i < 94; i += blockDim.x) s_lut[i] = E.lut[i];
+  for (int i = threadIdx.x; i < KE * P * (int)(sizeof(EV) / sizeof(float)); i += blockDim.x)
+    reinterpret_cast<float*>(s_zero)[i] = 0.f;
   __syncthreads();
   EV* Et = s_E + (size_t)(slot * 5 * KE) * P;
   unsigned char* cd = s_code + (size_t)slot * CB;
@@ -679,31 +691,43 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
           const int8_t* src = E.hbases + sh.off - start;   // src[row] = base of that row
           for (int x = lo + t; x < hi; x += P)
             cd[2 * (x & rmask) + ln] =
-                (unsigned char)(src[x] | (x == start ? kCodeFirst : 0) | (x == start + sh.n - 1 ? kCodeLast : 0));
+                (unsigned char)(src[x] | (x == start && start > 1 ? kCodeFirst : 0) |
+                                (x == start + sh.n - 1 ? kCodeLast : 0));
           start += sh.n;
         }
         for (int x = max(r0, start) + t; x < r1; x += P) cd[2 * (x & rmask) + ln] = 4;
       }
     };
-    // windows: every row where a haplotype begins in either lane, plus the row after each
-    // lane's end.  Events (FIRST for thread t at step b + t, LAST for thread P-1 at step
-    // b + P - 2) fall in windows [b, b + P).  Built once per unit.
+    // windows: every row b > 1 where a haplotype begins in either lane -- FIRST for thread
+    // t at step b + t, the previous haplotype's LAST for thread P-1 at step b + P - 2: the
+    // window [b, b + P) -- and each lane's final LAST, at step rows + P - 1 (one step).  The
+    // first haplotype of each lane needs no window (pre-initialised row 0, kCodeIdle fill).
+    // Built once per unit, sorted by start.
     if (first_q || cring) {
-      if (t == 0 && !cring) reinterpret_cast<unsigned short*>(cd)[0] = 0x0404;
       if (live) stage_rows(1, min(rows + 1, RS));
     }
     if (first_q) {
     if (live) {
-      if (t == 0) {                                   // merge the two lanes' window starts
+      if (t == 0) {                                   // merge the two lanes' windows by start
         int* wb = s_win + slot * kStreamMaxWin;
+        // lane walk: entry x of a lane with c haplotypes: x < c - 1 -> start of haplotype
+        // x + 1 (P steps); x == c - 1 -> the final LAST (one step, at rows + P - 1)
         int ia = 0, ib = 0, ra = 1, rb = 1, nw = 0;
         const int ca = U.cntA, cbn = U.cntB;
-        while (ia <= ca || ib <= cbn) {
-          const int va = ia <= ca ? ra : 0x7fffffff, vb = ib <= cbn ? rb : 0x7fffffff;
-          const int v = min(va, vb);
+        auto entry = [&](int x, int c, int& row, int e0) -> int {
+          if (x >= c) return 0x7fffffff;
+          if (x == c - 1) return (row + shaps[U.list + e0 + x].n + P - 2) | kWinShort;   // last row + P - 1
+          return row + shaps[U.list + e0 + x].n;                                       // next start
+        };
+        while (true) {
+          const int va = entry(ia, ca, ra, 0), vb = entry(ib, cbn, rb, ca);
+          const int sa = va & ~kWinShort, sbv = vb & ~kWinShort;
+          if (va == 0x7fffffff && vb == 0x7fffffff) break;
+          const bool takeA = vb == 0x7fffffff || (va != 0x7fffffff && sa <= sbv);
+          const int v = takeA ? va : vb;
           if (nw == 0 || wb[nw - 1] != v) wb[nw++] = v;
-          if (va == v) { if (ia < ca) ra += shaps[U.list + ia].n; ++ia; }
-          if (vb == v) { if (ib < cbn) rb += shaps[U.list + ca + ib].n; ++ib; }
+          if (takeA) { ra += shaps[U.list + ia].n; ++ia; }
+          else { rb += shaps[U.list + ca + ib].n; ++ib; }
         }
         s_nwin[slot] = nw;
       }
@@ -735,9 +759,9 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
     // the idle code N|N: rows before, between and after this thread's stream)
     auto ld_code = [&](int s) -> unsigned {
       const int i = s - t;
-      return (i >= 1 && i <= rows_q) ? (unsigned)cd16[(unsigned)i & rmask] : 0x0404u;
+      return (i >= 1 && i <= rows_q) ? (unsigned)cd16[(unsigned)i & rmask] : kIdle2;
     };
-    unsigned code = 0x0404u;
+    unsigned code = kIdle2;
     unsigned pf1 = ld_code(1);
     // stripe q > 0: thread 0's left neighbour is the previous stripe's column
     V* colPrev = team ? colX + (size_t)((q - 1) & 7) * 3 * col_rows : (q & 1) ? colY : colX;
@@ -779,15 +803,25 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
       const int lp = s_meta[slot * 4 + 0];
       const S b = s_bs[slot * 2 * kStreamMaxLaneHaps + (L == 0 ? 0 : s_unit[slot].cntA) + hc];
       const int p0 = q * W + t * K;                     // global padded position of k = 0
+      if (p0 > lp) {                                    // no left padding here (most threads)
 #pragma unroll
-      for (int k = 0; k < K; ++k) {
-        lane_ref<L>(M[k]) = 0;
-        lane_ref<L>(I[k]) = 0;
-        lane_ref<L>(D[k]) = (p0 + k < lp) ? b : (S)0;
+        for (int k = 0; k < K; ++k) {
+          lane_ref<L>(M[k]) = 0;
+          lane_ref<L>(I[k]) = 0;
+          lane_ref<L>(D[k]) = 0;
+        }
+        lane_ref<L>(dgD) = 0;
+      } else {
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          lane_ref<L>(M[k]) = 0;
+          lane_ref<L>(I[k]) = 0;
+          lane_ref<L>(D[k]) = (p0 + k < lp) ? b : (S)0;
+        }
+        lane_ref<L>(dgD) = (p0 - 1 < lp) ? b : (S)0;    // (stripe 0, thread 0: the boundary)
       }
       lane_ref<L>(dgM) = 0;
       lane_ref<L>(dgI) = 0;
-      lane_ref<L>(dgD) = (p0 - 1 < lp) ? b : (S)0;      // (stripe 0, thread 0: the boundary)
       if (t == 0 && q == 0) {
         lane_ref<L>(cb) = b;
         lane_ref<L>(nbM) = 0; lane_ref<L>(nbI) = 0; lane_ref<L>(nbD) = b;
@@ -883,8 +917,8 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
         if (code & (kCodeFirst << 8)) first_event(std::integral_constant<int, 1>{}, dgM, dgI, dgD, nbM, nbI, nbD);
       }
       const int cA = code & 7, cB = (code >> 8) & 7;
-      const EV* EA = Et + (cA * KE) * P + t;
-      const EV* EB = Et + (cB * KE) * P + t;
+      const EV* EA = cA == kCodeIdle ? s_zero + t : Et + (cA * KE) * P + t;
+      const EV* EB = cB == kCodeIdle ? s_zero + t : Et + (cB * KE) * P + t;
       // fast FP32 at occupancy 2 (K = 14, 16) has the registers for the carried values
       constexpr bool FUSED = !EXACT && (F64 ? !STRIPES : K >= 14);
       if constexpr (FUSED) {
@@ -968,16 +1002,33 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
       }
     };
 
-    // event-free stretches run the plain step; windows run the event-checking one; ring
-    // units restage a half-ring of row codes at the (warp-uniform) refill steps nr:
-    // at step (b+1)H + P the rows of block b (rows bH .. (b+1)H-1, last read at step
-    // (b+1)H + P - 2) are free and block b+2 (first read at step (b+2)H - 1) is written
+    // row 0 of each lane's first haplotype: the fill steps (kCodeIdle) keep it until the
+    // thread's first row, so no FIRST event is needed for it
+    if (sq) {
+      if (U.cntA > 0) first_event(std::integral_constant<int, 0>{}, xM, xI, xD, yM, yI, yD);
+      if (U.cntB > 0) first_event(std::integral_constant<int, 1>{}, xM, xI, xD, yM, yI, yD);
+    }
+
+    // event-free stretches run the plain step; windows run the event-checking one, for as
+    // long as any sub-warp of the warp is inside one of its windows; ring units restage a
+    // half-ring of row codes at the (warp-uniform) refill steps nr: at step (b+1)H + P the
+    // rows of block b (rows bH .. (b+1)H-1, last read at step (b+1)H + P - 2) are free and
+    // block b+2 (first read at step (b+2)H - 1) is written
     const int nwin = s_nwin[slot];
     const int* wb = s_win + slot * kStreamMaxWin;
+    // this sub-warp's earliest unfinished window [cur_s, cur_e), kept in registers
+    int wi = 0;
+    int cur_s = 0x7fffffff, cur_e = 0x7fffffff;
+    if (nwin > 0) { cur_s = wb[0] & ~kWinShort; cur_e = cur_s + ((wb[0] & kWinShort) ? 1 : P); }
+    int s = 1;
+    auto advance = [&]() {
+      while (cur_e <= s) {
+        if (++wi < nwin) { cur_s = wb[wi] & ~kWinShort; cur_e = cur_s + ((wb[wi] & kWinShort) ? 1 : P); }
+        else { cur_s = 0x7fffffff; cur_e = 0x7fffffff; }
+      }
+    };
     constexpr int H = RS / 2;
     int nr = __any_sync(FULL, cring && sq) ? H + P : 0x7fffffff;
-    int wi = 0;
-    int s = 1;
 #pragma unroll 1
     while (s <= steps) {
       if (s == nr) {
@@ -986,9 +1037,8 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
         __syncwarp();
         nr += H;
       }
-      while (wi < nwin && wb[wi] + P <= s) ++wi;
-      const int e_sw = wi < nwin ? wb[wi] : 0x7fffffff;
-      const int e = max((int)__reduce_min_sync(FULL, (unsigned)e_sw), s);
+      advance();
+      const int e = max((int)__reduce_min_sync(FULL, (unsigned)cur_s), s);
       const int fend = min(min(e, nr), steps + 1);
 #pragma unroll 1
       for (; s + 1 < fend; s += 2) {
@@ -1002,11 +1052,26 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
       }
       if (s > steps) break;
       if (s == nr) continue;                            // refill before the next step
-      const int wend = min(min(e + P, nr), steps + 1);
+      // some sub-warp is inside a window: event-checking steps, two per iteration (the
+      // register sets alternate like the plain steps; leaving after an odd step copies once)
 #pragma unroll 1
-      for (; s < wend; ++s) {
+      for (;;) {
         step(s, std::true_type{}, xM, xI, xD, yM, yI, yD);
-        xM = yM; xI = yI; xD = yD;
+        ++s;
+        bool stop = s > steps || s == nr;
+        if (!stop) {
+          advance();
+          stop = !__any_sync(FULL, cur_s <= s);
+        }
+        if (stop) {
+          xM = yM; xI = yI; xD = yD;
+          break;
+        }
+        step(s, std::true_type{}, yM, yI, yD, xM, xI, xD);
+        ++s;
+        if (s > steps || s == nr) break;
+        advance();
+        if (!__any_sync(FULL, cur_s <= s)) break;
       }
     }
     if constexpr (STRIPES) cp_async_wait_all();      // the ring is refilled by the next stripe
