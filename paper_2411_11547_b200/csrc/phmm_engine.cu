@@ -722,7 +722,7 @@ static int prepare_impl(phmm_ctx* ctx, const phmm_input* in, const phmm_options*
                 t = &tmpl.back();
                 ln = 0;
               }
-              t->lanes[ln].push_back(h);
+              t->lanes[ln].push_back(h);                     // (host-built modes: no separator rows)
               t->rows[ln] += n;
             }
           }

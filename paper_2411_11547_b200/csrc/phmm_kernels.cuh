@@ -312,6 +312,10 @@ constexpr unsigned kIdle2 = kCodeIdle | (kCodeIdle << 8);
 // window list entries: start row | kWinShort (a one-step window: the LAST event of a lane's
 // final haplotype) -- otherwise P steps (the FIRST events of a haplotype boundary)
 constexpr int kWinShort = 1 << 30;
+// FP64 retry units (kFast64) separate consecutive haplotypes of a lane by one kCodeIdle row:
+// it leaves M = I = 0, so a FIRST event only resets D (the FP64 kernel is issue-heavier in
+// its event windows); the other modes reset M, I and D and need no separator rows.
+template <int MODE> struct SepRows { static constexpr bool value = MODE == 1; };
 constexpr int kStreamCodeBytesPerCta = 32768;          // row-code staging, shared memory
 constexpr int kStreamMaxLaneHaps = 15;                 // haplotypes per lane of one unit
 constexpr int kStreamMaxWin = 2 * (kStreamMaxLaneHaps + 1);
@@ -440,7 +444,7 @@ __device__ __forceinline__ int stream_finish32(const EngineDev& E, float a, int 
 // units of tiling g (row capacity cap) appended to L; thread-serial, rare.
 __device__ __forceinline__ void emit_retry_units(const StreamUnit& U, const StreamHap* shaps, const unsigned* mask,
                                                  const RetryLists& L, int g, int cap, int m, int lane_haps,
-                                                 int cap_w = 1 << 30) {
+                                                 int cap_w, bool sep) {
   int lanes_n[2] = {0, 0}, rows_n[2] = {0, 0};
   StreamHap buf[2][kStreamMaxLaneHaps];
   auto emit = [&]() {
@@ -467,9 +471,10 @@ __device__ __forceinline__ void emit_retry_units(const StreamUnit& U, const Stre
       msk &= msk - 1;
       const StreamHap sh = shaps[e0 + e];
       int l2 = rows_n[0] <= rows_n[1] ? 0 : 1;
-      if (rows_n[l2] + sh.n > cap || lanes_n[l2] >= lane_haps) { emit(); l2 = 0; }
+      const int gap = sep && rows_n[l2] > 0 ? 1 : 0;     // separator row before it (SepRows)
+      if (rows_n[l2] + gap + sh.n > cap || lanes_n[l2] >= lane_haps) { emit(); l2 = 0; }
+      rows_n[l2] += sh.n + (sep && lanes_n[l2] > 0 ? 1 : 0);
       buf[l2][lanes_n[l2]++] = sh;
-      rows_n[l2] += sh.n;
     }
   }
   emit();
@@ -490,6 +495,7 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
          int num_units_arg, const int* __restrict__ num_units_dev, int* __restrict__ counter,
          void* __restrict__ colbuf_v, int col_rows) {
   constexpr bool F64 = ModeOf<MODE>::F64, EXACT = ModeOf<MODE>::EXACT;
+  constexpr bool SEP = SepRows<MODE>::value;
   using A = Lanes<F64>;
   using S = typename A::S;
   using V = typename A::V;
@@ -693,7 +699,10 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
             cd[2 * (x & rmask) + ln] =
                 (unsigned char)(src[x] | (x == start && start > 1 ? kCodeFirst : 0) |
                                 (x == start + sh.n - 1 ? kCodeLast : 0));
-          start += sh.n;
+          // separator row after every haplotype but the lane's last: kCodeIdle (M -> 0, I -> 0)
+          if (SEP && e + 1 < cnt && t == 0 && start + sh.n >= r0 && start + sh.n < r1)
+            cd[2 * ((start + sh.n) & rmask) + ln] = kCodeIdle;
+          start += sh.n + (SEP && e + 1 < cnt ? 1 : 0);
         }
         for (int x = max(r0, start) + t; x < r1; x += P) cd[2 * (x & rmask) + ln] = 4;
       }
@@ -717,7 +726,7 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
         auto entry = [&](int x, int c, int& row, int e0) -> int {
           if (x >= c) return 0x7fffffff;
           if (x == c - 1) return (row + shaps[U.list + e0 + x].n + P - 2) | kWinShort;   // last row + P - 1
-          return row + shaps[U.list + e0 + x].n;                                       // next start
+          return row + shaps[U.list + e0 + x].n + (SEP ? 1 : 0);                       // next start
         };
         while (true) {
           const int va = entry(ia, ca, ra, 0), vb = entry(ib, cbn, rb, ca);
@@ -726,8 +735,8 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
           const bool takeA = vb == 0x7fffffff || (va != 0x7fffffff && sa <= sbv);
           const int v = takeA ? va : vb;
           if (nw == 0 || wb[nw - 1] != v) wb[nw++] = v;
-          if (takeA) { ra += shaps[U.list + ia].n; ++ia; }
-          else { rb += shaps[U.list + ca + ib].n; ++ib; }
+          if (takeA) { ra += shaps[U.list + ia].n + (SEP ? 1 : 0); ++ia; }
+          else { rb += shaps[U.list + ca + ib].n + (SEP ? 1 : 0); ++ib; }
         }
         s_nwin[slot] = nw;
       }
@@ -797,32 +806,36 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
 
     // FIRST(lane L): reset the lane to row 0 of its next haplotype (event paths only run
     // inside windows and read their inputs from shared memory)
-    auto first_event = [&](auto lconst, V& dgM, V& dgI, V& dgD, V& nbM, V& nbI, V& nbD) {
+    // FULL (the unit's pre-initialisation): M = I = 0, D = the boundary in the left padding.
+    // Event (row 1 of a lane's next haplotype): the separator row before it (kCodeIdle)
+    // already left M = I = 0 in this thread and in the neighbour's diagonal values, so only
+    // D is reset.
+    auto first_event = [&](auto lconst, auto full, V& dgM, V& dgI, V& dgD, V& nbM, V& nbI, V& nbD) {
       constexpr int L = decltype(lconst)::value;
+      constexpr bool FULL = decltype(full)::value;
       const int hc = ++s_hc[2 * threadIdx.x + L];
       const int lp = s_meta[slot * 4 + 0];
-      const S b = s_bs[slot * 2 * kStreamMaxLaneHaps + (L == 0 ? 0 : s_unit[slot].cntA) + hc];
       const int p0 = q * W + t * K;                     // global padded position of k = 0
+      auto bval = [&]() { return s_bs[slot * 2 * kStreamMaxLaneHaps + (L == 0 ? 0 : s_unit[slot].cntA) + hc]; };
       if (p0 > lp) {                                    // no left padding here (most threads)
 #pragma unroll
         for (int k = 0; k < K; ++k) {
-          lane_ref<L>(M[k]) = 0;
-          lane_ref<L>(I[k]) = 0;
+          if (FULL) { lane_ref<L>(M[k]) = 0; lane_ref<L>(I[k]) = 0; }
           lane_ref<L>(D[k]) = 0;
         }
         lane_ref<L>(dgD) = 0;
       } else {
+        const S b = bval();
 #pragma unroll
         for (int k = 0; k < K; ++k) {
-          lane_ref<L>(M[k]) = 0;
-          lane_ref<L>(I[k]) = 0;
+          if (FULL) { lane_ref<L>(M[k]) = 0; lane_ref<L>(I[k]) = 0; }
           lane_ref<L>(D[k]) = (p0 + k < lp) ? b : (S)0;
         }
         lane_ref<L>(dgD) = (p0 - 1 < lp) ? b : (S)0;    // (stripe 0, thread 0: the boundary)
       }
-      lane_ref<L>(dgM) = 0;
-      lane_ref<L>(dgI) = 0;
+      if (FULL) { lane_ref<L>(dgM) = 0; lane_ref<L>(dgI) = 0; }
       if (t == 0 && q == 0) {
+        const S b = bval();
         lane_ref<L>(cb) = b;
         lane_ref<L>(nbM) = 0; lane_ref<L>(nbI) = 0; lane_ref<L>(nbD) = b;
       }
@@ -913,8 +926,9 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
       code = pf1;
       pf1 = ld_code(s + 1);
       if (CHECK && (code & ((kCodeFirst << 8) | kCodeFirst))) {
-        if (code & kCodeFirst) first_event(std::integral_constant<int, 0>{}, dgM, dgI, dgD, nbM, nbI, nbD);
-        if (code & (kCodeFirst << 8)) first_event(std::integral_constant<int, 1>{}, dgM, dgI, dgD, nbM, nbI, nbD);
+        using Full = std::integral_constant<bool, !SEP>;
+        if (code & kCodeFirst) first_event(std::integral_constant<int, 0>{}, Full{}, dgM, dgI, dgD, nbM, nbI, nbD);
+        if (code & (kCodeFirst << 8)) first_event(std::integral_constant<int, 1>{}, Full{}, dgM, dgI, dgD, nbM, nbI, nbD);
       }
       const int cA = code & 7, cB = (code >> 8) & 7;
       const EV* EA = cA == kCodeIdle ? s_zero + t : Et + (cA * KE) * P + t;
@@ -1005,8 +1019,8 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
     // row 0 of each lane's first haplotype: the fill steps (kCodeIdle) keep it until the
     // thread's first row, so no FIRST event is needed for it
     if (sq) {
-      if (U.cntA > 0) first_event(std::integral_constant<int, 0>{}, xM, xI, xD, yM, yI, yD);
-      if (U.cntB > 0) first_event(std::integral_constant<int, 1>{}, xM, xI, xD, yM, yI, yD);
+      if (U.cntA > 0) first_event(std::integral_constant<int, 0>{}, std::true_type{}, xM, xI, xD, yM, yI, yD);
+      if (U.cntB > 0) first_event(std::integral_constant<int, 1>{}, std::true_type{}, xM, xI, xD, yM, yI, yD);
     }
 
     // event-free stretches run the plain step; windows run the event-checking one, for as
@@ -1080,7 +1094,8 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
     if constexpr (MODE == kExact32 && STRIPES) {
       // long reads: guard-band pairs whose exact rerun underflowed -> striped FP64 units
       if (t == 0 && live && (s_flag[2 * slot] | s_flag[2 * slot + 1]))
-        emit_retry_units(U, shaps, s_flag + 2 * slot, E.r64b, kNumR64Geoms - 1, stream_cap_of(32), m, 1);
+        emit_retry_units(U, shaps, s_flag + 2 * slot, E.r64b, kNumR64Geoms - 1, stream_cap_of(32), m, 1, 1 << 30,
+                         SepRows<kFast64>::value);
     }
     if constexpr (MODE == kFast32) {
       // this unit's FP32-underflowed and guard-band pairs -> device-built stream units
@@ -1088,12 +1103,12 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
         if (s_flag[2 * slot] | s_flag[2 * slot + 1]) {
           const int g64 = r64_geom_for(m);
           emit_retry_units(U, shaps, s_flag + 2 * slot, E.r64, g64, stream_cap_of(r64_geom_P(g64)), m,
-                           E.r64.lane_haps, 256);
+                           E.r64.lane_haps, 256, SepRows<kFast64>::value);
         }
         if (s_band[2 * slot] | s_band[2 * slot + 1]) {
           const int gx = rx32_geom_for(m);
           emit_retry_units(U, shaps, s_band + 2 * slot, E.rx32, gx, stream_cap_of(rx32_geom_P(gx)), m,
-                           E.rx32.lane_haps, 512);
+                           E.rx32.lane_haps, 512, SepRows<kExact32>::value);
         }
       }
       // inline guard-band reruns (same tiling; the emission-table slot is free again)
