@@ -24,10 +24,11 @@ No collective on the data path — NCCL only carries the max-over-ranks timing.
   roofline  the dominant kernel (k_stream FP32 streaming wavefront, all tiling bins of the
             FP32 phase) against the FP32-FMA roofline of SURVEY.md §8(d): 148 SMs x 128
             lanes x f_SM / 8 ops per cell; plus the whole step and a per-phase breakdown.
-  cpu_baseline  the C oracle (a port of the reference recursion, oracle/) on the host
-            cores, bounded sample of the same workload, rank 0 only.
---impl reference times that CPU port alone (the reference package itself is numba-based and
-absent on the GPU box).
+  cpu_baseline  the reference's own CPU path (the unmodified pairhmm package installed in
+            baseline/_ref, numba, pairhmm.run on all host cores; kind "reference") on a
+            bounded sample of the same workload, rank 0 only, with the C port of its
+            recursion (oracle/, kind "port") beside it.
+--impl reference times the reference package alone (the C port when baseline/_ref is absent).
 """
 from __future__ import annotations
 
@@ -181,6 +182,93 @@ def cpu_baseline(flat, seconds, flags_retry=False):
                                                     if flags_retry else "", cores, dt)}
 
 
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+
+
+def reference_package():
+    """The unmodified reference package (pairhmm 0.1.0, numpy + numba) installed by
+    `pip install --no-index --no-deps --target baseline/_ref`, or None."""
+    if not os.path.isdir(os.path.join(REF_DIR, "pairhmm")):
+        return None
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    try:
+        import pairhmm
+        import numba  # noqa: F401
+    except ImportError:
+        return None
+    return pairhmm
+
+
+def _ref_batches(pairhmm, flat, b0, b1):
+    """Reference Batch objects (the reference's own types) for batches [b0, b1) of flat."""
+    out = []
+    for b in range(b0, b1):
+        reads = []
+        for r in range(int(flat.batch_read_off[b]), int(flat.batch_read_off[b + 1])):
+            s = slice(int(flat.read_off[r]), int(flat.read_off[r + 1]))
+            reads.append(pairhmm.ReadRecord(flat.read_bases[s], flat.bq[s], flat.iq[s], flat.dq[s], flat.gq[s]))
+        haps = [pairhmm.Haplotype(flat.hap_bases[int(flat.hap_off[h]):int(flat.hap_off[h + 1])])
+                for h in range(int(flat.batch_hap_off[b]), int(flat.batch_hap_off[b + 1]))]
+        out.append(pairhmm.Batch(reads, haps))
+    return out
+
+
+def reference_cpu(flat, seconds, flags_retry=False, warm=True):
+    """The reference's own CPU path, pairhmm.run(batches, default_configs('f32'),
+    workers=all cores) (pipeline.py:77-142), on the first batches of the workload, grown
+    until about `seconds` of work; GATK semantics re-score the pairs it flags
+    (NumericOverflowError, NaN) with pairhmm.run(..., default_configs('f64')) — the
+    reference has no automatic retry, so a caller does exactly this.  Cells = every pair's
+    m*n once (the GPU arm's accounting)."""
+    pairhmm = reference_package()
+    if pairhmm is None:
+        return None
+    cores = os.cpu_count() or 1
+    cf32, cf64 = pairhmm.default_configs("f32"), pairhmm.default_configs("f64")
+    nb = flat.batch_read_off.shape[0] - 1
+    if warm:                                   # numba JIT (cache=True) outside the timed region
+        w = _ref_batches(pairhmm, flat, 0, 1)
+        pairhmm.run(w, cf32, workers=1)
+        pairhmm.run(w, cf64, workers=1)
+    done = cells = retried = 0
+    step = 1
+    t_all = 0.0
+    while done < nb and t_all < seconds:
+        b1 = min(nb, done + step)
+        batches = _ref_batches(pairhmm, flat, done, b1)
+        t0 = time.perf_counter()
+        scores, rep = pairhmm.run(batches, cf32, workers=cores)
+        if flags_retry:
+            bad = np.flatnonzero(np.isnan(scores))
+            if bad.size:
+                items = pairhmm.enumerate_work_items(batches)
+                pairs = [pairhmm.Batch([batches[items[g].batch_index].reads[items[g].read_index]],
+                                       [batches[items[g].batch_index].haps[items[g].hap_index]]) for g in bad]
+                pairhmm.run(pairs, cf64, workers=cores)
+                retried += int(bad.size)
+        t_all += time.perf_counter() - t0
+        cells += int(rep.total_cells)
+        done = b1
+        step = min(step * 2, 64)
+    pr0 = int(flat.batch_read_off[done])
+    return {"value": cells / t_all / 1e9, "unit": "GCUPS", "cores": cores, "kind": "reference",
+            "cpu_model": cpu_model(),
+            "sample": "first %d of %d batches (%d reads, %.3g cells) of the same workload through the unmodified "
+                      "reference pairhmm.run(batches, default_configs('f32'), workers=%d)%s (numba %s), %.1f s"
+                      % (done, nb, pr0, cells, cores,
+                         " + pairhmm.run(..., default_configs('f64')) on its %d flagged pairs" % retried
+                         if flags_retry else "", _numba_version(), t_all)}
+
+
+def _numba_version():
+    try:
+        import numba
+        return numba.__version__
+    except ImportError:
+        return None
+
+
 def cpu_model():
     try:
         with open("/proc/cpuinfo") as f:
@@ -193,15 +281,26 @@ def cpu_model():
 
 
 def run_reference(args, ws, rank):
-    """--impl reference: the CPU port of the reference recursion on all host cores."""
+    """--impl reference: the reference's own CPU path (pairhmm.run from baseline/_ref, numba,
+    all host cores) on bounded samples of the workload; the C port of its recursion
+    (oracle/) when the package is not installed.  Rank 0 only."""
     if rank != 0:
         return 0
     from paper_2411_11547_b200 import datagen
     flat = datagen.workload(args.workload)
+    retry = args.workload in RETRY_WORKLOADS
+    use_pkg = reference_package() is not None
+    per = max(2.0, args.cpu_seconds / max(1, args.steps))
+
+    def sample(seconds, warm):
+        if use_pkg:
+            return reference_cpu(flat, seconds, retry, warm=warm)
+        return cpu_baseline(flat, seconds, retry)
+
     per_step = []
     base = None
     for i in range(args.warmup + args.steps):
-        b = cpu_baseline(flat, args.cpu_seconds / max(1, args.steps), args.workload in RETRY_WORKLOADS)
+        b = sample(per if i >= args.warmup else 1.0, warm=(i == 0))
         if i >= args.warmup:
             per_step.append(b["value"])
             base = b
@@ -465,7 +564,10 @@ def main():
         except Exception as exc:
             line["e2e_run"] = [{"error": repr(exc)}]
     if not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(full, args.cpu_seconds, bool(flags & _native.FLAG_RETRY_F64))
+        retry = bool(flags & _native.FLAG_RETRY_F64)
+        port = cpu_baseline(full, args.cpu_seconds, retry)
+        ref = reference_cpu(full, args.cpu_seconds, retry)
+        line["cpu_baseline"] = dict(ref, port=port) if ref is not None else port
     print(json.dumps(line))
     if ws > 1:
         dist.destroy_process_group()

@@ -51,6 +51,11 @@ struct PinnedAlloc {
   using value_type = T;
   PinnedAlloc() = default;
   template <class U> PinnedAlloc(const PinnedAlloc<U>&) {}
+  // default-initialise (no zero fill of POD elements on resize)
+  template <class U, class... A> void construct(U* p, A&&... a) {
+    if constexpr (sizeof...(A) == 0) ::new ((void*)p) U;
+    else ::new ((void*)p) U(std::forward<A>(a)...);
+  }
   T* allocate(size_t n) {
     void* p = nullptr;
     if (cudaMallocHost(&p, n * sizeof(T)) != cudaSuccess) throw std::bad_alloc();
@@ -310,7 +315,8 @@ struct phmm_ctx {
   int64_t device_budget = 0; // phmm_set_device_budget: bound on the device working set of phmm_score (0: none)
   size_t col_budget = kColBudget;        // boundary-column scratch bound of this context
   std::vector<phmm_ctx*> chunks;             // chunk contexts (phmm_score pipelining), lazy
-  std::vector<int64_t> c_roff, c_hoff, c_bro, c_bho;   // chunk views: rebased offsets
+  PinnedVec<int64_t> c_roff, c_hoff;         // chunk views: rebased offsets (pinned: async H2D)
+  std::vector<int64_t> c_bro, c_bho;
   double* h_acc = nullptr;   // pinned result staging (phmm_fetch)
   uint8_t* h_st = nullptr;
   int64_t h_res_cap = 0;
@@ -567,6 +573,7 @@ static int prepare_impl(phmm_ctx* ctx, const phmm_input* in, const phmm_options*
   CK(up(ctx->d_iq, in->ins_qual, RL));
   CK(up(ctx->d_dq, in->del_qual, RL));
   CK(up(ctx->d_gq, in->gcp_qual, RL));
+  trace.mark("h2d-reads");
   CK(up(ctx->d_roff, roff, R ? R + 1 : 0));
   CK(up(ctx->d_hbases, in->hap_bases, HL));
   CK(up(ctx->d_hoff, hoff, H ? H + 1 : 0));
@@ -581,21 +588,46 @@ static int prepare_impl(phmm_ctx* ctx, const phmm_input* in, const phmm_options*
   });
   ctx->read_m.resize(R); ctx->read_scale.resize(R); ctx->read_cfg.resize(R);
   std::vector<int> read_ncap(R, 1);
-  int64_t memo_m = -1;
-  int memo_cfg = -1;
-  for (int64_t r = 0; r < R; ++r) {
-    const int64_t m = roff[r + 1] - roff[r];
-    if (m > (int64_t)1 << 30) return ctx->fail(PHMM_ERR_INVALID, "read too long");
-    ctx->read_m[r] = (int)m;
-    if (m != memo_m) {                               // reads of a batch often share m
-      memo_cfg = -1;
-      for (int c : order)
-        if ((int64_t)opt->p[c] * opt->k[c] >= m) { memo_cfg = c; break; }
-      memo_m = m;
+  // host worker pool (shared with the chunk contexts of a pipelined call): large calls bind
+  // and plan on it
+  WorkerPool* pool = nullptr;
+  if (R >= (1 << 13)) {
+    phmm_ctx* owner = ctx->parent ? ctx->parent : ctx;
+    if (!owner->pool) {
+      const int hw = (int)std::max(1u, std::thread::hardware_concurrency());
+      owner->pool.reset(new WorkerPool(std::min(hw, kFinishThreads) - 1));
     }
-    ctx->read_cfg[r] = memo_cfg;
-    ctx->read_scale[r] = memo_cfg >= 0 ? opt->scale_log2[memo_cfg] : 0;
+    pool = owner->pool.get();
   }
+  auto par_for = [&](int64_t n, int tasks, const std::function<void(int64_t, int64_t)>& body) {
+    if (!pool || tasks <= 1 || n < 2 * tasks) { body(0, n); return; }
+    std::function<void(int)> task = [&](int i) { body(n * i / tasks, n * (i + 1) / tasks); };
+    pool->run(tasks, task);
+  };
+  std::vector<int> too_long;
+  std::mutex too_long_mu;
+  par_for(R, pool ? pool->size() + 1 : 1, [&](int64_t a, int64_t z) {
+    int64_t memo_m = -1;
+    int memo_cfg = -1;
+    for (int64_t r = a; r < z; ++r) {
+      const int64_t m = roff[r + 1] - roff[r];
+      if (m > (int64_t)1 << 30) {
+        std::lock_guard<std::mutex> lk(too_long_mu);
+        too_long.push_back((int)r);
+        continue;
+      }
+      ctx->read_m[r] = (int)m;
+      if (m != memo_m) {                               // reads of a batch often share m
+        memo_cfg = -1;
+        for (int c : order)
+          if ((int64_t)opt->p[c] * opt->k[c] >= m) { memo_cfg = c; break; }
+        memo_m = m;
+      }
+      ctx->read_cfg[r] = memo_cfg;
+      ctx->read_scale[r] = memo_cfg >= 0 ? opt->scale_log2[memo_cfg] : 0;
+    }
+  });
+  if (!too_long.empty()) return ctx->fail(PHMM_ERR_INVALID, "read too long");
   trace.mark("bind");
   // ---- pairs, hap pairing, units
   int64_t N = 0;
@@ -619,8 +651,6 @@ static int prepare_impl(phmm_ctx* ctx, const phmm_input* in, const phmm_options*
   int64_t r64_pairs[8] = {0}, rx32_pairs[8] = {0};
   bool long64 = false, long32 = false;          // streamed reads that stripe in the retry kernels
   int max_n = 1;
-  int64_t gid = 0;
-  std::vector<int> hidx;
   struct LaneTemplate {
     std::vector<int> lanes[2];
     int rows[2] = {0, 0};
@@ -634,9 +664,9 @@ static int prepare_impl(phmm_ctx* ctx, const phmm_input* in, const phmm_options*
     std::vector<LaneTemplate> tmpls[kMaxTilings];
     int tmpl_m = -1, tmpl_geom = -2;
   };
-  ModePlan mp[4];
+  ModePlan mp0[4];                              // tiling tables (copied per planning part)
   for (int md = 0; md < 4; ++md) {
-    ModePlan& M = mp[md];
+    ModePlan& M = mp0[md];
     M.n = kStreamTabN[md];
     for (int g = 0; g < M.n; ++g) M.wsort[g] = g;
     std::sort(M.wsort, M.wsort + M.n, [&](int x, int y) {
@@ -644,52 +674,79 @@ static int prepare_impl(phmm_ctx* ctx, const phmm_input* in, const phmm_options*
     });
     for (int i = 0; i < M.n; ++i) M.wsorted[i] = stream_tab(md)[M.wsort[i]].P * stream_tab(md)[M.wsort[i]].K;
   }
-  ctx->shaps.reserve(N);
   // Lane budget: a call too small to fill the GPU with long lanes (few pairs, long
   // haplotypes: c4) splits its units until there are ~2 per sub-warp slot (#SM x 8 warps
   // x 2 sub-warps); latency, not per-unit overhead, bounds such calls.  Large calls keep
-  // the row capacity as the only limit.
+  // the row capacity as the only limit.  Per batch: first pair id and first stream entry.
   int64_t lane_rows = INT64_MAX;
+  std::vector<int64_t> bgid(B + 1, 0), bsh(B + 1, 0);
   {
     int64_t all_rows = 0;
     for (int64_t b = 0; b < B; ++b) {
-      int64_t hs = 0;
+      const int64_t r0 = ctx->batch_read_off[b], r1 = ctx->batch_read_off[b + 1];
+      int64_t hs = 0, live = 0;
       for (int64_t h = ctx->batch_hap_off[b]; h < ctx->batch_hap_off[b + 1]; ++h) hs += ctx->hap_len[h];
-      all_rows += hs * (ctx->batch_read_off[b + 1] - ctx->batch_read_off[b]);
+      for (int64_t r = r0; r < r1; ++r) live += ctx->read_cfg[r] >= 0;
+      const int64_t nh = ctx->batch_hap_off[b + 1] - ctx->batch_hap_off[b];
+      all_rows += hs * (r1 - r0);
+      bgid[b + 1] = bgid[b] + nh * (r1 - r0);
+      bsh[b + 1] = bsh[b] + nh * live;
     }
     if (!getenv("PHMM_NO_LANE_BUDGET")) lane_rows = all_rows / (2 * 2 * (int64_t)ctx->num_sms * 16);
   }
-  for (int64_t b = 0; b < B; ++b) {
-    const int64_t r0 = ctx->batch_read_off[b], r1 = ctx->batch_read_off[b + 1];
-    const int64_t h0 = ctx->batch_hap_off[b], h1 = ctx->batch_hap_off[b + 1];
-    const int64_t nh = h1 - h0;
-    int ncap = 1;
-    int64_t batch_total = 0;
-    for (int64_t h = h0; h < h1; ++h) {
-      ncap = (int)std::max<int64_t>(ncap, ctx->hap_len[h]);
-      batch_total += ctx->hap_len[h];
-    }
-    max_n = std::max(max_n, ncap);
-    for (int md = 0; md < 4; ++md) {
-      mp[md].tmpl_m = -1;
-      mp[md].tmpl_geom = -2;
-      std::fill(mp[md].tvalid, mp[md].tvalid + kMaxTilings, false);
-      std::fill(mp[md].best_from, mp[md].best_from + kMaxTilings, -2);
-    }
-    hidx.resize(nh);
-    std::iota(hidx.begin(), hidx.end(), (int)h0);
-    std::stable_sort(hidx.begin(), hidx.end(), [&](int a, int c) { return ctx->hap_len[a] > ctx->hap_len[c]; });
-    for (int64_t r = r0; r < r1; ++r, gid += nh) {
-      read_ncap[r] = ncap;
-      const int cfg = ctx->read_cfg[r];
-      if (cfg < 0) continue;                         // config-too-small: host-side status
-      const int m = ctx->read_m[r];
-      const int scale = opt->scale_log2[cfg];
-      const bool f64 = opt->precision[cfg] == 1;
-      const bool exact = f64 || exact_mode || scale > 126;
-      const int mode = f64 ? kExact64 : exact ? kExact32 : kFast32;
-      slot_pairs[exact_slot_host(m)] += nh;             // any pair may land in its slot's lists
-      {
+  ctx->shaps.resize(bsh[B]);                     // default-initialised (PinnedAlloc::construct)
+  // Units of batches [b0, b1) into one part; parts are planned concurrently on the worker
+  // pool and merged in batch order, so the plan equals a sequential pass over the batches.
+  struct PlanPart {
+    std::vector<StreamUnit> su;
+    std::vector<uint16_t> key;                   // per unit: mode * kMaxTilings + template slot
+    std::vector<int> keys;                       // keys in order of first appearance
+    int key_geom[4 * kMaxTilings];
+    int key_rows[4 * kMaxTilings];
+    int64_t slot_pairs[kNumExactP] = {0, 0, 0, 0};
+    int64_t r64_pairs[8] = {0}, rx32_pairs[8] = {0};
+    bool long64 = false, long32 = false;         // streamed reads that stripe in the retry kernels
+    unsigned r64_geoms = 0, rx32_geoms = 0;
+    int max_n = 1;
+  };
+  auto plan_range = [&](int64_t b0, int64_t b1, PlanPart& pp) {
+    std::fill(pp.key_geom, pp.key_geom + 4 * kMaxTilings, -1);
+    std::fill(pp.key_rows, pp.key_rows + 4 * kMaxTilings, 0);
+    std::vector<int> hidx;
+    ModePlan mp[4];
+    for (int md = 0; md < 4; ++md) mp[md] = mp0[md];
+    StreamHap* sh_out = ctx->shaps.data() + bsh[b0];
+    int64_t gid = bgid[b0];
+    for (int64_t b = b0; b < b1; ++b) {
+      const int64_t r0 = ctx->batch_read_off[b], r1 = ctx->batch_read_off[b + 1];
+      const int64_t h0 = ctx->batch_hap_off[b], h1 = ctx->batch_hap_off[b + 1];
+      const int64_t nh = h1 - h0;
+      int ncap = 1;
+      int64_t batch_total = 0;
+      for (int64_t h = h0; h < h1; ++h) {
+        ncap = (int)std::max<int64_t>(ncap, ctx->hap_len[h]);
+        batch_total += ctx->hap_len[h];
+      }
+      pp.max_n = std::max(pp.max_n, ncap);
+      for (int md = 0; md < 4; ++md) {
+        mp[md].tmpl_m = -1;
+        mp[md].tmpl_geom = -2;
+        std::fill(mp[md].tvalid, mp[md].tvalid + kMaxTilings, false);
+        std::fill(mp[md].best_from, mp[md].best_from + kMaxTilings, -2);
+      }
+      hidx.resize(nh);
+      std::iota(hidx.begin(), hidx.end(), (int)h0);
+      std::stable_sort(hidx.begin(), hidx.end(), [&](int a, int c) { return ctx->hap_len[a] > ctx->hap_len[c]; });
+      for (int64_t r = r0; r < r1; ++r, gid += nh) {
+        read_ncap[r] = ncap;
+        const int cfg = ctx->read_cfg[r];
+        if (cfg < 0) continue;                         // config-too-small: host-side status
+        const int m = ctx->read_m[r];
+        const int scale = opt->scale_log2[cfg];
+        const bool f64 = opt->precision[cfg] == 1;
+        const bool exact = f64 || exact_mode || scale > 126;
+        const int mode = f64 ? kExact64 : exact ? kExact32 : kFast32;
+        pp.slot_pairs[exact_slot_host(m)] += nh;      // any pair may land in its slot's lists
         ModePlan& M = mp[mode];
         if (m != M.tmpl_m) {                           // lane template per (batch, tiling)
           M.tmpl_m = m;
@@ -727,42 +784,83 @@ static int prepare_impl(phmm_ctx* ctx, const phmm_input* in, const phmm_options*
             }
           }
         }
-        {
-          const std::vector<LaneTemplate>& tmpl = M.tmpls[(M.tmpl_geom & kStripedBin) ? kMaxTilings - 1 : M.tmpl_geom];
-          const int key = mode * kMaxTilings + ((M.tmpl_geom & kStripedBin) ? kMaxTilings - 1 : M.tmpl_geom);
-          if (sbin_index[key] < 0) {
-            sbin_index[key] = (int)ctx->sbins.size();
-            ctx->sbins.push_back(phmm_ctx::SBin{mode, M.tmpl_geom, 0, 0});
-          }
-          const uint8_t sbi = (uint8_t)sbin_index[key];
-          if (mode == kFast32) {                       // tilings its device-built units can use
-            const int g64 = r64_geom_for(m), gx = rx32_geom_for(m);
-            long64 |= m + 1 > kR64MaxW;
-            long32 |= m + 1 > kRX32MaxW;
-            if (g64 >= 0) { ctx->r64_geoms |= 1u << g64; r64_pairs[g64] += nh; }
-            if (gx >= 0) { ctx->rx32_geoms |= 1u << gx; rx32_pairs[gx] += nh; }
-          }
-          for (const LaneTemplate& t : tmpl) {
-            StreamUnit su;
-            su.read = (int)r;
-            su.list = (int)ctx->shaps.size();
-            su.cntA = (int)t.lanes[0].size(); su.cntB = (int)t.lanes[1].size();
-            su.rowsA = t.rows[0]; su.rowsB = t.rows[1];
-            su.ro = (int)roff[r];
-            su.m = m;
-            for (int ln = 0; ln < 2; ++ln)
-              for (int h : t.lanes[ln])
-                ctx->shaps.push_back(StreamHap{h, (int)(gid + (h - h0)), (int)hoff[h], (int)ctx->hap_len[h]});
-            ctx->su_all.push_back(su);
-            ctx->su_bin.push_back(sbi);
-            ctx->sbins[sbi].max_rows = std::max(ctx->sbins[sbi].max_rows, std::max(t.rows[0], t.rows[1]));
-          }
+        const int ts = (M.tmpl_geom & kStripedBin) ? kMaxTilings - 1 : M.tmpl_geom;
+        const std::vector<LaneTemplate>& tmpl = M.tmpls[ts];
+        const int key = mode * kMaxTilings + ts;
+        if (pp.key_geom[key] < 0) {
+          pp.key_geom[key] = M.tmpl_geom;
+          pp.keys.push_back(key);
+        }
+        if (mode == kFast32) {                         // tilings its device-built units can use
+          const int g64 = r64_geom_for(m), gx = rx32_geom_for(m);
+          pp.long64 |= m + 1 > kR64MaxW;
+          pp.long32 |= m + 1 > kRX32MaxW;
+          if (g64 >= 0) { pp.r64_geoms |= 1u << g64; pp.r64_pairs[g64] += nh; }
+          if (gx >= 0) { pp.rx32_geoms |= 1u << gx; pp.rx32_pairs[gx] += nh; }
+        }
+        for (const LaneTemplate& t : tmpl) {
+          StreamUnit su;
+          su.read = (int)r;
+          su.list = (int)(sh_out - ctx->shaps.data());
+          su.cntA = (int)t.lanes[0].size(); su.cntB = (int)t.lanes[1].size();
+          su.rowsA = t.rows[0]; su.rowsB = t.rows[1];
+          su.ro = (int)roff[r];
+          su.m = m;
+          for (int ln = 0; ln < 2; ++ln)
+            for (int h : t.lanes[ln])
+              *sh_out++ = StreamHap{h, (int)(gid + (h - h0)), (int)hoff[h], (int)ctx->hap_len[h]};
+          pp.su.push_back(su);
+          pp.key.push_back((uint16_t)key);
+          pp.key_rows[key] = std::max(pp.key_rows[key], std::max(t.rows[0], t.rows[1]));
         }
       }
-      (void)exact;
+    }
+  };
+  // parts: equal pair counts, a few per worker (large calls only)
+  int nparts = 1;
+  if (pool && N >= (1 << 16)) nparts = (int)std::min<int64_t>(B, 4 * (pool->size() + 1));
+  trace.mark("offsets");
+  std::vector<int64_t> pcut(nparts + 1, B);
+  pcut[0] = 0;
+  for (int i = 1, b = 0; i < nparts; ++i) {
+    while (b < B && bgid[b + 1] <= N * i / nparts) ++b;
+    pcut[i] = std::max<int64_t>(b, pcut[i - 1]);
+  }
+  std::vector<PlanPart> parts(nparts);
+  if (nparts == 1) {
+    plan_range(0, B, parts[0]);
+  } else {
+    std::function<void(int)> task = [&](int i) { plan_range(pcut[i], pcut[i + 1], parts[i]); };
+    pool->run(nparts, task);
+  }
+  trace.mark("plan-parts");
+  // merge in batch order: bins numbered by first appearance, units concatenated
+  int64_t nunits_all = 0;
+  for (const PlanPart& pp : parts) nunits_all += (int64_t)pp.su.size();
+  ctx->su_all.resize(nunits_all);
+  ctx->su_bin.resize(nunits_all);
+  {
+    int64_t o = 0;
+    for (const PlanPart& pp : parts) {
+      for (int key : pp.keys)
+        if (sbin_index[key] < 0) {
+          sbin_index[key] = (int)ctx->sbins.size();
+          ctx->sbins.push_back(phmm_ctx::SBin{key / kMaxTilings, pp.key_geom[key], 0, 0});
+        }
+      for (int key : pp.keys)
+        ctx->sbins[sbin_index[key]].max_rows = std::max(ctx->sbins[sbin_index[key]].max_rows, pp.key_rows[key]);
+      std::copy(pp.su.begin(), pp.su.end(), ctx->su_all.begin() + o);
+      for (size_t i = 0; i < pp.key.size(); ++i) ctx->su_bin[o + i] = (uint8_t)sbin_index[pp.key[i]];
+      o += (int64_t)pp.su.size();
+      for (int x = 0; x < kNumExactP; ++x) slot_pairs[x] += pp.slot_pairs[x];
+      for (int g = 0; g < 8; ++g) { r64_pairs[g] += pp.r64_pairs[g]; rx32_pairs[g] += pp.rx32_pairs[g]; }
+      long64 |= pp.long64; long32 |= pp.long32;
+      ctx->r64_geoms |= pp.r64_geoms; ctx->rx32_geoms |= pp.rx32_geoms;
+      max_n = std::max(max_n, pp.max_n);
     }
   }
   ctx->max_n = max_n;
+  trace.mark("merge");
   // LPT order per tiling: one stable counting sort on (bin, descending lane rows)
   const int nsbins = (int)ctx->sbins.size();
   const int64_t nsunits = (int64_t)ctx->su_all.size();
@@ -1395,12 +1493,17 @@ static int score_chunked(phmm_ctx* ctx, const phmm_input* in, const phmm_options
   };
   phmm_stats total;
   memset(&total, 0, sizeof(total));
+  // PHMM_TRACE=1: host timeline of the pipeline (ms since the call started)
+  const bool tr = getenv("PHMM_TRACE") != nullptr;
+  const auto tc0 = std::chrono::steady_clock::now();
+  auto tnow = [&]() { return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tc0).count(); };
   float span = 0.f;                  // first chunk's execute start -> last execute end
   bool span_set = false;
   // complete chunk c: device validation verdict, then finishing into the caller's slice
   auto complete = [&](int c) -> int {
     if (cut[c + 1] <= cut[c]) return PHMM_SUCCESS;
     phmm_ctx* cx = ctx->chunks[c % nctx];
+    const double tq = tnow();
     int rc = check_validation(cx);
     if (rc != PHMM_SUCCESS) return rc;
     phmm_stats cs;
@@ -1416,6 +1519,7 @@ static int score_chunked(phmm_ctx* ctx, const phmm_input* in, const phmm_options
     total.exact_pairs += cs.exact_pairs; total.f64_pairs += cs.f64_pairs;
     total.flagged_pairs += cs.flagged_pairs; total.h2d_bytes += cs.h2d_bytes; total.d2h_bytes += cs.d2h_bytes;
     total.kernel_launches += cs.kernel_launches; total.plan_ms += cs.plan_ms; total.d2h_ms += cs.d2h_ms;
+    if (tr) fprintf(stderr, "[phmm chunk %d] complete %.2f -> %.2f ms (device %.2f ms)\n", c, tq, tnow(), cs.device_ms);
     return PHMM_SUCCESS;
   };
   for (int c = 0; c < nchunks; ++c) {
@@ -1459,7 +1563,9 @@ static int score_chunked(phmm_ctx* ctx, const phmm_input* in, const phmm_options
     int64_t n = 0;
     cx->budget_div = std::min(nchunks, nctx);
     cx->col_budget = col_budget;
+    const double tp = tnow();
     int rc = phmm_prepare(cx, &sub, opt, &n);
+    if (tr) fprintf(stderr, "[phmm chunk %d] prepare %.2f -> %.2f ms (%lld pairs)\n", c, tp, tnow(), (long long)n);
     if (rc == PHMM_SUCCESS && !span_set) {     // timing origin: the first execute's start
       rc = cudaEventRecord(ctx->ev_span0, cx->stream) == cudaSuccess ? PHMM_SUCCESS : PHMM_ERR_CUDA;
       span_set = rc == PHMM_SUCCESS;
@@ -1494,21 +1600,29 @@ static int64_t batch_device_bytes(const phmm_input* in, int64_t b) {
   return 5 * rbytes + hbytes + 48 * (r1 - r0) + 16 * (h1 - h0) + kDevBytesPerPair * (r1 - r0) * (h1 - h0);
 }
 
-// equal-pair-count cut of the batches into nch contiguous chunks
-static std::vector<int64_t> equal_pair_cut(const phmm_input* in, int nch) {
+// cut of the batches into contiguous chunks with pair counts proportional to w[0..nch)
+static std::vector<int64_t> weighted_pair_cut(const phmm_input* in, const std::vector<int>& w) {
   const int64_t B = in->num_batches;
+  const int nch = (int)w.size();
   std::vector<int64_t> pairs(B + 1, 0);
   for (int64_t b = 0; b < B; ++b)
     pairs[b + 1] = pairs[b] + (in->batch_read_off[b + 1] - in->batch_read_off[b]) *
                                   (in->batch_hap_off[b + 1] - in->batch_hap_off[b]);
+  int64_t wsum = 0;
+  for (int x : w) wsum += x;
   std::vector<int64_t> cut(nch + 1, B);
   cut[0] = 0;
+  int64_t wacc = 0;
   for (int c = 1; c < nch; ++c) {
+    wacc += w[c - 1];
     int64_t b = cut[c - 1];
-    while (b < B && pairs[b] < pairs[B] * c / nch) ++b;
+    while (b < B && pairs[b] < pairs[B] * wacc / wsum) ++b;
     cut[c] = std::max(b, cut[c - 1]);
   }
   return cut;
+}
+static std::vector<int64_t> equal_pair_cut(const phmm_input* in, int nch) {
+  return weighted_pair_cut(in, std::vector<int>(nch, 1));
 }
 
 int phmm_set_device_budget(phmm_ctx* ctx, int64_t bytes) {
@@ -1603,10 +1717,16 @@ int phmm_score(phmm_ctx* ctx, const phmm_input* in, const phmm_options* opt, dou
     // large calls amortize the per-chunk post-pass latency: pipeline them regardless
     if (__builtin_popcount(classes) <= 2 || pairs >= kBigCallPairs) {
       CK(cudaSetDevice(ctx->device));
-      // per-chunk planning overhead vs pipeline depth: 3 chunks for ordinary calls, 4 for
-      // large ones (c2: 3 -> +15 % e2e over 4; c5: 4 -> +6 % over 3)
-      const int nch = score_chunks() > 0 ? score_chunks() : (pairs >= kBigCallPairs ? 4 : 3);
-      return score_chunked(ctx, in, opt, out_log10, out_status, stats, equal_pair_cut(in, nch), nch, kColBudget);
+      // per-chunk planning overhead vs pipeline depth: 3 equal chunks for ordinary calls
+      // (c2: +15 % e2e over 4).  Large calls ramp: the GPU idles while the first chunk is
+      // planned and the host finishes the last one after the GPU is done, so both are small
+      // (planning runs ~3x faster than the GPU scores, so chunk 1 is ready in time)
+      if (score_chunks() > 0)
+        return score_chunked(ctx, in, opt, out_log10, out_status, stats, equal_pair_cut(in, score_chunks()),
+                             score_chunks(), kColBudget);
+      const std::vector<int> w = pairs >= kBigCallPairs ? std::vector<int>{1, 2, 2, 2, 1} : std::vector<int>{1, 1, 1};
+      return score_chunked(ctx, in, opt, out_log10, out_status, stats, weighted_pair_cut(in, w), (int)w.size(),
+                           kColBudget);
     }
   }
   int64_t n = 0;

@@ -1043,11 +1043,16 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
     };
     constexpr int H = RS / 2;
     int nr = __any_sync(FULL, cring && sq) ? H + P : 0x7fffffff;
+    // Steps always run in pairs (plain or checked) so the two register sets alternate with
+    // no copies: a stretch that ends one step before a window starts the checked pair one
+    // step early (a checked step is correct anywhere), and steps past `steps` compute rows
+    // no one reads.  A refill may run one step after nr: block b + 2 is first read at step
+    // (b + 2)H - 1, far ahead (H > P + 2).
 #pragma unroll 1
     while (s <= steps) {
-      if (s == nr) {
+      if (s >= nr) {
         __syncwarp();
-        if (cring && sq) stage_rows(s - P + H, min(s - P + 2 * H, rows + 1));
+        if (cring && sq) stage_rows(nr - P + H, min(nr - P + 2 * H, rows + 1));
         __syncwarp();
         nr += H;
       }
@@ -1059,31 +1064,14 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
         step(s, std::false_type{}, xM, xI, xD, yM, yI, yD);
         step(s + 1, std::false_type{}, yM, yI, yD, xM, xI, xD);
       }
-      if (s < fend) {
-        step(s, std::false_type{}, xM, xI, xD, yM, yI, yD);
-        xM = yM; xI = yI; xD = yD;
-        ++s;
-      }
-      if (s > steps) break;
-      if (s == nr) continue;                            // refill before the next step
-      // some sub-warp is inside a window: event-checking steps, two per iteration (the
-      // register sets alternate like the plain steps; leaving after an odd step copies once)
+      if (s > steps || (s >= nr && s == fend)) continue;
+      // some sub-warp is inside a window (or one step before it): event-checking pairs
 #pragma unroll 1
       for (;;) {
         step(s, std::true_type{}, xM, xI, xD, yM, yI, yD);
-        ++s;
-        bool stop = s > steps || s == nr;
-        if (!stop) {
-          advance();
-          stop = !__any_sync(FULL, cur_s <= s);
-        }
-        if (stop) {
-          xM = yM; xI = yI; xD = yD;
-          break;
-        }
-        step(s, std::true_type{}, yM, yI, yD, xM, xI, xD);
-        ++s;
-        if (s > steps || s == nr) break;
+        step(s + 1, std::true_type{}, yM, yI, yD, xM, xI, xD);
+        s += 2;
+        if (s > steps || s >= nr) break;
         advance();
         if (!__any_sync(FULL, cur_s <= s)) break;
       }

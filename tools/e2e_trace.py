@@ -18,7 +18,7 @@ cfg = config_tuples(default_configs("f32"))
 ctx = _native.Context(0)
 for i in range(reps):
     t0 = time.perf_counter()
-    out, st, stats = ctx.score(flat, cfg, 0)
+    out, st, stats = ctx.score(flat, cfg, _native.FLAG_RETRY_F64 if "--retry" in sys.argv else 0)
     dt = time.perf_counter() - t0
     print("%s call %d: %.3f ms  e2e %.0f GCUPS  plan %.3f h2d %.3f dev %.3f d2h %.3f" % (
         name, i, dt * 1e3, stats.total_cells / dt / 1e9, stats.plan_ms, stats.h2d_ms, stats.device_ms, stats.d2h_ms),
