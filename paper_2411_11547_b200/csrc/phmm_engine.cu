@@ -650,6 +650,7 @@ static int prepare_impl(phmm_ctx* ctx, const phmm_input* in, const phmm_options*
   int64_t slot_pairs[kNumExactP] = {0, 0, 0, 0};
   int64_t r64_pairs[8] = {0}, rx32_pairs[8] = {0};
   bool long64 = false, long32 = false;          // streamed reads that stripe in the retry kernels
+  int64_t stripe_pairs = 0;                     // pairs of reads that stripe in the per-pair post-pass
   int max_n = 1;
   struct LaneTemplate {
     std::vector<int> lanes[2];
@@ -706,6 +707,7 @@ static int prepare_impl(phmm_ctx* ctx, const phmm_input* in, const phmm_options*
     int64_t slot_pairs[kNumExactP] = {0, 0, 0, 0};
     int64_t r64_pairs[8] = {0}, rx32_pairs[8] = {0};
     bool long64 = false, long32 = false;         // streamed reads that stripe in the retry kernels
+    int64_t stripe_pairs = 0;
     unsigned r64_geoms = 0, rx32_geoms = 0;
     int max_n = 1;
   };
@@ -747,6 +749,7 @@ static int prepare_impl(phmm_ctx* ctx, const phmm_input* in, const phmm_options*
         const bool exact = f64 || exact_mode || scale > 126;
         const int mode = f64 ? kExact64 : exact ? kExact32 : kFast32;
         pp.slot_pairs[exact_slot_host(m)] += nh;      // any pair may land in its slot's lists
+        if (m + 1 > 32 * kExactK) pp.stripe_pairs += nh;
         ModePlan& M = mp[mode];
         if (m != M.tmpl_m) {                           // lane template per (batch, tiling)
           M.tmpl_m = m;
@@ -855,6 +858,7 @@ static int prepare_impl(phmm_ctx* ctx, const phmm_input* in, const phmm_options*
       for (int x = 0; x < kNumExactP; ++x) slot_pairs[x] += pp.slot_pairs[x];
       for (int g = 0; g < 8; ++g) { r64_pairs[g] += pp.r64_pairs[g]; rx32_pairs[g] += pp.rx32_pairs[g]; }
       long64 |= pp.long64; long32 |= pp.long32;
+      stripe_pairs += pp.stripe_pairs;
       ctx->r64_geoms |= pp.r64_geoms; ctx->rx32_geoms |= pp.rx32_geoms;
       max_n = std::max(max_n, pp.max_n);
     }
@@ -936,7 +940,11 @@ static int prepare_impl(phmm_ctx* ctx, const phmm_input* in, const phmm_options*
     const size_t per_cta = (size_t)(kThreads / 32) * per_slot * sizeof(double);
     ctx->post_grid = ctx->num_sms * 2;
     if (max_m + 1 > 32 * kExactK) {
-      ctx->post_grid = (int)std::max<size_t>(1, std::min<size_t>(ctx->post_grid, ctx->col_budget / per_cta));
+      // a striped item runs on one warp (4 per CTA): more CTAs than ~items / 4 only add
+      // scratch (a 100k-base haplotype: 19 MB of columns per CTA)
+      const int64_t want = std::max<int64_t>(ctx->num_sms / 4, (stripe_pairs + 3) / 4);
+      ctx->post_grid = (int)std::max<size_t>(1, std::min<size_t>({(size_t)ctx->post_grid, ctx->col_budget / per_cta,
+                                                                 (size_t)want}));
       CK(ctx->d_cold.ensure((size_t)ctx->post_grid * (kThreads / 32) * per_slot));
     } else {
       CK(ctx->d_cold.ensure(1));       // never dereferenced: every post-pass read fits one stripe
@@ -1069,7 +1077,8 @@ static int prepare_impl(phmm_ctx* ctx, const phmm_input* in, const phmm_options*
       if (ctx->r64_geoms & (1u << g)) {
         const StreamKernel& K = striped_tab(kFast64);
         const int64_t per = col_per_cta(kFast64, K, max_n);
-        ctx->r64_grid = fit(ctx->num_sms * occ_cap(K.occ), per);
+        // every unit of the list holds >= 1 of its pairs: no more CTAs than that
+        ctx->r64_grid = fit((int)std::min<int64_t>(ctx->num_sms * occ_cap(K.occ), std::max<int64_t>(1, r64_pairs[g])), per);
         ctx->r64_col_off[g] = col_total;
         col_total += ctx->r64_grid * per;
       }
@@ -1079,7 +1088,7 @@ static int prepare_impl(phmm_ctx* ctx, const phmm_input* in, const phmm_options*
       if (ctx->rx32_geoms & (1u << g)) {
         const StreamKernel& K = striped_tab(kExact32);
         const int64_t per = col_per_cta(kExact32, K, max_n);
-        ctx->rx32_grid = fit(ctx->num_sms * occ_cap(K.occ), per);
+        ctx->rx32_grid = fit((int)std::min<int64_t>(ctx->num_sms * occ_cap(K.occ), std::max<int64_t>(1, rx32_pairs[g])), per);
         ctx->rx32_col_off[g] = col_total;
         col_total += ctx->rx32_grid * per;
       }

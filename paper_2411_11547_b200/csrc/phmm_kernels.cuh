@@ -339,7 +339,7 @@ template <int MODE> struct ModeOf {
   static constexpr bool EXACT = MODE == kExact32 || MODE == kExact64;
 };
 template <int MODE, int K> struct StreamOcc {
-  static constexpr int value = ModeOf<MODE>::F64 ? (K <= 4 ? 3 : 2) : (K <= 8 ? 4 : (K <= 12 ? 3 : 2));
+  static constexpr int value = ModeOf<MODE>::F64 ? (K <= 6 ? 3 : 2) : (K <= 8 ? 4 : (K <= 12 ? 3 : 2));
 };
 
 // Device-built stream units (one list per tiling): FP64 retries of FP32-underflowed pairs

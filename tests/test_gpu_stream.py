@@ -331,3 +331,34 @@ def test_run_device_budget_matches_unbounded():
     b, rb = run(flat, default_configs("f32"), retry_f64=True, device_budget_bytes=2 << 20)
     assert np.array_equal(a, b, equal_nan=True) and ra.total_cells == rb.total_cells
     assert ra.errors == rb.errors and ra.retried == rb.retried
+
+
+def test_100k_base_haplotype_linear_device_memory(engine, rng):
+    """A 100,000-base haplotype (and a long striped read against it) scores in every mode
+    without a per-haplotype-length scratch blow-up: the ring-mode row codes and the
+    grid-capped boundary columns keep the device working set bounded (reference.py:77-123
+    handles any n in linear space)."""
+    flat = _flat(rng, [([80, 250], [100000, 300], "derived"),
+                       ([700], [100000], "derived"),
+                       ([150], [100000], "random")])
+    ctx = _native.Context(0)
+    k32 = _check(ctx, flat)
+    assert (k32 == 0).any() and (k32 == 1).any()
+    ofl = oracle.Flat(**flat.as_dict())
+    ref64, k64 = oracle.score(ofl, "f64")
+    s, st, _ = ctx.score(flat, config_tuples(default_configs("f64")), 0)
+    assert np.array_equal(st & KIND, k64) and np.array_equal(s, ref64, equal_nan=True)
+    assert ctx.device_bytes() < (1536 << 20), ctx.device_bytes()
+    ctx.close()
+
+
+def test_c3_device_scratch_is_small(engine):
+    """Boundary-column scratch only where a read needs stripes: c3 (reads <= 250) keeps the
+    whole context's device working set near its inputs + per-pair lists."""
+    flat = datagen.workload("c3")
+    ctx = _native.Context(0)
+    ctx.score(flat, F32, _native.FLAG_RETRY_F64)
+    # inputs ~6.5 MB + per-pair buffers (acc, status, unit/entry lists sized for every pair)
+    per_pair = 200 * flat.num_pairs
+    assert ctx.device_bytes() < flat.nbytes() + per_pair + (64 << 20), ctx.device_bytes()
+    ctx.close()
