@@ -575,6 +575,7 @@ static int prepare_impl(phmm_ctx* ctx, const phmm_input* in, const phmm_options*
   CK(up(ctx->d_gq, in->gcp_qual, RL));
   trace.mark("h2d-reads");
   CK(up(ctx->d_roff, roff, R ? R + 1 : 0));
+  CK(ctx->d_hbases.ensure((size_t)HL + 16));     // + 16: the stream kernels read 16-byte chunks
   CK(up(ctx->d_hbases, in->hap_bases, HL));
   CK(up(ctx->d_hoff, hoff, H ? H + 1 : 0));
 

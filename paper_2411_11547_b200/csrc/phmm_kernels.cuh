@@ -695,10 +695,29 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
           const StreamHap sh = shaps[e0 + e];
           const int lo = max(r0, start), hi = min(r1, start + sh.n);
           const int8_t* src = E.hbases + sh.off - start;   // src[row] = base of that row
-          for (int x = lo + t; x < hi; x += P)
-            cd[2 * (x & rmask) + ln] =
-                (unsigned char)(src[x] | (x == start && start > 1 ? kCodeFirst : 0) |
-                                (x == start + sh.n - 1 ? kCodeLast : 0));
+          // coalesced 128-bit loads: thread t takes the aligned 16-byte chunks t, t + P, ...
+          // of the segment (the device copy of the haplotype bases is padded by 16 bytes)
+          const uintptr_t a_lo = reinterpret_cast<uintptr_t>(src + lo), a_hi = reinterpret_cast<uintptr_t>(src + hi);
+#pragma unroll 1
+          for (uintptr_t a = (a_lo & ~(uintptr_t)15) + 16 * (uintptr_t)t; a < a_hi; a += 16 * (uintptr_t)P) {
+            const uint4 v = __ldg(reinterpret_cast<const uint4*>(a));
+            const int x0 = (int)(reinterpret_cast<const int8_t*>(a) - src);
+            const unsigned w[4] = {v.x, v.y, v.z, v.w};
+            if (x0 >= lo && x0 + 16 <= hi) {            // interior chunk (almost all)
+#pragma unroll
+              for (int b = 0; b < 16; ++b)
+                cd[2 * ((x0 + b) & rmask) + ln] = (unsigned char)(w[b >> 2] >> (8 * (b & 3)));
+            } else {
+#pragma unroll
+              for (int b = 0; b < 16; ++b)
+                if (x0 + b >= lo && x0 + b < hi)
+                  cd[2 * ((x0 + b) & rmask) + ln] = (unsigned char)(w[b >> 2] >> (8 * (b & 3)));
+            }
+            // event flags of the haplotype's first / last row, by the thread that wrote it
+            const int fr = start > 1 ? start : -1, lr = start + sh.n - 1;
+            if (fr >= max(x0, lo) && fr < min(x0 + 16, hi)) cd[2 * (fr & rmask) + ln] |= kCodeFirst;
+            if (lr >= max(x0, lo) && lr < min(x0 + 16, hi)) cd[2 * (lr & rmask) + ln] |= kCodeLast;
+          }
           // separator row after every haplotype but the lane's last: kCodeIdle (M -> 0, I -> 0)
           if (SEP && e + 1 < cnt && t == 0 && start + sh.n >= r0 && start + sh.n < r1)
             cd[2 * ((start + sh.n) & rmask) + ln] = kCodeIdle;

@@ -162,6 +162,44 @@ __global__ void k_dfma(float* out, float a, float b, Rec* rec) {
   if (threadIdx.x == 0) rec[blockIdx.x] = {t0, t1, smid()};
 }
 
+
+// DFMA with 3 distinct per-chain 64-bit operands (6 register reads per instruction)
+__global__ void k_dfma3(float* out, float a, float b, Rec* rec) {
+  double x[8], y[8], z[8];
+  for (int i = 0; i < 8; i++) { x[i] = threadIdx.x * 0.001 + i; y[i] = a + i * 1e-3; z[i] = b - i * 1e-3; }
+  __syncthreads();
+  long long t0 = clock64();
+  #pragma unroll 4
+  for (int it = 0; it < ITERS / 4; it++) {
+    #pragma unroll
+    for (int i = 0; i < 8; i++) x[i] = fma(x[i], y[i], z[i]);
+  }
+  __syncthreads();
+  long long t1 = clock64();
+  double s = 0; for (int i = 0; i < 8; i++) s += x[i];
+  if (s == 12345.0) out[0] = (float)s;
+  if (threadIdx.x == 0) rec[blockIdx.x] = {t0, t1, smid()};
+}
+
+// the k_stream FP64 pattern: two lanes share a per-position coefficient (x = c*x + y)
+__global__ void k_dfma2l(float* out, float a, float b, Rec* rec) {
+  double x[8], y[8], c[4];
+  for (int i = 0; i < 8; i++) { x[i] = threadIdx.x * 0.001 + i; y[i] = b - i * 1e-3; }
+  for (int i = 0; i < 4; i++) c[i] = a + i * 1e-3;
+  __syncthreads();
+  long long t0 = clock64();
+  #pragma unroll 4
+  for (int it = 0; it < ITERS / 4; it++) {
+    #pragma unroll
+    for (int i = 0; i < 8; i++) x[i] = fma(c[i >> 1], x[i], y[i]);
+  }
+  __syncthreads();
+  long long t1 = clock64();
+  double s = 0; for (int i = 0; i < 8; i++) s += x[i];
+  if (s == 12345.0) out[0] = (float)s;
+  if (threadIdx.x == 0) rec[blockIdx.x] = {t0, t1, smid()};
+}
+
 __global__ void k_lds128(float* out, float a, float b, Rec* rec) {
   __shared__ float4 tab[1024];
   for (int i = threadIdx.x; i < 1024; i += blockDim.x) tab[i] = make_float4(i, a, b, i + 1);
@@ -249,6 +287,8 @@ int main() {
   measure(k_fmul2, "FMUL2", 8, ITERS, T, B, nsm);
   measure(k_fadd2, "FADD2", 8, ITERS, T, B, nsm);
   measure(k_dfma, "DFMA", 8, ITERS / 4, T, B, nsm);
+  measure(k_dfma3, "DFMA-3reg", 8, ITERS / 4, T, B, nsm);
+  measure(k_dfma2l, "DFMA-2lane", 8, ITERS / 4, T, B, nsm);
   measure(k_lds128, "LDS.128", 1, ITERS, T, B, nsm);
   measure(k_shfl, "SHFL", 4, ITERS, T, B, nsm);
   return 0;
