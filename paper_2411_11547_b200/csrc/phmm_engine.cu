@@ -677,9 +677,11 @@ static int prepare_impl(phmm_ctx* ctx, const phmm_input* in, const phmm_options*
     for (int i = 0; i < M.n; ++i) M.wsorted[i] = stream_tab(md)[M.wsort[i]].P * stream_tab(md)[M.wsort[i]].K;
   }
   // Lane budget: a call too small to fill the GPU with long lanes (few pairs, long
-  // haplotypes: c4) splits its units until there are ~2 per sub-warp slot (#SM x 8 warps
-  // x 2 sub-warps); latency, not per-unit overhead, bounds such calls.  Large calls keep
-  // the row capacity as the only limit.  Per batch: first pair id and first stream entry.
+  // haplotypes: c4, c3) splits its units until there are ~6 per sub-warp slot (#SM x 8
+  // warps x 2 sub-warps; PHMM_LANE_UNITS): the last wave's tail, not per-unit overhead,
+  // bounds such calls (c3: 2 -> 6 per slot, FP32 phase -6 %; c2 unchanged, 8 is worse).
+  // Large calls keep the row capacity as the only limit.  Per batch: first pair id and
+  // first stream entry.
   int64_t lane_rows = INT64_MAX;
   std::vector<int64_t> bgid(B + 1, 0), bsh(B + 1, 0);
   {
@@ -694,7 +696,11 @@ static int prepare_impl(phmm_ctx* ctx, const phmm_input* in, const phmm_options*
       bgid[b + 1] = bgid[b] + nh * (r1 - r0);
       bsh[b + 1] = bsh[b] + nh * live;
     }
-    if (!getenv("PHMM_NO_LANE_BUDGET")) lane_rows = all_rows / (2 * 2 * (int64_t)ctx->num_sms * 16);
+    static const int lane_units = [] {          // units per sub-warp slot targeted (PHMM_LANE_UNITS)
+      const char* e = getenv("PHMM_LANE_UNITS");
+      return e ? std::max(1, atoi(e)) : 6;
+    }();
+    if (!getenv("PHMM_NO_LANE_BUDGET")) lane_rows = all_rows / (2 * lane_units * (int64_t)ctx->num_sms * 16);
   }
   ctx->shaps.resize(bsh[B]);                     // default-initialised (PinnedAlloc::construct)
   // Units of batches [b0, b1) into one part; parts are planned concurrently on the worker
