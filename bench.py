@@ -480,10 +480,13 @@ def main():
         ctx.score(pflat, cfg, flags, out=res, status=res_st)
     barrier()
     t0 = time.perf_counter()
+    call_ms = []
     for _ in range(args.steps):
+        tc = time.perf_counter()
         out, ost, est = ctx.score(pflat, cfg, flags, out=res, status=res_st)
         if gather is not None:
             gather.put(shard.gids, out, ost)
+        call_ms.append((time.perf_counter() - tc) * 1e3)
     if ws > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -527,6 +530,8 @@ def main():
                             if flags & _native.FLAG_RETRY_F64 else "fast FP32 + guard band (reference f32 semantics)")},
         "roofline": {"bound": "fp32", "achieved": fast_gcups, "peak": peak, "unit": "GCUPS",
                      "frac": fast_gcups / peak, "traffic": traffic,
+                     "traffic_source": "ncu --set full dram__bytes_read.sum + dram__bytes_write.sum of the workload's "
+                                       "largest FP32 tiling bin, per launch (profiles/k_stream_traffic.json)",
                      "kernel": "k_stream<kFast32,P,K> FP32 streaming wavefront (all tiling bins of the FP32 phase)",
                      "algorithmic_units": "every pair's true m*n cells once (SURVEY §8(d): 8 FP32-pipe ops/cell)",
                      "peak_source": "SURVEY.md §8(d): %d SMs x %d FP32 lanes x sm_max_mhz %.0f (MEASURED_PEAKS.json) / %d ops per cell"
@@ -541,7 +546,8 @@ def main():
                                     "peak_fp64_gcups": peak64}},
         "e2e": {"value": e2e_value, "unit": "GCUPS", "h2d_bytes_per_step": int(est.h2d_bytes) * ws,
                 "d2h_bytes_per_step": int(est.d2h_bytes) * ws,
-                "api": "phmm_score (C-ABI) from pinned host buffers" + (" + shared-memory host gather" if ws > 1 else "")},
+                "api": "phmm_score (C-ABI) from pinned host buffers" + (" + shared-memory host gather" if ws > 1 else ""),
+                "call_ms_rank0": [round(x, 1) for x in call_ms]},
         "clocks": clk,
         "gpu_launches": int(launches),
         "engine": {"device_ms_mean": float(np.mean(dev_ms)), "fast_ms_mean": float(np.mean(fast_ms)),
@@ -575,15 +581,15 @@ def main():
 
 
 def profile_traffic(workload):
-    """dram bytes per launch of the dominant k_stream launch from the committed ncu
-    --set full capture of this workload (profiles/k_stream_traffic.json)."""
+    """dram bytes per launch of the workload's dominant k_stream launch from the committed
+    ncu --set full capture (profiles/k_stream_traffic.json; c5: the largest FP32 bin)."""
     path = os.path.join(ROOT, "profiles", "k_stream_traffic.json")
     try:
         with open(path) as f:
             d = json.load(f)
     except OSError:
         return None
-    d = d.get(workload, d) if isinstance(d, dict) else {}
+    d = d.get(workload) if isinstance(d, dict) else None
     return d.get("dram_bytes_per_launch") if isinstance(d, dict) else None
 
 
