@@ -778,19 +778,21 @@ static int prepare_impl(phmm_ctx* ctx, const phmm_input* in, const phmm_options*
             // new unit when a lane would exceed the tiling's row capacity or the call's
             // lane budget
             const int cap = (int)std::min<int64_t>(stream_cap(skern(mode, sg).P), std::max<int64_t>(lane_rows, 1));
+            // kFast32 lanes separate their haplotypes by one idle row (SepRows, phmm_kernels.cuh)
+            const int sep = mode == kFast32 ? 1 : 0;
             tmpl.emplace_back();
             for (int64_t x = 0; x < nh; ++x) {
               const int h = hidx[x];
               const int n = (int)ctx->hap_len[h];
               LaneTemplate* t = &tmpl.back();
               int ln = t->rows[0] <= t->rows[1] ? 0 : 1;
-              if ((t->rows[ln] > 0 && t->rows[ln] + n > cap) || (int)t->lanes[ln].size() >= kStreamMaxLaneHaps) {
+              if ((t->rows[ln] > 0 && t->rows[ln] + sep + n > cap) || (int)t->lanes[ln].size() >= kStreamMaxLaneHaps) {
                 tmpl.emplace_back();
                 t = &tmpl.back();
                 ln = 0;
               }
-              t->lanes[ln].push_back(h);                     // (host-built modes: no separator rows)
-              t->rows[ln] += n;
+              t->rows[ln] += n + (t->rows[ln] > 0 ? sep : 0);
+              t->lanes[ln].push_back(h);
             }
           }
         }

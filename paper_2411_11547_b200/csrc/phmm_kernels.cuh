@@ -312,10 +312,10 @@ constexpr unsigned kIdle2 = kCodeIdle | (kCodeIdle << 8);
 // window list entries: start row | kWinShort (a one-step window: the LAST event of a lane's
 // final haplotype) -- otherwise P steps (the FIRST events of a haplotype boundary)
 constexpr int kWinShort = 1 << 30;
-// FP64 retry units (kFast64) separate consecutive haplotypes of a lane by one kCodeIdle row:
-// it leaves M = I = 0, so a FIRST event only resets D (the FP64 kernel is issue-heavier in
-// its event windows); the other modes reset M, I and D and need no separator rows.
-template <int MODE> struct SepRows { static constexpr bool value = MODE == 1; };
+// The fast modes (kFast32 = 0, kFast64 = 1) separate consecutive haplotypes of a lane by one
+// kCodeIdle row: it leaves M = I = 0, so a FIRST event only resets D (a third of the event
+// work inside the checked steps); the exact modes reset M, I and D and need no separators.
+template <int MODE> struct SepRows { static constexpr bool value = MODE == 0 || MODE == 1; };
 constexpr int kStreamCodeBytesPerCta = 32768;          // row-code staging, shared memory
 constexpr int kStreamMaxLaneHaps = 15;                 // haplotypes per lane of one unit
 constexpr int kStreamMaxWin = 2 * (kStreamMaxLaneHaps + 1);
