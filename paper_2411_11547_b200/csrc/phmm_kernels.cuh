@@ -728,8 +728,12 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
     };
     // windows: every row b > 1 where a haplotype begins in either lane -- FIRST for thread
     // t at step b + t, the previous haplotype's LAST for thread P-1 at step b + P - 2: the
-    // window [b, b + P) -- and each lane's final LAST, at step rows + P - 1 (one step).  The
-    // first haplotype of each lane needs no window (pre-initialised row 0, kCodeIdle fill).
+    // window [b, b + P), from b - 1 with separator rows (thread 0 reads the idle separator at
+    // step b - 1) -- and each lane's final LAST, at step rows + P - 1 (one step).  The first
+    // haplotype of each lane needs no window (pre-initialised row 0; the fill steps 1 .. P-1,
+    // where threads still read the idle row 0, run checked).  Idle codes are only read in
+    // checked steps and in the drain (rows past the stream, whose values no one reads), so
+    // the plain step indexes the emission table without the idle-row select.
     // Built once per unit, sorted by start.
     if (first_q || cring) {
       if (live) stage_rows(1, min(rows + 1, RS));
@@ -745,7 +749,7 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
         auto entry = [&](int x, int c, int& row, int e0) -> int {
           if (x >= c) return 0x7fffffff;
           if (x == c - 1) return (row + shaps[U.list + e0 + x].n + P - 2) | kWinShort;   // last row + P - 1
-          return row + shaps[U.list + e0 + x].n + (SEP ? 1 : 0);                       // next start
+          return row + shaps[U.list + e0 + x].n;      // next start b (SEP: b - 1, its separator row)
         };
         while (true) {
           const int va = entry(ia, ca, ra, 0), vb = entry(ib, cbn, rb, ca);
@@ -950,8 +954,8 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
         if (code & (kCodeFirst << 8)) first_event(std::integral_constant<int, 1>{}, Full{}, dgM, dgI, dgD, nbM, nbI, nbD);
       }
       const int cA = code & 7, cB = (code >> 8) & 7;
-      const EV* EA = cA == kCodeIdle ? s_zero + t : Et + (cA * KE) * P + t;
-      const EV* EB = cB == kCodeIdle ? s_zero + t : Et + (cB * KE) * P + t;
+      const EV* EA = (CHECK && cA == kCodeIdle) ? s_zero + t : Et + (cA * KE) * P + t;
+      const EV* EB = (CHECK && cB == kCodeIdle) ? s_zero + t : Et + (cB * KE) * P + t;
       // fast FP32 at occupancy 2 (K = 14, 16) has the registers for the carried values
       constexpr bool FUSED = !EXACT && (F64 ? !STRIPES : K >= 14);
       if constexpr (FUSED) {
@@ -1049,14 +1053,15 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
     // block b+2 (first read at step (b+2)H - 1) is written
     const int nwin = s_nwin[slot];
     const int* wb = s_win + slot * kStreamMaxWin;
-    // this sub-warp's earliest unfinished window [cur_s, cur_e), kept in registers
-    int wi = 0;
-    int cur_s = 0x7fffffff, cur_e = 0x7fffffff;
-    if (nwin > 0) { cur_s = wb[0] & ~kWinShort; cur_e = cur_s + ((wb[0] & kWinShort) ? 1 : P); }
+    // this sub-warp's earliest unfinished window [cur_s, cur_e), kept in registers; the
+    // first is the fill [1, P)
+    constexpr int WL = P + (SEP ? 1 : 0);               // window length (from the separator row)
+    int wi = -1;
+    int cur_s = 1, cur_e = P;
     int s = 1;
     auto advance = [&]() {
       while (cur_e <= s) {
-        if (++wi < nwin) { cur_s = wb[wi] & ~kWinShort; cur_e = cur_s + ((wb[wi] & kWinShort) ? 1 : P); }
+        if (++wi < nwin) { cur_s = wb[wi] & ~kWinShort; cur_e = cur_s + ((wb[wi] & kWinShort) ? 1 : WL); }
         else { cur_s = 0x7fffffff; cur_e = 0x7fffffff; }
       }
     };
