@@ -793,6 +793,9 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
       const int i = s - t;
       return (i >= 1 && i <= rows_q) ? (unsigned)cd16[(unsigned)i & rmask] : kIdle2;
     };
+    // plain steps never read rows <= 0 (the fill runs checked) and ignore event bits, so
+    // the drain's rows past the stream may read any slot entry: no bounds check
+    auto ld_code_plain = [&](int s) -> unsigned { return (unsigned)cd16[(unsigned)(s - t) & (unsigned)(RS - 1)]; };
     unsigned code = kIdle2;
     unsigned pf1 = ld_code(1);
     // stripe q > 0: thread 0's left neighbour is the previous stripe's column
@@ -947,7 +950,7 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
         }
       }
       code = pf1;
-      pf1 = ld_code(s + 1);
+      pf1 = CHECK ? ld_code(s + 1) : ld_code_plain(s + 1);
       if (CHECK && (code & ((kCodeFirst << 8) | kCodeFirst))) {
         using Full = std::integral_constant<bool, !SEP>;
         if (code & kCodeFirst) first_event(std::integral_constant<int, 0>{}, Full{}, dgM, dgI, dgD, nbM, nbI, nbD);
@@ -1090,6 +1093,7 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
       }
       if (s > steps || (s >= nr && s == fend)) continue;
       // some sub-warp is inside a window (or one step before it): event-checking pairs
+      pf1 = ld_code(s);                                 // the plain steps' prefetch is unchecked
 #pragma unroll 1
       for (;;) {
         step(s, std::true_type{}, xM, xI, xD, yM, yI, yD);
