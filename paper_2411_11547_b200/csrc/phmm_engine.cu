@@ -1742,7 +1742,18 @@ int phmm_score(phmm_ctx* ctx, const phmm_input* in, const phmm_options* opt, dou
       if (score_chunks() > 0)
         return score_chunked(ctx, in, opt, out_log10, out_status, stats, equal_pair_cut(in, score_chunks()),
                              score_chunks(), kColBudget);
-      const std::vector<int> w = pairs >= kBigCallPairs ? std::vector<int>{1, 2, 2, 2, 1} : std::vector<int>{1, 1, 1};
+      std::vector<int> w = pairs >= kBigCallPairs ? std::vector<int>{1, 2, 2, 2, 1} : std::vector<int>{1, 1, 1};
+      if (const char* env = getenv("PHMM_CHUNK_WEIGHTS")) {     // experiments: "1,3,4,4,3,1"
+        std::vector<int> ew;
+        for (const char* p = env; *p;) {
+          char* end = nullptr;
+          const long v = strtol(p, &end, 10);
+          if (end == p) break;
+          if (v > 0) ew.push_back((int)v);
+          p = *end ? end + 1 : end;
+        }
+        if (!ew.empty() && (int)ew.size() <= kMaxScoreChunks) w = ew;
+      }
       return score_chunked(ctx, in, opt, out_log10, out_status, stats, weighted_pair_cut(in, w), (int)w.size(),
                            kColBudget);
     }

@@ -733,7 +733,7 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
     // haplotype of each lane needs no window (pre-initialised row 0; the fill steps 1 .. P-1,
     // where threads still read the idle row 0, run checked).  Idle codes are only read in
     // checked steps and in the drain (rows past the stream, whose values no one reads), so
-    // the plain step indexes the emission table without the idle-row select.
+    // the plain step indexes the emission table without the idle-row select (clamped to N).
     // Built once per unit, sorted by start.
     if (first_q || cring) {
       if (live) stage_rows(1, min(rows + 1, RS));
@@ -794,7 +794,7 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
       return (i >= 1 && i <= rows_q) ? (unsigned)cd16[(unsigned)i & rmask] : kIdle2;
     };
     // plain steps never read rows <= 0 (the fill runs checked) and ignore event bits, so
-    // the drain's rows past the stream may read any slot entry: no bounds check
+    // the drain's rows past the stream may read any entry of this slot: no bounds check
     auto ld_code_plain = [&](int s) -> unsigned { return (unsigned)cd16[(unsigned)(s - t) & (unsigned)(RS - 1)]; };
     unsigned code = kIdle2;
     unsigned pf1 = ld_code(1);
@@ -956,7 +956,10 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
         if (code & kCodeFirst) first_event(std::integral_constant<int, 0>{}, Full{}, dgM, dgI, dgD, nbM, nbI, nbD);
         if (code & (kCodeFirst << 8)) first_event(std::integral_constant<int, 1>{}, Full{}, dgM, dgI, dgD, nbM, nbI, nbD);
       }
-      const int cA = code & 7, cB = (code >> 8) & 7;
+      // plain steps read idle codes only in the drain (rows no one reads): they clamp to N
+      // (one IMNMX instead of the select, and the table read stays in this slot)
+      const int cA = CHECK ? (int)(code & 7) : min((int)(code & 7), 4);
+      const int cB = CHECK ? (int)((code >> 8) & 7) : min((int)((code >> 8) & 7), 4);
       const EV* EA = (CHECK && cA == kCodeIdle) ? s_zero + t : Et + (cA * KE) * P + t;
       const EV* EB = (CHECK && cB == kCodeIdle) ? s_zero + t : Et + (cB * KE) * P + t;
       // fast FP32 at occupancy 2 (K = 14, 16) has the registers for the carried values
