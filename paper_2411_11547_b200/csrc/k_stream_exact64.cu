@@ -3,11 +3,12 @@
 
 namespace phmm {
 
-// W = 32, 64, 96, 128, 192, 256
+// W = 32, 64, 96, 128, 192, 224, 256
 const StreamKernel* stream_table_exact64() {
   static const StreamKernel tab[kNumR64Geoms] = {SK<kExact64, 8, 4>(),  SK<kExact64, 16, 4>(),
                                                  SK<kExact64, 16, 6>(), SK<kExact64, 16, 8>(),
-                                                 SK<kExact64, 32, 6>(), SK<kExact64, 32, 8>()};
+                                                 SK<kExact64, 32, 6>(), SK<kExact64, 32, 7>(),
+                                                 SK<kExact64, 32, 8>()};
   return tab;
 }
 const StreamKernel& striped_exact64() {

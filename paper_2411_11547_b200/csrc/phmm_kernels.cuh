@@ -344,7 +344,7 @@ template <int MODE, int K> struct StreamOcc {
 
 // Device-built stream units (one list per tiling): FP64 retries of FP32-underflowed pairs
 // and bit-exact reruns of guard-band pairs, grouped per read by the FP32 stream kernel.
-constexpr int kNumR64Geoms = 6;     // FP64 retry:  (8,4) (16,4) (16,6) (16,8) (32,6) (32,8)
+constexpr int kNumR64Geoms = 7;     // FP64 retry:  (8,4) (16,4) (16,6) (16,8) (32,6) (32,7) (32,8)
 constexpr int kNumRX32Geoms = 8;    // exact FP32:  (8,4) (16,4) (16,6) (32,4) (32,6) (32,8) (32,12) (32,16)
 // haplotypes per lane of a device-built unit: short units keep these small post-pass
 // lists parallel (their count is unknown when the grid is sized)
@@ -353,7 +353,7 @@ constexpr int kInlineBand = 4;      // guard-band pairs a warp may rerun inline 
 // reads longer than the widest tiling stripe over it (k_stream handles Q > 1 stripes)
 __host__ __device__ __forceinline__ int r64_geom_for(int m) {
   const int w = m + 1;
-  return w <= 32 ? 0 : w <= 64 ? 1 : w <= 96 ? 2 : w <= 128 ? 3 : w <= 192 ? 4 : 5;
+  return w <= 32 ? 0 : w <= 64 ? 1 : w <= 96 ? 2 : w <= 128 ? 3 : w <= 192 ? 4 : w <= 224 ? 5 : 6;
 }
 __host__ __device__ __forceinline__ int r64_geom_P(int g) { return g == 0 ? 8 : (g <= 3 ? 16 : 32); }
 __host__ __device__ __forceinline__ int rx32_geom_for(int m) {
@@ -407,16 +407,19 @@ template <> struct Lanes<true> {
 };
 template <int L, class V> __device__ __forceinline__ auto& lane_ref(V& v) { return L == 0 ? v.x : v.y; }
 // emission-table chunks: float4 (4 positions, LDS.128) when K % 4 == 0, float2 (LDS.64)
-// for K = 10, 14; double2 in FP64
+// for K = 10, 14; double2 in FP64 (double for K = 7)
 __device__ __forceinline__ float ev_comp(const float4& v, int i) { return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w; }
 __device__ __forceinline__ float ev_comp(const float2& v, int i) { return i == 0 ? v.x : v.y; }
 __device__ __forceinline__ double ev_comp(const double2& v, int i) { return i == 0 ? v.x : v.y; }
+__device__ __forceinline__ double ev_comp(const double& v, int) { return v; }
 __device__ __forceinline__ void ev_pack(float4& e, const float* l) { e = make_float4(l[0], l[1], l[2], l[3]); }
 __device__ __forceinline__ void ev_pack(float2& e, const float* l) { e = make_float2(l[0], l[1]); }
 __device__ __forceinline__ void ev_pack(double2& e, const double* l) { e = make_double2(l[0], l[1]); }
+__device__ __forceinline__ void ev_pack(double& e, const double* l) { e = l[0]; }
 template <bool F64, int K> struct EChunk {
-  using type = typename std::conditional<F64, double2, typename std::conditional<K % 4 == 0, float4, float2>::type>::type;
-  static constexpr int width = F64 ? 2 : (K % 4 == 0 ? 4 : 2);
+  using type = typename std::conditional<F64, typename std::conditional<K % 2 == 0, double2, double>::type,
+                                         typename std::conditional<K % 4 == 0, float4, float2>::type>::type;
+  static constexpr int width = F64 ? (K % 2 == 0 ? 2 : 1) : (K % 4 == 0 ? 4 : 2);
 };
 template <class V, class S> __device__ __forceinline__ V flush2(V v, S thr) {
   v.x = v.x >= thr ? v.x : (S)0;            // reference store flush (wavefront.py:134-136)
