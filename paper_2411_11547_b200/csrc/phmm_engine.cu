@@ -280,6 +280,7 @@ struct Trace {
 struct phmm_ctx {
   int device = 0;
   int num_sms = 148;
+  size_t total_mem = 0;                      // device memory (bytes)
   cudaStream_t stream = nullptr;
   cudaEvent_t ev_start = nullptr, ev_fast0 = nullptr, ev_fast1 = nullptr, ev_end = nullptr;   // execute
   cudaEvent_t ev_post1 = nullptr;                       // execute: end of the concurrent post-pass
@@ -412,6 +413,7 @@ static int init_ctx(phmm_ctx* ctx, int device) {
   if (prop.major != 10) return ctx->fail(PHMM_ERR_CUDA, "device %s is sm_%d%d; libphmm is built for sm_100a",
                                          prop.name, prop.major, prop.minor);
   ctx->num_sms = prop.multiProcessorCount;
+  ctx->total_mem = prop.totalGlobalMem;
   CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
   CK(cudaEventCreateWithFlags(&ctx->ev_pre, cudaEventDisableTiming));
   for (int a = 0; a < phmm_ctx::kAux; ++a) {
@@ -1602,6 +1604,7 @@ static int score_chunked(phmm_ctx* ctx, const phmm_input* in, const phmm_options
       return ctx->fail(rc, "%s", ctx->chunks[c % nctx]->err.c_str());
     }
   }
+  if (tr) fprintf(stderr, "[phmm chunks] done %.2f ms\n", tnow());
   total.device_ms = span;
   ctx->last_dev_ms = span;
   ctx->last_fast_ms = (float)total.fast_ms;
@@ -1673,6 +1676,7 @@ int phmm_device_bytes(const phmm_ctx* ctx, int64_t* bytes) {
 int phmm_score(phmm_ctx* ctx, const phmm_input* in, const phmm_options* opt, double* out_log10,
                uint8_t* out_status, phmm_stats* stats) {
   if (!ctx) return PHMM_ERR_INVALID;
+  Trace trace;
   const bool structure = in && opt && in->batch_read_off && in->batch_hap_off && in->read_off && in->hap_off &&
                          in->num_batches > 0;
   // validate the structure first (the chunk views index the offset arrays)
@@ -1690,12 +1694,14 @@ int phmm_score(phmm_ctx* ctx, const phmm_input* in, const phmm_options* opt, dou
   // free device memory -- half of that.  Over budget, the call streams through chunk
   // contexts reused round-robin, each chunk within budget / kBudgetCtx.
   constexpr int kBudgetCtx = 3;
+  trace.mark("structure");
   if (ok) {
     int64_t budget = ctx->device_budget;
     int64_t est = 0;
     std::vector<int64_t> best(in->num_batches);
     for (int64_t b = 0; b < in->num_batches; ++b) est += (best[b] = batch_device_bytes(in, b));
-    if (budget == 0) {
+    // (cudaMemGetInfo costs ~10 ms: only asked when the call is a sizeable part of HBM)
+    if (budget == 0 && est > (int64_t)(ctx->total_mem / 8)) {
       size_t free_b = 0, total_b = 0;
       CK(cudaSetDevice(ctx->device));
       if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess && est > (int64_t)(free_b * 0.6))
@@ -1719,30 +1725,35 @@ int phmm_score(phmm_ctx* ctx, const phmm_input* in, const phmm_options* opt, dou
                            std::min<int>(kBudgetCtx, (int)cut.size() - 1), col);
     }
   }
+  trace.mark("budget");
+  trace.print("score");
   if (ok && in->num_batches >= 2 * std::max(3, score_chunks()) && score_chunks() != 1 && score_chunking_enabled() &&
       pairs >= kScoreChunkMinPairs) {
     // Only regular calls are pipelined: reads spanning many tiling widths split into many
     // small per-tiling kernels per chunk, and each chunk's latency-bound post-pass (guard
     // band, FP64 retries) then queues behind the next chunks' persistent grids.
+    // large calls amortize the per-chunk post-pass latency: pipeline them regardless (and
+    // skip the O(reads) width-class scan)
     static const int kW[] = {16, 32, 48, 64, 80, 96, 112, 128, 160, 192, 224, 256, 320, 384, 448, 512};
     unsigned classes = 0;
-    for (int64_t r = 0; r < in->num_reads; ++r) {
+    for (int64_t r = 0; pairs < kBigCallPairs && r < in->num_reads && __builtin_popcount(classes) <= 2; ++r) {
       const int64_t m = in->read_off[r + 1] - in->read_off[r];
       int c = 0;
       while (c < 15 && kW[c] < m + 1) ++c;
       classes |= 1u << c;
     }
-    // large calls amortize the per-chunk post-pass latency: pipeline them regardless
     if (__builtin_popcount(classes) <= 2 || pairs >= kBigCallPairs) {
       CK(cudaSetDevice(ctx->device));
       // per-chunk planning overhead vs pipeline depth: 3 equal chunks for ordinary calls
       // (c2: +15 % e2e over 4).  Large calls ramp: the GPU idles while the first chunk is
       // planned and the host finishes the last one after the GPU is done, so both are small
-      // (planning runs ~3x faster than the GPU scores, so chunk 1 is ready in time)
+      // (planning runs ~4x faster than the GPU scores, so chunk 1 is ready in time).
+      // c5 (tools/sweep_chunks.sh): 1,3,4,4,3,1 281.6 ms < 1,2,4,4,4,1 282.5 < 1,2,3,3,3,2,1
+      // 283.6 < 1,4,6,4,1 284.6 < 1,3,4,4,4 286.5 < 1,2,2,2,1 288.0
       if (score_chunks() > 0)
         return score_chunked(ctx, in, opt, out_log10, out_status, stats, equal_pair_cut(in, score_chunks()),
                              score_chunks(), kColBudget);
-      std::vector<int> w = pairs >= kBigCallPairs ? std::vector<int>{1, 2, 2, 2, 1} : std::vector<int>{1, 1, 1};
+      std::vector<int> w = pairs >= kBigCallPairs ? std::vector<int>{1, 3, 4, 4, 3, 1} : std::vector<int>{1, 1, 1};
       if (const char* env = getenv("PHMM_CHUNK_WEIGHTS")) {     // experiments: "1,3,4,4,3,1"
         std::vector<int> ew;
         for (const char* p = env; *p;) {
