@@ -1,7 +1,7 @@
 """Wall time of repeated phmm_score calls (pinned inputs, caller-owned result buffers, like
 bench.py's e2e loop); PHMM_TRACE=1 adds the per-chunk host timeline on stderr.
 
-usage: python tools/e2e_calls.py [workload] [calls] [--retry]
+usage: python tools/e2e_calls.py [workload[:num_batches]] [calls] [--retry]
 """
 import os
 import sys
@@ -14,10 +14,11 @@ import bench  # noqa: E402
 from paper_2411_11547_b200 import _native, datagen, default_configs  # noqa: E402
 from paper_2411_11547_b200.pipeline import config_tuples  # noqa: E402
 
-name = sys.argv[1] if len(sys.argv) > 1 else "c5"
+spec = sys.argv[1] if len(sys.argv) > 1 else "c5"
+name, _, nb = spec.partition(":")
 calls = int(sys.argv[2]) if len(sys.argv) > 2 else 10
 flags = _native.FLAG_RETRY_F64 if "--retry" in sys.argv else 0
-flat = bench.pinned_copy(datagen.workload(name))
+flat = bench.pinned_copy(datagen.workload(name, num_batches=int(nb) if nb else None))
 cfg = config_tuples(default_configs("f32"))
 ctx = _native.Context(0)
 res = np.empty(flat.num_pairs, np.float64)
