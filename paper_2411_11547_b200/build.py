@@ -28,7 +28,8 @@ FLAT_OUT = os.path.join(HERE, "_lib", "_phmm_flatten" + (sysconfig.get_config_va
 OBJ = os.path.join(HERE, "_lib", "obj")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-         "-Xcompiler", "-fPIC", "-Xcompiler", "-pthread", "-Xptxas", "-warn-spills"]
+         "-Xcompiler", "-fPIC", "-Xcompiler", "-pthread", "-Xptxas", "-warn-spills"] + \
+    os.environ.get("PHMM_NVCC_EXTRA", "").split()          # experiments: e.g. -DPHMM_UNROLL4
 
 
 def _obj(src: str) -> str:
