@@ -528,7 +528,6 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
   const V zero2 = A::zero();
   const S thr = A::thr();
   __shared__ StreamUnit s_unit[4 * G];
-  __shared__ int s_hc[2 * 128];
   __shared__ int s_win[4 * G * kStreamMaxWin];
   __shared__ S s_bs[4 * G * 2 * kStreamMaxLaneHaps];
   __shared__ int s_meta[4 * G * 4];
@@ -782,8 +781,7 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
       s_nwin[slot] = 0;
     }
     }                                                   // first_q
-    s_hc[2 * threadIdx.x] = -1;                         // current haplotype per lane
-    s_hc[2 * threadIdx.x + 1] = -1;
+    int hcA = -1, hcB = -1;                             // current haplotype per lane
     __syncwarp();
 
     // ---- the stream
@@ -833,6 +831,8 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
     if constexpr (STRIPES)
       if (col_in) col_fill(1);
 
+    // threads whose FIRST needs the haplotype's boundary value: left padding, or thread 0
+    const bool slow_first = (q * W + t * K <= s_meta[slot * 4 + 0]) || (t == 0 && q == 0);
     // FIRST(lane L): reset the lane to row 0 of its next haplotype (event paths only run
     // inside windows and read their inputs from shared memory)
     // FULL (the unit's pre-initialisation): M = I = 0, D = the boundary in the left padding.
@@ -842,7 +842,7 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
     auto first_event = [&](auto lconst, auto full, V& dgM, V& dgI, V& dgD, V& nbM, V& nbI, V& nbD) {
       constexpr int L = decltype(lconst)::value;
       constexpr bool FULL = decltype(full)::value;
-      const int hc = ++s_hc[2 * threadIdx.x + L];
+      const int hc = L == 0 ? hcA : hcB;                // incremented by the caller
       const int lp = s_meta[slot * 4 + 0];
       const int p0 = q * W + t * K;                     // global padded position of k = 0
       auto bval = [&]() { return s_bs[slot * 2 * kStreamMaxLaneHaps + (L == 0 ? 0 : s_unit[slot].cntA) + hc]; };
@@ -873,7 +873,7 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
     auto last_event = [&](auto lconst) {
       constexpr int L = decltype(lconst)::value;
       const StreamUnit& SU = s_unit[slot];
-      const int hc = s_hc[2 * threadIdx.x + L];
+      const int hc = L == 0 ? hcA : hcB;
       const StreamHap sh = shaps[SU.list + (L == 0 ? 0 : SU.cntA) + hc];
       S res;
       if constexpr (EXACT)                              // j-ordered sum (wavefront.py:156-160)
@@ -954,10 +954,36 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
       }
       code = pf1;
       pf1 = CHECK ? ld_code(s + 1) : ld_code_plain(s + 1);
-      if (CHECK && (code & ((kCodeFirst << 8) | kCodeFirst))) {
+      if constexpr (CHECK && SEP && F64) {
+        // separator rows already zeroed M and I: a FIRST resets D and the diagonal D, done
+        // predicated by every thread (no divergent branch between consecutive checked
+        // steps); threads with left padding and thread 0 (the boundary) also take the
+        // handler.  FP64 (32,8) / (32,7) -1.5 %; in FP32 the selects cost more than the
+        // branch saves (c2 +4 %), so FP32 keeps the branchy handler.
+        const bool fA = (code & kCodeFirst) != 0, fB = (code & (kCodeFirst << 8)) != 0;
+        hcA += fA ? 1 : 0;
+        hcB += fB ? 1 : 0;
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          if (fA) D[k].x = 0;
+          if (fB) D[k].y = 0;
+        }
+        if (fA) dgD.x = 0;
+        if (fB) dgD.y = 0;
+        if (slow_first && (fA || fB)) {
+          if (fA) first_event(std::integral_constant<int, 0>{}, std::false_type{}, dgM, dgI, dgD, nbM, nbI, nbD);
+          if (fB) first_event(std::integral_constant<int, 1>{}, std::false_type{}, dgM, dgI, dgD, nbM, nbI, nbD);
+        }
+      } else if (CHECK && (code & ((kCodeFirst << 8) | kCodeFirst))) {
         using Full = std::integral_constant<bool, !SEP>;
-        if (code & kCodeFirst) first_event(std::integral_constant<int, 0>{}, Full{}, dgM, dgI, dgD, nbM, nbI, nbD);
-        if (code & (kCodeFirst << 8)) first_event(std::integral_constant<int, 1>{}, Full{}, dgM, dgI, dgD, nbM, nbI, nbD);
+        if (code & kCodeFirst) {
+          ++hcA;
+          first_event(std::integral_constant<int, 0>{}, Full{}, dgM, dgI, dgD, nbM, nbI, nbD);
+        }
+        if (code & (kCodeFirst << 8)) {
+          ++hcB;
+          first_event(std::integral_constant<int, 1>{}, Full{}, dgM, dgI, dgD, nbM, nbI, nbD);
+        }
       }
       // plain steps read idle codes only in the drain (rows no one reads): they clamp to N
       // (one IMNMX instead of the select, and the table read stays in this slot)
@@ -1051,8 +1077,8 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
     // row 0 of each lane's first haplotype: the fill steps (kCodeIdle) keep it until the
     // thread's first row, so no FIRST event is needed for it
     if (sq) {
-      if (U.cntA > 0) first_event(std::integral_constant<int, 0>{}, std::true_type{}, xM, xI, xD, yM, yI, yD);
-      if (U.cntB > 0) first_event(std::integral_constant<int, 1>{}, std::true_type{}, xM, xI, xD, yM, yI, yD);
+      if (U.cntA > 0) { hcA = 0; first_event(std::integral_constant<int, 0>{}, std::true_type{}, xM, xI, xD, yM, yI, yD); }
+      if (U.cntB > 0) { hcB = 0; first_event(std::integral_constant<int, 1>{}, std::true_type{}, xM, xI, xD, yM, yI, yD); }
     }
 
     // event-free stretches run the plain step; windows run the event-checking one, for as
