@@ -569,7 +569,7 @@ def main():
             line["e2e_run"] = [e2e_run("c2"), e2e_run("c3")]
         except Exception as exc:
             line["e2e_run"] = [{"error": repr(exc)}]
-    if not args.no_cpu_baseline:
+    if not args.no_cpu_baseline and ws == 1:          # contract: rank 0 at N = 1 only
         retry = bool(flags & _native.FLAG_RETRY_F64)
         port = cpu_baseline(full, args.cpu_seconds, retry)
         ref = reference_cpu(full, args.cpu_seconds, retry)
