@@ -132,6 +132,12 @@ int phmm_score(phmm_ctx* ctx, const phmm_input* in, const phmm_options* opt,
  * (partition.py:88-119, pipeline.py:116-136: contiguous global-id chunks, each within the
  * budget, the next staged while the current one computes) for inputs larger than HBM. */
 int phmm_set_device_budget(phmm_ctx* ctx, int64_t bytes);
+/* Pipelining depth of phmm_score: 0 (the default) = automatic -- calls of >= 2^20 pairs
+ * stream through six chunk contexts with ramped sizes (1,3,4,4,3,1)/16, so host planning,
+ * H2D, kernels and the host finishing of different chunks overlap; smaller calls run one
+ * pass.  n in 2..8 pipelines every call of >= 2n batches through n equal chunks (results
+ * are identical either way: pairs are independent).  1 = never pipeline. */
+int phmm_set_pipeline(phmm_ctx* ctx, int n);
 /* Device bytes currently allocated by the context and its chunk contexts. */
 int phmm_device_bytes(const phmm_ctx* ctx, int64_t* bytes);
 

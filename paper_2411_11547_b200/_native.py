@@ -62,7 +62,8 @@ class PhmmStats(ctypes.Structure):
 # every symbol include/phmm.h declares (tests/test_abi.py checks the .so exports them)
 EXPORTS = ("phmm_abi_version", "phmm_create", "phmm_destroy", "phmm_last_error", "phmm_score",
            "phmm_prepare", "phmm_execute", "phmm_fetch", "phmm_fast_geometry", "phmm_last_timing",
-           "phmm_last_phases", "phmm_forward_matrices", "phmm_set_device_budget", "phmm_device_bytes")
+           "phmm_last_phases", "phmm_forward_matrices", "phmm_set_device_budget", "phmm_device_bytes",
+           "phmm_set_pipeline")
 
 _lib = None
 
@@ -106,6 +107,8 @@ def load():
     L.phmm_forward_matrices.restype = ctypes.c_int
     L.phmm_set_device_budget.argtypes = [_vp, _i64]
     L.phmm_set_device_budget.restype = ctypes.c_int
+    L.phmm_set_pipeline.argtypes = [_vp, _i32]
+    L.phmm_set_pipeline.restype = ctypes.c_int
     L.phmm_device_bytes.argtypes = [_vp, ctypes.POINTER(_i64)]
     L.phmm_device_bytes.restype = ctypes.c_int
     if L.phmm_abi_version() != 1:
@@ -230,6 +233,11 @@ class Context:
         """Bound the device working set of score() (0: none; see phmm_set_device_budget)."""
         with self._lock:
             self._check(self._L.phmm_set_device_budget(self._h, int(nbytes)))
+
+    def set_pipeline(self, n: int):
+        """phmm_score pipelining depth (0 automatic, 1 never, 2..8 equal chunks)."""
+        with self._lock:
+            self._check(self._L.phmm_set_pipeline(self._h, int(n)))
 
     def device_bytes(self) -> int:
         v = _i64()

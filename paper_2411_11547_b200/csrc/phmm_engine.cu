@@ -169,24 +169,6 @@ int col_rows_for(int P, int max_rows) { return std::max(stream_cap_of(P), max_ro
 constexpr int kR64MaxW = 256, kRX32MaxW = 512;   // widest FP64 / exact-FP32 retry tilings
 
 constexpr int kMaxScoreChunks = 8;
-int score_chunks() {                          // phmm_score pipelining depth (PHMM_CHUNKS)
-  static int v = -1;
-  if (v < 0) {
-    const char* env = getenv("PHMM_CHUNKS");
-    v = env ? std::max(1, std::min(kMaxScoreChunks, atoi(env))) : 0;   // 0: by call size
-  }
-  return v;
-}
-constexpr int64_t kScoreChunkMinPairs = 32768;
-bool score_chunking_enabled() {
-  static int v = -1;
-  if (v < 0) {
-    const char* env = getenv("PHMM_NO_CHUNK");
-    v = (env && env[0] == '1') ? 0 : 1;
-  }
-  return v == 1;
-}
-
 // Small persistent worker pool for host-side data-parallel loops (result finishing).
 class WorkerPool {
  public:
@@ -314,6 +296,7 @@ struct phmm_ctx {
   phmm_ctx* parent = nullptr;
   int budget_div = 1;        // chunk contexts: number of chunks sharing the band budget
   int64_t device_budget = 0; // phmm_set_device_budget: bound on the device working set of phmm_score (0: none)
+  int pipeline = 0;          // phmm_set_pipeline: 0 automatic, 1 never, n equal chunks
   size_t col_budget = kColBudget;        // boundary-column scratch bound of this context
   std::vector<phmm_ctx*> chunks;             // chunk contexts (phmm_score pipelining), lazy
   PinnedVec<int64_t> c_roff, c_hoff;         // chunk views: rebased offsets (pinned: async H2D)
@@ -1642,14 +1625,18 @@ static std::vector<int64_t> weighted_pair_cut(const phmm_input* in, const std::v
   }
   return cut;
 }
-static std::vector<int64_t> equal_pair_cut(const phmm_input* in, int nch) {
-  return weighted_pair_cut(in, std::vector<int>(nch, 1));
-}
 
 int phmm_set_device_budget(phmm_ctx* ctx, int64_t bytes) {
   if (!ctx) return PHMM_ERR_INVALID;
   if (bytes < 0) return ctx->fail(PHMM_ERR_INVALID, "negative device budget");
   ctx->device_budget = bytes;
+  return PHMM_SUCCESS;
+}
+
+int phmm_set_pipeline(phmm_ctx* ctx, int n) {
+  if (!ctx) return PHMM_ERR_INVALID;
+  if (n < 0 || n > kMaxScoreChunks) return ctx->fail(PHMM_ERR_INVALID, "pipeline depth %d not in 0..%d", n, kMaxScoreChunks);
+  ctx->pipeline = n;
   return PHMM_SUCCESS;
 }
 
@@ -1727,44 +1714,30 @@ int phmm_score(phmm_ctx* ctx, const phmm_input* in, const phmm_options* opt, dou
   }
   trace.mark("budget");
   trace.print("score");
-  if (ok && in->num_batches >= 2 * std::max(3, score_chunks()) && score_chunks() != 1 && score_chunking_enabled() &&
-      pairs >= kScoreChunkMinPairs) {
-    // Only regular calls are pipelined: reads spanning many tiling widths split into many
-    // small per-tiling kernels per chunk, and each chunk's latency-bound post-pass (guard
-    // band, FP64 retries) then queues behind the next chunks' persistent grids.
-    // large calls amortize the per-chunk post-pass latency: pipeline them regardless (and
-    // skip the O(reads) width-class scan)
-    static const int kW[] = {16, 32, 48, 64, 80, 96, 112, 128, 160, 192, 224, 256, 320, 384, 448, 512};
-    unsigned classes = 0;
-    for (int64_t r = 0; pairs < kBigCallPairs && r < in->num_reads && __builtin_popcount(classes) <= 2; ++r) {
-      const int64_t m = in->read_off[r + 1] - in->read_off[r];
-      int c = 0;
-      while (c < 15 && kW[c] < m + 1) ++c;
-      classes |= 1u << c;
-    }
-    if (__builtin_popcount(classes) <= 2 || pairs >= kBigCallPairs) {
-      CK(cudaSetDevice(ctx->device));
-      // per-chunk planning overhead vs pipeline depth: 3 equal chunks for ordinary calls
-      // (c2: +15 % e2e over 4).  Large calls ramp: the GPU idles while the first chunk is
-      // planned and the host finishes the last one after the GPU is done, so both are small
-      // (planning runs ~4x faster than the GPU scores, so chunk 1 is ready in time).
-      // c5 (tools/sweep_chunks.sh): 1,3,4,4,3,1 281.6 ms < 1,2,4,4,4,1 282.5 < 1,2,3,3,3,2,1
-      // 283.6 < 1,4,6,4,1 284.6 < 1,3,4,4,4 286.5 < 1,2,2,2,1 288.0
-      if (score_chunks() > 0)
-        return score_chunked(ctx, in, opt, out_log10, out_status, stats, equal_pair_cut(in, score_chunks()),
-                             score_chunks(), kColBudget);
-      std::vector<int> w = pairs >= kBigCallPairs ? std::vector<int>{1, 3, 4, 4, 3, 1} : std::vector<int>{1, 1, 1};
-      if (const char* env = getenv("PHMM_CHUNK_WEIGHTS")) {     // experiments: "1,3,4,4,3,1"
-        std::vector<int> ew;
-        for (const char* p = env; *p;) {
-          char* end = nullptr;
-          const long v = strtol(p, &end, 10);
-          if (end == p) break;
-          if (v > 0) ew.push_back((int)v);
-          p = *end ? end + 1 : end;
-        }
-        if (!ew.empty() && (int)ew.size() <= kMaxScoreChunks) w = ew;
+  // Pipelining (phmm_set_pipeline): large calls ramp -- the GPU idles while the first
+  // chunk is planned and the host finishes the last one after the GPU is done, so both are
+  // small (planning runs ~4x faster than the GPU scores, so chunk 1 is ready in time).
+  // c5 (tools/sweep_chunks.sh): 1,3,4,4,3,1 281.6 ms < 1,2,4,4,4,1 282.5 < 1,2,3,3,3,2,1
+  // 283.6 < 1,4,6,4,1 284.6 < 1,3,4,4,4 286.5 < 1,2,2,2,1 288.0; the ramp also wins at
+  // 1.25M pairs (41 vs 52 ms one-pass).  Below 2^20 pairs one pass is as fast or faster
+  // (c2 2.2 vs 2.4 ms with 3 chunks; 131k-524k pairs equal; tools/sweep_chunks_*.sh).
+  if (ok && ctx->pipeline != 1) {
+    std::vector<int> w;
+    if (ctx->pipeline > 1 && in->num_batches >= 2 * ctx->pipeline) w.assign(ctx->pipeline, 1);
+    else if (ctx->pipeline == 0 && pairs >= kBigCallPairs) w = {1, 3, 4, 4, 3, 1};
+    if (const char* env = getenv("PHMM_CHUNK_WEIGHTS"); env && !w.empty()) {   // experiments
+      std::vector<int> ew;
+      for (const char* p = env; *p;) {
+        char* end = nullptr;
+        const long v = strtol(p, &end, 10);
+        if (end == p) break;
+        if (v > 0) ew.push_back((int)v);
+        p = *end ? end + 1 : end;
       }
+      if (!ew.empty() && (int)ew.size() <= kMaxScoreChunks) w = ew;
+    }
+    if (!w.empty() && in->num_batches >= 2 * (int64_t)w.size()) {
+      CK(cudaSetDevice(ctx->device));
       return score_chunked(ctx, in, opt, out_log10, out_status, stats, weighted_pair_cut(in, w), (int)w.size(),
                            kColBudget);
     }

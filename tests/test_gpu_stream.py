@@ -151,42 +151,50 @@ def test_partial_underflow_units_and_degenerate_reads(engine, rng):
 
 
 def test_chunked_score_matches_resident_path(engine):
-    """phmm_score pipelines large calls over chunk contexts; results must equal the
-    one-pass prepare/execute/fetch path bit for bit (FP32 + guard band + FP64 retry)."""
+    """phmm_score pipelines calls over chunk contexts (automatic for >= 2^20 pairs,
+    phmm_set_pipeline forces it); results must equal the one-pass prepare/execute/fetch
+    path bit for bit (FP32 + guard band + FP64 retry)."""
     from paper_2411_11547_b200 import datagen
-    # regular calls (one read length, one haplotype length) are the pipelined ones
+    piped = _native.Context(0)
+    piped.set_pipeline(4)
     derived = datagen.workload("c2", num_batches=520)          # 33,280 pairs -> 4 chunks
     indep = datagen.generate_synthetic_flat(num_batches=520, reads_per_batch=16, haps_per_batch=4,
                                             read_len_spec=120, hap_len_spec=200, seed=SEED_CHUNK,
                                             mode="independent")     # every pair underflows FP32
     for flat, flags in ((derived, 0), (derived, _native.FLAG_EXACT), (indep, 0),
                         (indep, _native.FLAG_RETRY_F64)):
-        assert flat.num_pairs >= 32768
-        a, sa, st = engine.score(flat, F32, flags)
+        a, sa, st = piped.score(flat, F32, flags)
         engine.prepare(flat, F32, flags)
         engine.execute()
         b, sb, _ = engine.fetch()
         assert np.array_equal(a, b, equal_nan=True) and np.array_equal(sa, sb)
         assert st.num_pairs == flat.num_pairs
+    # ramped automatic pipelining is exercised by the 1M-pair test (test_gpu_parity.py)
+    piped.close()
+    with pytest.raises(Exception):
+        engine.set_pipeline(9)
 
 
 def test_chunked_score_rejects_invalid_chunk_and_recovers(engine):
     from paper_2411_11547_b200 import datagen
     from paper_2411_11547_b200.errors import DataError
+    piped = _native.Context(0)
+    piped.set_pipeline(4)
     flat = datagen.workload("c2", num_batches=520)
     bad = FlatBatches(**{f: np.array(getattr(flat, f), copy=True) for f in FlatBatches.FIELDS})
     bad.hap_bases[-3] = 9                                     # last chunk: invalid base code
     with pytest.raises(DataError):
-        engine.score(bad, F32, 0)
+        piped.score(bad, F32, 0)
     bad = FlatBatches(**{f: np.array(getattr(flat, f), copy=True) for f in FlatBatches.FIELDS})
     bad.bq[5] = 200                                           # first chunk: invalid quality
     with pytest.raises(DataError):
-        engine.score(bad, F32, 0)
-    a, sa, _ = engine.score(flat, F32, 0)                     # the context is still healthy
+        piped.score(bad, F32, 0)
+    a, sa, _ = piped.score(flat, F32, 0)                     # the context is still healthy
     engine.prepare(flat, F32, 0)
     engine.execute()
     b, sb, _ = engine.fetch()
     assert np.array_equal(a, b, equal_nan=True) and np.array_equal(sa, sb)
+    piped.close()
 
 
 @pytest.mark.parametrize("seed", [1, 2, 3, 4])

@@ -1,7 +1,7 @@
 """Wall time of repeated phmm_score calls (pinned inputs, caller-owned result buffers, like
 bench.py's e2e loop); PHMM_TRACE=1 adds the per-chunk host timeline on stderr.
 
-usage: python tools/e2e_calls.py [workload[:num_batches]] [calls] [--retry]
+usage: python tools/e2e_calls.py [workload[:num_batches]] [calls] [--retry] [--pipeline=n]
 """
 import os
 import sys
@@ -21,6 +21,9 @@ flags = _native.FLAG_RETRY_F64 if "--retry" in sys.argv else 0
 flat = bench.pinned_copy(datagen.workload(name, num_batches=int(nb) if nb else None))
 cfg = config_tuples(default_configs("f32"))
 ctx = _native.Context(0)
+for a in sys.argv:
+    if a.startswith("--pipeline="):
+        ctx.set_pipeline(int(a.split("=", 1)[1]))
 res = np.empty(flat.num_pairs, np.float64)
 st = np.empty(flat.num_pairs, np.uint8)
 for i in range(calls):
