@@ -979,9 +979,17 @@ static int prepare_impl(phmm_ctx* ctx, const phmm_input* in, const phmm_options*
   const bool rx32 = streamed > 0 && ctx->rx32_geoms;
   if (!r64) ctx->r64_geoms = 0;
   if (!rx32) ctx->rx32_geoms = 0;
+  // second-stage FP64 units (r64b: guard-band pairs whose exact rerun underflows) live in
+  // a second region of the FP64 unit list of their tiling: long reads (widest tiling), and
+  // every tiling of a large call (per-pair FP64 is latency bound: c5 5.4 ms for 53k pairs)
+  const bool big = streamed >= kBigCallPairs;
+  unsigned r64b_geoms = 0;
   for (int g = 0; g < kNumR64Geoms; ++g)
-    if (ctx->r64_geoms & (1u << g))   // widest tiling, long reads: a second region (r64b)
-      CK(ctx->d_r64u[g].ensure(r64_pairs[g] * (g == kNumR64Geoms - 1 && long64 && rx32 ? 2 : 1)));
+    if (r64 && rx32 && (ctx->r64_geoms & (1u << g)) && (big || (g == kNumR64Geoms - 1 && long64)))
+      r64b_geoms |= 1u << g;
+  for (int g = 0; g < kNumR64Geoms; ++g)
+    if (ctx->r64_geoms & (1u << g))
+      CK(ctx->d_r64u[g].ensure(r64_pairs[g] * ((r64b_geoms >> g) & 1 ? 2 : 1)));
   for (int g = 0; g < kNumRX32Geoms; ++g)
     if (ctx->rx32_geoms & (1u << g)) CK(ctx->d_rx32u[g].ensure(rx32_pairs[g]));
   if (r64) CK(ctx->d_r64h.ensure(streamed));
@@ -1018,22 +1026,22 @@ static int prepare_impl(phmm_ctx* ctx, const phmm_input* in, const phmm_options*
     L.hap_cap = geoms ? (int)streamed : 0;
     // short units keep small post-pass lists parallel (their size is unknown when the
     // grid is sized); large calls get longer units (less fill/drain and setup per pair)
-    const bool big = streamed >= kBigCallPairs;
     L.lane_haps = &L == &E.r64 ? (big ? 4 : kRetryLaneHaps64) : (big ? 3 : kRetryLaneHapsX32);
   };
   lists(E.r64, ctx->d_r64u, kNumR64Geoms, ctx->d_r64h, ctx->r64_geoms, kCtrR64, r64_pairs);
   lists(E.rx32, ctx->d_rx32u, kNumRX32Geoms, ctx->d_rx32h, ctx->rx32_geoms, kCtrRX32, rx32_pairs);
-  // second stage for long reads: guard-band pairs whose striped exact rerun underflows get
-  // striped FP64 units in the upper half of the widest FP64 list (haplotype entries share
-  // the first stage's array), run after the post-pass instead of the per-pair kernel
+  // second stage: guard-band pairs whose exact rerun underflows get FP64 stream units in
+  // the upper half of their tiling's FP64 list (haplotype entries share the first stage's
+  // array: the two sets of pairs are disjoint), run after the post-pass instead of the
+  // per-pair kernel
   {
-    const int g = kNumR64Geoms - 1;
     E.r64b = E.r64;
     for (int x = 0; x < 8; ++x) E.r64b.units[x] = nullptr;
     E.r64b.count = ctx->d_counters.p + kCtrR64b;
-    E.r64b.lane_haps = 1;
-    E.r64b.enabled = (r64 && rx32 && long64 && (ctx->r64_geoms & (1u << g))) ? 1 : 0;
-    if (E.r64b.enabled) E.r64b.units[g] = ctx->d_r64u[g].p + r64_pairs[g];
+    E.r64b.lane_haps = big ? E.r64.lane_haps : 1;
+    E.r64b.enabled = r64b_geoms ? 1 : 0;
+    for (int g = 0; g < kNumR64Geoms; ++g)
+      if ((r64b_geoms >> g) & 1) E.r64b.units[g] = ctx->d_r64u[g].p + r64_pairs[g];
   }
   // grids of the stream launches, and boundary-column space for the ones that can meet
   // striped units (reads longer than the tiling width): per sub-warp slot 2 columns x
@@ -1109,6 +1117,17 @@ static int record_timing(phmm_ctx* ctx) {
   ctx->last_dev_ms = dev;
   ctx->last_fast_ms = fast;
   for (int i = 0; i < 4; ++i) ctx->last_phase_ms[i] = ph[i];
+  if (getenv("PHMM_TRACE")) {                 // post-pass list sizes (device-appended)
+    int c[kBinCounters];
+    if (cudaMemcpy(c, ctx->d_counters.p, sizeof(c), cudaMemcpyDeviceToHost) == cudaSuccess) {
+      int r64 = 0, rx32 = 0;
+      for (int g = 0; g < 8; ++g) { r64 += c[kCtrR64 + g]; rx32 += c[kCtrRX32 + g]; }
+      fprintf(stderr, "[phmm lists] per-pair ex32 %d %d %d %d | ex64 %d %d %d %d | fx64 %d %d %d %d | "
+                      "stream units r64 %d (entries %d) rx32 %d (entries %d)\n",
+              c[0], c[1], c[2], c[3], c[4], c[5], c[6], c[7], c[20], c[21], c[22], c[23], r64, c[kCtrR64 + 8],
+              rx32, c[kCtrRX32 + 8]);
+    }
+  }
   return PHMM_SUCCESS;
 }
 
@@ -1211,12 +1230,13 @@ int phmm_execute(phmm_ctx* ctx) {
     }
   CK(join());
   CK(cudaEventRecord(ctx->ev_post1, st));
-  if (E.r64b.enabled) {                 // long reads: band pairs whose exact rerun underflowed
-    const int g = kNumR64Geoms - 1;
-    const StreamKernel& SKn = striped_tab(kFast64);
-    SKn.launch(dim3(ctx->r64_grid), SKn.smem, st, E, E.r64b.units[g], E.r64b.haps, E.r64b.unit_cap[g],
-               E.r64b.count + g, ctx->d_counters.p + kCtrR64bWork + g, ctx->d_colstream.p + ctx->r64_col_off[g],
-               col_rows_for(SKn.P, ctx->max_n));
+  for (int g = kNumR64Geoms - 1; g >= 0; --g) {   // band pairs whose exact rerun underflowed
+    if (!E.r64b.units[g]) continue;
+    const bool str = ctx->r64_col_off[g] >= 0;
+    const StreamKernel& SKn = str ? striped_tab(kFast64) : stream_table_fast64()[g];
+    SKn.launch(dim3(str ? ctx->r64_grid : ctx->num_sms * occ_cap(SKn.occ)), SKn.smem, st, E, E.r64b.units[g],
+               E.r64b.haps, E.r64b.unit_cap[g], E.r64b.count + g, ctx->d_counters.p + kCtrR64bWork + g,
+               str ? ctx->d_colstream.p + ctx->r64_col_off[g] : nullptr, col_rows_for(SKn.P, ctx->max_n));
     ++launches;
   }
   if (ctx->flags & PHMM_FLAG_RETRY_F64) {

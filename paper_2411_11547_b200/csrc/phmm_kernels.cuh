@@ -893,7 +893,8 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
         const bool bad = !(res > 0.f) || !isfinite(res);
         if (bad && E.retry_f64) {
           E.status[sh.pair] = kStatusRetriedF64;
-          if (STRIPES && E.r64b.enabled) s_flag[2 * slot + L] |= 1u << hc;   // -> striped FP64 unit
+          const int g64 = r64_geom_for(mm);
+          if (E.r64b.enabled && E.r64b.units[g64]) s_flag[2 * slot + L] |= 1u << hc;   // -> FP64 stream unit
           else append_item(E.fx64, E.fx64_count, E.list_cap, exact_slot_for(mm), ExactItem{sh.pair, SU.read, sh.hap, 0});
         } else {
           E.acc[sh.pair] = (double)res;
@@ -1139,11 +1140,14 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
     if constexpr (STRIPES) cp_async_wait_all();      // the ring is refilled by the next stripe
     __syncwarp();
     }                                                   // stripes
-    if constexpr (MODE == kExact32 && STRIPES) {
-      // long reads: guard-band pairs whose exact rerun underflowed -> striped FP64 units
-      if (t == 0 && live && (s_flag[2 * slot] | s_flag[2 * slot + 1]))
-        emit_retry_units(U, shaps, s_flag + 2 * slot, E.r64b, kNumR64Geoms - 1, stream_cap_of(32), m, 1, 1 << 30,
-                         SepRows<kFast64>::value);
+    if constexpr (MODE == kExact32) {
+      // guard-band pairs whose exact rerun underflowed -> second-stage FP64 stream units
+      // (long reads, and every read of a large call; otherwise the per-pair FP64 list)
+      if (t == 0 && live && (s_flag[2 * slot] | s_flag[2 * slot + 1])) {
+        const int g64 = r64_geom_for(m);
+        emit_retry_units(U, shaps, s_flag + 2 * slot, E.r64b, g64, stream_cap_of(r64_geom_P(g64)), m,
+                         E.r64b.lane_haps, 256, SepRows<kFast64>::value);
+      }
     }
     if constexpr (MODE == kFast32) {
       // this unit's FP32-underflowed and guard-band pairs -> device-built stream units
