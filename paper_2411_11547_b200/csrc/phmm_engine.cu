@@ -895,6 +895,20 @@ static int prepare_impl(phmm_ctx* ctx, const phmm_input* in, const phmm_options*
     ctx->sbin_order.resize(nsbins);
     std::iota(ctx->sbin_order.begin(), ctx->sbin_order.end(), 0);
     std::stable_sort(ctx->sbin_order.begin(), ctx->sbin_order.end(), [&](int a, int b) { return work[a] > work[b]; });
+    if (trace.on) {                          // per bin: units, true cells, computed cells
+      for (int bi = 0; bi < nsbins; ++bi) {
+        const StreamKernel& g = skern(ctx->sbins[bi].mode, ctx->sbins[bi].geom);
+        double tc = 0, cc = 0;
+        for (int64_t i = ctx->sbins[bi].dev_off; i < ctx->sbins[bi].dev_off + ctx->sbins[bi].count; ++i) {
+          const StreamUnit& u = ctx->h_sunits[i];
+          const int64_t Q = (u.m + g.P * g.K) / (g.P * g.K);
+          cc += 2.0 * Q * g.P * g.K * (std::max(u.rowsA, u.rowsB) + g.P - 1);
+          tc += (double)u.m * (u.rowsA + u.rowsB);
+        }
+        fprintf(stderr, "[phmm bin] mode %d P %d K %d%s units %lld true %.4g computed %.4g\n", ctx->sbins[bi].mode, g.P,
+                g.K, (ctx->sbins[bi].geom & kStripedBin) ? " striped" : "", (long long)ctx->sbins[bi].count, tc, cc);
+      }
+    }
   }
   trace.mark("units");
   auto t1 = std::chrono::steady_clock::now();
