@@ -611,18 +611,21 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
     //   dl, ep, zt with the f64 -> dtype casts of wavefront.py:347-355.
     S al[K], be[K], dl[K], ep[K], zt[K];
     V M[K], I[K], D[K];
-    double dprev = 1.0, cprev = 1.0;                  // fast modes: d, c of position p - 1
+    // the fast FP32 mode derives its coefficients in FP32 (a few ulp against the 1e-4 bar;
+    // the FP64 retry keeps FP64 coefficients for its 1e-9 bar)
+    using CT = typename std::conditional<MODE == kFast32, float, double>::type;
+    CT dprev = 1, cprev = 1;                          // fast modes: d, c of position p - 1
     if constexpr (!EXACT) {
       const int pp = q * W + t * K - 1;
       if (pp >= Lp && pp < Lp + m) {
         const int i0 = pp - Lp;
-        const double d = s_lut[E.iq[ro + i0]], z = s_lut[E.dq[ro + i0]];
-        double anext = 1.0, bnext = 0.0, bI = 1.0;
+        const CT d = (CT)s_lut[E.iq[ro + i0]], z = (CT)s_lut[E.dq[ro + i0]];
+        CT anext = 1, bnext = 0, bI = 1;
         if (i0 + 1 < m) {
-          anext = (1.0 - s_lut[E.iq[ro + i0 + 1]]) - s_lut[E.dq[ro + i0 + 1]];
-          bnext = bI = 1.0 - s_lut[E.gq[ro + i0 + 1]];
+          anext = ((CT)1 - (CT)s_lut[E.iq[ro + i0 + 1]]) - (CT)s_lut[E.dq[ro + i0 + 1]];
+          bnext = bI = (CT)1 - (CT)s_lut[E.gq[ro + i0 + 1]];
         }
-        dprev = bI * d / ((1.0 - d) - z);
+        dprev = bI * d / (((CT)1 - d) - z);
         cprev = bnext * z / anext;
       }
     }
@@ -649,19 +652,20 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
             al[k] = (S)((1.0 - d) - z); be[k] = (S)(1.0 - e); dl[k] = (S)d; ep[k] = (S)e;
             zt[k] = (i0 + 1 < m) ? (S)z : (S)0;         // D(m, .) never reaches the score
             lm = (S)(1.0 - qe); lx = (S)(qe / 3.0);
-          } else {                                      // fast modes (computed in f64)
-            double anext = 1.0, bnext = 0.0, bI = 1.0;  // alpha, beta of position i+1
+          } else {                                      // fast modes (CT arithmetic)
+            const CT cd = (CT)d, cz = (CT)z, ce = (CT)e, cqe = (CT)qe;
+            CT anext = 1, bnext = 0, bI = 1;            // alpha, beta of position i+1
             if (i0 + 1 < m) {
-              anext = (1.0 - s_lut[E.iq[ro + i0 + 1]]) - s_lut[E.dq[ro + i0 + 1]];
-              bnext = bI = 1.0 - s_lut[E.gq[ro + i0 + 1]];
+              anext = ((CT)1 - (CT)s_lut[E.iq[ro + i0 + 1]]) - (CT)s_lut[E.dq[ro + i0 + 1]];
+              bnext = bI = (CT)1 - (CT)s_lut[E.gq[ro + i0 + 1]];
             }
-            const double dcur = bI * d / ((1.0 - d) - z);
-            const double ccur = bnext * z / anext;      // 0 for the last position
+            const CT dcur = bI * cd / (((CT)1 - cd) - cz);
+            const CT ccur = bnext * cz / anext;         // 0 for the last position
             // beta_i = 0 (gcp q = 0): r = inf -> NaN accumulator -> exact rerun
-            be[k] = (S)(bI * e / (1.0 - e) * dprev / dcur);
-            dl[k] = (S)dprev; zt[k] = (S)cprev; ep[k] = (S)e;
+            be[k] = (S)(bI * ce / ((CT)1 - ce) * dprev / dcur);
+            dl[k] = (S)dprev; zt[k] = (S)cprev; ep[k] = (S)ce;
             dprev = dcur; cprev = ccur;
-            lm = (S)(anext * (1.0 - qe)); lx = (S)(anext * (qe / 3.0));
+            lm = (S)(anext * ((CT)1 - cqe)); lx = (S)(anext * (cqe / (CT)3));
           }
 #pragma unroll
           for (int c = 0; c < 5; ++c) lam[c][kk] = (rc == c || rc == 4 || c == 4) ? lm : lx;
