@@ -615,6 +615,7 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
     // the FP64 retry keeps FP64 coefficients for its 1e-9 bar)
     using CT = typename std::conditional<MODE == kFast32, float, double>::type;
     CT dprev = 1, cprev = 1;                          // fast modes: d, c of position p - 1
+    CT ia = -1;                                       // 1 / alpha of the next position, once known
     if constexpr (!EXACT) {
       const int pp = q * W + t * K - 1;
       if (pp >= Lp && pp < Lp + m) {
@@ -625,8 +626,9 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
           anext = ((CT)1 - (CT)s_lut[E.iq[ro + i0 + 1]]) - (CT)s_lut[E.dq[ro + i0 + 1]];
           bnext = bI = (CT)1 - (CT)s_lut[E.gq[ro + i0 + 1]];
         }
+        ia = (CT)1 / anext;
         dprev = bI * d / (((CT)1 - d) - z);
-        cprev = bnext * z / anext;
+        cprev = bnext * z * ia;
       }
     }
 #pragma unroll
@@ -659,12 +661,15 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
               anext = ((CT)1 - (CT)s_lut[E.iq[ro + i0 + 1]]) - (CT)s_lut[E.dq[ro + i0 + 1]];
               bnext = bI = (CT)1 - (CT)s_lut[E.gq[ro + i0 + 1]];
             }
-            const CT dcur = bI * cd / (((CT)1 - cd) - cz);
-            const CT ccur = bnext * cz / anext;         // 0 for the last position
+            // two divisions per position: 1/alpha carries to the next position
+            const CT inv_alpha = ia >= 0 ? ia : (CT)1 / (((CT)1 - cd) - cz);
+            const CT inv_anext = (CT)1 / anext;
+            const CT dcur = bI * cd * inv_alpha;
+            const CT ccur = bnext * cz * inv_anext;     // 0 for the last position
             // beta_i = 0 (gcp q = 0): r = inf -> NaN accumulator -> exact rerun
-            be[k] = (S)(bI * ce / ((CT)1 - ce) * dprev / dcur);
+            be[k] = (S)(bI * ce * dprev / (((CT)1 - ce) * dcur));
             dl[k] = (S)dprev; zt[k] = (S)cprev; ep[k] = (S)ce;
-            dprev = dcur; cprev = ccur;
+            dprev = dcur; cprev = ccur; ia = inv_anext;
             lm = (S)(anext * ((CT)1 - cqe)); lx = (S)(anext * (cqe / (CT)3));
           }
 #pragma unroll
