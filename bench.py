@@ -476,8 +476,10 @@ def main():
         dist.barrier()
         if rank != 0:
             gather = HostGather(gather_name(), n_total, create=False)
-    for _ in range(2):
-        ctx.score(pflat, cfg, flags, out=res, status=res_st)
+    for _ in range(2):                      # warm-up (also first-touches the gather pages)
+        out, ost, _ = ctx.score(pflat, cfg, flags, out=res, status=res_st)
+        if gather is not None:
+            gather.put(shard.gids, out, ost)
     barrier()
     t0 = time.perf_counter()
     call_ms = []

@@ -21,7 +21,7 @@ SOURCES = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
 HEADERS = sorted(glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(CSRC, "*.cuh"))) + [
     os.path.join(ROOT, "include", "phmm.h")]
 OUT = os.path.join(HERE, "_lib", "libphmm.so")
-HOST_SRC = [os.path.join(CSRC, "datagen.cpp"), os.path.join(CSRC, "batchio.cpp")]
+HOST_SRC = [os.path.join(CSRC, "datagen.cpp"), os.path.join(CSRC, "batchio.cpp"), os.path.join(CSRC, "gather.cpp")]
 HOST_OUT = os.path.join(HERE, "_lib", "libphmm_host.so")   # host-only: input generator, batch text I/O
 FLAT_SRC = os.path.join(CSRC, "flatten.cpp")                # CPython extension: Batch list -> flat arrays
 FLAT_OUT = os.path.join(HERE, "_lib", "_phmm_flatten" + (sysconfig.get_config_var("EXT_SUFFIX") or ".so"))

@@ -205,6 +205,26 @@ def score_sharded(flat: FlatBatches, config_rows, flags: int, devices):
     return scores, status, total
 
 
+_scatter = []
+
+
+def _scatter_fn():
+    """phmm_scatter_results from libphmm_host.so (host-only library), or None."""
+    if not _scatter:
+        import ctypes
+        import os
+        fn = None
+        path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libphmm_host.so")
+        try:
+            fn = ctypes.CDLL(path).phmm_scatter_results
+            fn.restype = None
+            fn.argtypes = [ctypes.c_void_p] * 5 + [ctypes.c_int64]
+        except (OSError, AttributeError):
+            fn = None
+        _scatter.append(fn)
+    return _scatter[0]
+
+
 class HostGather:
     """Host-side gather for one process per GPU: a shared-memory (float64 scores, uint8
     status) array of the whole batch list; each rank scatters its shard's results at
@@ -230,8 +250,20 @@ class HostGather:
         self.status = np.ndarray((num_pairs,), np.uint8, buffer=self.shm.buf, offset=num_pairs * 8)
 
     def put(self, gids: np.ndarray, scores: np.ndarray, status: np.ndarray):
-        self.scores[gids] = scores
-        self.status[gids] = status
+        """scores/status of a shard at their global ids (ascending runs: a streaming copy in
+        libphmm_host.so's phmm_scatter_results; numpy fancy assignment without it)."""
+        fn = _scatter_fn()
+        n = int(gids.shape[0])
+        if fn is None or n == 0:
+            self.scores[gids] = scores
+            self.status[gids] = status
+            return
+        g = np.ascontiguousarray(gids, dtype=np.int64)
+        sc = np.ascontiguousarray(scores, dtype=np.float64)
+        st = np.ascontiguousarray(status, dtype=np.uint8)
+        if g.min() < 0 or g.max() >= self.scores.shape[0]:
+            raise IndexError("global id out of range")
+        fn(self.scores.ctypes.data, self.status.ctypes.data, g.ctypes.data, sc.ctypes.data, st.ctypes.data, n)
 
     def close(self):
         self.scores = self.status = None
