@@ -115,3 +115,30 @@ def test_check_budget_first_item_matches_per_item_definition():
             check_budget(flat, cfgs, budget)
         assert str(err.value) == ("work item %d alone needs ~%d bytes, over the %d-byte budget"
                                   % (over[0], est[over[0]], budget))
+
+
+def test_host_gather_scatter_matches_numpy():
+    """HostGather.put (libphmm_host.so streaming scatter over ascending global-id runs)
+    writes exactly what numpy fancy assignment writes, for run-structured and scattered
+    ids; out-of-range ids raise."""
+    import os
+    from paper_2411_11547_b200.shards import HostGather
+    rng = np.random.default_rng(7)
+    n = 5000
+    name = "phmm_test_scatter_%d" % os.getpid()
+    g = HostGather(name, n, create=True)
+    try:
+        for gids in (np.arange(100, 900, dtype=np.int64),
+                     np.sort(rng.choice(n, 1200, replace=False)).astype(np.int64),
+                     np.concatenate([np.arange(10, 30), np.arange(40, 41), np.arange(4000, 4999)]).astype(np.int64)):
+            sc = rng.random(gids.shape[0])
+            st = rng.integers(0, 255, gids.shape[0]).astype(np.uint8)
+            want_sc, want_st = g.scores.copy(), g.status.copy()
+            want_sc[gids] = sc
+            want_st[gids] = st
+            g.put(gids, sc, st)
+            assert np.array_equal(g.scores, want_sc) and np.array_equal(g.status, want_st)
+        with pytest.raises(IndexError):
+            g.put(np.array([n], np.int64), np.zeros(1), np.zeros(1, np.uint8))
+    finally:
+        g.close()
