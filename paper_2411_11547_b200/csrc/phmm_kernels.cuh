@@ -43,7 +43,7 @@ struct StreamUnit {                       // 32 B
   int read;
   int list;                               // StreamHap entries: lane A [list, list+cntA),
   int cntA, cntB;                         //                    lane B [list+cntA, +cntB)
-  int rowsA, rowsB;                       // sum of the lane's haplotype lengths
+  int rowsA, rowsB;                       // the lane's rows: haplotype lengths (+ separator rows, fast modes)
   int ro, m;                              // read offset / length (saves a dependent load)
 };
 struct StreamHap { int hap, pair, off, n; };   // haplotype, pair id, base offset, length
