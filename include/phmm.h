@@ -133,7 +133,7 @@ int phmm_score(phmm_ctx* ctx, const phmm_input* in, const phmm_options* opt,
  * budget, the next staged while the current one computes) for inputs larger than HBM. */
 int phmm_set_device_budget(phmm_ctx* ctx, int64_t bytes);
 /* Pipelining depth of phmm_score: 0 (the default) = automatic -- calls of >= 2^20 pairs
- * stream through six chunk contexts with ramped sizes (1,3,4,4,3,1)/16, so host planning,
+ * stream through six chunk contexts with ramped sizes (1,3,5,5,3,1)/18, so host planning,
  * H2D, kernels and the host finishing of different chunks overlap; smaller calls run one
  * pass.  n in 2..8 pipelines every call of >= 2n batches through n equal chunks (results
  * are identical either way: pairs are independent).  1 = never pipeline. */

@@ -1751,14 +1751,14 @@ int phmm_score(phmm_ctx* ctx, const phmm_input* in, const phmm_options* opt, dou
   // Pipelining (phmm_set_pipeline): large calls ramp -- the GPU idles while the first
   // chunk is planned and the host finishes the last one after the GPU is done, so both are
   // small (planning runs ~4x faster than the GPU scores, so chunk 1 is ready in time).
-  // c5 (tools/sweep_chunks.sh): 1,3,4,4,3,1 281.6 ms < 1,2,4,4,4,1 282.5 < 1,2,3,3,3,2,1
-  // 283.6 < 1,4,6,4,1 284.6 < 1,3,4,4,4 286.5 < 1,2,2,2,1 288.0; the ramp also wins at
+  // c5 (tools/sweep_chunks.sh): 1,3,5,5,3,1 276.1 ms < 1,3,4,4,3,1 277.0 < 1,4,6,6,4,1 277.7
+  // < 1,2,4,4,4,1 < 1,6,8,8,6,2 281.7 < 1,4,6,4,1 < 1,3,4,4,4 < 1,2,2,2,1; the ramp also wins at
   // 1.25M pairs (41 vs 52 ms one-pass).  Below 2^20 pairs one pass is as fast or faster
   // (c2 2.2 vs 2.4 ms with 3 chunks; 131k-524k pairs equal; tools/sweep_chunks_*.sh).
   if (ok && ctx->pipeline != 1) {
     std::vector<int> w;
     if (ctx->pipeline > 1 && in->num_batches >= 2 * ctx->pipeline) w.assign(ctx->pipeline, 1);
-    else if (ctx->pipeline == 0 && pairs >= kBigCallPairs) w = {1, 3, 4, 4, 3, 1};
+    else if (ctx->pipeline == 0 && pairs >= kBigCallPairs) w = {1, 3, 5, 5, 3, 1};
     if (const char* env = getenv("PHMM_CHUNK_WEIGHTS"); env && !w.empty()) {   // experiments
       std::vector<int> ew;
       for (const char* p = env; *p;) {
