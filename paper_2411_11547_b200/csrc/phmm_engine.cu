@@ -836,9 +836,11 @@ static int prepare_impl(phmm_ctx* ctx, const phmm_input* in, const phmm_options*
   for (const PlanPart& pp : parts) nunits_all += (int64_t)pp.su.size();
   ctx->su_all.resize(nunits_all);
   ctx->su_bin.resize(nunits_all);
+  std::vector<int64_t> part_off(nparts + 1, 0);
   {
     int64_t o = 0;
-    for (const PlanPart& pp : parts) {
+    for (int ip = 0; ip < nparts; ++ip) {
+      const PlanPart& pp = parts[ip];
       for (int key : pp.keys)
         if (sbin_index[key] < 0) {
           sbin_index[key] = (int)ctx->sbins.size();
@@ -846,9 +848,9 @@ static int prepare_impl(phmm_ctx* ctx, const phmm_input* in, const phmm_options*
         }
       for (int key : pp.keys)
         ctx->sbins[sbin_index[key]].max_rows = std::max(ctx->sbins[sbin_index[key]].max_rows, pp.key_rows[key]);
-      std::copy(pp.su.begin(), pp.su.end(), ctx->su_all.begin() + o);
-      for (size_t i = 0; i < pp.key.size(); ++i) ctx->su_bin[o + i] = (uint8_t)sbin_index[pp.key[i]];
+      part_off[ip] = o;
       o += (int64_t)pp.su.size();
+      part_off[ip + 1] = o;
       for (int x = 0; x < kNumExactP; ++x) slot_pairs[x] += pp.slot_pairs[x];
       for (int g = 0; g < 8; ++g) { r64_pairs[g] += pp.r64_pairs[g]; rx32_pairs[g] += pp.rx32_pairs[g]; }
       long64 |= pp.long64; long32 |= pp.long32;
@@ -857,30 +859,65 @@ static int prepare_impl(phmm_ctx* ctx, const phmm_input* in, const phmm_options*
       max_n = std::max(max_n, pp.max_n);
     }
   }
+  // the parts' units and bin ids, concatenated in batch order (on the pool)
+  auto copy_part = [&](int ip) {
+    const PlanPart& pp = parts[ip];
+    std::copy(pp.su.begin(), pp.su.end(), ctx->su_all.begin() + part_off[ip]);
+    for (size_t i = 0; i < pp.key.size(); ++i) ctx->su_bin[part_off[ip] + i] = (uint8_t)sbin_index[pp.key[i]];
+  };
+  if (nparts == 1) {
+    copy_part(0);
+  } else {
+    std::function<void(int)> task = copy_part;
+    pool->run(nparts, task);
+  }
   ctx->max_n = max_n;
   trace.mark("merge");
-  // LPT order per tiling: one stable counting sort on (bin, descending lane rows)
+  // LPT order per tiling: one stable counting sort on (bin, descending lane rows), over the
+  // parts in parallel (per-part histograms, key-major then part-ordered offsets)
   const int nsbins = (int)ctx->sbins.size();
   const int64_t nsunits = (int64_t)ctx->su_all.size();
   std::vector<int> bmax(nsbins, 0), bbase(nsbins + 1, 0);
-  for (int64_t i = 0; i < nsunits; ++i) {
-    const StreamUnit& u = ctx->su_all[i];
-    bmax[ctx->su_bin[i]] = std::max(bmax[ctx->su_bin[i]], std::max(u.rowsA, u.rowsB));
-  }
+  for (int bi = 0; bi < nsbins; ++bi) bmax[bi] = ctx->sbins[bi].max_rows;   // longest lane of the bin
   for (int bi = 0; bi < nsbins; ++bi) bbase[bi + 1] = bbase[bi] + bmax[bi] + 1;
   auto key = [&](int64_t i) {
     const StreamUnit& u = ctx->su_all[i];
     const int bi = ctx->su_bin[i];
     return bbase[bi] + bmax[bi] - std::max(u.rowsA, u.rowsB);
   };
-  ctx->su_cnt.assign(bbase[nsbins] + 1, 0);
-  for (int64_t i = 0; i < nsunits; ++i) ++ctx->su_cnt[key(i) + 1];
-  for (int k = 1; k <= bbase[nsbins]; ++k) ctx->su_cnt[k] += ctx->su_cnt[k - 1];
+  const int nkeys = bbase[nsbins];
+  const int nsort = nparts == 1 ? 1 : std::min(nparts, pool->size() + 1);
+  std::vector<int64_t> scut(nsort + 1);
+  for (int i = 0; i <= nsort; ++i) scut[i] = nsunits * i / nsort;
+  std::vector<std::vector<int64_t>> hist(nsort);
+  auto count_part = [&](int ip) {
+    hist[ip].assign(nkeys, 0);
+    for (int64_t i = scut[ip]; i < scut[ip + 1]; ++i) ++hist[ip][key(i)];
+  };
+  if (nsort == 1) count_part(0);
+  else { std::function<void(int)> task = count_part; pool->run(nsort, task); }
+  ctx->su_cnt.assign(nkeys + 1, 0);           // su_cnt[k]: first slot of key k
+  {
+    int64_t o = 0;
+    for (int k = 0; k < nkeys; ++k) {
+      ctx->su_cnt[k] = (int)o;
+      for (int ip = 0; ip < nsort; ++ip) {
+        const int64_t c = hist[ip][k];
+        hist[ip][k] = o;                        // this part's first slot for key k
+        o += c;
+      }
+    }
+    ctx->su_cnt[nkeys] = (int)o;
+  }
   for (int bi = 0; bi < nsbins; ++bi) ctx->sbins[bi].dev_off = ctx->su_cnt[bbase[bi]];
   for (int bi = 0; bi < nsbins; ++bi)
     ctx->sbins[bi].count = (bi + 1 < nsbins ? ctx->su_cnt[bbase[bi + 1]] : nsunits) - ctx->sbins[bi].dev_off;
   ctx->h_sunits.resize(nsunits);
-  for (int64_t i = 0; i < nsunits; ++i) ctx->h_sunits[ctx->su_cnt[key(i)]++] = ctx->su_all[i];
+  auto scatter_part = [&](int ip) {
+    for (int64_t i = scut[ip]; i < scut[ip + 1]; ++i) ctx->h_sunits[hist[ip][key(i)]++] = ctx->su_all[i];
+  };
+  if (nsort == 1) scatter_part(0);
+  else { std::function<void(int)> task = scatter_part; pool->run(nsort, task); }
   // launch order of the concurrent tiling bins: largest total work first, so the small
   // bins fill the tails of the large ones
   {
