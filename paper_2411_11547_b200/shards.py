@@ -245,6 +245,13 @@ class HostGather:
             self.shm = shared_memory.SharedMemory(name=name, create=True, size=size)
         else:
             self.shm = shared_memory.SharedMemory(name=name)
+            # the creating rank owns the segment (it unlinks it); attaching ranks must not
+            # have Python's resource tracker unlink it, or warn about a "leak", at exit
+            try:
+                from multiprocessing import resource_tracker
+                resource_tracker.unregister(self.shm._name, "shared_memory")
+            except (ImportError, AttributeError, KeyError):
+                pass
         self.owner = create
         self.scores = np.ndarray((num_pairs,), np.float64, buffer=self.shm.buf, offset=0)
         self.status = np.ndarray((num_pairs,), np.uint8, buffer=self.shm.buf, offset=num_pairs * 8)
