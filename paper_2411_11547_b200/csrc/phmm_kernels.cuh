@@ -421,6 +421,16 @@ template <bool F64, int K> struct EChunk {
                                          typename std::conditional<K % 4 == 0, float4, float2>::type>::type;
   static constexpr int width = F64 ? (K % 2 == 0 ? 2 : 1) : (K % 4 == 0 ? 4 : 2);
 };
+// FP32 pairs: the flush as a packed multiply by {v >= thr} in {1, 0} (FSET + FSET + FMUL2
+// instead of two compare-and-selects); exact because the values are finite and
+// non-negative, and harmless when ptxas fuses the product into a later packed add
+// (1*v + x and 0*v + x round like v + x and x)
+__device__ __forceinline__ float2 flush2(float2 v, float thr) {
+  float mx, my;
+  asm("set.ge.f32.f32 %0, %1, %2;" : "=f"(mx) : "f"(v.x), "f"(thr));
+  asm("set.ge.f32.f32 %0, %1, %2;" : "=f"(my) : "f"(v.y), "f"(thr));
+  return __fmul2_rn(v, make_float2(mx, my));
+}
 template <class V, class S> __device__ __forceinline__ V flush2(V v, S thr) {
   v.x = v.x >= thr ? v.x : (S)0;            // reference store flush (wavefront.py:134-136)
   v.y = v.y >= thr ? v.y : (S)0;
