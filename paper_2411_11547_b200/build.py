@@ -66,7 +66,7 @@ def build_flatten(force: bool = False, verbose: bool = False) -> str:
         return FLAT_OUT
     os.makedirs(os.path.dirname(FLAT_OUT), exist_ok=True)
     import numpy
-    cmd = ["g++", "-O2", "-std=c++17", "-shared", "-fPIC", "-I", sysconfig.get_paths()["include"],
+    cmd = ["g++", "-O2", "-std=c++17", "-shared", "-fPIC", "-pthread", "-I", sysconfig.get_paths()["include"],
            "-I", numpy.get_include(), "-o", FLAT_OUT + ".tmp", FLAT_SRC]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)

@@ -21,6 +21,8 @@
 
 #include <cstdint>
 #include <cstring>
+#include <algorithm>
+#include <thread>
 #include <vector>
 
 namespace {
@@ -159,17 +161,24 @@ PyObject* flatten(PyObject*, PyObject* arg) {
       char* d[5];
       for (int x = 0; x < 5; ++x) d[x] = PyByteArray_AS_STRING(tr[x]);
       const size_t R = rlen.size();
-      Py_BEGIN_ALLOW_THREADS
-      for (size_t r = 0; r < R; ++r)
-        for (int x = 0; x < 5; ++x) {
-          memcpy(d[x], rv.p[5 * r + x], (size_t)rlen[r]);
-          d[x] += rlen[r];
-        }
       char* dh = PyByteArray_AS_STRING(hb);
-      for (size_t h = 0; h < hlen.size(); ++h) {
-        memcpy(dh, hv.p[h], (size_t)hlen[h]);
-        dh += hlen[h];
-      }
+      Py_BEGIN_ALLOW_THREADS
+      // the copy (and the page faults of the fresh buffers) on a few threads, over read /
+      // haplotype ranges; each range's destination offset is a prefix of the lengths
+      std::vector<int64_t> roffs(R + 1, 0), hoffs(hlen.size() + 1, 0);
+      for (size_t r = 0; r < R; ++r) roffs[r + 1] = roffs[r] + rlen[r];
+      for (size_t h = 0; h < hlen.size(); ++h) hoffs[h + 1] = hoffs[h] + hlen[h];
+      const int nt = (int)std::max<int64_t>(1, std::min<int64_t>(8, (RL + HL) >> 22));   // >= 4 MB per thread
+      auto work = [&](int i) {
+        for (size_t r = R * i / nt; r < R * (i + 1) / nt; ++r)
+          for (int x = 0; x < 5; ++x) memcpy(d[x] + roffs[r], rv.p[5 * r + x], (size_t)rlen[r]);
+        const size_t H = hlen.size();
+        for (size_t h = H * i / nt; h < H * (i + 1) / nt; ++h) memcpy(dh + hoffs[h], hv.p[h], (size_t)hlen[h]);
+      };
+      std::vector<std::thread> th;
+      for (int i = 1; i < nt; ++i) th.emplace_back(work, i);
+      work(0);
+      for (auto& t : th) t.join();
       Py_END_ALLOW_THREADS
       out = Py_BuildValue("(NNNNNNNNNN)", tr[0], tr[1], tr[2], tr[3], tr[4],
                           new_bytes(rlen.data(), (Py_ssize_t)(rlen.size() * 8)), hb,
