@@ -370,3 +370,20 @@ def test_c3_device_scratch_is_small(engine):
     per_pair = 200 * flat.num_pairs
     assert ctx.device_bytes() < flat.nbytes() + per_pair + (64 << 20), ctx.device_bytes()
     ctx.close()
+
+
+@pytest.mark.parametrize("n", [2, 3, 5, 8])
+def test_pipeline_depths_bit_identical(engine, n):
+    """phmm_set_pipeline(n): n equal chunk contexts give bit-identical results to the one
+    pass (pairs are independent), with the FP64 retry and the guard band in play."""
+    flat = datagen.workload("c3", num_batches=40)
+    want, wst, _ = engine.score(flat, F32, _native.FLAG_RETRY_F64)   # < 2^20 pairs: one pass
+    ctx = _native.Context(0)
+    ctx.set_pipeline(n)
+    got, gst, st = ctx.score(flat, F32, _native.FLAG_RETRY_F64)
+    assert np.array_equal(got, want, equal_nan=True) and np.array_equal(gst, wst)
+    assert st.num_pairs == flat.num_pairs and st.device_ms > 0
+    ctx.set_pipeline(1)                                            # never pipeline
+    got1, gst1, _ = ctx.score(flat, F32, _native.FLAG_RETRY_F64)
+    assert np.array_equal(got1, want, equal_nan=True) and np.array_equal(gst1, wst)
+    ctx.close()
