@@ -541,6 +541,12 @@ def main():
                      "frac_at_sampled_clock": (fast_gcups / (nsm * FP32_LANES_PER_SM * clk["sm_mhz"] * 1e6 / OPS_PER_CELL / 1e9)
                                                if clk.get("sm_mhz") else None),
                      "whole_step_frac": value / ws / peak,
+                     # transparency only: the flop form, 11 flops per cell
+                     # against 2 x 128 lanes x f_SM (not the denominator: 5 of the 8 ops
+                     # are not FMAs); microbench FFMA2 peaks at 106 lanes/clk/SM, so 128
+                     # stays the lane peak (profiles/r02_microbench_pipes.txt)
+                     "flop_form": {"peak_gcups": nsm * 2 * FP32_LANES_PER_SM * sm_max * 1e6 / 11 / 1e9,
+                                   "frac": fast_gcups / (nsm * 2 * FP32_LANES_PER_SM * sm_max * 1e6 / 11 / 1e9)},
                      "fast_share_of_step": float(np.mean(fast_ms) / np.mean(dev_ms)),
                      "phases_ms": dict(zip(PHASES, ph_mean.tolist())),
                      "fp64_retry": {"pairs": int(retried.sum()), "cells": retry_cells,
