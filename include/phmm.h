@@ -138,6 +138,12 @@ int phmm_set_device_budget(phmm_ctx* ctx, int64_t bytes);
  * pass.  n in 2..8 pipelines every call of >= 2n batches through n equal chunks (results
  * are identical either way: pairs are independent).  1 = never pipeline. */
 int phmm_set_pipeline(phmm_ctx* ctx, int n);
+/* Page-lock (pin) / release a caller-owned host buffer so the uploads from it are DMA
+ * transfers that overlap the host planning (cudaHostRegister).  For buffers a caller
+ * reuses across calls (the Python run() flattening arena); pinned-allocated buffers need
+ * neither. */
+int phmm_pin_host(void* ptr, int64_t bytes);
+int phmm_unpin_host(void* ptr);
 /* Device bytes currently allocated by the context and its chunk contexts. */
 int phmm_device_bytes(const phmm_ctx* ctx, int64_t* bytes);
 

@@ -63,7 +63,7 @@ class PhmmStats(ctypes.Structure):
 EXPORTS = ("phmm_abi_version", "phmm_create", "phmm_destroy", "phmm_last_error", "phmm_score",
            "phmm_prepare", "phmm_execute", "phmm_fetch", "phmm_fast_geometry", "phmm_last_timing",
            "phmm_last_phases", "phmm_forward_matrices", "phmm_set_device_budget", "phmm_device_bytes",
-           "phmm_set_pipeline")
+           "phmm_set_pipeline", "phmm_pin_host", "phmm_unpin_host")
 
 _lib = None
 
@@ -107,6 +107,10 @@ def load():
     L.phmm_forward_matrices.restype = ctypes.c_int
     L.phmm_set_device_budget.argtypes = [_vp, _i64]
     L.phmm_set_device_budget.restype = ctypes.c_int
+    L.phmm_pin_host.argtypes = [_vp, _i64]
+    L.phmm_pin_host.restype = ctypes.c_int
+    L.phmm_unpin_host.argtypes = [_vp]
+    L.phmm_unpin_host.restype = ctypes.c_int
     L.phmm_set_pipeline.argtypes = [_vp, _i32]
     L.phmm_set_pipeline.restype = ctypes.c_int
     L.phmm_device_bytes.argtypes = [_vp, ctypes.POINTER(_i64)]
@@ -285,3 +289,18 @@ def context(device: int = 0) -> Context:
             ctx = Context(device)
             _contexts[device] = ctx
         return ctx
+
+
+def pin_host(arr: np.ndarray) -> bool:
+    """Page-lock a host array for DMA uploads (phmm_pin_host); False when unavailable."""
+    try:
+        return load().phmm_pin_host(arr.ctypes.data, arr.nbytes) == SUCCESS
+    except (OSError, EngineUnavailableError):
+        return False
+
+
+def unpin_host(arr: np.ndarray) -> None:
+    try:
+        load().phmm_unpin_host(arr.ctypes.data)
+    except (OSError, EngineUnavailableError):
+        pass

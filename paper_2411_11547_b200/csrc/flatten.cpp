@@ -74,11 +74,35 @@ struct Spans {
   }
 };
 
+// Instances of a class with __slots__ (the package's frozen slotted dataclasses) keep each
+// field at a fixed offset: resolve the member descriptors once per type and read the
+// fields directly (no dict, no attribute-lookup machinery).  ok = false: not slotted.
+struct SlotOffsets {
+  PyTypeObject* tp = nullptr;
+  bool ok = false;
+  Py_ssize_t off[5] = {0, 0, 0, 0, 0};
+  void resolve(PyTypeObject* t, PyObject* const* names, int n) {
+    tp = t;
+    ok = true;
+    for (int x = 0; x < n && ok; ++x) {
+      PyObject* d = _PyType_Lookup(t, names[x]);          // borrowed
+      ok = d && Py_IS_TYPE(d, &PyMemberDescr_Type) &&
+           reinterpret_cast<PyMemberDescrObject*>(d)->d_member->type == Py_T_OBJECT_EX;
+      if (ok) off[x] = reinterpret_cast<PyMemberDescrObject*>(d)->d_member->offset;
+    }
+  }
+  // borrowed field x of obj (nullptr: unset)
+  PyObject* get(PyObject* obj, int x) const { return *reinterpret_cast<PyObject**>(reinterpret_cast<char*>(obj) + off[x]); }
+};
+
 PyObject* new_bytes(const void* src, Py_ssize_t n) {
   return PyByteArray_FromStringAndSize(static_cast<const char*>(src), n);
 }
 
-PyObject* flatten(PyObject*, PyObject* arg) {
+PyObject* flatten(PyObject*, PyObject* args) {
+  PyObject* arg = nullptr;
+  PyObject* alloc_fn = Py_None;   // optional alloc(RL, HL) -> 6 writable buffers (reused arena)
+  if (!PyArg_ParseTuple(args, "O|O", &arg, &alloc_fn)) return nullptr;
   PyObject* seq = PySequence_Fast(arg, "batches must be a sequence");
   if (!seq) return nullptr;
   const Py_ssize_t B = PySequence_Fast_GET_SIZE(seq);
@@ -114,6 +138,7 @@ PyObject* flatten(PyObject*, PyObject* arg) {
   }
   // pass 2: buffer views and lengths
   Spans rv(ok ? 5 * nreads : 0), hv(ok ? nhaps : 0);
+  SlotOffsets rslots, hslots;
   rlen.reserve(nreads);
   hlen.reserve(nhaps);
   for (Py_ssize_t b = 0; ok && b < B; ++b) {
@@ -122,15 +147,23 @@ PyObject* flatten(PyObject*, PyObject* arg) {
     for (Py_ssize_t r = 0; ok && r < bre[b]; ++r) {
       PyObject* rd = PySequence_Fast_GET_ITEM(rs, r);
       const size_t first = rv.n.size();
-      // instance __dict__ lookups (a frozen dataclass stores its fields there) instead of
-      // five generic attribute lookups; anything else -> getattr
-      PyObject* dict = PyObject_GenericGetDict(rd, nullptr);
-      if (!dict) PyErr_Clear();
-      for (int x = 0; ok && x < 5; ++x) {
-        PyObject* a = dict ? PyDict_GetItemWithError(dict, kNames[x]) : nullptr;
-        ok = a ? rv.take(a, kTracks[x]) : (!PyErr_Occurred() && rv.get(rd, kNames[x], kTracks[x]));
+      if (Py_TYPE(rd) != rslots.tp) rslots.resolve(Py_TYPE(rd), kNames, 5);
+      if (rslots.ok) {                // slotted record: fields at fixed offsets
+        for (int x = 0; ok && x < 5; ++x) {
+          PyObject* a = rslots.get(rd, x);
+          ok = a ? rv.take(a, kTracks[x]) : rv.get(rd, kNames[x], kTracks[x]);
+        }
+      } else {
+        // instance __dict__ lookups (a frozen dataclass stores its fields there) instead of
+        // five generic attribute lookups; anything else -> getattr
+        PyObject* dict = PyObject_GenericGetDict(rd, nullptr);
+        if (!dict) PyErr_Clear();
+        for (int x = 0; ok && x < 5; ++x) {
+          PyObject* a = dict ? PyDict_GetItemWithError(dict, kNames[x]) : nullptr;
+          ok = a ? rv.take(a, kTracks[x]) : (!PyErr_Occurred() && rv.get(rd, kNames[x], kTracks[x]));
+        }
+        Py_XDECREF(dict);
       }
-      Py_XDECREF(dict);
       if (!ok) break;
       const Py_ssize_t m = rv.n[first];
       for (int x = 1; ok && x < 5; ++x)
@@ -143,7 +176,10 @@ PyObject* flatten(PyObject*, PyObject* arg) {
       RL += m;
     }
     for (Py_ssize_t h = 0; ok && h < bha[b]; ++h) {
-      ok = hv.get(PySequence_Fast_GET_ITEM(hs, h), kNames[0], kTracks[0]);
+      PyObject* hp = PySequence_Fast_GET_ITEM(hs, h);
+      if (Py_TYPE(hp) != hslots.tp) hslots.resolve(Py_TYPE(hp), kNames, 1);
+      PyObject* a = hslots.ok ? hslots.get(hp, 0) : nullptr;
+      ok = a ? hv.take(a, kTracks[0]) : hv.get(hp, kNames[0], kTracks[0]);
       if (ok) {
         hlen.push_back(hv.n.back());
         HL += hlen.back();
@@ -152,16 +188,43 @@ PyObject* flatten(PyObject*, PyObject* arg) {
   }
   PyObject* out = nullptr;
   if (ok) {
-    PyObject* tr[5];
-    for (int x = 0; x < 5; ++x) tr[x] = PyByteArray_FromStringAndSize(nullptr, RL);
-    PyObject* hb = PyByteArray_FromStringAndSize(nullptr, HL);
-    bool alloc = hb != nullptr;
-    for (int x = 0; x < 5; ++x) alloc = alloc && tr[x] != nullptr;
+    PyObject* tr[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+    PyObject* hb = nullptr;
+    char* d[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+    char* dh = nullptr;
+    Py_buffer ab[6];
+    int nab = 0;
+    bool alloc = true;
+    if (alloc_fn != Py_None) {        // caller's arena: already-faulted pages, no fresh allocation
+      PyObject* got = PyObject_CallFunction(alloc_fn, "nn", (Py_ssize_t)RL, (Py_ssize_t)HL);
+      PyObject* fast = got ? PySequence_Fast(got, "alloc must return a sequence") : nullptr;
+      Py_XDECREF(got);
+      alloc = fast && PySequence_Fast_GET_SIZE(fast) == 6;
+      for (int x = 0; alloc && x < 6; ++x) {
+        PyObject* o = PySequence_Fast_GET_ITEM(fast, x);
+        alloc = PyObject_GetBuffer(o, &ab[x], PyBUF_WRITABLE | PyBUF_C_CONTIGUOUS) == 0;
+        if (alloc) {
+          ++nab;
+          alloc = ab[x].len >= (x < 5 ? RL : HL);
+          if (!alloc) PyErr_SetString(PyExc_ValueError, "alloc returned a buffer too small");
+          Py_INCREF(o);
+          if (x < 5) { tr[x] = o; d[x] = static_cast<char*>(ab[x].buf); }
+          else { hb = o; dh = static_cast<char*>(ab[x].buf); }
+        }
+      }
+      Py_XDECREF(fast);
+    } else {
+      for (int x = 0; x < 5; ++x) tr[x] = PyByteArray_FromStringAndSize(nullptr, RL);
+      hb = PyByteArray_FromStringAndSize(nullptr, HL);
+      alloc = hb != nullptr;
+      for (int x = 0; x < 5; ++x) alloc = alloc && tr[x] != nullptr;
+      if (alloc) {
+        for (int x = 0; x < 5; ++x) d[x] = PyByteArray_AS_STRING(tr[x]);
+        dh = PyByteArray_AS_STRING(hb);
+      }
+    }
     if (alloc) {
-      char* d[5];
-      for (int x = 0; x < 5; ++x) d[x] = PyByteArray_AS_STRING(tr[x]);
       const size_t R = rlen.size();
-      char* dh = PyByteArray_AS_STRING(hb);
       Py_BEGIN_ALLOW_THREADS
       // the copy (and the page faults of the fresh buffers) on a few threads, over read /
       // haplotype ranges; each range's destination offset is a prefix of the lengths
@@ -190,6 +253,7 @@ PyObject* flatten(PyObject*, PyObject* arg) {
       Py_XDECREF(hb);
       if (!PyErr_Occurred()) PyErr_NoMemory();
     }
+    for (int x = 0; x < nab; ++x) PyBuffer_Release(&ab[x]);
   }
   for (PyObject* o : keep) Py_DECREF(o);
   Py_DECREF(seq);
@@ -197,7 +261,8 @@ PyObject* flatten(PyObject*, PyObject* arg) {
 }
 
 PyMethodDef kMethods[] = {
-    {"flatten", flatten, METH_O, "flatten(batches) -> 10 bytearrays (see flatten.cpp)"},
+    {"flatten", flatten, METH_VARARGS,
+     "flatten(batches, alloc=None) -> 10 buffers (see flatten.cpp); alloc(RL, HL) may supply the 6 data buffers"},
     {nullptr, nullptr, 0, nullptr}};
 
 PyModuleDef kModule = {PyModuleDef_HEAD_INIT, "_phmm_flatten", "Batch list -> flat arrays", -1, kMethods};

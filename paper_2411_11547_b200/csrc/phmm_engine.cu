@@ -1711,6 +1711,16 @@ int phmm_set_pipeline(phmm_ctx* ctx, int n) {
   return PHMM_SUCCESS;
 }
 
+int phmm_pin_host(void* ptr, int64_t bytes) {
+  if (!ptr || bytes <= 0) return PHMM_ERR_INVALID;
+  return cudaHostRegister(ptr, (size_t)bytes, cudaHostRegisterDefault) == cudaSuccess ? PHMM_SUCCESS : PHMM_ERR_CUDA;
+}
+
+int phmm_unpin_host(void* ptr) {
+  if (!ptr) return PHMM_ERR_INVALID;
+  return cudaHostUnregister(ptr) == cudaSuccess ? PHMM_SUCCESS : PHMM_ERR_CUDA;
+}
+
 int phmm_device_bytes(const phmm_ctx* ctx, int64_t* bytes) {
   if (!ctx || !bytes) return PHMM_ERR_INVALID;
   auto one = [](const phmm_ctx* c) -> int64_t {

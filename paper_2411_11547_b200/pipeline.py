@@ -30,6 +30,7 @@ BudgetError (partition.py:104-112).
 """
 from __future__ import annotations
 
+import threading
 import time
 from dataclasses import dataclass, field
 
@@ -37,7 +38,7 @@ import numpy as np
 
 from . import _native
 from .errors import InvalidMeasurementError
-from .model import FlatBatches, default_configs
+from .model import FlatArena, FlatBatches, default_configs
 from .partition import DEFAULT_BUDGET_BYTES, check_budget, config_index
 
 _NOT_EXECUTED = ("config-too-small", "degenerate-transition", "data")
@@ -65,6 +66,42 @@ class RunReport:
     errors: list = field(default_factory=list)
     retried: list = field(default_factory=list)     # global ids rescued by the FP64 retry
     engine: dict = field(default_factory=dict)      # libphmm phmm_stats of the call
+
+
+_ARENAS = threading.local()
+
+
+class _PinnedArena(FlatArena):
+    """The flattening arena of run(), page-locked (phmm_pin_host) so the engine's uploads
+    from it are DMA transfers overlapping the host planning; re-pinned when it grows."""
+
+    def __init__(self):
+        super().__init__()
+        self._pinned = []
+
+    def alloc(self, read_bytes: int, hap_bytes: int):
+        old = (self._tracks, self._haps)
+        bufs = super().alloc(read_bytes, hap_bytes)
+        if self._tracks is not old[0] or self._haps is not old[1] or not self._pinned:
+            for a in self._pinned:
+                _native.unpin_host(a)
+            self._pinned = [a for a in (self._tracks, self._haps) if a.nbytes and _native.pin_host(a)]
+        return bufs
+
+    def __del__(self):
+        try:
+            for a in getattr(self, "_pinned", []):
+                _native.unpin_host(a)
+        except Exception:             # interpreter shutdown: the process releases the pages
+            pass
+
+
+def _arena() -> FlatArena:
+    """This thread's flattening scratch (run() holds its flat arrays only for the call)."""
+    a = getattr(_ARENAS, "arena", None)
+    if a is None:
+        a = _ARENAS.arena = _PinnedArena()
+    return a
 
 
 def config_tuples(configs):
@@ -128,7 +165,7 @@ def run(batches, configs=None, budget_bytes: int = DEFAULT_BUDGET_BYTES, workers
         raise ValueError("workers must be >= 1")
     if configs is None:
         configs = default_configs()
-    flat = batches if isinstance(batches, FlatBatches) else FlatBatches.from_batches(batches)
+    flat = batches if isinstance(batches, FlatBatches) else FlatBatches.from_batches(batches, _arena())
     check_budget(flat, configs, budget_bytes)
     n = flat.num_pairs
     t0 = time.perf_counter()
