@@ -1063,7 +1063,11 @@ static int prepare_impl(phmm_ctx* ctx, const phmm_input* in, const phmm_options*
   E.band_inline = ctx->d_counters.p + 16;
   // inline guard-band reruns are slow per pair (scalar exact recursion inside an FP32
   // warp): a budget per call, split between the chunk contexts of a pipelined call
-  E.band_budget = 2 * ctx->num_sms / std::max(1, ctx->budget_div);
+  static const int band_pct = [] {              // experiments: PHMM_BAND_INLINE (% of #SM per launch)
+    const char* e = getenv("PHMM_BAND_INLINE");
+    return e ? std::max(0, atoi(e)) : 200;
+  }();
+  E.band_budget = band_pct * ctx->num_sms / 100 / std::max(1, ctx->budget_div);
   // tilings that cannot get work (no streamed read of that width) stay null
   auto lists = [&](RetryLists& L, DBuf<StreamUnit>* u, int ng, DBuf<StreamHap>& h, unsigned geoms, int base,
                    const int64_t* gpairs) {
