@@ -1065,7 +1065,7 @@ static int prepare_impl(phmm_ctx* ctx, const phmm_input* in, const phmm_options*
   // warp): a budget per call, split between the chunk contexts of a pipelined call
   static const int band_pct = [] {              // experiments: PHMM_BAND_INLINE (% of #SM per launch)
     const char* e = getenv("PHMM_BAND_INLINE");
-    return e ? std::max(0, atoi(e)) : 200;
+    return e ? std::max(0, atoi(e)) : 50;       // c3 -1..2 %, c2 unchanged (was 200)
   }();
   E.band_budget = band_pct * ctx->num_sms / 100 / std::max(1, ctx->budget_div);
   // tilings that cannot get work (no streamed read of that width) stay null
