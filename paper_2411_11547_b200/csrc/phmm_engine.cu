@@ -70,7 +70,7 @@ template <class T> using PinnedVec = std::vector<T, PinnedAlloc<T>>;
 // Stream tiling tables per mode (k_stream_<mode>.cu); kFast32's first kNumFastGeoms entries
 // are the geometry table PHMM_FAST_GEOM ("PxK") selects from
 constexpr int kNumFastGeoms = 13;
-constexpr int kMaxTilings = 24;
+constexpr int kMaxTilings = 28;
 static_assert(kNumStreamFast32 <= kMaxTilings, "tiling table");
 const int kStreamTabN[4] = {kNumStreamFast32, kNumR64Geoms, kNumRX32Geoms, kNumR64Geoms};
 const StreamKernel* stream_tab(int mode) {

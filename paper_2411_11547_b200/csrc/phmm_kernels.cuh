@@ -406,8 +406,8 @@ template <> struct Lanes<true> {
   static __device__ __forceinline__ S thr() { return 0x1p-970; }
 };
 template <int L, class V> __device__ __forceinline__ auto& lane_ref(V& v) { return L == 0 ? v.x : v.y; }
-// emission-table chunks: float4 (4 positions, LDS.128) when K % 4 == 0, float2 (LDS.64)
-// for K = 10, 14; double2 in FP64 (double for K = 7)
+// emission-table chunks: float4 (4 positions, LDS.128) when K % 4 == 0 and for odd K (the
+// last chunk padded), float2 (LDS.64) for K = 10, 14; double2 in FP64 (double for K = 7)
 __device__ __forceinline__ float ev_comp(const float4& v, int i) { return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w; }
 __device__ __forceinline__ float ev_comp(const float2& v, int i) { return i == 0 ? v.x : v.y; }
 __device__ __forceinline__ double ev_comp(const double2& v, int i) { return i == 0 ? v.x : v.y; }
@@ -417,9 +417,11 @@ __device__ __forceinline__ void ev_pack(float2& e, const float* l) { e = make_fl
 __device__ __forceinline__ void ev_pack(double2& e, const double* l) { e = make_double2(l[0], l[1]); }
 __device__ __forceinline__ void ev_pack(double& e, const double* l) { e = l[0]; }
 template <bool F64, int K> struct EChunk {
+  static constexpr bool F4 = !F64 && (K % 4 == 0 || K % 2 == 1);   // odd K: last chunk padded
   using type = typename std::conditional<F64, typename std::conditional<K % 2 == 0, double2, double>::type,
-                                         typename std::conditional<K % 4 == 0, float4, float2>::type>::type;
-  static constexpr int width = F64 ? (K % 2 == 0 ? 2 : 1) : (K % 4 == 0 ? 4 : 2);
+                                         typename std::conditional<F4, float4, float2>::type>::type;
+  static constexpr int width = F64 ? (K % 2 == 0 ? 2 : 1) : (F4 ? 4 : 2);
+  static constexpr int chunks = (K + width - 1) / width;
 };
 // FP32 pairs: the flush as a packed multiply by {v >= thr} in {1, 0} (FSET + FSET + FMUL2
 // instead of two compare-and-selects); exact because the values are finite and
@@ -514,9 +516,9 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
   using V = typename A::V;
   using EV = typename EChunk<F64, K>::type;
   constexpr int EW = EChunk<F64, K>::width;
-  constexpr int W = P * K, G = 32 / P, KE = K / EW;
+  constexpr int W = P * K, G = 32 / P, KE = EChunk<F64, K>::chunks;
   constexpr int CB = kStreamCodeBytesPerCta / (4 * G);
-  static_assert(K % EW == 0 && K >= 4, "K multiple of the emission chunk");
+  static_assert(K >= 4 && (K % EW == 0 || (!F64 && !EXACT)), "padded emission chunks: fast FP32 only");
   constexpr unsigned FULL = 0xffffffffu;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double* s_lut = reinterpret_cast<double*>(smem_raw);
@@ -648,6 +650,11 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
       for (int kk = 0; kk < EW; ++kk) {
         const int k = ke * EW + kk;
         const int p = q * W + t * K + k;
+        if (k >= K) {                                   // padding of the last chunk (odd K)
+#pragma unroll
+          for (int c = 0; c < 5; ++c) lam[c][kk] = 0;
+          continue;
+        }
         M[k] = zero2; I[k] = zero2; D[k] = zero2;
         if (p < Lp) {                                   // left padding
           if constexpr (EXACT) { al[k] = 0; be[k] = 0; dl[k] = 0; ep[k] = 1; zt[k] = 0; }
@@ -1026,6 +1033,7 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
 #pragma unroll
           for (int kk = 0; kk < EW; ++kk) {
             const int k = ke * EW + kk;
+            if (k >= K) continue;                       // padded chunk (odd K)
             const V mo = M[k], io = I[k], dold = D[k];
             D[k] = A::fma(ep[k], dold, mo);
             V x = A::fma(dl[k], pio, pmo);
@@ -1047,6 +1055,7 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
 #pragma unroll
           for (int kk = EW - 1; kk >= 0; --kk) {
             const int k = ke * EW + kk;
+            if (k >= K) continue;                       // padded chunk (odd K)
             const V pm = (k > 0) ? M[k - 1] : dgM;
             const V pi = (k > 0) ? I[k - 1] : dgI;
             const V pd = (k > 0) ? D[k - 1] : dgD;

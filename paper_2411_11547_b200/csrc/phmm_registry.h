@@ -30,18 +30,19 @@ void launch_stream_t(dim3 g, size_t smem, cudaStream_t s, const EngineDev& E, co
 }
 template <int MODE, int P, int K, bool STRIPES = false>
 StreamKernel SK() {
-  const size_t elem = ModeOf<MODE>::F64 ? sizeof(double) : sizeof(float);   // 5*K*P entries per slot
+  const size_t elem = ModeOf<MODE>::F64 ? sizeof(double) : sizeof(float);   // 5*Kp*P entries per slot
+  constexpr int Kp = EChunk<ModeOf<MODE>::F64, K>::chunks * EChunk<ModeOf<MODE>::F64, K>::width;   // K, padded
   // striped instantiations add the boundary-column ring: per sub-warp slot 3 x kColRing
   // two-lane values
   return StreamKernel{P, K, STRIPES ? 2 : StreamOcc<MODE, K>::value,
-                      96 * sizeof(double) + (size_t)4 * (32 / P) * 5 * K * P * elem + kStreamCodeBytesPerCta +
+                      96 * sizeof(double) + (size_t)4 * (32 / P) * 5 * Kp * P * elem + kStreamCodeBytesPerCta +
                           (STRIPES ? (size_t)4 * (32 / P) * 3 * kColRing * 2 * elem : 0),
                       (const void*)k_stream<MODE, P, K, STRIPES>, launch_stream_t<MODE, P, K, STRIPES>};
 }
 
 // tiling tables per mode (k_stream_<mode>.cu); kFast32's first 13 entries are the
 // geometry table PHMM_FAST_GEOM indexes
-constexpr int kNumStreamFast32 = 19;
+constexpr int kNumStreamFast32 = 23;
 const StreamKernel* stream_table_fast32();
 const StreamKernel* stream_table_fast64();     // kNumR64Geoms, indexed by r64_geom_for(m)
 const StreamKernel* stream_table_exact32();    // kNumRX32Geoms, indexed by rx32_geom_for(m)
