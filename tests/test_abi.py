@@ -56,6 +56,9 @@ def test_fast_geometry_is_host_only(lib):
         P, K, Q = _native.fast_geometry(m, 300)
         assert P * K * Q >= m + 1
     assert lib.phmm_fast_geometry(0, 5, None, None, None) == -1
+    # reads of 128-255 bases pad to a 16-row grid: odd-K tilings between the even ones
+    assert [_native.fast_geometry(m, 300)[:2] for m in (143, 175, 207, 239, 255)] == [
+        (16, 9), (16, 11), (16, 13), (16, 15), (16, 16)]
 
 
 def test_no_device_fails_loudly():

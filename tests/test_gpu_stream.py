@@ -116,8 +116,10 @@ def test_many_haplotypes_split_units_and_unbalanced_lanes(engine, rng):
 
 
 def test_every_tiling_width(engine, rng):
-    # read lengths across all single-stripe widths W = 16 .. 512 and their edges
-    ms = [1, 14, 15, 16, 31, 32, 47, 48, 63, 64, 95, 96, 127, 128, 191, 192, 255, 256, 383, 384, 511]
+    # read lengths across all single-stripe widths W = 16 .. 512 and their edges (143, 175,
+    # 207, 239: the odd-K tilings (16, 9 / 11 / 13 / 15) with a padded emission chunk)
+    ms = [1, 14, 15, 16, 31, 32, 47, 48, 63, 64, 95, 96, 127, 128, 143, 159, 175, 191, 192, 207, 223, 239,
+          255, 256, 383, 384, 511]
     flat = _flat(rng, [([m, max(1, m // 2)], [int(x) for x in rng.integers(50, 400, size=5)], "derived")
                        for m in ms])
     _check(engine, flat)
