@@ -407,20 +407,17 @@ template <> struct Lanes<true> {
 };
 template <int L, class V> __device__ __forceinline__ auto& lane_ref(V& v) { return L == 0 ? v.x : v.y; }
 // emission-table chunks: float4 (4 positions, LDS.128) when K % 4 == 0 and for odd K (the
-// last chunk padded), float2 (LDS.64) for K = 10, 14; double2 in FP64 (double for K = 7)
+// last chunk padded), float2 (LDS.64) for K = 10, 14; double2 in FP64 (odd K padded)
 __device__ __forceinline__ float ev_comp(const float4& v, int i) { return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w; }
 __device__ __forceinline__ float ev_comp(const float2& v, int i) { return i == 0 ? v.x : v.y; }
 __device__ __forceinline__ double ev_comp(const double2& v, int i) { return i == 0 ? v.x : v.y; }
-__device__ __forceinline__ double ev_comp(const double& v, int) { return v; }
 __device__ __forceinline__ void ev_pack(float4& e, const float* l) { e = make_float4(l[0], l[1], l[2], l[3]); }
 __device__ __forceinline__ void ev_pack(float2& e, const float* l) { e = make_float2(l[0], l[1]); }
 __device__ __forceinline__ void ev_pack(double2& e, const double* l) { e = make_double2(l[0], l[1]); }
-__device__ __forceinline__ void ev_pack(double& e, const double* l) { e = l[0]; }
 template <bool F64, int K> struct EChunk {
   static constexpr bool F4 = !F64 && (K % 4 == 0 || K % 2 == 1);   // odd K: last chunk padded
-  using type = typename std::conditional<F64, typename std::conditional<K % 2 == 0, double2, double>::type,
-                                         typename std::conditional<F4, float4, float2>::type>::type;
-  static constexpr int width = F64 ? (K % 2 == 0 ? 2 : 1) : (F4 ? 4 : 2);
+  using type = typename std::conditional<F64, double2, typename std::conditional<F4, float4, float2>::type>::type;
+  static constexpr int width = F64 ? 2 : (F4 ? 4 : 2);
   static constexpr int chunks = (K + width - 1) / width;
 };
 // FP32 pairs: the flush as a packed multiply by {v >= thr} in {1, 0} (FSET + FSET + FMUL2
@@ -518,7 +515,7 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
   constexpr int EW = EChunk<F64, K>::width;
   constexpr int W = P * K, G = 32 / P, KE = EChunk<F64, K>::chunks;
   constexpr int CB = kStreamCodeBytesPerCta / (4 * G);
-  static_assert(K >= 4 && (K % EW == 0 || (!F64 && !EXACT)), "padded emission chunks: fast FP32 only");
+  static_assert(K >= 4, "tiling");
   constexpr unsigned FULL = 0xffffffffu;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double* s_lut = reinterpret_cast<double*>(smem_raw);
