@@ -270,7 +270,7 @@ struct phmm_ctx {
   cudaEvent_t ev_up0 = nullptr, ev_up1 = nullptr;       // prepare: uploads + device validation
   cudaEvent_t ev_d0 = nullptr, ev_d1 = nullptr;         // fetch: D2H of the results
   cudaEvent_t ev_pre = nullptr;
-  static constexpr int kAux = 8;              // side streams: kernels of a phase run concurrently
+  static constexpr int kAux = 16;             // side streams: kernels of a phase run concurrently
   cudaStream_t aux[kAux] = {};
   cudaEvent_t ev_join[kAux] = {};
   std::string err;
