@@ -231,7 +231,7 @@ PyObject* flatten(PyObject*, PyObject* args) {
       std::vector<int64_t> roffs(R + 1, 0), hoffs(hlen.size() + 1, 0);
       for (size_t r = 0; r < R; ++r) roffs[r + 1] = roffs[r] + rlen[r];
       for (size_t h = 0; h < hlen.size(); ++h) hoffs[h + 1] = hoffs[h] + hlen[h];
-      const int nt = (int)std::max<int64_t>(1, std::min<int64_t>(8, (RL + HL) >> 22));   // >= 4 MB per thread
+      const int nt = (int)std::max<int64_t>(1, std::min<int64_t>(8, (5 * RL + HL) >> 21));   // >= 2 MB per thread
       auto work = [&](int i) {
         for (size_t r = R * i / nt; r < R * (i + 1) / nt; ++r)
           for (int x = 0; x < 5; ++x) memcpy(d[x] + roffs[r], rv.p[5 * r + x], (size_t)rlen[r]);

@@ -125,10 +125,15 @@ def score_flat(flat: FlatBatches, configs, retry_f64=False, exact=False, device=
             ctx.set_device_budget(0)
 
 
+# status kind -> error kind name, as an object array (one vectorised gather per call)
+_KIND_NAME_ARR = np.array([_native.KIND_NAMES.get(k) for k in range(256)], dtype=object)
+
+
 def errors_from_status(status: np.ndarray) -> list:
+    """[(global pair id, kind name)] of the failed pairs, in pair order."""
     kinds = status & _native.ST_KIND_MASK
     bad = np.flatnonzero(kinds != _native.ST_OK)
-    return [(int(g), _native.KIND_NAMES[int(kinds[g])]) for g in bad]
+    return list(zip(bad.tolist(), _KIND_NAME_ARR[kinds[bad]].tolist()))
 
 
 def _config_cells(flat: FlatBatches, configs, status: np.ndarray, device_s: float):
