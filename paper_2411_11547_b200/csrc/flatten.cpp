@@ -20,8 +20,13 @@
 #include <numpy/arrayobject.h>
 
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <deque>
 #include <thread>
 #include <vector>
 
@@ -33,14 +38,13 @@ namespace {
 struct Spans {
   std::vector<const char*> p;
   std::vector<Py_ssize_t> n;
-  std::vector<Py_buffer> views;
-  size_t nviews = 0;
-  explicit Spans(size_t cap) : views(cap) {
+  std::deque<Py_buffer> views;        // buffer-protocol exports only (stable addresses)
+  explicit Spans(size_t cap) {
     p.reserve(cap);
     n.reserve(cap);
   }
   ~Spans() {
-    for (size_t i = 0; i < nviews; ++i) PyBuffer_Release(&views[i]);
+    for (Py_buffer& v : views) PyBuffer_Release(&v);
   }
   bool get(PyObject* obj, PyObject* name, const char* attr) {
     PyObject* a = PyObject_GetAttr(obj, name);
@@ -61,9 +65,12 @@ struct Spans {
       if (!ok) PyErr_Format(PyExc_ValueError, "%s must be a contiguous 1-D array of 1-byte elements", attr);
       return ok;
     }
-    Py_buffer& b = views[nviews];
-    if (PyObject_GetBuffer(a, &b, PyBUF_C_CONTIGUOUS | PyBUF_FORMAT) != 0) return false;
-    ++nviews;
+    views.emplace_back();
+    Py_buffer& b = views.back();
+    if (PyObject_GetBuffer(a, &b, PyBUF_C_CONTIGUOUS | PyBUF_FORMAT) != 0) {
+      views.pop_back();
+      return false;
+    }
     if (b.itemsize != 1 || b.ndim != 1) {
       PyErr_Format(PyExc_ValueError, "%s must be a 1-D array of 1-byte elements", attr);
       return false;
@@ -114,6 +121,11 @@ PyObject* flatten(PyObject*, PyObject* args) {
     kReads = PyUnicode_InternFromString("reads");
     kHaps = PyUnicode_InternFromString("haps");
   }
+  // PHMM_TRACE=1: stage times on stderr
+  static const bool trace = getenv("PHMM_TRACE") != nullptr;
+  const auto t0 = std::chrono::steady_clock::now();
+  auto ms = [&]() { return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count(); };
+  double t_pass1 = 0, t_pass2 = 0, t_alloc = 0;
   std::vector<int64_t> bre(B), bha(B), rlen, hlen;
   int64_t RL = 0, HL = 0;
   bool ok = true;
@@ -136,16 +148,83 @@ PyObject* flatten(PyObject*, PyObject* args) {
     nreads += (size_t)bre[b];
     nhaps += (size_t)bha[b];
   }
+  // every read record in order: pass 2 prefetches the records and their track arrays a few
+  // reads ahead (the objects are scattered over the heap; the walk is latency bound)
+  std::vector<PyObject*> recs;
+  recs.reserve(nreads);
+  for (Py_ssize_t b = 0; ok && b < B; ++b) {
+    PyObject** it = PySequence_Fast_ITEMS(keep[2 * b]);
+    recs.insert(recs.end(), it, it + bre[b]);
+  }
+  t_pass1 = ms();
   // pass 2: buffer views and lengths
   Spans rv(ok ? 5 * nreads : 0), hv(ok ? nhaps : 0);
   SlotOffsets rslots, hslots;
   rlen.reserve(nreads);
   hlen.reserve(nhaps);
+  // Fast path: every read a record of one slotted type whose five tracks are 1-D contiguous
+  // 1-byte numpy arrays of equal length (the package's ReadRecord).  The views are plain
+  // field reads, taken on several threads while this thread keeps the GIL (no Python code
+  // runs meanwhile, so the objects cannot change); anything else -> the serial walk below,
+  // which also produces the error messages.
+  bool fast = false;
+  if (ok && nreads >= 4096) {
+    PyTypeObject* tp = Py_TYPE(recs[0]);
+    rslots.resolve(tp, kNames, 5);
+    if (rslots.ok) {
+      rv.p.resize(5 * nreads);
+      rv.n.resize(5 * nreads);
+      rlen.resize(nreads);
+      const int nt = (int)std::min<size_t>(8, nreads / 2048);
+      std::atomic<bool> bad{false};
+      std::vector<int64_t> part(nt, 0);
+      auto work = [&](int i) {
+        int64_t sum = 0;
+        for (size_t r = nreads * i / nt; r < nreads * (i + 1) / nt; ++r) {
+          PyObject* rd = recs[r];
+          if (Py_TYPE(rd) != tp || bad.load(std::memory_order_relaxed)) { bad = true; return; }
+          Py_ssize_t m = 0;
+          for (int x = 0; x < 5; ++x) {
+            PyObject* a = rslots.get(rd, x);
+            if (!a || Py_TYPE(a) != &PyArray_Type) { bad = true; return; }
+            PyArrayObject* arr = reinterpret_cast<PyArrayObject*>(a);
+            const Py_ssize_t n = PyArray_NDIM(arr) == 1 ? PyArray_DIM(arr, 0) : -1;
+            if (n < 0 || PyArray_ITEMSIZE(arr) != 1 || !PyArray_IS_C_CONTIGUOUS(arr) || (x > 0 && n != m)) {
+              bad = true;
+              return;
+            }
+            m = n;
+            rv.p[5 * r + x] = static_cast<const char*>(PyArray_DATA(arr));
+            rv.n[5 * r + x] = n;
+          }
+          rlen[r] = m;
+          sum += m;
+        }
+        part[i] = sum;
+      };
+      std::vector<std::thread> th;
+      for (int i = 1; i < nt; ++i) th.emplace_back(work, i);
+      work(0);
+      for (auto& t : th) t.join();
+      if (!bad) {
+        fast = true;
+        for (int64_t v : part) RL += v;
+      } else {
+        rv.p.clear();
+        rv.n.clear();
+        rlen.clear();
+      }
+    }
+  }
+  size_t gi = 0;                      // global read index
+  constexpr size_t kAhead = 8;
   for (Py_ssize_t b = 0; ok && b < B; ++b) {
-    PyObject* rs = keep[2 * b];
     PyObject* hs = keep[2 * b + 1];
-    for (Py_ssize_t r = 0; ok && r < bre[b]; ++r) {
-      PyObject* rd = PySequence_Fast_GET_ITEM(rs, r);
+    for (Py_ssize_t r = 0; ok && !fast && r < bre[b]; ++r, ++gi) {
+      PyObject* rd = recs[gi];
+      if (gi + 2 * kAhead < recs.size()) __builtin_prefetch(recs[gi + 2 * kAhead]);
+      if (gi + kAhead < recs.size() && rslots.ok && Py_TYPE(recs[gi + kAhead]) == rslots.tp)
+        for (int x = 0; x < 5; ++x) __builtin_prefetch(rslots.get(recs[gi + kAhead], x));
       const size_t first = rv.n.size();
       if (Py_TYPE(rd) != rslots.tp) rslots.resolve(Py_TYPE(rd), kNames, 5);
       if (rslots.ok) {                // slotted record: fields at fixed offsets
@@ -186,6 +265,7 @@ PyObject* flatten(PyObject*, PyObject* args) {
       }
     }
   }
+  t_pass2 = ms();
   PyObject* out = nullptr;
   if (ok) {
     PyObject* tr[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
@@ -223,15 +303,16 @@ PyObject* flatten(PyObject*, PyObject* args) {
         dh = PyByteArray_AS_STRING(hb);
       }
     }
+    t_alloc = ms();
     if (alloc) {
       const size_t R = rlen.size();
+      const int nt = (int)std::max<int64_t>(1, std::min<int64_t>(8, (5 * RL + HL) >> 21));   // >= 2 MB per thread
       Py_BEGIN_ALLOW_THREADS
       // the copy (and the page faults of the fresh buffers) on a few threads, over read /
       // haplotype ranges; each range's destination offset is a prefix of the lengths
       std::vector<int64_t> roffs(R + 1, 0), hoffs(hlen.size() + 1, 0);
       for (size_t r = 0; r < R; ++r) roffs[r + 1] = roffs[r] + rlen[r];
       for (size_t h = 0; h < hlen.size(); ++h) hoffs[h + 1] = hoffs[h] + hlen[h];
-      const int nt = (int)std::max<int64_t>(1, std::min<int64_t>(8, (5 * RL + HL) >> 21));   // >= 2 MB per thread
       auto work = [&](int i) {
         for (size_t r = R * i / nt; r < R * (i + 1) / nt; ++r)
           for (int x = 0; x < 5; ++x) memcpy(d[x] + roffs[r], rv.p[5 * r + x], (size_t)rlen[r]);
@@ -243,6 +324,9 @@ PyObject* flatten(PyObject*, PyObject* args) {
       work(0);
       for (auto& t : th) t.join();
       Py_END_ALLOW_THREADS
+      if (trace)
+        fprintf(stderr, "[flatten] reads %zu haps %zu: batches %.3f views %.3f alloc %.3f copy %.3f ms (%d threads)\n",
+                R, hlen.size(), t_pass1, t_pass2 - t_pass1, t_alloc - t_pass2, ms() - t_alloc, nt);
       out = Py_BuildValue("(NNNNNNNNNN)", tr[0], tr[1], tr[2], tr[3], tr[4],
                           new_bytes(rlen.data(), (Py_ssize_t)(rlen.size() * 8)), hb,
                           new_bytes(hlen.data(), (Py_ssize_t)(hlen.size() * 8)),

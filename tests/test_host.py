@@ -24,3 +24,15 @@ def test_errors_from_status_pairs_in_order():
     assert errors_from_status(st) == [(2, "numeric-overflow"), (5, "config-too-small"),
                                       (7, "degenerate-transition")]
     assert errors_from_status(np.zeros(0, np.uint8)) == []
+
+
+def test_native_flatten_falls_back_to_the_serial_walk():
+    # one record whose track is a bytes object (buffer protocol, not an ndarray): the
+    # threaded view pass bails out and the serial walk produces the same arrays
+    flat = datagen.workload("c2", num_batches=256)
+    batches = flat.to_batches()
+    rec = batches[200].reads[3]
+    object.__setattr__(rec, "ins_qual", bytes(np.asarray(rec.ins_qual)))
+    a = FlatBatches.from_batches(batches)
+    for k in FlatBatches.FIELDS:
+        assert np.array_equal(getattr(a, k), getattr(flat, k)), k
