@@ -273,6 +273,7 @@ struct phmm_ctx {
   static constexpr int kAux = 16;             // side streams: kernels of a phase run concurrently
   cudaStream_t aux[kAux] = {};
   cudaEvent_t ev_join[kAux] = {};
+  cudaEvent_t ev_x32[kAux] = {};              // execute: exact-FP32 post-pass launches done
   std::string err;
   std::vector<double> lut;
 
@@ -402,6 +403,7 @@ static int init_ctx(phmm_ctx* ctx, int device) {
   for (int a = 0; a < phmm_ctx::kAux; ++a) {
     CK(cudaStreamCreateWithFlags(&ctx->aux[a], cudaStreamNonBlocking));
     CK(cudaEventCreateWithFlags(&ctx->ev_join[a], cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&ctx->ev_x32[a], cudaEventDisableTiming));
   }
   CK(cudaEventCreate(&ctx->ev_start));
   CK(cudaEventCreate(&ctx->ev_fast0));
@@ -465,6 +467,7 @@ int phmm_destroy(phmm_ctx* ctx) {
   for (int a = 0; a < phmm_ctx::kAux; ++a) {
     if (ctx->aux[a]) { cudaStreamSynchronize(ctx->aux[a]); cudaStreamDestroy(ctx->aux[a]); }
     if (ctx->ev_join[a]) cudaEventDestroy(ctx->ev_join[a]);
+    if (ctx->ev_x32[a]) cudaEventDestroy(ctx->ev_x32[a]);
   }
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
@@ -1268,6 +1271,7 @@ int phmm_execute(phmm_ctx* ctx) {
     SKn.launch(dim3(grid), SKn.smem, ctx->aux[a], E, L.units[g], L.haps, L.unit_cap[g], L.count + g, work,
                col_off >= 0 ? ctx->d_colstream.p + col_off : nullptr, col_rows_for(SKn.P, ctx->max_n));
     ++launches;
+    return a;
   };
   for (int g = kNumR64Geoms - 1; g >= 0; --g)
     if (ctx->r64_geoms & (1u << g)) {
@@ -1276,17 +1280,41 @@ int phmm_execute(phmm_ctx* ctx) {
       post(SKn, E.r64, g, ctx->d_counters.p + kCtrR64Work + g, ctx->r64_col_off[g],
            str ? ctx->r64_grid : ctx->num_sms * occ_cap(SKn.occ));
     }
+  bool x32_on[phmm_ctx::kAux] = {};
   for (int g = kNumRX32Geoms - 1; g >= 0; --g)
     if (ctx->rx32_geoms & (1u << g)) {
       const bool str = ctx->rx32_col_off[g] >= 0;
       const StreamKernel& SKn = str ? striped_tab(kExact32) : stream_table_exact32()[g];
-      post(SKn, E.rx32, g, ctx->d_counters.p + kCtrRX32Work + g, ctx->rx32_col_off[g],
-           str ? ctx->rx32_grid : ctx->num_sms * occ_cap(SKn.occ));
+      x32_on[post(SKn, E.rx32, g, ctx->d_counters.p + kCtrRX32Work + g, ctx->rx32_col_off[g],
+                  str ? ctx->rx32_grid : ctx->num_sms * occ_cap(SKn.occ))] = true;
     }
+  // second-stage FP64 units (guard-band pairs whose exact rerun underflowed) depend only on
+  // the exact-FP32 stream kernels: single-stripe tilings start on a side stream as soon as
+  // those are done, beside the first-stage FP64 units (c5: their 3-4 ms tail overlapped);
+  // striped ones share their tiling's boundary columns with the first stage and run after it
+  bool r64b_side = false;
+  for (int g = 0; g < kNumR64Geoms; ++g) r64b_side |= E.r64b.units[g] && ctx->r64_col_off[g] < 0;
+  if (r64b_side) {
+    const int a = 0;                                // after the (short) per-pair exact FP32 list
+    for (int x = 0; x < phmm_ctx::kAux; ++x)
+      if (x32_on[x] && x != a) {
+        CK(cudaEventRecord(ctx->ev_x32[x], ctx->aux[x]));
+        CK(cudaStreamWaitEvent(ctx->aux[a], ctx->ev_x32[x], 0));
+      }
+    used[a] = true;
+    for (int g = kNumR64Geoms - 1; g >= 0; --g) {
+      if (!E.r64b.units[g] || ctx->r64_col_off[g] >= 0) continue;
+      const StreamKernel& SKn = stream_table_fast64()[g];
+      SKn.launch(dim3(ctx->num_sms * occ_cap(SKn.occ)), SKn.smem, ctx->aux[a], E, E.r64b.units[g], E.r64b.haps,
+                 E.r64b.unit_cap[g], E.r64b.count + g, ctx->d_counters.p + kCtrR64bWork + g, nullptr,
+                 col_rows_for(SKn.P, ctx->max_n));
+      ++launches;
+    }
+  }
   CK(join());
   CK(cudaEventRecord(ctx->ev_post1, st));
-  for (int g = kNumR64Geoms - 1; g >= 0; --g) {   // band pairs whose exact rerun underflowed
-    if (!E.r64b.units[g]) continue;
+  for (int g = kNumR64Geoms - 1; g >= 0; --g) {   // striped second-stage units
+    if (!E.r64b.units[g] || ctx->r64_col_off[g] < 0) continue;
     const bool str = ctx->r64_col_off[g] >= 0;
     const StreamKernel& SKn = str ? striped_tab(kFast64) : stream_table_fast64()[g];
     SKn.launch(dim3(str ? ctx->r64_grid : ctx->num_sms * occ_cap(SKn.occ)), SKn.smem, st, E, E.r64b.units[g],
