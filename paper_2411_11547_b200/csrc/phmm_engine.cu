@@ -1829,15 +1829,20 @@ int phmm_score(phmm_ctx* ctx, const phmm_input* in, const phmm_options* opt, dou
   trace.print("score");
   // Pipelining (phmm_set_pipeline): large calls ramp -- the GPU idles while the first
   // chunk is planned and the host finishes the last one after the GPU is done, so both are
-  // small (planning runs ~4x faster than the GPU scores, so chunk 1 is ready in time).
-  // c5 (tools/sweep_chunks.sh): 1,3,5,5,3,1 276.1 ms < 1,3,4,4,3,1 277.0 < 1,4,6,6,4,1 277.7
-  // < 1,2,4,4,4,1 < 1,6,8,8,6,2 281.7 < 1,4,6,4,1 < 1,3,4,4,4 < 1,2,2,2,1; the ramp also wins at
-  // 1.25M pairs (41 vs 52 ms one-pass).  Below 2^20 pairs one pass is as fast or faster
-  // (c2 2.2 vs 2.4 ms with 3 chunks; 131k-524k pairs equal; tools/sweep_chunks_*.sh).
+  // small (planning runs ~4x faster than the GPU scores, so chunk 1 is ready in time); the
+  // middle chunks stay large (each chunk's phases end in a tail).  e2e per call
+  // (tools/sweep_chunks_n8.sh): 1.25M pairs (the per-GPU share of c5 at N = 8) 1,5,1 38.0 ms
+  // < 1,4,1 38.5 < 1,3,3,1 39.6 < 1,3,5,5,3,1 40.6 < one pass 52; 2.5M 1,6,1 / 1,5,1 72.7 <
+  // 1,3,5,5,3,1 75.2; 5M 1,4,8,4,1 137.3 < 1,3,6,3,1 138.2 < 1,3,5,5,3,1 140.2 < 1,5,1 141;
+  // c5 (10M) 1,4,8,8,4,1 267.7 < 1,4,8,4,1 268.5 < 1,3,5,5,3,1 270.2 < 1,6,6,1 276 < 1,8,1
+  // 305.  Below 2^20 pairs one pass is as fast or faster (c2 2.1 vs 2.3+ ms chunked, c3
+  // 3.8 vs 4.0+; tools/sweep_chunks_small2.sh).
   if (ok && ctx->pipeline != 1) {
     std::vector<int> w;
     if (ctx->pipeline > 1 && in->num_batches >= 2 * ctx->pipeline) w.assign(ctx->pipeline, 1);
-    else if (ctx->pipeline == 0 && pairs >= kBigCallPairs) w = {1, 3, 5, 5, 3, 1};
+    else if (ctx->pipeline == 0 && pairs >= 8000000) w = {1, 4, 8, 8, 4, 1};
+    else if (ctx->pipeline == 0 && pairs >= 3500000) w = {1, 4, 8, 4, 1};
+    else if (ctx->pipeline == 0 && pairs >= kBigCallPairs) w = {1, 5, 1};
     if (const char* env = getenv("PHMM_CHUNK_WEIGHTS"); env && !w.empty()) {   // experiments
       std::vector<int> ew;
       for (const char* p = env; *p;) {

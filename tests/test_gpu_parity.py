@@ -161,7 +161,7 @@ def test_prepare_execute_fetch_is_rerunnable(engine):
 
 def test_million_pair_gatk_call_against_oracle(engine):
     """A >= 1M-pair GATK-shaped call (the c5 prefix of 2,048 batches = 1,048,576 pairs)
-    with the FP64 retry: the big-call branches (6 ramped pipelined chunk contexts, longer
+    with the FP64 retry: the big-call branches (3 ramped pipelined chunk contexts, longer
     device-built retry units) against the oracle -- f32 for every pair, f64 on the
     flagged subset; chunked-call stats are filled (device time span, FP32 phases)."""
     flat = datagen.workload("c5", num_batches=2048)
