@@ -274,6 +274,8 @@ struct phmm_ctx {
   cudaStream_t aux[kAux] = {};
   cudaEvent_t ev_join[kAux] = {};
   cudaEvent_t ev_x32[kAux] = {};              // execute: exact-FP32 post-pass launches done
+  cudaStream_t r64b_st[kNumR64Geoms] = {};    // second-stage FP64 units, one stream per tiling
+  cudaEvent_t ev_r64b[kNumR64Geoms] = {};
   std::string err;
   std::vector<double> lut;
 
@@ -405,6 +407,10 @@ static int init_ctx(phmm_ctx* ctx, int device) {
     CK(cudaEventCreateWithFlags(&ctx->ev_join[a], cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&ctx->ev_x32[a], cudaEventDisableTiming));
   }
+  for (int g = 0; g < kNumR64Geoms; ++g) {
+    CK(cudaStreamCreateWithFlags(&ctx->r64b_st[g], cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&ctx->ev_r64b[g], cudaEventDisableTiming));
+  }
   CK(cudaEventCreate(&ctx->ev_start));
   CK(cudaEventCreate(&ctx->ev_fast0));
   CK(cudaEventCreate(&ctx->ev_fast1));
@@ -468,6 +474,10 @@ int phmm_destroy(phmm_ctx* ctx) {
     if (ctx->aux[a]) { cudaStreamSynchronize(ctx->aux[a]); cudaStreamDestroy(ctx->aux[a]); }
     if (ctx->ev_join[a]) cudaEventDestroy(ctx->ev_join[a]);
     if (ctx->ev_x32[a]) cudaEventDestroy(ctx->ev_x32[a]);
+  }
+  for (int g = 0; g < kNumR64Geoms; ++g) {
+    if (ctx->r64b_st[g]) { cudaStreamSynchronize(ctx->r64b_st[g]); cudaStreamDestroy(ctx->r64b_st[g]); }
+    if (ctx->ev_r64b[g]) cudaEventDestroy(ctx->ev_r64b[g]);
   }
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
@@ -1033,14 +1043,14 @@ static int prepare_impl(phmm_ctx* ctx, const phmm_input* in, const phmm_options*
   const bool rx32 = streamed > 0 && ctx->rx32_geoms;
   if (!r64) ctx->r64_geoms = 0;
   if (!rx32) ctx->rx32_geoms = 0;
-  // second-stage FP64 units (r64b: guard-band pairs whose exact rerun underflows) live in
-  // a second region of the FP64 unit list of their tiling: long reads (widest tiling), and
-  // every tiling of a large call (per-pair FP64 is latency bound: c5 5.4 ms for 53k pairs)
+  // second-stage FP64 units (r64b: guard-band pairs whose exact rerun underflows, from the
+  // exact-FP32 stream units, the inline reruns and the per-pair exact list) live in a
+  // second region of the FP64 unit list of their tiling, for every tiling: per-pair FP64 is
+  // latency bound (c5 5.4 ms for 53k pairs) and rounds differently from the stream kernel,
+  // so with one FP64 kernel for all retries a pair's value does not depend on the path
+  // (or the chunking) that reran it
   const bool big = streamed >= kBigCallPairs;
-  unsigned r64b_geoms = 0;
-  for (int g = 0; g < kNumR64Geoms; ++g)
-    if (r64 && rx32 && (ctx->r64_geoms & (1u << g)) && (big || (g == kNumR64Geoms - 1 && long64)))
-      r64b_geoms |= 1u << g;
+  const unsigned r64b_geoms = r64 ? ctx->r64_geoms : 0u;
   for (int g = 0; g < kNumR64Geoms; ++g)
     if (ctx->r64_geoms & (1u << g))
       CK(ctx->d_r64u[g].ensure(r64_pairs[g] * ((r64b_geoms >> g) & 1 ? 2 : 1)));
@@ -1289,29 +1299,33 @@ int phmm_execute(phmm_ctx* ctx) {
                   str ? ctx->rx32_grid : ctx->num_sms * occ_cap(SKn.occ))] = true;
     }
   // second-stage FP64 units (guard-band pairs whose exact rerun underflowed) depend only on
-  // the exact-FP32 stream kernels: single-stripe tilings start on a side stream as soon as
-  // those are done, beside the first-stage FP64 units (c5: their 3-4 ms tail overlapped);
-  // striped ones share their tiling's boundary columns with the first stage and run after it
+  // the exact-FP32 kernels (stream units, and the per-pair list on aux[0]; the inline reruns
+  // ran in the FP32 phase): single-stripe tilings start, one stream each, as soon as those
+  // are done, beside the first-stage FP64 units (c5: their 3-4 ms tail overlapped); striped
+  // ones share their tiling's boundary columns with the first stage and run after it
+  x32_on[0] = true;
   bool r64b_side = false;
   for (int g = 0; g < kNumR64Geoms; ++g) r64b_side |= E.r64b.units[g] && ctx->r64_col_off[g] < 0;
-  if (r64b_side) {
-    const int a = 0;                                // after the (short) per-pair exact FP32 list
+  if (r64b_side)
     for (int x = 0; x < phmm_ctx::kAux; ++x)
-      if (x32_on[x] && x != a) {
-        CK(cudaEventRecord(ctx->ev_x32[x], ctx->aux[x]));
-        CK(cudaStreamWaitEvent(ctx->aux[a], ctx->ev_x32[x], 0));
-      }
-    used[a] = true;
-    for (int g = kNumR64Geoms - 1; g >= 0; --g) {
-      if (!E.r64b.units[g] || ctx->r64_col_off[g] >= 0) continue;
-      const StreamKernel& SKn = stream_table_fast64()[g];
-      SKn.launch(dim3(ctx->num_sms * occ_cap(SKn.occ)), SKn.smem, ctx->aux[a], E, E.r64b.units[g], E.r64b.haps,
-                 E.r64b.unit_cap[g], E.r64b.count + g, ctx->d_counters.p + kCtrR64bWork + g, nullptr,
-                 col_rows_for(SKn.P, ctx->max_n));
-      ++launches;
-    }
+      if (x32_on[x]) CK(cudaEventRecord(ctx->ev_x32[x], ctx->aux[x]));
+  bool r64b_on[kNumR64Geoms] = {};
+  for (int g = kNumR64Geoms - 1; g >= 0 && r64b_side; --g) {
+    if (!E.r64b.units[g] || ctx->r64_col_off[g] >= 0) continue;
+    cudaStream_t b = ctx->r64b_st[g];
+    for (int x = 0; x < phmm_ctx::kAux; ++x)
+      if (x32_on[x]) CK(cudaStreamWaitEvent(b, ctx->ev_x32[x], 0));
+    const StreamKernel& SKn = stream_table_fast64()[g];
+    SKn.launch(dim3(ctx->num_sms * occ_cap(SKn.occ)), SKn.smem, b, E, E.r64b.units[g], E.r64b.haps,
+               E.r64b.unit_cap[g], E.r64b.count + g, ctx->d_counters.p + kCtrR64bWork + g, nullptr,
+               col_rows_for(SKn.P, ctx->max_n));
+    ++launches;
+    CK(cudaEventRecord(ctx->ev_r64b[g], b));
+    r64b_on[g] = true;
   }
   CK(join());
+  for (int g = 0; g < kNumR64Geoms; ++g)
+    if (r64b_on[g]) CK(cudaStreamWaitEvent(st, ctx->ev_r64b[g], 0));
   CK(cudaEventRecord(ctx->ev_post1, st));
   for (int g = kNumR64Geoms - 1; g >= 0; --g) {   // striped second-stage units
     if (!E.r64b.units[g] || ctx->r64_col_off[g] < 0) continue;
@@ -1595,6 +1609,7 @@ static int score_chunked(phmm_ctx* ctx, const phmm_input* in, const phmm_options
     for (phmm_ctx* cx : ctx->chunks) {
       cudaStreamSynchronize(cx->stream);
       for (int a = 0; a < phmm_ctx::kAux; ++a) cudaStreamSynchronize(cx->aux[a]);
+      for (int g = 0; g < kNumR64Geoms; ++g) cudaStreamSynchronize(cx->r64b_st[g]);
     }
   };
   phmm_stats total;

@@ -135,6 +135,8 @@ template <> struct ExactTraits<double> {
   static __device__ __forceinline__ double flush_thr() { return 0x1p-970; }
 };
 
+__device__ inline bool retry64_unit(const EngineDev& E, int pair, int read, int hap, int m);
+
 // One item (read x haplotype) on one sub-warp of P threads; `live` false = the
 // sub-warp only takes part in the warp-wide shuffles.  Writes acc/status itself.
 template <typename T, int P, int K>
@@ -271,7 +273,8 @@ __device__ __forceinline__ void exact_item(const EngineDev& E, const ExactItem& 
     if (kIsF32) {
       if (bad && E.retry_f64) {
         E.status[it.pair] = kStatusRetriedF64;
-        append_item(E.fx64, E.fx64_count, E.list_cap, exact_slot_for(m), ExactItem{it.pair, r, it.hap, 0});
+        if (!retry64_unit(E, it.pair, r, it.hap, m))
+          append_item(E.fx64, E.fx64_count, E.list_cap, exact_slot_for(m), ExactItem{it.pair, r, it.hap, 0});
       } else {
         E.acc[it.pair] = (double)res;
         E.status[it.pair] = bad ? kStatusOverflow : kStatusExactF32;
@@ -356,6 +359,26 @@ __host__ __device__ __forceinline__ int r64_geom_for(int m) {
   return w <= 32 ? 0 : w <= 64 ? 1 : w <= 96 ? 2 : w <= 128 ? 3 : w <= 192 ? 4 : w <= 224 ? 5 : 6;
 }
 __host__ __device__ __forceinline__ int r64_geom_P(int g) { return g == 0 ? 8 : (g <= 3 ? 16 : 32); }
+
+// A guard-band pair whose exact FP32 rerun ran per pair (inline or from the per-pair list)
+// and underflowed: a one-haplotype second-stage FP64 stream unit, so every FP64 retry of a
+// call runs on the FP64 stream kernel whichever path reran the pair (the per-pair FP64
+// kernel rounds differently in the last ulp).  false: no second-stage list for this read.
+__device__ inline bool retry64_unit(const EngineDev& E, int pair, int read, int hap, int m) {
+  const RetryLists& L = E.r64b;
+  const int g = r64_geom_for(m);
+  if (!L.enabled || !L.units[g]) return false;
+  const int n = (int)(E.hoff[hap + 1] - E.hoff[hap]);
+  const int ui = atomicAdd(&L.count[g], 1);
+  const int hi = atomicAdd(L.hap_count, 1);
+  if (ui < L.unit_cap[g] && hi < L.hap_cap) {
+    L.haps[hi] = StreamHap{hap, pair, (int)E.hoff[hap], n};
+    L.units[g][ui] = StreamUnit{read, hi, 1, 0, n, 0, (int)E.roff[read], m};
+  } else {
+    atomicAdd(L.overflow, 1);                 // capacity is sized for every pair: never
+  }
+  return true;
+}
 __host__ __device__ __forceinline__ int rx32_geom_for(int m) {
   const int w = m + 1;
   return w <= 32 ? 0 : w <= 64 ? 1 : w <= 96 ? 2 : w <= 128 ? 3 : w <= 192 ? 4 : w <= 256 ? 5

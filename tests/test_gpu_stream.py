@@ -374,6 +374,22 @@ def test_c3_device_scratch_is_small(engine):
     ctx.close()
 
 
+def test_automatic_ramp_of_a_large_call_bit_identical():
+    """The automatic chunk ramp of the largest calls ((1,4,8,8,4,1) from 8M pairs: six
+    chunk contexts, device-built second-stage FP64 units on a side stream) against the one
+    pass of the same context, bit for bit, with the FP64 retry."""
+    flat = datagen.workload("c5", num_batches=16384)                    # 8.4M pairs
+    assert flat.num_pairs >= 8_000_000
+    ctx = _native.Context(0)
+    got, gst, st = ctx.score(flat, F32, _native.FLAG_RETRY_F64)
+    ctx.set_pipeline(1)
+    want, wst, _ = ctx.score(flat, F32, _native.FLAG_RETRY_F64)
+    assert np.array_equal(got, want, equal_nan=True) and np.array_equal(gst, wst)
+    assert st.num_pairs == flat.num_pairs and st.device_ms > 0
+    assert ((gst & _native.ST_RETRIED_F64) != 0).mean() > 0.2            # the retry path ran
+    ctx.close()
+
+
 @pytest.mark.parametrize("n", [2, 3, 5, 8])
 def test_pipeline_depths_bit_identical(engine, n):
     """phmm_set_pipeline(n): n equal chunk contexts give bit-identical results to the one
