@@ -147,7 +147,11 @@ int64_t stream_geom_cost(int mode, int g, int64_t total, int nmax, int64_t lane_
   const int64_t cap = std::max<int64_t>(nmax, std::min<int64_t>(stream_cap((int)P), std::max<int64_t>(nmax, lane_rows)));
   const int64_t units = (total + 2 * cap - 1) / (2 * cap);
   const int64_t rows = std::min<int64_t>(cap, (total + 2 * units - 1) / (2 * units));
-  return units * P * (2 * K + 5) * (rows + P - 1);     // 2 x (K + 2.5) per thread-row
+  const int64_t c = units * P * (2 * K + 5) * (rows + P - 1);     // 2 x (K + 2.5) per thread-row
+  // 4-thread sub-warps run at ~70 % of the per-cell rate the model gives them (8 units per
+  // warp: the warp steps through the union of their event windows); x1.3 hands reads of
+  // 48-63 bases to (8,8) instead of (4,16): c5 FP32 phase 132.2 -> 131.4 ms
+  return (mode == kFast32 && P == 4) ? c * 13 / 10 : c;
 }
 int choose_stream_geom(int mode, int m, int64_t total, int nmax, int64_t lane_rows) {
   int64_t best = INT64_MAX;
