@@ -3,10 +3,10 @@
 
 namespace phmm {
 
-// the geometry table (W = 16 .. 512), then K = 10, 14 tilings (2-wide emission chunks)
-// for widths 80 .. 448, then odd-K P = 16 tilings (W = 144 .. 240; the last emission chunk
-// padded) that halve the W >= m + 1 padding of reads 128 .. 255 long (odd-K P = 8 tilings
-// for reads 64 .. 127: c5 -1 ms, c3 +6 % from the extra small bins)
+// the geometry table (W = 16 .. 512), then K = 10, 14 tilings for widths 80 .. 448, then
+// odd-K P = 16 tilings (W = 144 .. 240) that halve the W >= m + 1 padding of reads
+// 128 .. 255 long (odd-K P = 8 tilings for reads 64 .. 127: c5 -1 ms, c3 +6 % from the
+// extra small bins); K % 4 != 0 pads the last float4 emission chunk
 const StreamKernel* stream_table_fast32() {
   static const StreamKernel tab[kNumStreamFast32] = {
       SK<kFast32, 4, 4>(),   SK<kFast32, 4, 8>(),   SK<kFast32, 4, 12>(),  SK<kFast32, 4, 16>(),

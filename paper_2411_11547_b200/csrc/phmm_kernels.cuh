@@ -429,18 +429,16 @@ template <> struct Lanes<true> {
   static __device__ __forceinline__ S thr() { return 0x1p-970; }
 };
 template <int L, class V> __device__ __forceinline__ auto& lane_ref(V& v) { return L == 0 ? v.x : v.y; }
-// emission-table chunks: float4 (4 positions, LDS.128) when K % 4 == 0 and for odd K (the
-// last chunk padded), float2 (LDS.64) for K = 10, 14; double2 in FP64 (odd K padded)
+// emission-table chunks: float4 (4 positions, LDS.128) in FP32, double2 in FP64; the last
+// chunk is padded when K is not a multiple of the width (K = 14: 4 LDS.128 per lane-step
+// instead of 7 LDS.64, c5 FP32 phase -0.7 %)
 __device__ __forceinline__ float ev_comp(const float4& v, int i) { return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w; }
-__device__ __forceinline__ float ev_comp(const float2& v, int i) { return i == 0 ? v.x : v.y; }
 __device__ __forceinline__ double ev_comp(const double2& v, int i) { return i == 0 ? v.x : v.y; }
 __device__ __forceinline__ void ev_pack(float4& e, const float* l) { e = make_float4(l[0], l[1], l[2], l[3]); }
-__device__ __forceinline__ void ev_pack(float2& e, const float* l) { e = make_float2(l[0], l[1]); }
 __device__ __forceinline__ void ev_pack(double2& e, const double* l) { e = make_double2(l[0], l[1]); }
 template <bool F64, int K> struct EChunk {
-  static constexpr bool F4 = !F64 && (K % 4 == 0 || K % 2 == 1);   // odd K: last chunk padded
-  using type = typename std::conditional<F64, double2, typename std::conditional<F4, float4, float2>::type>::type;
-  static constexpr int width = F64 ? 2 : (F4 ? 4 : 2);
+  using type = typename std::conditional<F64, double2, float4>::type;
+  static constexpr int width = F64 ? 2 : 4;
   static constexpr int chunks = (K + width - 1) / width;
 };
 // FP32 pairs: the flush as a packed multiply by {v >= thr} in {1, 0} (FSET + FSET + FMUL2
