@@ -342,7 +342,7 @@ template <int MODE> struct ModeOf {
   static constexpr bool EXACT = MODE == kExact32 || MODE == kExact64;
 };
 template <int MODE, int K> struct StreamOcc {
-  static constexpr int value = ModeOf<MODE>::F64 ? (K <= 6 ? 3 : 2) : (K <= 8 ? 4 : (K <= 12 ? 3 : 2));
+  static constexpr int value = ModeOf<MODE>::F64 ? (K <= 6 ? 3 : 2) : (K <= 8 ? 4 : (K <= (MODE == 0 ? 11 : 12) ? 3 : 2));
 };
 
 // Device-built stream units (one list per tiling): FP64 retries of FP32-underflowed pairs
@@ -1037,7 +1037,7 @@ k_stream(const EngineDev E, const StreamUnit* __restrict__ units, const StreamHa
       const EV* EA = (CHECK && cA == kCodeIdle) ? s_zero + t : Et + (cA * KE) * P + t;
       const EV* EB = (CHECK && cB == kCodeIdle) ? s_zero + t : Et + (cB * KE) * P + t;
       // fast FP32 at occupancy 2 (K = 14, 16) has the registers for the carried values
-      constexpr bool FUSED = !EXACT && (F64 ? !STRIPES : K >= 14);
+      constexpr bool FUSED = !EXACT && (F64 ? !STRIPES : K >= 12);
       if constexpr (FUSED) {
         // one ascending pass: position k's D'', M~ and I'' from position k's and k-1's
         // previous-step values (carried in pmo/pio/pdo) and k-1's new M~, I'' -- step s+1
