@@ -1098,7 +1098,8 @@ static int prepare_impl(phmm_ctx* ctx, const phmm_input* in, const phmm_options*
     L.hap_cap = geoms ? (int)streamed : 0;
     // short units keep small post-pass lists parallel (their size is unknown when the
     // grid is sized); large calls get longer units (less fill/drain and setup per pair)
-    L.lane_haps = &L == &E.r64 ? (big ? 4 : kRetryLaneHaps64) : (big ? 3 : kRetryLaneHapsX32);
+    // (c5, FP64 / exact lane haplotypes: 8 / 5 250.7 ms < 4 / 5 252.4 < 4 / 3 252.9 < 3 / 3 257.6)
+    L.lane_haps = &L == &E.r64 ? (big ? 8 : kRetryLaneHaps64) : (big ? 5 : kRetryLaneHapsX32);
   };
   lists(E.r64, ctx->d_r64u, kNumR64Geoms, ctx->d_r64h, ctx->r64_geoms, kCtrR64, r64_pairs);
   lists(E.rx32, ctx->d_rx32u, kNumRX32Geoms, ctx->d_rx32h, ctx->rx32_geoms, kCtrRX32, rx32_pairs);
