@@ -98,7 +98,8 @@ const int kStripedGeom[4] = {12, kNumR64Geoms - 1, kNumRX32Geoms - 1, kNumR64Geo
 constexpr int kCtrR64 = 32, kCtrRX32 = 44, kCtrR64Work = 56, kCtrRX32Work = 64;
 constexpr int kCtrR64b = 72, kCtrR64bWork = 80;   // second-stage striped FP64 units: counts, work
 constexpr int kBinCounters = 96;                  // fixed counter slots before the per-bin counters
-constexpr int64_t kBigCallPairs = 1 << 20;        // device-built retry units grow above this
+constexpr int64_t kBigCallPairs = 1 << 20;        // phmm_score pipelines calls above this
+constexpr int64_t kMidCallPairs = 1 << 16;        // device-built retry units grow above this
 constexpr int kFinishThreads = 16;                // host threads finishing log10 in phmm_fetch
 // scratch bound for boundary columns of long haplotypes (striped stream bins, post-pass);
 // contexts of a budgeted phmm_score use an eighth of their chunk budget instead
@@ -1053,7 +1054,7 @@ static int prepare_impl(phmm_ctx* ctx, const phmm_input* in, const phmm_options*
   // latency bound (c5 5.4 ms for 53k pairs) and rounds differently from the stream kernel,
   // so with one FP64 kernel for all retries a pair's value does not depend on the path
   // (or the chunking) that reran it
-  const bool big = streamed >= kBigCallPairs;
+  const bool longer = streamed >= kMidCallPairs;   // longer device-built retry units
   const unsigned r64b_geoms = r64 ? ctx->r64_geoms : 0u;
   for (int g = 0; g < kNumR64Geoms; ++g)
     if (ctx->r64_geoms & (1u << g))
@@ -1098,8 +1099,9 @@ static int prepare_impl(phmm_ctx* ctx, const phmm_input* in, const phmm_options*
     L.hap_cap = geoms ? (int)streamed : 0;
     // short units keep small post-pass lists parallel (their size is unknown when the
     // grid is sized); large calls get longer units (less fill/drain and setup per pair)
-    // (c5, FP64 / exact lane haplotypes: 8 / 5 250.7 ms < 4 / 5 252.4 < 4 / 3 252.9 < 3 / 3 257.6)
-    L.lane_haps = &L == &E.r64 ? (big ? 8 : kRetryLaneHaps64) : (big ? 5 : kRetryLaneHapsX32);
+    // (FP64 / exact lane haplotypes: c5 8 / 5 250.7 ms < 4 / 5 252.4 < 4 / 3 252.9 < 3 / 3
+    // 257.6; 512k pairs 8 / 5 13.5 ms < 4 / 3 13.6 < 2 / 1 13.9; c3 (65k) equal)
+    L.lane_haps = &L == &E.r64 ? (longer ? 8 : kRetryLaneHaps64) : (longer ? 5 : kRetryLaneHapsX32);
   };
   lists(E.r64, ctx->d_r64u, kNumR64Geoms, ctx->d_r64h, ctx->r64_geoms, kCtrR64, r64_pairs);
   lists(E.rx32, ctx->d_rx32u, kNumRX32Geoms, ctx->d_rx32h, ctx->rx32_geoms, kCtrRX32, rx32_pairs);
@@ -1111,7 +1113,7 @@ static int prepare_impl(phmm_ctx* ctx, const phmm_input* in, const phmm_options*
     E.r64b = E.r64;
     for (int x = 0; x < 8; ++x) E.r64b.units[x] = nullptr;
     E.r64b.count = ctx->d_counters.p + kCtrR64b;
-    E.r64b.lane_haps = big ? E.r64.lane_haps : 1;
+    E.r64b.lane_haps = longer ? E.r64.lane_haps : 1;
     E.r64b.enabled = r64b_geoms ? 1 : 0;
     for (int g = 0; g < kNumR64Geoms; ++g)
       if ((r64b_geoms >> g) & 1) E.r64b.units[g] = ctx->d_r64u[g].p + r64_pairs[g];
