@@ -1857,12 +1857,13 @@ int phmm_score(phmm_ctx* ctx, const phmm_input* in, const phmm_options* opt, dou
   // < 1,4,1 38.5 < 1,3,3,1 39.6 < 1,3,5,5,3,1 40.6 < one pass 52; 2.5M 1,6,1 / 1,5,1 72.7 <
   // 1,3,5,5,3,1 75.2; 5M 1,4,8,4,1 137.3 < 1,3,6,3,1 138.2 < 1,3,5,5,3,1 140.2 < 1,5,1 141;
   // c5 (10M) 1,4,8,8,4,1 267.7 < 1,4,8,4,1 268.5 < 1,3,5,5,3,1 270.2 < 1,6,6,1 276 < 1,8,1
-  // 305.  Below 2^20 pairs one pass is as fast or faster (c2 2.1 vs 2.3+ ms chunked, c3
+  // 305; after the round's post-pass changes 1,5,10,10,5,1 260.3 < 1,6,14,14,6,1 260.6 <
+  // 1,6,12,12,6,1 260.8 < 1,4,8,8,4,1 261.2 < 1,8,16,16,8,1 262.  Below 2^20 pairs one pass is as fast or faster (c2 2.1 vs 2.3+ ms chunked, c3
   // 3.8 vs 4.0+; tools/sweep_chunks_small2.sh).
   if (ok && ctx->pipeline != 1) {
     std::vector<int> w;
     if (ctx->pipeline > 1 && in->num_batches >= 2 * ctx->pipeline) w.assign(ctx->pipeline, 1);
-    else if (ctx->pipeline == 0 && pairs >= 8000000) w = {1, 4, 8, 8, 4, 1};
+    else if (ctx->pipeline == 0 && pairs >= 8000000) w = {1, 5, 10, 10, 5, 1};
     else if (ctx->pipeline == 0 && pairs >= 3500000) w = {1, 4, 8, 4, 1};
     else if (ctx->pipeline == 0 && pairs >= kBigCallPairs) w = {1, 5, 1};
     if (const char* env = getenv("PHMM_CHUNK_WEIGHTS"); env && !w.empty()) {   // experiments
