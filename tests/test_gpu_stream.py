@@ -375,7 +375,7 @@ def test_c3_device_scratch_is_small(engine):
 
 
 def test_automatic_ramp_of_a_large_call_bit_identical():
-    """The automatic chunk ramp of the largest calls ((1,4,8,8,4,1) from 8M pairs: six
+    """The automatic chunk ramp of the largest calls ((1,5,10,10,5,1) from 8M pairs: six
     chunk contexts, device-built second-stage FP64 units on a side stream) against the one
     pass of the same context, bit for bit, with the FP64 retry."""
     flat = datagen.workload("c5", num_batches=16384)                    # 8.4M pairs
